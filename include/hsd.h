@@ -1,0 +1,179 @@
+/*
+ * hsd.h -- C ABI of the B200-native hidden-state tree speculative decoder
+ * (arXiv 2602.21224, "Make Every Draft Count", system name Lyanna).
+ *
+ * One library call = one stage of the per-step draft-tree verify-and-reuse loop
+ * (section 3 Overview). Citations: P:<line> = PAPER.md line.
+ *
+ * Conventions (all entry points):
+ *  - Every call is asynchronous on the stream given to hsd_init_model, except
+ *    where stated ("synchronous"). Outputs go into CALLER-OWNED buffers whose
+ *    location (host or device) is stated per argument.
+ *  - Host-checkable preconditions (contract violations: bad sizes, k > V,
+ *    B < 1, N < 1, token outside [0, V), more requests than max_batch, wrong call
+ *    order) return HSD_EINVAL / HSD_ESTATE BEFORE any launch, with text in
+ *    hsd_last_error(). Device-side violations set a device error word that is
+ *    surfaced as HSD_EDEVICE by hsd_sync().
+ *  - A context owns all its device memory (weights, paged KV pools, the
+ *    token-info table, workspace); it is used by one host thread at a time.
+ *  - Layout words: "row-major [a, b]" means element (i, j) at i*b + j.
+ *  - Requests are independent. Random streams use the GLOBAL request id
+ *    (req_offset + local index) so batch sharding across GPUs never changes a
+ *    result.
+ */
+#ifndef HSD_H
+#define HSD_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hsd_ctx hsd_ctx;
+
+typedef enum {
+  HSD_OK = 0,
+  HSD_EINVAL = -1,   /* contract violation (host-checked, nothing launched)   */
+  HSD_ENOMEM = -2,   /* device allocation failed                               */
+  HSD_ECUDA = -3,    /* CUDA runtime / launch error                            */
+  HSD_ENCCL = -4,    /* reserved: collective error                             */
+  HSD_ESTATE = -5,   /* call order violated (e.g. verify before build)         */
+  HSD_EUNSUP = -6,   /* configuration not supported by this build              */
+  HSD_EDEVICE = -7   /* a kernel detected a violation on the device            */
+} hsd_status;
+
+enum { HSD_FP32_VERIFY = 0, HSD_BF16 = 1 };          /* hsd_config.precision   */
+enum { HSD_GREEDY = 0, HSD_STOCHASTIC = 1 };         /* hsd_config.accept_mode */
+enum {                                               /* hsd_config.flags       */
+  HSD_FLAG_RESAMPLE = 1u << 0,  /* Alg. 2 re-sampling              */
+  HSD_FLAG_FUSION = 1u << 1,    /* verification fusion             */
+  HSD_FLAG_PLANTED = 1u << 2,   /* planted-continuation perf mode (DESIGN R24) */
+  HSD_FLAG_ZERO_TABLE = 1u << 3,/* token info off: Alg. 1 == beam tree */
+  HSD_FLAG_TCGEN05 = 1u << 4    /* bf16 GEMMs on tcgen05 (else SIMT FFMA)       */
+};
+
+#define HSD_MAX_PLANT_DEPTH 16
+
+typedef struct {
+  /* target model shape (Llama decoder)                   */
+  int32_t vocab, hidden, layers, q_heads, kv_heads, head_dim, ffn;
+  float rope_theta, rms_eps;
+  /* tree / method parameters: N steps (tree depth), branch k, budget B
+     (non-root nodes), re-sample budget B_r and threshold r,
+     hot tokens V_h (0 = dense table), low-rank d (R7; 0 -> hidden/16)  */
+  int32_t steps_N, branch_k, budget_B, resample_budget_Br, resample_threshold_r;
+  int32_t hot_tokens, table_rank;
+  /* capacity                                                                 */
+  int32_t max_batch, max_ctx, page_size;
+  int32_t precision;    /* HSD_FP32_VERIFY | HSD_BF16                          */
+  int32_t accept_mode;  /* HSD_GREEDY | HSD_STOCHASTIC                         */
+  float temperature;    /* stochastic mode only                                */
+  uint64_t seed;        /* Philox seed for weights and sampling (R23)           */
+  uint32_t flags;       /* HSD_FLAG_*                                          */
+  int32_t req_offset;   /* global id of local request 0 (batch sharding)       */
+  /* HOST pointer, vocab entries, rank -> token id (rank 0 = most frequent);
+     required when hot_tokens > 0 (defines the hot set, R5), else may be NULL.
+     Copied during hsd_init_model.                                            */
+  const int32_t* vocab_perm;
+  /* planted mode: acceptance rates a_1..a_N (R24)                            */
+  float plant_rates[HSD_MAX_PLANT_DEPTH];
+} hsd_config;
+
+/* Fill *cfg with neutral defaults (flags RESAMPLE|FUSION, B_r 4, r 1, page 64). */
+void hsd_config_defaults(hsd_config* cfg);
+
+/* Create a context on `device`, allocate every pool and generate the weights on
+ * the device from Philox (R23), precompute RoPE tables, and build the
+ * token-info table W_collapsed = W_E W1 W2 with row RMSNorm and 2-D hot pruning
+ * (P:290-296). `cuda_stream` is a cudaStream_t (NULL = legacy
+ * default stream). Synchronous. On failure *out is NULL.                      */
+hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, hsd_ctx** out);
+
+/* Prefill `n_req` (<= max_batch) requests. h_tokens: HOST row-major
+ * [n_req, stride] int32 prompt tokens, request r uses h_tokens[r*stride ...
+ * + h_lens[r]). h_lens: HOST [n_req], 2 <= len, len + max_new + N + T <=
+ * max_ctx. Runs the target causally over each prompt (writes KV), picks the
+ * first token (argmax, or Gumbel sample in stochastic mode, R22), and runs the
+ * draft layer over pairs (H_{j-1}, t_j), j = 1..len-1 (R1). d_first: DEVICE
+ * [n_req] int32 output (may be NULL). Resets the step counter.              */
+hsd_status hsd_prefill(hsd_ctx* ctx, int32_t n_req, const int32_t* h_tokens, int32_t stride,
+                       const int32_t* h_lens, int32_t* d_first);
+
+/* Planted mode only: HOST row-major [n_req, stride] greedy continuation tokens
+ * indexed by absolute position (R24). Copied. */
+hsd_status hsd_set_plant(hsd_ctx* ctx, const int32_t* h_plant, int32_t stride);
+
+/* Read-only device view of the current draft tree (valid until the next
+ * mutating call). Arrays are row-major per request, T_max = B + B_r + 1 slots:
+ * tok [b, T_max] int32, par [b, T_max] int32 (-1 root), depth [b, T_max] int32,
+ * logjoint [b, T_max] float, n [b] int32 node count, anc [b, T_max, anc_words]
+ * uint64 ancestor bitmask (bit s of row u set iff slot s is u or an ancestor
+ * of u; P:95 tree attention).                                                 */
+typedef struct {
+  const int32_t* tok; const int32_t* par; const int32_t* depth; const float* logjoint;
+  const int32_t* n; const uint64_t* anc;
+  int32_t batch, t_max, anc_words;
+} hsd_tree_view;
+
+/* Read-only device view of the last verification: logits [b, T_max, vocab]
+ * float32 (target logits per slot), argmax [b, T_max] int32, hidden
+ * [b, T_max, hidden] float32 (pre-final-norm H).                             */
+typedef struct {
+  const float* logits; const int32_t* argmax; const float* hidden;
+  int32_t batch, t_max, vocab, hidden_dim;
+} hsd_verify_view;
+
+/* S0 + S1: draft chain, one-pass logits, Alg. 1 tree
+ * (P:310-353), prune to B, fuse the pending re-sampled tree and prune
+ * to B + B_r, linearise + ancestor masks. `out` may be NULL. */
+hsd_status hsd_build_tree(hsd_ctx* ctx, hsd_tree_view* out);
+
+/* Replace the tree built by hsd_build_tree with a caller tree (teacher
+ * forcing in parity tests). HOST arrays [n_req, t_max] tok/par/depth and
+ * [n_req] n; slots depth-major, parents before children. */
+hsd_status hsd_force_tree(hsd_ctx* ctx, const int32_t* h_tok, const int32_t* h_par,
+                          const int32_t* h_depth, const int32_t* h_n);
+
+/* S2: target forward over the tree slots with tree-masked attention over the
+ * paged KV cache + the tree; writes the slots' K/V at cache
+ * positions p..p+T-1. `out` may be NULL. Requires hsd_build_tree. */
+hsd_status hsd_verify_tree(hsd_ctx* ctx, hsd_verify_view* out);
+
+/* S3 + S4: acceptance walk (greedy P:378 / stochastic R13), KV compaction of
+ * the accepted path, hidden-state gather for the next draft prefill, and Alg. 2
+ * re-sampling into the pending tree. d_emitted: DEVICE [b, N+1]
+ * int32 (accepted draft tokens then the bonus token; unused entries -1);
+ * d_n_emitted: DEVICE [b] int32 (m+1). Either may be NULL. Requires
+ * hsd_verify_tree. */
+hsd_status hsd_accept_and_compact(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n_emitted);
+
+/* One whole step = build_tree + verify_tree + accept_and_compact, captured in
+ * a CUDA graph on first use and replayed afterwards (no host sync inside). */
+hsd_status hsd_step(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n_emitted);
+
+/* hsd_step with HOST outputs: emitted [b, N+1] and n [b] are copied
+ * device->host inside the call (synchronous). The end-to-end API. */
+hsd_status hsd_step_host(hsd_ctx* ctx, int32_t* h_emitted, int32_t* h_n_emitted);
+
+/* Wait for the context stream; returns HSD_EDEVICE if a kernel flagged a
+ * violation (and resets the flag), HSD_ECUDA on a CUDA error. Synchronous. */
+hsd_status hsd_sync(hsd_ctx* ctx);
+
+/* Debug/test access to named device tensors (e.g. "kv", "draft_logits",
+ * "table", "pos", "pend_tok", "acc_slots", "bonus"). Fills a device pointer,
+ * dtype code (0 f32, 1 bf16, 2 i32, 3 u64) and up to 4 dims. */
+typedef struct { void* ptr; int32_t dtype; int32_t ndim; int64_t dims[4]; } hsd_tensor;
+hsd_status hsd_get_tensor(hsd_ctx* ctx, const char* name, hsd_tensor* out);
+
+/* Number of this library's kernels launched on the ctx since creation. */
+int64_t hsd_kernel_launches(const hsd_ctx* ctx);
+
+hsd_status hsd_destroy(hsd_ctx* ctx);
+const char* hsd_last_error(const hsd_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSD_H */

@@ -1,0 +1,207 @@
+// accept.cu -- S3 acceptance walk and S4 compaction / state update.
+//
+// Greedy (PAPER.md:378, :449 T = 0): from the root slot follow the child whose
+//   token equals the target argmax at the current slot; the bonus token is the
+//   argmax where the walk stops.
+// Stochastic (reading R13): children in slot order are accepted with
+//   p(c) / (1 - sum_rejected p) against a Philox uniform u(req, step, slot,
+//   rank); if all are rejected the bonus is a Gumbel-max sample from the
+//   residual (V minus the rejected tokens); at a leaf the bonus ~ p.
+// Compaction: KV[p + j] <- KV[p + s_j] for the accepted slots s_j (s_j >= j); each
+//   thread loads all its source elements before storing (in-place hazard).
+#include "kernels.cuh"
+#include "accept.cuh"
+
+namespace {
+constexpr int WT = 256;
+
+// lse of x/T over V (CTA-wide, deterministic)
+HSD_DEV float row_lse(const float* x, int V, float invT, float* red) {
+  float m = -INFINITY, s = 0.f;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) {
+    float v = x[j] * invT;
+    if (v > m) { s = s * expf(m - v) + 1.f; m = v; }
+    else s += expf(v - m);
+  }
+  float M = block_max(m, red);
+  s = (m == -INFINITY) ? 0.f : s * expf(m - M);
+  s = block_sum(s, red);
+  return M + logf(s);
+}
+
+// Gumbel-max over v not in `excl` (n_excl entries): argmax_v x_v/T - log(-log U_v)
+HSD_DEV int gumbel_argmax(const float* x, int V, float invT, uint32_t seed, uint32_t req, uint32_t step,
+                          uint32_t slot, const int* excl, int n_excl, float* redf, int* redi) {
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int b4 = threadIdx.x; b4 * 4 < V; b4 += blockDim.x) {
+    u32x4 c = {(uint32_t)b4, slot, step, req};
+    u32x4 r = philox4x32_10(c, seed, TAG_GUMBEL);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int v = b4 * 4 + q;
+      if (v >= V) break;
+      bool ex = false;
+      for (int e = 0; e < n_excl; ++e) ex |= (excl[e] == v);
+      if (ex) continue;
+      float u = unit_open(lane_of(r, q));
+      float z = x[v] * invT - logf(-logf(u));
+      if (better(z, v, bv, bi)) { bv = z; bi = v; }
+    }
+  }
+  warp_argmax(bv, bi);
+  int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) { redf[w] = bv; redi[w] = bi; }
+  __syncthreads();
+  if (w == 0) {
+    int nw = blockDim.x >> 5;
+    bv = lane < nw ? redf[lane] : -INFINITY;
+    bi = lane < nw ? redi[lane] : 0x7fffffff;
+    warp_argmax(bv, bi);
+    if (lane == 0) redi[0] = bi;
+  }
+  __syncthreads();
+  int res = redi[0];
+  __syncthreads();
+  return res;
+}
+
+__global__ void __launch_bounds__(WT) walk_kernel(AcceptParams P) {
+  __shared__ float red[32];
+  __shared__ int redi[32];
+  __shared__ int acc[32], m_sh, bonus_sh, cur_sh, done_sh, excl[64], n_excl;
+  const int req = blockIdx.x, T = P.t_max;
+  const int* tok = P.t_tok + req * T;
+  const int* par = P.t_par + req * T;
+  const int n = P.t_n[req];
+  if (threadIdx.x == 0) { m_sh = 0; cur_sh = 0; done_sh = 0; }
+  __syncthreads();
+  if (P.mode == 0) {
+    if (threadIdx.x == 0) {
+      int cur = 0, m = 0;
+      while (true) {
+        int a = P.argmax[req * T + cur];
+        int nxt = -1;
+        for (int s = cur + 1; s < n; ++s)
+          if (par[s] == cur && tok[s] == a) { nxt = s; break; }
+        if (nxt < 0 || m >= P.N) { bonus_sh = a; break; }
+        acc[m++] = nxt;
+        cur = nxt;
+      }
+      m_sh = m;
+    }
+    __syncthreads();
+  } else {
+    const float invT = 1.0f / P.temperature;
+    const uint32_t rq = (uint32_t)(P.req_offset + req), st = (uint32_t)(*P.step);
+    while (true) {
+      int cur = cur_sh;
+      const float* x = P.logits + ((size_t)req * T + cur) * P.V;
+      float lse = row_lse(x, P.V, invT, red);
+      if (threadIdx.x == 0) {
+        n_excl = 0;
+        float S = 0.f;
+        int took = -1, rank = 0;
+        for (int s = cur + 1; s < n && took < 0; ++s) {
+          if (par[s] != cur) continue;
+          int t = tok[s];
+          float pc = expf(x[t] * invT - lse);
+          u32x4 c = {(uint32_t)cur, (uint32_t)rank, st, rq};
+          float u = unit_open(philox4x32_10(c, P.seed, TAG_ACCEPT).x);
+          float denom = 1.f - S;
+          float pres = denom > 0.f ? pc / denom : 0.f;
+          if (u < pres) took = s;
+          else { if (n_excl < 64) excl[n_excl++] = t; S += pc; }
+          ++rank;
+        }
+        if (took >= 0 && m_sh < P.N) { acc[m_sh++] = took; cur_sh = took; }
+        else done_sh = 1;
+      }
+      __syncthreads();
+      if (done_sh) {
+        int b = gumbel_argmax(x, P.V, invT, P.seed, rq, st, (uint32_t)cur, excl, n_excl, red, redi);
+        if (threadIdx.x == 0) bonus_sh = b;
+        break;
+      }
+    }
+    __syncthreads();
+  }
+  // outputs
+  const int m = m_sh;
+  for (int j = threadIdx.x; j <= P.N; j += blockDim.x) {
+    int v = -1;
+    if (j < m) v = tok[acc[j]];
+    else if (j == m) v = bonus_sh;
+    P.emitted[req * (P.N + 1) + j] = v;
+  }
+  for (int j = threadIdx.x; j < P.N; j += blockDim.x) P.acc_slots[req * P.N + j] = j < m ? acc[j] : -1;
+  if (threadIdx.x == 0) {
+    P.acc_n[req] = m;
+    P.bonus[req] = bonus_sh;
+    P.n_emitted[req] = m + 1;
+  }
+}
+
+// KV compaction: grid (b, layers, 2*Hkv); thread d moves dim d of rows j=1..m.
+template <typename T>
+__global__ void compact_kernel(CompactParams P) {
+  const int req = blockIdx.x, layer = blockIdx.y, kh = blockIdx.z;
+  const int kind = kh / P.kv_heads, h = kh % P.kv_heads;
+  const int m = P.acc_n[req];
+  if (m == 0) return;
+  const int p = P.p[req], hd = P.head_dim, ps = P.page_size;
+  T* base = (T*)P.kv_base + (size_t)layer * P.layer_stride;
+  for (int d = threadIdx.x; d < hd; d += blockDim.x) {
+    T vals[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j >= m) break;
+      int key = p + P.acc_slots[req * P.N + j];
+      int page = P.block_table[(size_t)req * P.pages_per_req + key / ps];
+      vals[j] = base[((((size_t)page * 2 + kind) * P.kv_heads + h) * ps + key % ps) * hd + d];
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j >= m) break;
+      int key = p + 1 + j;
+      int page = P.block_table[(size_t)req * P.pages_per_req + key / ps];
+      base[((((size_t)page * 2 + kind) * P.kv_heads + h) * ps + key % ps) * hd + d] = vals[j];
+    }
+  }
+}
+
+// state update: pending draft pairs, root, position, step counter
+__global__ void commit_kernel(CommitParams P) {
+  const int req = blockIdx.x;
+  const int m = P.acc_n[req];
+  const int n = P.hidden;
+  for (int j = 0; j <= m; ++j) {
+    int slot = j == 0 ? 0 : P.acc_slots[req * P.N + j - 1];
+    const float* src = P.Hverify + ((size_t)req * P.t_max + slot) * n;
+    float* dst = P.pend_H + ((size_t)req * (P.N + 1) + j) * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  }
+  if (threadIdx.x == 0) {
+    for (int j = 0; j <= P.N; ++j)
+      P.pend_tok[req * (P.N + 1) + j] = j <= m ? P.emitted[req * (P.N + 1) + j] : -1;
+    P.n_pend[req] = m + 1;
+    P.root_tok[req] = P.bonus[req];
+    P.p[req] += m + 1;
+    if (req == 0) atomicAdd(P.step, 1);
+  }
+}
+}  // namespace
+
+void launch_walk(const AcceptParams& P, int n_req, cudaStream_t st) {
+  if (n_req > 0) walk_kernel<<<n_req, WT, 0, st>>>(P);
+}
+void launch_compact(const CompactParams& P, int n_req, int layers, DType dt, cudaStream_t st) {
+  if (n_req <= 0) return;
+  dim3 grid(n_req, layers, 2 * P.kv_heads);
+  if (dt == DT_F32) compact_kernel<float><<<grid, 128, 0, st>>>(P);
+  else compact_kernel<bf16><<<grid, 128, 0, st>>>(P);
+}
+void launch_commit(const CommitParams& P, int n_req, cudaStream_t st) {
+  if (n_req > 0) commit_kernel<<<n_req, 256, 0, st>>>(P);
+}

@@ -1,0 +1,105 @@
+// common.cuh -- shared device helpers of the sm_100a kernels (product side).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#define HSD_DEV __device__ __forceinline__
+
+typedef __nv_bfloat16 bf16;
+
+enum DType { DT_F32 = 0, DT_BF16 = 1, DT_I32 = 2, DT_U64 = 3 };
+
+// ---------------------------------------------------------------- conversion
+HSD_DEV float to_f32(float x) { return x; }
+HSD_DEV float to_f32(bf16 x) { return __bfloat162float(x); }
+template <typename T> HSD_DEV T from_f32(float x);
+template <> HSD_DEV float from_f32<float>(float x) { return x; }
+template <> HSD_DEV bf16 from_f32<bf16>(float x) { return __float2bfloat16_rn(x); }
+
+// ---------------------------------------------------------------- Philox4x32-10
+// Salmon et al. (SC'11). Product-side implementation; checked against the
+// Random123 known-answer vectors in tests/test_gpu_*.py.
+struct u32x4 { uint32_t x, y, z, w; };
+
+HSD_DEV u32x4 philox4x32_10(u32x4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    u32x4 n;
+    n.x = hi1 ^ c.y ^ k0; n.y = lo1; n.z = hi0 ^ c.w ^ k1; n.w = lo0;
+    c = n;
+  }
+  return c;
+}
+HSD_DEV uint32_t lane_of(const u32x4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+// sampling uniform in (0,1): ((x>>8)+0.5)*2^-24 (exact in fp32)
+HSD_DEV float unit_open(uint32_t x) { return ((float)(x >> 8) + 0.5f) * 5.9604644775390625e-08f; }
+
+#define TAG_ACCEPT 0x5EED0001u
+#define TAG_GUMBEL 0x5EED0002u
+#define TAG_PLANT 0x5EED0003u
+
+// ---------------------------------------------------------------- reductions
+HSD_DEV float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+HSD_DEV float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// block-wide sum with a fixed (deterministic) reduction tree; `red` >= 32 floats
+HSD_DEV float block_sum(float v, float* red) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  float t = (threadIdx.x < (unsigned)nw) ? red[threadIdx.x] : 0.f;
+  if (w == 0) t = warp_sum(t);
+  if (threadIdx.x == 0) red[0] = t;
+  __syncthreads();
+  float r = red[0];
+  __syncthreads();
+  return r;
+}
+HSD_DEV float block_max(float v, float* red) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  float t = (threadIdx.x < (unsigned)nw) ? red[threadIdx.x] : -INFINITY;
+  if (w == 0) t = warp_max(t);
+  if (threadIdx.x == 0) red[0] = t;
+  __syncthreads();
+  float r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// (value desc, index asc) "better" comparison used by argmax / top-k (R8)
+HSD_DEV bool better(float va, int ia, float vb, int ib) {
+  return va > vb || (va == vb && ia < ib);
+}
+// warp argmax over (value, index) pairs with the tie rule above
+HSD_DEV void warp_argmax(float& v, int& i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, v, o);
+    int oi = __shfl_xor_sync(0xffffffffu, i, o);
+    if (better(ov, oi, v, i)) { v = ov; i = oi; }
+  }
+}
+
+// ---------------------------------------------------------------- error word
+#define DEV_ERR_BAD_TREE 1
+#define DEV_ERR_BAD_TOKEN 2
+#define DEV_ERR_OVERFLOW 4

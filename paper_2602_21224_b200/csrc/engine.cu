@@ -1,0 +1,922 @@
+// engine.cu -- hsd_ctx and the C ABI of include/hsd.h.
+//
+// Orchestrates one step of the draft-tree verify-and-reuse loop
+// as a fixed sequence of kernel launches on the context stream, sized for the
+// padded maxima (b x T_max verify slots, b x (N+1) draft rows) with every
+// data-dependent count kept on the device, so a whole step is capturable in one
+// CUDA graph and replayed with no host synchronisation.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <cmath>
+#include <string>
+#include <vector>
+#include <algorithm>
+
+#include "../../include/hsd.h"
+#include "kernels.cuh"
+#include "tree.cuh"
+#include "accept.cuh"
+#include "gemm_tc.cuh"
+
+int64_t g_hsd_launches = 0;
+
+namespace {
+constexpr int PREFILL_CHUNK = 1024;
+constexpr int MAXN_TREE = 256;
+
+// ------------------------------------------------------------------ row metadata kernels
+struct MetaBuf {
+  int32_t *tok, *pos, *kvpos, *req, *klo, *khi, *slot;
+  RowMeta view(const int32_t* tbase, const uint64_t* anc, int t_max, int anc_words) const {
+    RowMeta m;
+    m.tok = tok; m.pos = pos; m.kvpos = kvpos; m.req = req; m.klo = klo; m.khi = khi; m.slot = slot;
+    m.tbase = tbase; m.anc = anc; m.t_max = t_max; m.anc_words = anc_words;
+    return m;
+  }
+};
+
+// verify rows r*T + s: slot s of request r's tree at position p + depth, K/V
+// stored at p + s; sees the committed cache [0, p) plus its tree ancestors.
+__global__ void meta_verify_kernel(MetaBuf mb, int T, const int32_t* t_n, const int32_t* t_tok,
+                                   const int32_t* t_depth, const int32_t* p) {
+  int r = blockIdx.x, s = threadIdx.x;
+  if (s >= T) return;
+  int row = r * T + s;
+  bool act = s < t_n[r];
+  mb.tok[row] = act ? t_tok[row] : 0;
+  mb.pos[row] = act ? p[r] + t_depth[row] : -1;
+  mb.kvpos[row] = p[r] + s;
+  mb.req[row] = r;
+  mb.klo[row] = 0;
+  mb.khi[row] = p[r];
+  mb.slot[row] = act ? s : -1;
+}
+
+// draft prefill rows r*(N+1) + j: pending pair j at position p - n_pend + 1 + j,
+// causal over the draft KV positions [1, pos] (reading R1/R2).
+__global__ void meta_dprefill_kernel(MetaBuf mb, int R, const int32_t* n_pend, const int32_t* pend_tok,
+                                     const int32_t* p) {
+  int r = blockIdx.x, j = threadIdx.x;
+  if (j >= R) return;
+  int row = r * R + j;
+  int np = n_pend[r];
+  bool act = j < np;
+  int pos = p[r] - np + 1 + j;
+  mb.tok[row] = act ? pend_tok[row] : 0;
+  mb.pos[row] = act ? pos : -1;
+  mb.kvpos[row] = act ? pos : 0;
+  mb.req[row] = r;
+  mb.klo[row] = 1;
+  mb.khi[row] = act ? pos + 1 : 0;
+  mb.slot[row] = -1;
+}
+
+// chain step i: row r at position p + i, causal over draft KV [1, p + i]
+__global__ void meta_chain_kernel(MetaBuf mb, int b, int i, const int32_t* p) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= b) return;
+  int pos = p[r] + i;
+  mb.tok[r] = 0; mb.pos[r] = pos; mb.kvpos[r] = pos; mb.req[r] = r;
+  mb.klo[r] = 1; mb.khi[r] = pos + 1; mb.slot[r] = -1;
+}
+
+// h_1 = draft output at the last pending row -> xw[r] and chain[r][0]
+__global__ void gather_last_kernel(const float* x, int R, const int32_t* n_pend, int n, float* xw, float* chain,
+                                   int N) {
+  int r = blockIdx.x;
+  const float* src = x + ((size_t)r * R + n_pend[r] - 1) * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    xw[(size_t)r * n + i] = src[i];
+    chain[((size_t)r * N) * n + i] = src[i];
+  }
+}
+
+__global__ void copy_chain_kernel(const float* xw, int n, float* chain, int N, int i) {
+  int r = blockIdx.x;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) chain[((size_t)r * N + i) * n + c] = xw[(size_t)r * n + c];
+}
+
+// first token after prefill: argmax (greedy) or Gumbel sample with step 0, slot 0 (R22);
+// then the pending draft pair (H_{P0-1}, t_{P0}) and the request state.
+__global__ void first_token_kernel(const float* logits, int V, int mode, float invT, uint32_t seed, int req_g,
+                                   int r, const float* Hlast, int n, int P0, int N, float* pend_H,
+                                   int32_t* pend_tok, int32_t* n_pend, int32_t* root_tok, int32_t* p,
+                                   int32_t* d_first) {
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int b4 = threadIdx.x; b4 * 4 < V; b4 += blockDim.x) {
+    u32x4 c = {(uint32_t)b4, 0u, 0u, (uint32_t)req_g};
+    u32x4 rr = philox4x32_10(c, seed, TAG_GUMBEL);
+    for (int q = 0; q < 4; ++q) {
+      int v = b4 * 4 + q;
+      if (v >= V) break;
+      float z = mode == 0 ? logits[v] : logits[v] * invT - logf(-logf(unit_open(lane_of(rr, q))));
+      if (better(z, v, bv, bi)) { bv = z; bi = v; }
+    }
+  }
+  warp_argmax(bv, bi);
+  int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { sv[w] = bv; si[w] = bi; }
+  __syncthreads();
+  if (w == 0) {
+    int nw = blockDim.x >> 5;
+    bv = lane < nw ? sv[lane] : -INFINITY;
+    bi = lane < nw ? si[lane] : 0x7fffffff;
+    warp_argmax(bv, bi);
+    if (lane == 0) si[0] = bi;
+  }
+  __syncthreads();
+  int t = si[0];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) pend_H[((size_t)r * (N + 1)) * n + i] = Hlast[i];
+  if (threadIdx.x == 0) {
+    pend_tok[r * (N + 1)] = t;
+    for (int j = 1; j <= N; ++j) pend_tok[r * (N + 1) + j] = -1;
+    n_pend[r] = 1;
+    root_tok[r] = t;
+    p[r] = P0;
+    if (d_first) d_first[r] = t;
+  }
+}
+
+__global__ void gather_same_kernel_f32(const float* src, const int32_t* idx, int n, float* dst) {
+  int r = blockIdx.x;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[(size_t)r * n + i] = src[(size_t)idx[r] * n + i];
+}
+__global__ void gather_same_kernel_bf16(const bf16* src, const int32_t* idx, int n, bf16* dst) {
+  int r = blockIdx.x;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[(size_t)r * n + i] = src[(size_t)idx[r] * n + i];
+}
+__global__ void f32_to_dt_kernel(const float* src, size_t count, bf16* dst) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+}  // namespace
+
+// ====================================================================== context
+struct LayerW { void *wqkv, *wo, *wgu, *wd; };
+
+struct hsd_ctx {
+  hsd_config cfg;
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  DType dt = DT_F32;
+  size_t esz = 4;
+  int n, L, Hq, Hkv, hd, f, V, qd, kd, qkvd;
+  int N, k, B, Br, r, Vh, d;
+  int T, W;          // verify slots, anc words
+  int maxb, b = 0;   // capacity, active requests
+  bool use_tc = false;
+  // weights
+  void *embed = nullptr, *head = nullptr, *head_rank = nullptr, *fc = nullptr;
+  std::vector<LayerW> layers;
+  LayerW draft{};
+  void* table = nullptr;
+  int32_t *perm_d = nullptr, *rank_d = nullptr;
+  float *rope_cos = nullptr, *rope_sin = nullptr;
+  int max_pos = 0;
+  // KV
+  void *kv_t = nullptr, *kv_d = nullptr;
+  size_t kv_layer_elems = 0;
+  int pages_per_req = 0, page_size = 64;
+  int32_t* block_table = nullptr;
+  // state
+  int32_t *p, *root_tok, *n_pend, *pend_tok, *step;
+  float* pend_H;
+  int* err;
+  int32_t *pt_n, *pt_tok, *pt_par, *pt_depth;
+  float* pt_lj;
+  int32_t *t_n, *t_tok, *t_par, *t_depth;
+  float* t_lj;
+  uint64_t* t_anc;
+  int32_t *acc_n, *acc_slots, *bonus, *emitted, *n_emitted;
+  int32_t* plant = nullptr;
+  int plant_stride = 0;
+  // workspace
+  int Mcap;
+  float *x_d, *xw, *Hver, *chain, *big, *draft_logits, *logits, *x_p, *H_prompt, *attn_ws;
+  size_t attn_ws_floats;
+  void *a, *qb, *ob;
+  int32_t* argmax;
+  MetaBuf mv, md, mc, mp;
+  // host staging for e2e
+  int32_t *h_pinned = nullptr;
+  // graph
+  cudaGraphExec_t graph = nullptr;
+  int64_t graph_kernels = 0;
+  int stage = 0;       // 0 idle, 1 tree built, 2 verified
+  int64_t launches0 = 0, graph_replays = 0;
+  std::vector<void*> allocs;
+  std::string errmsg;
+};
+
+static hsd_status fail(hsd_ctx* c, hsd_status s, const std::string& m) {
+  if (c) c->errmsg = m;
+  return s;
+}
+
+#define CU(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess) {                                                    \
+      return fail(ctx, HSD_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    }                                                                           \
+  } while (0)
+
+static void* dalloc(hsd_ctx* c, size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  cudaMemsetAsync(p, 0, bytes, c->st);
+  c->allocs.push_back(p);
+  return p;
+}
+
+// GEMM dispatch: C[M,N] (+)= A[M,K] W[N,K]^T
+static void gemm(hsd_ctx* c, const void* A, int lda, const void* Wt, int ldw, float* C, int ldc, int M, int N,
+                 int K, bool acc) {
+  if (c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, N, K, lda, ldw)) {
+    g_hsd_launches += gemm_tc_bf16((const bf16*)A, lda, (const bf16*)Wt, ldw, C, ldc, M, N, K, acc, c->st);
+  } else {
+    gemm_simt(A, lda, Wt, ldw, c->dt, C, ldc, M, N, K, acc, c->st);
+    g_hsd_launches += 1;
+  }
+}
+
+static KVLayer kv_layer(hsd_ctx* c, void* pool, int layer) {
+  KVLayer kv;
+  kv.base = (char*)pool + (size_t)layer * c->kv_layer_elems * c->esz;
+  kv.block_table = c->block_table;
+  kv.pages_per_req = c->pages_per_req;
+  kv.page_size = c->page_size;
+  kv.kv_heads = c->Hkv;
+  kv.head_dim = c->hd;
+  return kv;
+}
+
+// One Llama decoder layer over M padded rows (R rows per request, n_req requests),
+// residual stream x (fp32) updated in place.
+static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, int n_req, const RowMeta& m,
+                          const KVLayer& kv, int max_keys) {
+  const int n = c->n;
+  launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st);
+  gemm(c, c->a, n, w.wqkv, n, c->big, c->qkvd, M, c->qkvd, n, false);
+  launch_qkv_rope_kv(c->big, M, m, c->rope_cos, c->rope_sin, c->Hq, kv, c->qb, c->dt, c->st);
+  launch_attention(c->qb, M, R, n_req, m, kv, c->Hq, c->dt, max_keys, c->ob, c->attn_ws, c->attn_ws_floats,
+                   c->st);
+  gemm(c, c->ob, c->qd, w.wo, c->qd, x, n, M, n, c->qd, true);
+  launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st);
+  gemm(c, c->a, n, w.wgu, n, c->big, 2 * c->f, M, 2 * c->f, n, false);
+  launch_swiglu(c->big, M, c->f, c->a, c->dt, m.pos, c->st);
+  gemm(c, c->a, c->f, w.wd, c->f, x, n, M, n, c->f, true);
+  g_hsd_launches += 6;  // rmsnorm x2, rope_kv, attention(+merge counted below), swiglu
+}
+
+// ---------------------------------------------------------------------- stages
+static void stage_build(hsd_ctx* c) {
+  const int b = c->b, N = c->N, n = c->n, R = N + 1;
+  const int kvmax = c->max_pos;
+  // S0 (1): draft prefill of the pending pairs x_j = W_fc [H_{j-1}; E(t_j)] (R1)
+  meta_dprefill_kernel<<<b, 32 * ((R + 31) / 32), 0, c->st>>>(c->md, R, c->n_pend, c->pend_tok, c->p);
+  RowMeta mdv = c->md.view(nullptr, nullptr, 0, 0);
+  launch_draft_concat(c->pend_H, c->md.tok, c->md.pos, c->embed, c->dt, b * R, n, c->a, c->st);
+  gemm(c, c->a, 2 * n, c->fc, 2 * n, c->x_d, n, b * R, n, 2 * n, false);
+  layer_forward(c, c->draft, c->x_d, b * R, R, b, mdv, kv_layer(c, c->kv_d, 0), kvmax);
+  gather_last_kernel<<<b, 256, 0, c->st>>>(c->x_d, R, c->n_pend, n, c->xw, c->chain, N);
+  g_hsd_launches += 3;
+  // S0 (2): chain h_{i+1} = TL(h_i) at positions p + i (R2)
+  RowMeta mcv = c->mc.view(nullptr, nullptr, 0, 0);
+  for (int i = 1; i < N; ++i) {
+    meta_chain_kernel<<<(b + 127) / 128, 128, 0, c->st>>>(c->mc, b, i, c->p);
+    layer_forward(c, c->draft, c->xw, b, 1, b, mcv, kv_layer(c, c->kv_d, 0), kvmax);
+    copy_chain_kernel<<<b, 256, 0, c->st>>>(c->xw, n, c->chain, N, i);
+    g_hsd_launches += 2;
+  }
+  // S1a: one-pass logits L = RMSNorm_f(H_chain) W_head^T, rank order
+  launch_rmsnorm(c->chain, b * N, n, c->cfg.rms_eps, c->a, c->dt, nullptr, c->st);
+  gemm(c, c->a, n, c->head_rank, n, c->draft_logits, c->V, b * N, c->V, n, false);
+  g_hsd_launches += 1;
+  // S1b + S1c: Alg. 1, prune, fuse, linearise (+ planting)
+  TreeParams P{};
+  P.N = N; P.k = c->k; P.B = c->B; P.Br = c->Br; P.r = c->r; P.V = c->V; P.Vh = c->Vh; P.t_max = c->T;
+  P.anc_words = c->W;
+  P.fusion = (c->cfg.flags & HSD_FLAG_FUSION) ? 1 : 0;
+  P.resample = (c->cfg.flags & HSD_FLAG_RESAMPLE) ? 1 : 0;
+  P.zero_table = (c->cfg.flags & HSD_FLAG_ZERO_TABLE) ? 1 : 0;
+  P.L = c->draft_logits; P.table = c->table; P.tdt = c->dt; P.perm = c->perm_d; P.rank_of = c->rank_d;
+  P.root_tok = c->root_tok;
+  P.pt_n = c->pt_n; P.pt_tok = c->pt_tok; P.pt_par = c->pt_par; P.pt_depth = c->pt_depth; P.pt_lj = c->pt_lj;
+  P.t_n = c->t_n; P.t_tok = c->t_tok; P.t_par = c->t_par; P.t_depth = c->t_depth; P.t_lj = c->t_lj;
+  P.t_anc = c->t_anc;
+  P.p = c->p; P.step = c->step;
+  P.plant = (c->cfg.flags & HSD_FLAG_PLANTED) ? c->plant : nullptr;
+  P.plant_stride = c->plant_stride;
+  for (int i = 0; i < HSD_MAX_PLANT_DEPTH_DEV; ++i) P.plant_rates[i] = c->cfg.plant_rates[i];
+  P.seed = (uint32_t)c->cfg.seed; P.req_offset = c->cfg.req_offset; P.err = c->err;
+  launch_tree(P, TREE_MODE_FRESH, b, c->st);
+  g_hsd_launches += 1;
+}
+
+static void stage_verify(hsd_ctx* c) {
+  const int b = c->b, T = c->T, n = c->n, M = b * T;
+  meta_verify_kernel<<<b, 32 * ((T + 31) / 32), 0, c->st>>>(c->mv, T, c->t_n, c->t_tok, c->t_depth, c->p);
+  RowMeta m = c->mv.view(c->p, c->t_anc, T, c->W);
+  launch_embed(c->embed, c->dt, c->mv.tok, c->mv.pos, M, n, c->Hver, c->st);
+  g_hsd_launches += 2;
+  for (int l = 0; l < c->L; ++l) layer_forward(c, c->layers[l], c->Hver, M, T, b, m, kv_layer(c, c->kv_t, l), c->max_pos);
+  launch_rmsnorm(c->Hver, M, n, c->cfg.rms_eps, c->a, c->dt, c->mv.pos, c->st);
+  gemm(c, c->a, n, c->head, n, c->logits, c->V, M, c->V, n, false);
+  launch_argmax_rows(c->logits, M, c->V, c->mv.pos, c->argmax, c->st);
+  g_hsd_launches += 2;
+}
+
+static void stage_accept(hsd_ctx* c, int32_t* d_emitted, int32_t* d_n) {
+  const int b = c->b;
+  AcceptParams A{};
+  A.mode = c->cfg.accept_mode == HSD_STOCHASTIC ? 1 : 0;
+  A.N = c->N; A.t_max = c->T; A.V = c->V; A.temperature = c->cfg.temperature;
+  A.seed = (uint32_t)c->cfg.seed; A.req_offset = c->cfg.req_offset;
+  A.t_tok = c->t_tok; A.t_par = c->t_par; A.t_n = c->t_n; A.argmax = c->argmax; A.logits = c->logits;
+  A.step = c->step;
+  A.acc_n = c->acc_n; A.acc_slots = c->acc_slots; A.bonus = c->bonus; A.emitted = c->emitted;
+  A.n_emitted = c->n_emitted;
+  launch_walk(A, b, c->st);
+  CompactParams C{};
+  C.kv_base = c->kv_t; C.layer_stride = c->kv_layer_elems; C.block_table = c->block_table;
+  C.pages_per_req = c->pages_per_req; C.page_size = c->page_size; C.kv_heads = c->Hkv; C.head_dim = c->hd;
+  C.N = c->N; C.acc_n = c->acc_n; C.acc_slots = c->acc_slots; C.p = c->p;
+  launch_compact(C, b, c->L, c->dt, c->st);
+  // Alg. 2 re-sampling into the pending tree (reads acc_n, bonus, draft logits)
+  TreeParams P{};
+  P.N = c->N; P.k = c->k; P.B = c->B; P.Br = c->Br; P.r = c->r; P.V = c->V; P.Vh = c->Vh; P.t_max = c->T;
+  P.anc_words = c->W;
+  P.fusion = (c->cfg.flags & HSD_FLAG_FUSION) ? 1 : 0;
+  P.resample = (c->cfg.flags & HSD_FLAG_RESAMPLE) ? 1 : 0;
+  P.zero_table = (c->cfg.flags & HSD_FLAG_ZERO_TABLE) ? 1 : 0;
+  P.L = c->draft_logits; P.table = c->table; P.tdt = c->dt; P.perm = c->perm_d; P.rank_of = c->rank_d;
+  P.pt_n = c->pt_n; P.pt_tok = c->pt_tok; P.pt_par = c->pt_par; P.pt_depth = c->pt_depth; P.pt_lj = c->pt_lj;
+  P.acc_n = c->acc_n; P.bonus = c->bonus; P.err = c->err;
+  launch_tree(P, TREE_MODE_RESAMPLE, b, c->st);
+  CommitParams M{};
+  M.N = c->N; M.t_max = c->T; M.hidden = c->n; M.Hverify = c->Hver;
+  M.acc_n = c->acc_n; M.acc_slots = c->acc_slots; M.emitted = c->emitted; M.bonus = c->bonus;
+  M.pend_H = c->pend_H; M.pend_tok = c->pend_tok; M.n_pend = c->n_pend; M.root_tok = c->root_tok; M.p = c->p;
+  M.step = c->step;
+  launch_commit(M, b, c->st);
+  g_hsd_launches += 4;
+  if (d_emitted) cudaMemcpyAsync(d_emitted, c->emitted, sizeof(int32_t) * b * (c->N + 1), cudaMemcpyDeviceToDevice, c->st);
+  if (d_n) cudaMemcpyAsync(d_n, c->n_emitted, sizeof(int32_t) * b, cudaMemcpyDeviceToDevice, c->st);
+}
+
+// ====================================================================== C ABI
+extern "C" {
+
+void hsd_config_defaults(hsd_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->rope_theta = 10000.f; c->rms_eps = 1e-5f;
+  c->resample_budget_Br = 4; c->resample_threshold_r = 1;
+  c->page_size = 64; c->precision = HSD_BF16; c->accept_mode = HSD_GREEDY; c->temperature = 1.f;
+  c->flags = HSD_FLAG_RESAMPLE | HSD_FLAG_FUSION;
+  c->max_batch = 1;
+}
+
+const char* hsd_last_error(const hsd_ctx* ctx) { return ctx ? ctx->errmsg.c_str() : "null context"; }
+
+int64_t hsd_kernel_launches(const hsd_ctx* ctx) {
+  return ctx ? (g_hsd_launches - ctx->launches0) + ctx->graph_replays * ctx->graph_kernels : 0;
+}
+
+static std::string check_config(const hsd_config* c) {
+  if (c->vocab < 2 || c->hidden < 1 || c->layers < 0 || c->q_heads < 1 || c->kv_heads < 1 || c->ffn < 1)
+    return "model shape must be positive (vocab >= 2)";
+  if (c->q_heads % c->kv_heads) return "q_heads must be a multiple of kv_heads";
+  if (c->head_dim < 2 || c->head_dim % 2 || c->head_dim > 128) return "head_dim must be even and <= 128";
+  if (c->q_heads * c->head_dim < 1) return "bad heads";
+  if (c->steps_N < 1 || c->steps_N > 16) return "steps_N must be in [1, 16] (contract violation: N < 1)";
+  if (c->branch_k < 1 || c->branch_k > 8) return "branch_k must be in [1, 8]";
+  if (c->branch_k > c->vocab) return "k > |V| (contract violation)";
+  if (c->budget_B < 1) return "budget_B must be >= 1 (contract violation: B < 1)";
+  if (c->resample_budget_Br < 0 || c->resample_threshold_r < 0) return "B_r and r must be >= 0";
+  long cand = 1 + c->branch_k + (long)(c->steps_N - 1) * c->branch_k * c->branch_k;
+  if (cand > MAXN_TREE) return "1 + k + (N-1)k^2 candidate nodes exceed the device tree capacity (256)";
+  if (c->budget_B + c->resample_budget_Br + 1 > MAXN_TREE) return "B + B_r + 1 exceeds 256 verify slots";
+  if (c->hot_tokens < 0 || c->hot_tokens > c->vocab) return "hot_tokens out of range";
+  if (c->hot_tokens > 0 && c->vocab_perm == nullptr) return "hot_tokens > 0 requires vocab_perm";
+  if (c->max_batch < 1 || c->max_ctx < 2) return "max_batch >= 1 and max_ctx >= 2 required";
+  if (c->page_size < 1) return "page_size >= 1";
+  if (c->precision != HSD_FP32_VERIFY && c->precision != HSD_BF16) return "precision must be FP32_VERIFY or BF16";
+  if (c->accept_mode != HSD_GREEDY && c->accept_mode != HSD_STOCHASTIC) return "bad accept_mode";
+  if (c->accept_mode == HSD_STOCHASTIC && !(c->temperature > 0.f)) return "temperature must be > 0";
+  return "";
+}
+
+hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, hsd_ctx** out) {
+  if (!out) return HSD_EINVAL;
+  *out = nullptr;
+  if (!cfg) return HSD_EINVAL;
+  std::string why = check_config(cfg);
+  if (!why.empty()) {
+    static thread_local std::string last;
+    last = why;
+    fprintf(stderr, "hsd_init_model: %s\n", why.c_str());
+    return HSD_EINVAL;
+  }
+  hsd_ctx* ctx = new hsd_ctx();
+  ctx->cfg = *cfg;
+  ctx->dev = device;
+  ctx->launches0 = g_hsd_launches;
+  CU(cudaSetDevice(device));
+  ctx->st = (cudaStream_t)cuda_stream;
+  hsd_ctx* c = ctx;
+  c->dt = cfg->precision == HSD_BF16 ? DT_BF16 : DT_F32;
+  c->esz = c->dt == DT_BF16 ? 2 : 4;
+  c->use_tc = (cfg->flags & HSD_FLAG_TCGEN05) && c->dt == DT_BF16;
+  c->n = cfg->hidden; c->L = cfg->layers; c->Hq = cfg->q_heads; c->Hkv = cfg->kv_heads; c->hd = cfg->head_dim;
+  c->f = cfg->ffn; c->V = cfg->vocab; c->qd = c->Hq * c->hd; c->kd = c->Hkv * c->hd; c->qkvd = c->qd + 2 * c->kd;
+  c->N = cfg->steps_N; c->k = cfg->branch_k; c->B = cfg->budget_B; c->Br = cfg->resample_budget_Br;
+  c->r = cfg->resample_threshold_r;
+  c->Vh = cfg->hot_tokens > 0 ? cfg->hot_tokens : c->V;
+  c->d = cfg->table_rank > 0 ? cfg->table_rank : std::max(1, c->n / 16);
+  c->T = c->B + c->Br + 1;
+  c->W = (c->T + 63) / 64;
+  c->maxb = cfg->max_batch;
+  c->page_size = cfg->page_size;
+  const int n = c->n, V = c->V;
+  const size_t es = c->esz;
+  bool fail_alloc = false;
+  auto A = [&](size_t bytes) {
+    void* p = dalloc(c, bytes);
+    if (!p) fail_alloc = true;
+    return p;
+  };
+  // ---- weights (R23): Philox, tensor ids as in DESIGN.md section 4
+  const uint32_t seed = (uint32_t)cfg->seed;
+  auto sc = [](int fan_in) { return sqrtf(3.0f / (float)fan_in); };
+  c->embed = A((size_t)V * n * es);
+  c->head = A((size_t)V * n * es);
+  c->fc = A((size_t)n * 2 * n * es);
+  if (fail_alloc) { hsd_destroy(c); return HSD_ENOMEM; }
+  launch_philox_fill(c->embed, c->dt, (size_t)V * n, seed, 1, 1.0f, c->st);
+  launch_philox_fill(c->head, c->dt, (size_t)V * n, seed, 2, sc(n), c->st);
+  launch_philox_fill(c->fc, c->dt, (size_t)n * 2 * n, seed, 5, sc(2 * n), c->st);
+  auto make_layer = [&](uint32_t tid0) {
+    LayerW w;
+    w.wqkv = A((size_t)c->qkvd * n * es);
+    w.wo = A((size_t)n * c->qd * es);
+    w.wgu = A((size_t)2 * c->f * n * es);
+    w.wd = A((size_t)n * c->f * es);
+    if (fail_alloc) return w;
+    launch_philox_fill(w.wqkv, c->dt, (size_t)c->qd * n, seed, tid0 + 0, sc(n), c->st);
+    launch_philox_fill((char*)w.wqkv + (size_t)c->qd * n * es, c->dt, (size_t)c->kd * n, seed, tid0 + 1, sc(n), c->st);
+    launch_philox_fill((char*)w.wqkv + (size_t)(c->qd + c->kd) * n * es, c->dt, (size_t)c->kd * n, seed, tid0 + 2,
+                       sc(n), c->st);
+    launch_philox_fill(w.wo, c->dt, (size_t)n * c->qd, seed, tid0 + 3, sc(c->qd), c->st);
+    launch_philox_fill(w.wgu, c->dt, (size_t)c->f * n, seed, tid0 + 4, sc(n), c->st);
+    launch_philox_fill((char*)w.wgu + (size_t)c->f * n * es, c->dt, (size_t)c->f * n, seed, tid0 + 5, sc(n), c->st);
+    launch_philox_fill(w.wd, c->dt, (size_t)n * c->f, seed, tid0 + 6, sc(c->f), c->st);
+    return w;
+  };
+  for (int l = 0; l < c->L; ++l) c->layers.push_back(make_layer(100 + 8 * l));
+  c->draft = make_layer(60);
+  if (fail_alloc) { hsd_destroy(c); return HSD_ENOMEM; }
+  // ---- vocab permutation (hot set, R5)
+  std::vector<int32_t> perm, rank;
+  if (cfg->hot_tokens > 0) {
+    perm.assign(cfg->vocab_perm, cfg->vocab_perm + V);
+    rank.assign(V, -1);
+    for (int i = 0; i < V; ++i) {
+      if (perm[i] < 0 || perm[i] >= V || rank[perm[i]] >= 0) {
+        hsd_destroy(c);
+        fprintf(stderr, "hsd_init_model: vocab_perm is not a permutation\n");
+        return HSD_EINVAL;
+      }
+      rank[perm[i]] = i;
+    }
+    c->perm_d = (int32_t*)A(sizeof(int32_t) * V);
+    c->rank_d = (int32_t*)A(sizeof(int32_t) * V);
+    if (fail_alloc) { hsd_destroy(c); return HSD_ENOMEM; }
+    CU(cudaMemcpyAsync(c->perm_d, perm.data(), sizeof(int32_t) * V, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->rank_d, rank.data(), sizeof(int32_t) * V, cudaMemcpyHostToDevice, c->st));
+    // draft head rows in rank order, so hot columns of L are contiguous
+    c->head_rank = A((size_t)V * n * es);
+    if (fail_alloc) { hsd_destroy(c); return HSD_ENOMEM; }
+    if (c->dt == DT_F32) gather_same_kernel_f32<<<V, 256, 0, c->st>>>((const float*)c->head, c->perm_d, n, (float*)c->head_rank);
+    else gather_same_kernel_bf16<<<V, 256, 0, c->st>>>((const bf16*)c->head, c->perm_d, n, (bf16*)c->head_rank);
+  } else {
+    c->head_rank = c->head;
+  }
+  // ---- token-info table W_collapsed = W_E W1 W2, row RMSNorm, 2-D hot prune
+  {
+    const int d = c->d, Vh = c->Vh;
+    void* w1 = A((size_t)d * n * es);
+    void* w2 = A((size_t)V * d * es);
+    float* Esel = (float*)A((size_t)Vh * n * 4);
+    float* W1f = (float*)A((size_t)d * n * 4);
+    float* W2f = (float*)A((size_t)V * d * 4);
+    float* C1 = (float*)A((size_t)Vh * d * 4);
+    int chunk = (int)std::max<size_t>(1, std::min<size_t>(Vh, (size_t)(512u << 20) / ((size_t)V * 4)));
+    float* C2 = (float*)A((size_t)chunk * V * 4);
+    c->table = A((size_t)Vh * Vh * es);
+    if (fail_alloc) { hsd_destroy(c); return HSD_ENOMEM; }
+    launch_philox_fill(w1, c->dt, (size_t)d * n, seed, 3, sc(n), c->st);
+    launch_philox_fill(w2, c->dt, (size_t)V * d, seed, 4, sc(d), c->st);
+    launch_gather_rows_f32(c->embed, c->dt, c->perm_d, Vh, n, Esel, c->st);
+    launch_gather_rows_f32(w1, c->dt, nullptr, d, n, W1f, c->st);
+    launch_gather_rows_f32(w2, c->dt, c->perm_d, V, d, W2f, c->st);
+    gemm_simt(Esel, n, W1f, n, DT_F32, C1, d, Vh, d, n, false, c->st);
+    for (int r0 = 0; r0 < Vh; r0 += chunk) {
+      int rows = std::min(chunk, Vh - r0);
+      gemm_simt(C1 + (size_t)r0 * d, d, W2f, d, DT_F32, C2, V, rows, V, d, false, c->st);
+      launch_table_rows(C2, rows, V, Vh, nullptr, (char*)c->table + (size_t)r0 * Vh * es, c->dt, c->st);
+    }
+    CU(cudaStreamSynchronize(c->st));
+    for (void* p : {w1, w2, (void*)Esel, (void*)W1f, (void*)W2f, (void*)C1, (void*)C2}) {
+      cudaFree(p);
+      c->allocs.erase(std::find(c->allocs.begin(), c->allocs.end(), p));
+    }
+  }
+  // ---- RoPE tables (host double precision)
+  c->pages_per_req = (cfg->max_ctx + c->T + c->N + 8 + c->page_size - 1) / c->page_size;
+  c->max_pos = c->pages_per_req * c->page_size;
+  {
+    int half = c->hd / 2;
+    std::vector<float> hc((size_t)c->max_pos * half), hs((size_t)c->max_pos * half);
+    for (int pos = 0; pos < c->max_pos; ++pos)
+      for (int i = 0; i < half; ++i) {
+        double inv = std::pow((double)cfg->rope_theta, -(2.0 * i) / (double)c->hd);
+        double ang = (double)pos * inv;
+        hc[(size_t)pos * half + i] = (float)std::cos(ang);
+        hs[(size_t)pos * half + i] = (float)std::sin(ang);
+      }
+    c->rope_cos = (float*)A(hc.size() * 4);
+    c->rope_sin = (float*)A(hs.size() * 4);
+    if (fail_alloc) { hsd_destroy(c); return HSD_ENOMEM; }
+    CU(cudaMemcpyAsync(c->rope_cos, hc.data(), hc.size() * 4, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->rope_sin, hs.data(), hs.size() * 4, cudaMemcpyHostToDevice, c->st));
+    CU(cudaStreamSynchronize(c->st));
+  }
+  // ---- paged KV pools + identity block table
+  {
+    const int b = c->maxb;
+    c->kv_layer_elems = (size_t)b * c->pages_per_req * 2 * c->Hkv * c->page_size * c->hd;
+    c->kv_t = A(c->kv_layer_elems * es * std::max(1, c->L));
+    c->kv_d = A(c->kv_layer_elems * es);
+    c->block_table = (int32_t*)A(sizeof(int32_t) * b * c->pages_per_req);
+    if (fail_alloc) { hsd_destroy(c); return HSD_ENOMEM; }
+    std::vector<int32_t> bt((size_t)b * c->pages_per_req);
+    for (size_t i = 0; i < bt.size(); ++i) bt[i] = (int32_t)i;
+    CU(cudaMemcpyAsync(c->block_table, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice, c->st));
+  }
+  // ---- state + workspace
+  {
+    const int b = c->maxb, T = c->T, N = c->N, Br1 = c->Br + 1;
+    auto I = [&](size_t cnt) { return (int32_t*)A(cnt * 4); };
+    auto F = [&](size_t cnt) { return (float*)A(cnt * 4); };
+    c->p = I(b); c->root_tok = I(b); c->n_pend = I(b); c->pend_tok = I((size_t)b * (N + 1)); c->step = I(1);
+    c->pend_H = F((size_t)b * (N + 1) * n); c->err = (int*)I(1);
+    c->pt_n = I(b); c->pt_tok = I((size_t)b * Br1); c->pt_par = I((size_t)b * Br1); c->pt_depth = I((size_t)b * Br1);
+    c->pt_lj = F((size_t)b * Br1);
+    c->t_n = I(b); c->t_tok = I((size_t)b * T); c->t_par = I((size_t)b * T); c->t_depth = I((size_t)b * T);
+    c->t_lj = F((size_t)b * T); c->t_anc = (uint64_t*)A((size_t)b * T * c->W * 8);
+    c->acc_n = I(b); c->acc_slots = I((size_t)b * N); c->bonus = I(b); c->emitted = I((size_t)b * (N + 1));
+    c->n_emitted = I(b);
+    c->Mcap = std::max({b * T, b * (N + 1), PREFILL_CHUNK});
+    const int Mc = c->Mcap;
+    const size_t wa = std::max({(size_t)2 * n, (size_t)c->qd, (size_t)c->f});
+    c->a = A((size_t)Mc * wa * es);
+    c->qb = A((size_t)Mc * c->qd * es);
+    c->ob = A((size_t)Mc * c->qd * es);
+    c->big = F((size_t)Mc * std::max(c->qkvd, 2 * c->f));
+    c->x_d = F((size_t)b * (N + 1) * n);
+    c->xw = F((size_t)b * n);
+    c->Hver = F((size_t)b * T * n);
+    c->chain = F((size_t)b * N * n);
+    c->draft_logits = F((size_t)b * N * V);
+    c->logits = F((size_t)std::max(b * T, 1) * V);
+    c->argmax = I((size_t)b * T);
+    c->x_p = F((size_t)PREFILL_CHUNK * n);
+    c->H_prompt = F((size_t)(cfg->max_ctx + 1) * n);
+    c->attn_ws_floats = attention_ws_floats(std::max(b * T, b * (N + 1)), c->Hq, c->hd, 16);
+    c->attn_ws = F(c->attn_ws_floats);
+    auto meta = [&](MetaBuf& m, size_t rows) {
+      m.tok = I(rows); m.pos = I(rows); m.kvpos = I(rows); m.req = I(rows); m.klo = I(rows); m.khi = I(rows);
+      m.slot = I(rows);
+    };
+    meta(c->mv, (size_t)b * T);
+    meta(c->md, (size_t)b * (N + 1));
+    meta(c->mc, (size_t)b);
+    meta(c->mp, (size_t)PREFILL_CHUNK);
+    if (fail_alloc) { hsd_destroy(c); return HSD_ENOMEM; }
+    if (cudaMallocHost(&c->h_pinned, sizeof(int32_t) * (size_t)b * (N + 2)) != cudaSuccess) c->h_pinned = nullptr;
+  }
+  CU(cudaStreamSynchronize(c->st));
+  CU(cudaGetLastError());
+  *out = c;
+  return HSD_OK;
+}
+
+hsd_status hsd_prefill(hsd_ctx* ctx, int32_t n_req, const int32_t* h_tokens, int32_t stride, const int32_t* h_lens,
+                       int32_t* d_first) {
+  if (!ctx) return HSD_EINVAL;
+  hsd_ctx* c = ctx;
+  if (n_req < 1 || n_req > c->maxb) return fail(c, HSD_EINVAL, "n_req must be in [1, max_batch]");
+  if (!h_tokens || !h_lens || stride < 1) return fail(c, HSD_EINVAL, "null prompt arrays");
+  for (int r = 0; r < n_req; ++r) {
+    if (h_lens[r] < 2 || h_lens[r] > stride || h_lens[r] > c->cfg.max_ctx)
+      return fail(c, HSD_EINVAL, "prompt length must be in [2, min(stride, max_ctx)]");
+    for (int i = 0; i < h_lens[r]; ++i)
+      if (h_tokens[(size_t)r * stride + i] < 0 || h_tokens[(size_t)r * stride + i] >= c->V)
+        return fail(c, HSD_EINVAL, "token outside [0, V) (contract violation)");
+  }
+  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+  c->b = n_req;
+  const int n = c->n, N = c->N;
+  CU(cudaMemsetAsync(c->step, 0, 4, c->st));
+  CU(cudaMemsetAsync(c->step, 0, 4, c->st));
+  // step counter starts at 1 for the first speculative step (0 = prefill)
+  {
+    int one = 1;
+    CU(cudaMemcpyAsync(c->step, &one, 4, cudaMemcpyHostToDevice, c->st));
+    CU(cudaStreamSynchronize(c->st));
+  }
+  std::vector<int32_t> ones(c->maxb, 1);
+  CU(cudaMemcpyAsync(c->pt_n, ones.data(), 4 * n_req, cudaMemcpyHostToDevice, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  std::vector<int32_t> tok, pos, kvpos, req, klo, khi, slot;
+  for (int r = 0; r < n_req; ++r) {
+    const int P0 = h_lens[r];
+    const int32_t* pt = h_tokens + (size_t)r * stride;
+    // target causal forward over the prompt, chunked
+    for (int s0 = 0; s0 < P0; s0 += PREFILL_CHUNK) {
+      int M = std::min(PREFILL_CHUNK, P0 - s0);
+      tok.resize(M); pos.resize(M); kvpos.resize(M); req.resize(M); klo.resize(M); khi.resize(M); slot.resize(M);
+      for (int i = 0; i < M; ++i) {
+        tok[i] = pt[s0 + i]; pos[i] = s0 + i; kvpos[i] = s0 + i; req[i] = r; klo[i] = 0; khi[i] = s0 + i + 1;
+        slot[i] = -1;
+      }
+      CU(cudaMemcpyAsync(c->mp.tok, tok.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      CU(cudaMemcpyAsync(c->mp.pos, pos.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      CU(cudaMemcpyAsync(c->mp.kvpos, kvpos.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      CU(cudaMemcpyAsync(c->mp.req, req.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      CU(cudaMemcpyAsync(c->mp.klo, klo.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      CU(cudaMemcpyAsync(c->mp.khi, khi.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      CU(cudaMemcpyAsync(c->mp.slot, slot.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      RowMeta m = c->mp.view(nullptr, nullptr, 0, 0);
+      // rows of this chunk belong to request r: pass them as one "request" with
+      // the block table row r by offsetting the row->request map (req[] = r).
+      launch_embed(c->embed, c->dt, c->mp.tok, c->mp.pos, M, n, c->x_p, c->st);
+      g_hsd_launches += 1;
+      for (int l = 0; l < c->L; ++l)
+        layer_forward(c, c->layers[l], c->x_p, M, M, 1, m, kv_layer(c, c->kv_t, l), s0 + M);
+      CU(cudaMemcpyAsync(c->H_prompt + (size_t)s0 * n, c->x_p, sizeof(float) * M * n, cudaMemcpyDeviceToDevice, c->st));
+      CU(cudaStreamSynchronize(c->st));
+    }
+    // logits of the last prompt position -> first token (R22)
+    const float* Hlast = c->H_prompt + (size_t)(P0 - 1) * n;
+    launch_rmsnorm(Hlast, 1, n, c->cfg.rms_eps, c->a, c->dt, nullptr, c->st);
+    gemm(c, c->a, n, c->head, n, c->logits, c->V, 1, c->V, n, false);
+    first_token_kernel<<<1, 512, 0, c->st>>>(c->logits, c->V, c->cfg.accept_mode == HSD_STOCHASTIC ? 1 : 0,
+                                             1.0f / c->cfg.temperature, (uint32_t)c->cfg.seed,
+                                             c->cfg.req_offset + r, r, Hlast, n, P0, N, c->pend_H, c->pend_tok,
+                                             c->n_pend, c->root_tok, c->p, d_first);
+    g_hsd_launches += 2;
+    // draft prefill over pairs j = 1..P0-1: x_j = W_fc [H_{j-1}; E(t_j)] (R1)
+    for (int j0 = 1; j0 < P0; j0 += PREFILL_CHUNK) {
+      int M = std::min(PREFILL_CHUNK, P0 - j0);
+      tok.resize(M); pos.resize(M); kvpos.resize(M); req.resize(M); klo.resize(M); khi.resize(M); slot.resize(M);
+      for (int i = 0; i < M; ++i) {
+        int j = j0 + i;
+        tok[i] = pt[j]; pos[i] = j; kvpos[i] = j; req[i] = r; klo[i] = 1; khi[i] = j + 1; slot[i] = -1;
+      }
+      CU(cudaMemcpyAsync(c->mp.tok, tok.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      CU(cudaMemcpyAsync(c->mp.pos, pos.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      CU(cudaMemcpyAsync(c->mp.kvpos, kvpos.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      CU(cudaMemcpyAsync(c->mp.req, req.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      CU(cudaMemcpyAsync(c->mp.klo, klo.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      CU(cudaMemcpyAsync(c->mp.khi, khi.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      CU(cudaMemcpyAsync(c->mp.slot, slot.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+      RowMeta m = c->mp.view(nullptr, nullptr, 0, 0);
+      launch_draft_concat(c->H_prompt + (size_t)(j0 - 1) * n, c->mp.tok, c->mp.pos, c->embed, c->dt, M, n, c->a,
+                          c->st);
+      gemm(c, c->a, 2 * n, c->fc, 2 * n, c->x_p, n, M, n, 2 * n, false);
+      layer_forward(c, c->draft, c->x_p, M, M, 1, m, kv_layer(c, c->kv_d, 0), j0 + M);
+      g_hsd_launches += 1;
+      CU(cudaStreamSynchronize(c->st));
+    }
+  }
+  CU(cudaStreamSynchronize(c->st));
+  CU(cudaGetLastError());
+  c->stage = 0;
+  return HSD_OK;
+}
+
+hsd_status hsd_set_plant(hsd_ctx* ctx, const int32_t* h_plant, int32_t stride) {
+  if (!ctx || !h_plant || stride < 1) return fail(ctx, HSD_EINVAL, "bad plant array");
+  hsd_ctx* c = ctx;
+  if (c->b < 1) return fail(c, HSD_ESTATE, "hsd_set_plant needs hsd_prefill first");
+  if (c->plant) {
+    cudaFree(c->plant);
+    c->allocs.erase(std::find(c->allocs.begin(), c->allocs.end(), (void*)c->plant));
+  }
+  c->plant = (int32_t*)dalloc(c, sizeof(int32_t) * (size_t)c->b * stride);
+  if (!c->plant) return fail(c, HSD_ENOMEM, "plant alloc");
+  c->plant_stride = stride;
+  CU(cudaMemcpyAsync(c->plant, h_plant, sizeof(int32_t) * (size_t)c->b * stride, cudaMemcpyHostToDevice, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+  return HSD_OK;
+}
+
+static void fill_tree_view(hsd_ctx* c, hsd_tree_view* v) {
+  if (!v) return;
+  v->tok = c->t_tok; v->par = c->t_par; v->depth = c->t_depth; v->logjoint = c->t_lj; v->n = c->t_n;
+  v->anc = c->t_anc; v->batch = c->b; v->t_max = c->T; v->anc_words = c->W;
+}
+static void fill_verify_view(hsd_ctx* c, hsd_verify_view* v) {
+  if (!v) return;
+  v->logits = c->logits; v->argmax = c->argmax; v->hidden = c->Hver;
+  v->batch = c->b; v->t_max = c->T; v->vocab = c->V; v->hidden_dim = c->n;
+}
+
+hsd_status hsd_build_tree(hsd_ctx* ctx, hsd_tree_view* out) {
+  if (!ctx) return HSD_EINVAL;
+  if (ctx->b < 1) return fail(ctx, HSD_ESTATE, "hsd_build_tree before hsd_prefill");
+  stage_build(ctx);
+  CU(cudaGetLastError());
+  ctx->stage = 1;
+  fill_tree_view(ctx, out);
+  return HSD_OK;
+}
+
+hsd_status hsd_force_tree(hsd_ctx* ctx, const int32_t* h_tok, const int32_t* h_par, const int32_t* h_depth,
+                          const int32_t* h_n) {
+  if (!ctx || !h_tok || !h_par || !h_depth || !h_n) return fail(ctx, HSD_EINVAL, "null tree arrays");
+  hsd_ctx* c = ctx;
+  if (c->stage != 1) return fail(c, HSD_ESTATE, "hsd_force_tree must follow hsd_build_tree");
+  const int T = c->T, W = c->W, b = c->b;
+  std::vector<uint64_t> anc((size_t)b * T * W, 0);
+  for (int r = 0; r < b; ++r) {
+    int nn = h_n[r];
+    if (nn < 1 || nn > T) return fail(c, HSD_EINVAL, "tree node count out of range");
+    for (int s = 0; s < nn; ++s) {
+      int pa = h_par[r * T + s];
+      if ((s == 0) != (pa < 0) || pa >= s) return fail(c, HSD_EINVAL, "parents must precede children");
+      if (h_tok[r * T + s] < 0 || h_tok[r * T + s] >= c->V) return fail(c, HSD_EINVAL, "token outside [0, V)");
+      uint64_t* a = &anc[((size_t)r * T + s) * W];
+      if (pa >= 0) std::memcpy(a, &anc[((size_t)r * T + pa) * W], W * 8);
+      a[s >> 6] |= 1ull << (s & 63);
+    }
+  }
+  CU(cudaMemcpyAsync(c->t_tok, h_tok, 4 * b * T, cudaMemcpyHostToDevice, c->st));
+  CU(cudaMemcpyAsync(c->t_par, h_par, 4 * b * T, cudaMemcpyHostToDevice, c->st));
+  CU(cudaMemcpyAsync(c->t_depth, h_depth, 4 * b * T, cudaMemcpyHostToDevice, c->st));
+  CU(cudaMemcpyAsync(c->t_n, h_n, 4 * b, cudaMemcpyHostToDevice, c->st));
+  CU(cudaMemcpyAsync(c->t_anc, anc.data(), 8 * anc.size(), cudaMemcpyHostToDevice, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  return HSD_OK;
+}
+
+hsd_status hsd_verify_tree(hsd_ctx* ctx, hsd_verify_view* out) {
+  if (!ctx) return HSD_EINVAL;
+  if (ctx->stage != 1) return fail(ctx, HSD_ESTATE, "hsd_verify_tree requires hsd_build_tree");
+  stage_verify(ctx);
+  CU(cudaGetLastError());
+  ctx->stage = 2;
+  fill_verify_view(ctx, out);
+  return HSD_OK;
+}
+
+hsd_status hsd_accept_and_compact(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n_emitted) {
+  if (!ctx) return HSD_EINVAL;
+  if (ctx->stage != 2) return fail(ctx, HSD_ESTATE, "hsd_accept_and_compact requires hsd_verify_tree");
+  stage_accept(ctx, d_emitted, d_n_emitted);
+  CU(cudaGetLastError());
+  ctx->stage = 0;
+  return HSD_OK;
+}
+
+hsd_status hsd_step(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n_emitted) {
+  if (!ctx) return HSD_EINVAL;
+  hsd_ctx* c = ctx;
+  if (c->b < 1) return fail(c, HSD_ESTATE, "hsd_step before hsd_prefill");
+  if (c->stage != 0) return fail(c, HSD_ESTATE, "hsd_step in the middle of a staged step");
+  if (!c->graph) {
+    if (c->st == nullptr) {
+      // graphs cannot capture the legacy stream: run eagerly
+      stage_build(c); stage_verify(c); stage_accept(c, nullptr, nullptr);
+      CU(cudaGetLastError());
+    } else {
+      int64_t before = g_hsd_launches;
+      cudaGraph_t g;
+      CU(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+      stage_build(c); stage_verify(c); stage_accept(c, nullptr, nullptr);
+      CU(cudaStreamEndCapture(c->st, &g));
+      c->graph_kernels = g_hsd_launches - before;
+      g_hsd_launches = before;  // counted per replay instead
+      CU(cudaGraphInstantiate(&c->graph, g, 0));
+      cudaGraphDestroy(g);
+    }
+  }
+  if (c->graph) {
+    CU(cudaGraphLaunch(c->graph, c->st));
+    c->graph_replays++;
+  }
+  if (d_emitted) CU(cudaMemcpyAsync(d_emitted, c->emitted, 4 * c->b * (c->N + 1), cudaMemcpyDeviceToDevice, c->st));
+  if (d_n_emitted) CU(cudaMemcpyAsync(d_n_emitted, c->n_emitted, 4 * c->b, cudaMemcpyDeviceToDevice, c->st));
+  return HSD_OK;
+}
+
+hsd_status hsd_step_host(hsd_ctx* ctx, int32_t* h_emitted, int32_t* h_n_emitted) {
+  hsd_status s = hsd_step(ctx, nullptr, nullptr);
+  if (s != HSD_OK) return s;
+  hsd_ctx* c = ctx;
+  const int b = c->b, N = c->N;
+  if (c->h_pinned) {
+    CU(cudaMemcpyAsync(c->h_pinned, c->emitted, 4 * b * (N + 1), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(c->h_pinned + b * (N + 1), c->n_emitted, 4 * b, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    if (h_emitted) std::memcpy(h_emitted, c->h_pinned, 4 * b * (N + 1));
+    if (h_n_emitted) std::memcpy(h_n_emitted, c->h_pinned + b * (N + 1), 4 * b);
+  } else {
+    if (h_emitted) CU(cudaMemcpyAsync(h_emitted, c->emitted, 4 * b * (N + 1), cudaMemcpyDeviceToHost, c->st));
+    if (h_n_emitted) CU(cudaMemcpyAsync(h_n_emitted, c->n_emitted, 4 * b, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+  }
+  return HSD_OK;
+}
+
+hsd_status hsd_sync(hsd_ctx* ctx) {
+  if (!ctx) return HSD_EINVAL;
+  CU(cudaStreamSynchronize(ctx->st));
+  CU(cudaGetLastError());
+  int e = 0;
+  CU(cudaMemcpy(&e, ctx->err, 4, cudaMemcpyDeviceToHost));
+  if (e) {
+    cudaMemset(ctx->err, 0, 4);
+    return fail(ctx, HSD_EDEVICE, "device-side violation flag " + std::to_string(e));
+  }
+  return HSD_OK;
+}
+
+hsd_status hsd_get_tensor(hsd_ctx* ctx, const char* name, hsd_tensor* out) {
+  if (!ctx || !name || !out) return HSD_EINVAL;
+  hsd_ctx* c = ctx;
+  const int b = std::max(c->b, 1), T = c->T, N = c->N, n = c->n, Br1 = c->Br + 1;
+  const int adt = c->dt == DT_BF16 ? 1 : 0;
+  auto set = [&](void* p, int dt, std::initializer_list<int64_t> dims) {
+    out->ptr = p; out->dtype = dt; out->ndim = (int)dims.size();
+    int i = 0;
+    for (auto d : dims) out->dims[i++] = d;
+    return HSD_OK;
+  };
+  std::string s(name);
+  if (s == "p") return set(c->p, 2, {b});
+  if (s == "root_tok") return set(c->root_tok, 2, {b});
+  if (s == "step") return set(c->step, 2, {1});
+  if (s == "n_pend") return set(c->n_pend, 2, {b});
+  if (s == "pend_tok") return set(c->pend_tok, 2, {b, N + 1});
+  if (s == "pend_H") return set(c->pend_H, 0, {b, N + 1, n});
+  if (s == "chain") return set(c->chain, 0, {b, N, n});
+  if (s == "draft_logits") return set(c->draft_logits, 0, {b, N, c->V});
+  if (s == "tree_tok") return set(c->t_tok, 2, {b, T});
+  if (s == "tree_par") return set(c->t_par, 2, {b, T});
+  if (s == "tree_depth") return set(c->t_depth, 2, {b, T});
+  if (s == "tree_lj") return set(c->t_lj, 0, {b, T});
+  if (s == "tree_n") return set(c->t_n, 2, {b});
+  if (s == "tree_anc") return set(c->t_anc, 3, {b, T, c->W});
+  if (s == "pt_n") return set(c->pt_n, 2, {b});
+  if (s == "pt_tok") return set(c->pt_tok, 2, {b, Br1});
+  if (s == "pt_par") return set(c->pt_par, 2, {b, Br1});
+  if (s == "pt_depth") return set(c->pt_depth, 2, {b, Br1});
+  if (s == "pt_lj") return set(c->pt_lj, 0, {b, Br1});
+  if (s == "verify_logits") return set(c->logits, 0, {b, T, c->V});
+  if (s == "verify_argmax") return set(c->argmax, 2, {b, T});
+  if (s == "verify_hidden") return set(c->Hver, 0, {b, T, n});
+  if (s == "acc_n") return set(c->acc_n, 2, {b});
+  if (s == "acc_slots") return set(c->acc_slots, 2, {b, N});
+  if (s == "bonus") return set(c->bonus, 2, {b});
+  if (s == "emitted") return set(c->emitted, 2, {b, N + 1});
+  if (s == "n_emitted") return set(c->n_emitted, 2, {b});
+  if (s == "table") return set(c->table, adt, {c->Vh, c->Vh});
+  if (s == "embed") return set(c->embed, adt, {c->V, n});
+  if (s == "head") return set(c->head, adt, {c->V, n});
+  if (s == "kv") return set(c->kv_t, adt, {std::max(1, c->L), c->maxb * c->pages_per_req, 2, (int64_t)c->Hkv * c->page_size * c->hd});
+  if (s == "kv_draft") return set(c->kv_d, adt, {1, c->maxb * c->pages_per_req, 2, (int64_t)c->Hkv * c->page_size * c->hd});
+  if (s == "layer0_wqkv" && c->L > 0) return set(c->layers[0].wqkv, adt, {c->qkvd, n});
+  return fail(c, HSD_EINVAL, "unknown tensor name " + s);
+}
+
+hsd_status hsd_destroy(hsd_ctx* ctx) {
+  if (!ctx) return HSD_EINVAL;
+  if (ctx->st) cudaStreamSynchronize(ctx->st);
+  else cudaDeviceSynchronize();
+  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  delete ctx;
+  return HSD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,56 @@
+// kernels.cuh -- launcher declarations shared by the engine (product side).
+#pragma once
+#include "common.cuh"
+
+// Per-row metadata of one forward pass (rows are padded; pos < 0 = inactive).
+struct RowMeta {
+  const int32_t* tok;    // [M] token (embedding input), may be null
+  const int32_t* pos;    // [M] RoPE position, -1 = inactive row
+  const int32_t* kvpos;  // [M] cache position the row's K/V is written to
+  const int32_t* req;    // [M] request index (block-table row)
+  const int32_t* klo;    // [M] unconditional visible keys [klo, khi)
+  const int32_t* khi;
+  const int32_t* slot;   // [M] tree slot (-1 = none); tree keys at tbase[req] + s
+  const int32_t* tbase;  // [b] first cache position of the tree region
+  const uint64_t* anc;   // [b, t_max, anc_words] ancestor masks
+  int t_max, anc_words;
+};
+
+// Paged KV pool of one layer: page p, kind (0=K,1=V), kv head h, slot s, dim d at
+// base + (((p*2 + kind)*Hkv + h)*page_size + s)*hd + d.
+struct KVLayer {
+  void* base;
+  const int32_t* block_table;  // [b, pages_per_req]
+  int pages_per_req, page_size, kv_heads, head_dim;
+};
+
+// init.cu
+void launch_philox_fill(void* out, DType dt, size_t count, uint32_t seed, uint32_t tid, float scale,
+                        cudaStream_t st);
+void launch_table_rows(const float* E, int rows, int V, int Vh, const int32_t* col_of_rank,
+                       void* table, DType dt, cudaStream_t st);
+void launch_gather_rows_f32(const void* src, DType dt, const int32_t* idx, int rows, int n, float* dst,
+                            cudaStream_t st);
+
+// gemm_simt.cu: C[M,N] (+)= A[M,K] W[N,K]^T, fp32 accumulation, fixed k order.
+void gemm_simt(const void* A, int lda, const void* W, int ldw, DType dt, float* C, int ldc, int M, int N,
+               int K, bool accumulate, cudaStream_t st);
+
+// layers.cu
+void launch_rmsnorm(const float* x, int M, int n, float eps, void* out, DType dt, const int32_t* pos,
+                    cudaStream_t st);
+void launch_embed(const void* E, DType dt, const int32_t* tok, const int32_t* pos, int M, int n, float* x,
+                  cudaStream_t st);
+void launch_qkv_rope_kv(const float* qkv, int M, const RowMeta& m, const float* rope_cos,
+                        const float* rope_sin, int Hq, const KVLayer& kv, void* q_out, DType dt,
+                        cudaStream_t st);
+void launch_swiglu(const float* gu, int M, int f, void* out, DType dt, const int32_t* pos, cudaStream_t st);
+void launch_argmax_rows(const float* x, int M, int V, const int32_t* pos, int32_t* out, cudaStream_t st);
+void launch_draft_concat(const float* Hprev, const int32_t* tok, const int32_t* pos, const void* E,
+                         DType dt, int M, int n, void* out, cudaStream_t st);
+
+// attention.cu
+void launch_attention(const void* q, int M, int rows_per_req, int n_req, const RowMeta& m, const KVLayer& kv,
+                      int Hq, DType dt, int max_keys, void* out, float* ws, size_t ws_floats,
+                      cudaStream_t st);
+size_t attention_ws_floats(int M, int Hq, int hd, int max_splits);
