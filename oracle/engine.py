@@ -58,10 +58,11 @@ class Engine:
         self.trace = []      # per step, per request: dict of intermediate results
 
     # ------------------------------------------------------------------
-    def prefill(self, prompts):
+    def prefill(self, prompts, first_tokens=None):
         """Causal target forward over each prompt (plain decode of the prompt),
-        first token = argmax (greedy) or a Gumbel sample (slot 0, step 0); then
-        the draft layer over pairs j = 1..P0-1; pair P0 stays pending."""
+        first token = argmax (greedy) or a Gumbel sample (slot 0, step 0) unless
+        `first_tokens` forces it (lockstep tests); then the draft layer over
+        pairs j = 1..P0-1; pair P0 stays pending."""
         m = self.m
         first = []
         for r, prompt in enumerate(prompts):
@@ -73,7 +74,9 @@ class Engine:
                     q.kv[l][0].append(k); q.kv[l][1].append(v)
                 q.H.append(H)
                 q.tokens.append(int(t))
-            if self.accept == "greedy":
+            if first_tokens is not None:
+                t1 = int(first_tokens[r])
+            elif self.accept == "greedy":
                 t1 = argmax_lowest(logits)
             else:
                 U = gumbel_uniforms(self.seed, self.req_offset + r, 0, 0, m.cfg.vocab)

@@ -1,0 +1,159 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+fp32-verify mode: identical tree topology, accepted slots,
+emitted tokens and compaction, flagged decisions (oracle margin < 1e-4 x row
+max |logit|) excepted; bf16 mode: logits within 2e-2 row-normwise relative
+error (reading R21), identical decisions where the margin exceeds 1e-2.
+"""
+import numpy as np
+import pytest
+import torch
+
+from synth import get_config, prompts, vocab_permutation
+from oracle.model import Model, layer_tid
+from oracle.table import TokenInfoTable
+from oracle.engine import greedy_decode
+from tests.gpu_lockstep import Lockstep
+
+pytestmark = pytest.mark.gpu
+
+hsd = pytest.importorskip("paper_2602_21224_b200.hsd")
+
+
+def ctx_for(cfg, precision, **kw):
+    return hsd.init_model(cfg, device=0, precision=precision, **kw)
+
+
+@pytest.mark.parametrize("precision", [hsd.FP32_VERIFY, hsd.BF16])
+def test_weights_bit_exact(precision):
+    cfg = get_config("c1")
+    ctx = ctx_for(cfg, precision, seed=7)
+    m = Model(cfg, seed=7, precision="fp32" if precision == hsd.FP32_VERIFY else "bf16")
+    emb = ctx.tensor("embed").float().cpu().numpy()
+    head = ctx.tensor("head").float().cpu().numpy()
+    wqkv = ctx.tensor("layer0_wqkv").float().cpu().numpy()
+    assert np.array_equal(emb, m.embed) and np.array_equal(head, m.head)
+    lw = m.layers[0]
+    assert np.array_equal(wqkv, np.concatenate([lw.wq, lw.wk, lw.wv]))
+    ctx.destroy()
+
+
+@pytest.mark.parametrize("precision,hot", [(hsd.FP32_VERIFY, 0), (hsd.BF16, 0), (hsd.FP32_VERIFY, 64)])
+def test_token_info_table(precision, hot):
+    cfg = get_config("c1").replace(vocab=512 if hot else 256, hot_tokens=hot)
+    perm = vocab_permutation(cfg.vocab, 0)
+    ctx = ctx_for(cfg, precision, seed=3, vocab_perm=perm if hot else None)
+    tab = ctx.tensor("table").float().cpu().numpy()
+    m = Model(cfg, seed=3, precision="fp32" if precision == hsd.FP32_VERIFY else "bf16", layers=0)
+    ot = TokenInfoTable(m, hot_tokens=hot, perm=perm if hot else None)
+    Vh = hot or cfg.vocab
+    rank_tok = perm[:Vh] if hot else np.arange(cfg.vocab)
+    tol = 1e-5 if precision == hsd.FP32_VERIFY else 1e-2
+    for rk in range(0, Vh, max(1, Vh // 16)):
+        ref = ot.row(int(rank_tok[rk]))[rank_tok]
+        np.testing.assert_allclose(tab[rk], ref, atol=tol * np.abs(ref).max())
+    ctx.destroy()
+
+
+def run_lockstep(cfg, precision, steps, seed=0, batch=1, planted=False, accept="greedy", hot=0, tol=None,
+                 flag=None, expect_no_flags=False, tcgen05=False):
+    perm = vocab_permutation(cfg.vocab, 0) if hot else None
+    pr = prompts(cfg, batch=batch)
+    m = Model(cfg, seed=seed, precision="fp32" if precision == hsd.FP32_VERIFY else "bf16")
+    table = TokenInfoTable(m, hot_tokens=hot, perm=perm)
+    plant, rates, flags = None, None, hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION
+    ref = [greedy_decode(m, p, steps * (cfg.steps_N + 1) + cfg.steps_N + 4)[0] for p in pr] \
+        if (planted or accept == "greedy") else None
+    if planted:
+        plant = [np.concatenate([p, r]) for p, r in zip(pr, ref)]
+        rates = [1.0, 0.9, 0.8, 0.7, 0.7, 0.7, 0.7, 0.7]
+        flags |= hsd.FLAG_PLANTED
+    ctx = ctx_for(cfg, precision, seed=seed, max_batch=batch, flags=flags, accept=accept, vocab_perm=perm,
+                  plant_rates=rates, max_ctx=cfg.prompt_len + steps * (cfg.steps_N + 1) + 8, tcgen05=tcgen05)
+    ls = Lockstep(ctx, cfg, m, table, pr, seed=seed, accept=accept, plant=plant, plant_rates=rates, perm=perm,
+                  logit_tol=tol or (1e-4 if precision == hsd.FP32_VERIFY else 2e-2),
+                  flag_margin=flag or (1e-4 if precision == hsd.FP32_VERIFY else 1e-2))
+    first, ofirst = ls.start()
+    if planted:
+        ctx.set_plant(np.stack(plant))
+    if accept == "greedy" and precision == hsd.FP32_VERIFY:
+        assert list(first) == list(ofirst)
+    accs = []
+    for _ in range(steps):
+        rep = ls.step()
+        accs += [a for a, _ in rep]
+    ctx.sync()
+    if ref is not None and precision == hsd.FP32_VERIFY:
+        for r in range(batch):
+            got = ls.emitted[r]
+            assert got == ref[r][:len(got)], "GPU speculative output != oracle plain greedy decode"
+    if expect_no_flags:
+        assert ls.flags == 0
+    ctx.destroy()
+    return ls, accs
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_lockstep_c1_fp32_greedy(seed):
+    ls, accs = run_lockstep(get_config("c1"), hsd.FP32_VERIFY, steps=16, seed=seed, expect_no_flags=True)
+    assert ls.checked["tree"] == 16 and ls.checked["accept"] == 16
+
+
+def test_lockstep_c1_fp32_planted_accepts():
+    ls, accs = run_lockstep(get_config("c1"), hsd.FP32_VERIFY, steps=12, planted=True)
+    assert max(accs) >= 2 and ls.checked["accept"] >= 10
+
+
+def test_lockstep_c1_bf16():
+    ls, accs = run_lockstep(get_config("c1"), hsd.BF16, steps=10)
+    assert ls.max_err["verify"] <= 2e-2 and ls.max_err["L"] <= 2e-2
+
+
+def test_lockstep_c1_stochastic():
+    cfg = get_config("c1").replace(accept="stochastic")
+    ls, accs = run_lockstep(cfg, hsd.FP32_VERIFY, steps=12, accept="stochastic")
+    assert ls.checked["accept"] >= 10
+
+
+def test_lockstep_hot_pruned_gqa_batch2():
+    cfg = get_config("c1").replace(vocab=512, hot_tokens=64, kv_heads=2, batch=2)
+    ls, accs = run_lockstep(cfg, hsd.FP32_VERIFY, steps=8, batch=2, hot=64, planted=True)
+    assert ls.checked["tree"] >= 14
+
+
+def test_step_graph_equals_staged_calls():
+    """hsd_step (CUDA-graph replay) emits exactly what the staged calls emit."""
+    cfg = get_config("c1")
+    pr = prompts(cfg)
+    outs = []
+    for graph in (False, True):
+        stream = torch.cuda.Stream()
+        ctx = ctx_for(cfg, hsd.FP32_VERIFY, seed=1, max_ctx=200)
+        ctx2 = hsd.init_model(cfg, device=0, precision=hsd.FP32_VERIFY, seed=1, max_ctx=200,
+                              stream=stream.cuda_stream)
+        c = ctx2 if graph else ctx
+        c.prefill(pr)
+        em = []
+        for _ in range(10):
+            if graph:
+                e, n = c.step_host()
+            else:
+                c.build_tree(); c.verify_tree(); c.accept_and_compact()
+                e = c.tensor("emitted").cpu().numpy(); n = c.tensor("n_emitted").cpu().numpy()
+            em += list(e[0, :n[0]])
+        outs.append(em)
+        assert c.kernel_launches() > 0
+        ctx.destroy(); ctx2.destroy()
+    assert outs[0] == outs[1]
+
+
+def test_contract_violations_are_host_checked():
+    cfg = get_config("c1")
+    ctx = ctx_for(cfg, hsd.FP32_VERIFY, seed=0)
+    with pytest.raises(hsd.HsdError) as e:
+        ctx.prefill(np.array([[1, 2, 999]]))          # token outside [0, V)
+    assert e.value.status == hsd.HSD_EINVAL
+    with pytest.raises(hsd.HsdError) as e:
+        ctx.verify_tree()                             # call order
+    assert e.value.status in (hsd.HSD_ESTATE,)
+    ctx.destroy()
