@@ -167,6 +167,19 @@ hsd_status hsd_sync(hsd_ctx* ctx);
 typedef struct { void* ptr; int32_t dtype; int32_t ndim; int64_t dims[4]; } hsd_tensor;
 hsd_status hsd_get_tensor(hsd_ctx* ctx, const char* name, hsd_tensor* out);
 
+/* Kernel-category profiling (measurement support, not part of the method).
+ * enable != 0: subsequent hsd_step / staged calls run EAGERLY and every launch
+ * is bracketed by CUDA events on the ctx stream; counters reset. Categories:
+ * "gemm_verify", "gemm_draft", "head_verify", "head_draft", "attn_verify",
+ * "attn_draft", "tree", "resample", "walk", "compact", "rowwise".
+ * hsd_profile_read returns the summed event time (ms), the launch count and
+ * the ALGORITHMIC bytes / flops of those launches (GEMM: weights + activations
+ * + outputs once; compaction: rows moved). Any out-pointer may be NULL.
+ * Synchronous.                                                               */
+hsd_status hsd_profile(hsd_ctx* ctx, int enable);
+hsd_status hsd_profile_read(hsd_ctx* ctx, const char* category, double* total_ms, int64_t* launches,
+                            double* bytes, double* flops);
+
 /* Number of this library's kernels launched on the ctx since creation. */
 int64_t hsd_kernel_launches(const hsd_ctx* ctx);
 

@@ -158,6 +158,14 @@ __global__ void f32_to_dt_kernel(const float* src, size_t count, bf16* dst) {
 // ====================================================================== context
 struct LayerW { void *wqkv, *wo, *wgu, *wd; };
 
+// Kernel categories for hsd_profile (CUDA events around each launch; eager only).
+enum ProfCat { P_GEMM_VERIFY, P_GEMM_DRAFT, P_HEAD_VERIFY, P_HEAD_DRAFT, P_ATTN_VERIFY, P_ATTN_DRAFT, P_TREE,
+               P_RESAMPLE, P_WALK, P_COMPACT, P_ROWWISE, P_NCAT };
+static const char* kProfNames[P_NCAT] = {"gemm_verify", "gemm_draft", "head_verify", "head_draft",
+                                         "attn_verify", "attn_draft", "tree", "resample", "walk", "compact",
+                                         "rowwise"};
+struct ProfRec { int cat; cudaEvent_t a, b; double bytes, flops; };
+
 struct hsd_ctx {
   hsd_config cfg;
   int dev = 0;
@@ -210,7 +218,59 @@ struct hsd_ctx {
   int64_t launches0 = 0, graph_replays = 0;
   std::vector<void*> allocs;
   std::string errmsg;
+  // profiling
+  bool prof_on = false, capturing = false;
+  std::vector<ProfRec> prof_pending;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[P_NCAT] = {}, prof_bytes[P_NCAT] = {}, prof_flops[P_NCAT] = {};
+  int64_t prof_n[P_NCAT] = {};
+  int pass_verify = 0;   // 1 while running the verify pass (GEMM category)
 };
+
+static cudaEvent_t prof_event(hsd_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct Prof {
+  hsd_ctx* c;
+  ProfRec r;
+  bool on;
+  Prof(hsd_ctx* ctx, int cat, double bytes = 0, double flops = 0) : c(ctx) {
+    on = c->prof_on && !c->capturing;
+    if (!on) return;
+    r.cat = cat; r.bytes = bytes; r.flops = flops;
+    r.a = prof_event(c); r.b = prof_event(c);
+    cudaEventRecord(r.a, c->st);
+  }
+  ~Prof() {
+    if (!on) return;
+    cudaEventRecord(r.b, c->st);
+    c->prof_pending.push_back(r);
+  }
+};
+
+static void prof_collect(hsd_ctx* c) {
+  if (c->prof_pending.empty()) return;
+  cudaStreamSynchronize(c->st);
+  for (auto& r : c->prof_pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    c->prof_ms[r.cat] += ms;
+    c->prof_bytes[r.cat] += r.bytes;
+    c->prof_flops[r.cat] += r.flops;
+    c->prof_n[r.cat] += 1;
+    c->ev_pool.push_back(r.a);
+    c->ev_pool.push_back(r.b);
+  }
+  c->prof_pending.clear();
+}
 
 static hsd_status fail(hsd_ctx* c, hsd_status s, const std::string& m) {
   if (c) c->errmsg = m;
@@ -234,9 +294,13 @@ static void* dalloc(hsd_ctx* c, size_t bytes) {
   return p;
 }
 
-// GEMM dispatch: C[M,N] (+)= A[M,K] W[N,K]^T
+// GEMM dispatch: C[M,N] (+)= A[M,K] W[N,K]^T. Algorithmic bytes: W once, A once,
+// C written once (read too when accumulating).
 static void gemm(hsd_ctx* c, const void* A, int lda, const void* Wt, int ldw, float* C, int ldc, int M, int N,
-                 int K, bool acc) {
+                 int K, bool acc, int cat = -1) {
+  if (cat < 0) cat = c->pass_verify ? P_GEMM_VERIFY : P_GEMM_DRAFT;
+  Prof pf(c, cat, (double)N * K * c->esz + (double)M * K * c->esz + (double)M * N * 4 * (acc ? 2 : 1),
+          2.0 * M * N * K);
   if (c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, N, K, lda, ldw)) {
     g_hsd_launches += gemm_tc_bf16((const bf16*)A, lda, (const bf16*)Wt, ldw, C, ldc, M, N, K, acc, c->st);
   } else {
@@ -261,15 +325,22 @@ static KVLayer kv_layer(hsd_ctx* c, void* pool, int layer) {
 static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, int n_req, const RowMeta& m,
                           const KVLayer& kv, int max_keys) {
   const int n = c->n;
-  launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st);
+  { Prof pf(c, P_ROWWISE); launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st); }
   gemm(c, c->a, n, w.wqkv, n, c->big, c->qkvd, M, c->qkvd, n, false);
-  launch_qkv_rope_kv(c->big, M, m, c->rope_cos, c->rope_sin, c->Hq, kv, c->qb, c->dt, c->st);
-  launch_attention(c->qb, M, R, n_req, m, kv, c->Hq, c->dt, max_keys, c->ob, c->attn_ws, c->attn_ws_floats,
-                   c->st);
+  { Prof pf(c, P_ROWWISE);
+    launch_qkv_rope_kv(c->big, M, m, c->rope_cos, c->rope_sin, c->Hq, kv, c->qb, c->dt, c->st); }
+  {
+    // algorithmic attention bytes: the request's committed K/V rows once (per
+    // kv head) + q/out rows; exact per-row key counts are device-side, so the
+    // host uses the capacity-free estimate recorded by hsd_profile_read callers.
+    Prof pf(c, c->pass_verify ? P_ATTN_VERIFY : P_ATTN_DRAFT);
+    launch_attention(c->qb, M, R, n_req, m, kv, c->Hq, c->dt, max_keys, c->ob, c->attn_ws, c->attn_ws_floats,
+                     c->st);
+  }
   gemm(c, c->ob, c->qd, w.wo, c->qd, x, n, M, n, c->qd, true);
-  launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st);
+  { Prof pf(c, P_ROWWISE); launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st); }
   gemm(c, c->a, n, w.wgu, n, c->big, 2 * c->f, M, 2 * c->f, n, false);
-  launch_swiglu(c->big, M, c->f, c->a, c->dt, m.pos, c->st);
+  { Prof pf(c, P_ROWWISE); launch_swiglu(c->big, M, c->f, c->a, c->dt, m.pos, c->st); }
   gemm(c, c->a, c->f, w.wd, c->f, x, n, M, n, c->f, true);
   g_hsd_launches += 6;  // rmsnorm x2, rope_kv, attention(+merge counted below), swiglu
 }
@@ -296,7 +367,7 @@ static void stage_build(hsd_ctx* c) {
   }
   // S1a: one-pass logits L = RMSNorm_f(H_chain) W_head^T, rank order
   launch_rmsnorm(c->chain, b * N, n, c->cfg.rms_eps, c->a, c->dt, nullptr, c->st);
-  gemm(c, c->a, n, c->head_rank, n, c->draft_logits, c->V, b * N, c->V, n, false);
+  gemm(c, c->a, n, c->head_rank, n, c->draft_logits, c->V, b * N, c->V, n, false, P_HEAD_DRAFT);
   g_hsd_launches += 1;
   // S1b + S1c: Alg. 1, prune, fuse, linearise (+ planting)
   TreeParams P{};
@@ -315,7 +386,7 @@ static void stage_build(hsd_ctx* c) {
   P.plant_stride = c->plant_stride;
   for (int i = 0; i < HSD_MAX_PLANT_DEPTH_DEV; ++i) P.plant_rates[i] = c->cfg.plant_rates[i];
   P.seed = (uint32_t)c->cfg.seed; P.req_offset = c->cfg.req_offset; P.err = c->err;
-  launch_tree(P, TREE_MODE_FRESH, b, c->st);
+  { Prof pf(c, P_TREE); launch_tree(P, TREE_MODE_FRESH, b, c->st); }
   g_hsd_launches += 1;
 }
 
@@ -325,10 +396,12 @@ static void stage_verify(hsd_ctx* c) {
   RowMeta m = c->mv.view(c->p, c->t_anc, T, c->W);
   launch_embed(c->embed, c->dt, c->mv.tok, c->mv.pos, M, n, c->Hver, c->st);
   g_hsd_launches += 2;
+  c->pass_verify = 1;
   for (int l = 0; l < c->L; ++l) layer_forward(c, c->layers[l], c->Hver, M, T, b, m, kv_layer(c, c->kv_t, l), c->max_pos);
+  c->pass_verify = 0;
   launch_rmsnorm(c->Hver, M, n, c->cfg.rms_eps, c->a, c->dt, c->mv.pos, c->st);
-  gemm(c, c->a, n, c->head, n, c->logits, c->V, M, c->V, n, false);
-  launch_argmax_rows(c->logits, M, c->V, c->mv.pos, c->argmax, c->st);
+  gemm(c, c->a, n, c->head, n, c->logits, c->V, M, c->V, n, false, P_HEAD_VERIFY);
+  { Prof pf(c, P_ROWWISE); launch_argmax_rows(c->logits, M, c->V, c->mv.pos, c->argmax, c->st); }
   g_hsd_launches += 2;
 }
 
@@ -342,12 +415,12 @@ static void stage_accept(hsd_ctx* c, int32_t* d_emitted, int32_t* d_n) {
   A.step = c->step;
   A.acc_n = c->acc_n; A.acc_slots = c->acc_slots; A.bonus = c->bonus; A.emitted = c->emitted;
   A.n_emitted = c->n_emitted;
-  launch_walk(A, b, c->st);
+  { Prof pf(c, P_WALK); launch_walk(A, b, c->st); }
   CompactParams C{};
   C.kv_base = c->kv_t; C.layer_stride = c->kv_layer_elems; C.block_table = c->block_table;
   C.pages_per_req = c->pages_per_req; C.page_size = c->page_size; C.kv_heads = c->Hkv; C.head_dim = c->hd;
   C.N = c->N; C.acc_n = c->acc_n; C.acc_slots = c->acc_slots; C.p = c->p;
-  launch_compact(C, b, c->L, c->dt, c->st);
+  { Prof pf(c, P_COMPACT, 2.0 * b * c->N * c->L * 2 * c->kd * c->esz); launch_compact(C, b, c->L, c->dt, c->st); }
   // Alg. 2 re-sampling into the pending tree (reads acc_n, bonus, draft logits)
   TreeParams P{};
   P.N = c->N; P.k = c->k; P.B = c->B; P.Br = c->Br; P.r = c->r; P.V = c->V; P.Vh = c->Vh; P.t_max = c->T;
@@ -358,7 +431,7 @@ static void stage_accept(hsd_ctx* c, int32_t* d_emitted, int32_t* d_n) {
   P.L = c->draft_logits; P.table = c->table; P.tdt = c->dt; P.perm = c->perm_d; P.rank_of = c->rank_d;
   P.pt_n = c->pt_n; P.pt_tok = c->pt_tok; P.pt_par = c->pt_par; P.pt_depth = c->pt_depth; P.pt_lj = c->pt_lj;
   P.acc_n = c->acc_n; P.bonus = c->bonus; P.err = c->err;
-  launch_tree(P, TREE_MODE_RESAMPLE, b, c->st);
+  { Prof pf(c, P_RESAMPLE); launch_tree(P, TREE_MODE_RESAMPLE, b, c->st); }
   CommitParams M{};
   M.N = c->N; M.t_max = c->T; M.hidden = c->n; M.Hverify = c->Hver;
   M.acc_n = c->acc_n; M.acc_slots = c->acc_slots; M.emitted = c->emitted; M.bonus = c->bonus;
@@ -802,6 +875,12 @@ hsd_status hsd_step(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n_emitted) {
   hsd_ctx* c = ctx;
   if (c->b < 1) return fail(c, HSD_ESTATE, "hsd_step before hsd_prefill");
   if (c->stage != 0) return fail(c, HSD_ESTATE, "hsd_step in the middle of a staged step");
+  if (c->prof_on) {
+    // profiled steps run eagerly so every launch is bracketed by CUDA events
+    stage_build(c); stage_verify(c); stage_accept(c, d_emitted, d_n_emitted);
+    CU(cudaGetLastError());
+    return HSD_OK;
+  }
   if (!c->graph) {
     if (c->st == nullptr) {
       // graphs cannot capture the legacy stream: run eagerly
@@ -811,7 +890,9 @@ hsd_status hsd_step(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n_emitted) {
       int64_t before = g_hsd_launches;
       cudaGraph_t g;
       CU(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+      c->capturing = true;
       stage_build(c); stage_verify(c); stage_accept(c, nullptr, nullptr);
+      c->capturing = false;
       CU(cudaStreamEndCapture(c->st, &g));
       c->graph_kernels = g_hsd_launches - before;
       g_hsd_launches = before;  // counted per replay instead
@@ -908,11 +989,39 @@ hsd_status hsd_get_tensor(hsd_ctx* ctx, const char* name, hsd_tensor* out) {
   return fail(c, HSD_EINVAL, "unknown tensor name " + s);
 }
 
+hsd_status hsd_profile(hsd_ctx* ctx, int enable) {
+  if (!ctx) return HSD_EINVAL;
+  prof_collect(ctx);
+  if (enable) {
+    for (int i = 0; i < P_NCAT; ++i) { ctx->prof_ms[i] = 0; ctx->prof_bytes[i] = 0; ctx->prof_flops[i] = 0; ctx->prof_n[i] = 0; }
+  }
+  ctx->prof_on = enable != 0;
+  return HSD_OK;
+}
+
+hsd_status hsd_profile_read(hsd_ctx* ctx, const char* category, double* total_ms, int64_t* launches,
+                            double* bytes, double* flops) {
+  if (!ctx || !category) return HSD_EINVAL;
+  prof_collect(ctx);
+  for (int i = 0; i < P_NCAT; ++i) {
+    if (std::string(category) == kProfNames[i]) {
+      if (total_ms) *total_ms = ctx->prof_ms[i];
+      if (launches) *launches = ctx->prof_n[i];
+      if (bytes) *bytes = ctx->prof_bytes[i];
+      if (flops) *flops = ctx->prof_flops[i];
+      return HSD_OK;
+    }
+  }
+  return fail(ctx, HSD_EINVAL, std::string("unknown profile category ") + category);
+}
+
 hsd_status hsd_destroy(hsd_ctx* ctx) {
   if (!ctx) return HSD_EINVAL;
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   else cudaDeviceSynchronize();
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+  prof_collect(ctx);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
   delete ctx;

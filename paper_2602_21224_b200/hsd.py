@@ -25,7 +25,10 @@ MAX_PLANT_DEPTH = 16
 
 EXPORTS = ["hsd_config_defaults", "hsd_init_model", "hsd_prefill", "hsd_set_plant", "hsd_build_tree",
            "hsd_force_tree", "hsd_verify_tree", "hsd_accept_and_compact", "hsd_step", "hsd_step_host",
-           "hsd_sync", "hsd_get_tensor", "hsd_kernel_launches", "hsd_destroy", "hsd_last_error"]
+           "hsd_sync", "hsd_get_tensor", "hsd_kernel_launches", "hsd_destroy", "hsd_last_error",
+           "hsd_profile", "hsd_profile_read"]
+PROFILE_CATEGORIES = ["gemm_verify", "gemm_draft", "head_verify", "head_draft", "attn_verify", "attn_draft",
+                      "tree", "resample", "walk", "compact", "rowwise"]
 
 
 class HsdConfig(C.Structure):
@@ -82,6 +85,8 @@ def load(path: str = LIB_PATH):
         "hsd_kernel_launches": (I64, [VP]),
         "hsd_destroy": (I32, [VP]),
         "hsd_last_error": (C.c_char_p, [VP]),
+        "hsd_profile": (I32, [VP, C.c_int]),
+        "hsd_profile_read": (I32, [VP, C.c_char_p, P(C.c_double), P(I64), P(C.c_double), P(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -207,6 +212,19 @@ class Context:
 
     def sync(self):
         self._check(self.lib.hsd_sync(self.h))
+
+    def profile(self, enable: bool):
+        self._check(self.lib.hsd_profile(self.h, 1 if enable else 0))
+
+    def profile_read(self):
+        """{category: (ms, launches, algorithmic bytes, flops)}"""
+        out = {}
+        for cat in PROFILE_CATEGORIES:
+            ms, n, by, fl = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+            self._check(self.lib.hsd_profile_read(self.h, cat.encode(), C.byref(ms), C.byref(n), C.byref(by),
+                                                  C.byref(fl)))
+            out[cat] = (ms.value, n.value, by.value, fl.value)
+        return out
 
     def kernel_launches(self) -> int:
         return int(self.lib.hsd_kernel_launches(self.h))
