@@ -180,6 +180,15 @@ hsd_status hsd_profile(hsd_ctx* ctx, int enable);
 hsd_status hsd_profile_read(hsd_ctx* ctx, const char* category, double* total_ms, int64_t* launches,
                             double* bytes, double* flops);
 
+/* Test hook: one GEMM of the library, C[M,N] (+)= A[M,K] W[N,K]^T, DEVICE
+ * pointers, row-major with leading dimensions lda/ldw/ldc (elements).
+ * dtype 0 = fp32 operands (SIMT FFMA kernel), 1 = bf16 operands; use_tc = 1
+ * selects the tcgen05 kernel (bf16 only). C is fp32. Asynchronous on `stream`.
+ * Returns HSD_EUNSUP if use_tc is requested for an unsupported shape.        */
+hsd_status hsd_debug_gemm(const void* A, int32_t lda, const void* W, int32_t ldw, float* C, int32_t ldc,
+                          int32_t M, int32_t N, int32_t K, int32_t accumulate, int32_t dtype, int32_t use_tc,
+                          void* stream);
+
 /* Number of this library's kernels launched on the ctx since creation. */
 int64_t hsd_kernel_launches(const hsd_ctx* ctx);
 

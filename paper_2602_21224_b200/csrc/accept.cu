@@ -159,14 +159,14 @@ __global__ void compact_kernel(CompactParams P) {
       if (j >= m) break;
       int key = p + P.acc_slots[req * P.N + j];
       int page = P.block_table[(size_t)req * P.pages_per_req + key / ps];
-      vals[j] = base[((((size_t)page * 2 + kind) * P.kv_heads + h) * ps + key % ps) * hd + d];
+      vals[j] = base[kv_offset(page, kind, P.kv_heads, h, ps, hd, key % ps, d)];
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       if (j >= m) break;
       int key = p + 1 + j;
       int page = P.block_table[(size_t)req * P.pages_per_req + key / ps];
-      base[((((size_t)page * 2 + kind) * P.kv_heads + h) * ps + key % ps) * hd + d] = vals[j];
+      base[kv_offset(page, kind, P.kv_heads, h, ps, hd, key % ps, d)] = vals[j];
     }
   }
 }

@@ -20,10 +20,9 @@ constexpr int NW = 8;      // warps per CTA
 constexpr int MAXHD = 128;
 
 template <typename T>
-HSD_DEV const T* kv_row(const KVLayer& kv, int req, int key, int kind, int h) {
+HSD_DEV T kv_elem(const KVLayer& kv, int req, int key, int kind, int h, int d) {
   int page = kv.block_table[(size_t)req * kv.pages_per_req + key / kv.page_size];
-  int slot = key % kv.page_size;
-  return (const T*)kv.base + ((((size_t)page * 2 + kind) * kv.kv_heads + h) * kv.page_size + slot) * kv.head_dim;
+  return ((const T*)kv.base)[kv_offset(page, kind, kv.kv_heads, h, kv.page_size, kv.head_dim, key % kv.page_size, d)];
 }
 
 HSD_DEV bool visible(const RowMeta& m, int row, int req, int key) {
@@ -93,8 +92,8 @@ __global__ void __launch_bounds__(NW * 32) attention_kernel(const T* __restrict_
       int kk = i / hd, d = i % hd, key = c0 + kk;
       float kvk = 0.f, kvv = 0.f;
       if (key < max_keys) {
-        kvk = to_f32(kv_row<T>(kv, req, key, 0, h)[d]);
-        kvv = to_f32(kv_row<T>(kv, req, key, 1, h)[d]);
+        kvk = to_f32(kv_elem<T>(kv, req, key, 0, h, d));
+        kvv = to_f32(kv_elem<T>(kv, req, key, 1, h, d));
       }
       Ks[kk * (hd + 1) + d] = kvk;
       Vs[kk * hd + d] = kvv;

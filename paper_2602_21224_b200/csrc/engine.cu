@@ -225,7 +225,27 @@ struct hsd_ctx {
   double prof_ms[P_NCAT] = {}, prof_bytes[P_NCAT] = {}, prof_flops[P_NCAT] = {};
   int64_t prof_n[P_NCAT] = {};
   int pass_verify = 0;   // 1 while running the verify pass (GEMM category)
+  double attn_bytes = 0; // algorithmic bytes of the next attention launch (profile mode)
 };
+
+// Profile mode only (eager, synchronising): per-request positions and tree
+// sizes on the host, to state attention's algorithmic bytes per launch:
+// every visible K/V row once + the q rows read + the output rows written.
+static double attn_bytes_for(hsd_ctx* c, int pass, int chain_i) {
+  if (!c->prof_on || c->capturing) return 0;
+  std::vector<int32_t> p(c->b), tn(c->b), np(c->b);
+  cudaStreamSynchronize(c->st);
+  cudaMemcpy(p.data(), c->p, 4 * c->b, cudaMemcpyDeviceToHost);
+  cudaMemcpy(tn.data(), c->t_n, 4 * c->b, cudaMemcpyDeviceToHost);
+  cudaMemcpy(np.data(), c->n_pend, 4 * c->b, cudaMemcpyDeviceToHost);
+  double keys = 0, rows = 0;
+  for (int r = 0; r < c->b; ++r) {
+    if (pass == 0) { keys += p[r] + tn[r]; rows += tn[r]; }          // verify
+    else if (pass == 1) { keys += p[r]; rows += np[r]; }             // draft prefill (positions 1..p)
+    else { keys += p[r] + chain_i; rows += 1; }                       // chain step i
+  }
+  return keys * 2.0 * c->kd * c->esz + rows * 2.0 * c->qd * c->esz;
+}
 
 static cudaEvent_t prof_event(hsd_ctx* c) {
   if (!c->ev_pool.empty()) {
@@ -333,9 +353,14 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
     // algorithmic attention bytes: the request's committed K/V rows once (per
     // kv head) + q/out rows; exact per-row key counts are device-side, so the
     // host uses the capacity-free estimate recorded by hsd_profile_read callers.
-    Prof pf(c, c->pass_verify ? P_ATTN_VERIFY : P_ATTN_DRAFT);
-    launch_attention(c->qb, M, R, n_req, m, kv, c->Hq, c->dt, max_keys, c->ob, c->attn_ws, c->attn_ws_floats,
-                     c->st);
+    Prof pf(c, c->pass_verify ? P_ATTN_VERIFY : P_ATTN_DRAFT, c->attn_bytes);
+    int tc_launched = -1;
+    if (c->use_tc && attention_tc_supported(c->hd, c->page_size, c->dt))
+      tc_launched = launch_attention_tc(c->qb, M, R, n_req, m, kv, c->Hq, max_keys, c->ob, c->attn_ws,
+                                        c->attn_ws_floats, c->kv_layer_elems, c->st);
+    if (tc_launched < 0)
+      launch_attention(c->qb, M, R, n_req, m, kv, c->Hq, c->dt, max_keys, c->ob, c->attn_ws, c->attn_ws_floats,
+                       c->st);
   }
   gemm(c, c->ob, c->qd, w.wo, c->qd, x, n, M, n, c->qd, true);
   { Prof pf(c, P_ROWWISE); launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st); }
@@ -352,6 +377,7 @@ static void stage_build(hsd_ctx* c) {
   // S0 (1): draft prefill of the pending pairs x_j = W_fc [H_{j-1}; E(t_j)] (R1)
   meta_dprefill_kernel<<<b, 32 * ((R + 31) / 32), 0, c->st>>>(c->md, R, c->n_pend, c->pend_tok, c->p);
   RowMeta mdv = c->md.view(nullptr, nullptr, 0, 0);
+  c->attn_bytes = attn_bytes_for(c, 1, 0);
   launch_draft_concat(c->pend_H, c->md.tok, c->md.pos, c->embed, c->dt, b * R, n, c->a, c->st);
   gemm(c, c->a, 2 * n, c->fc, 2 * n, c->x_d, n, b * R, n, 2 * n, false);
   layer_forward(c, c->draft, c->x_d, b * R, R, b, mdv, kv_layer(c, c->kv_d, 0), kvmax);
@@ -361,6 +387,7 @@ static void stage_build(hsd_ctx* c) {
   RowMeta mcv = c->mc.view(nullptr, nullptr, 0, 0);
   for (int i = 1; i < N; ++i) {
     meta_chain_kernel<<<(b + 127) / 128, 128, 0, c->st>>>(c->mc, b, i, c->p);
+    c->attn_bytes = attn_bytes_for(c, 2, i);
     layer_forward(c, c->draft, c->xw, b, 1, b, mcv, kv_layer(c, c->kv_d, 0), kvmax);
     copy_chain_kernel<<<b, 256, 0, c->st>>>(c->xw, n, c->chain, N, i);
     g_hsd_launches += 2;
@@ -397,6 +424,7 @@ static void stage_verify(hsd_ctx* c) {
   launch_embed(c->embed, c->dt, c->mv.tok, c->mv.pos, M, n, c->Hver, c->st);
   g_hsd_launches += 2;
   c->pass_verify = 1;
+  c->attn_bytes = attn_bytes_for(c, 0, 0);
   for (int l = 0; l < c->L; ++l) layer_forward(c, c->layers[l], c->Hver, M, T, b, m, kv_layer(c, c->kv_t, l), c->max_pos);
   c->pass_verify = 0;
   launch_rmsnorm(c->Hver, M, n, c->cfg.rms_eps, c->a, c->dt, c->mv.pos, c->st);
@@ -987,6 +1015,20 @@ hsd_status hsd_get_tensor(hsd_ctx* ctx, const char* name, hsd_tensor* out) {
   if (s == "kv_draft") return set(c->kv_d, adt, {1, c->maxb * c->pages_per_req, 2, (int64_t)c->Hkv * c->page_size * c->hd});
   if (s == "layer0_wqkv" && c->L > 0) return set(c->layers[0].wqkv, adt, {c->qkvd, n});
   return fail(c, HSD_EINVAL, "unknown tensor name " + s);
+}
+
+hsd_status hsd_debug_gemm(const void* A, int32_t lda, const void* W, int32_t ldw, float* C, int32_t ldc,
+                          int32_t M, int32_t N, int32_t K, int32_t accumulate, int32_t dtype, int32_t use_tc,
+                          void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (use_tc) {
+    if (dtype != 1 || !gemm_tc_supported(M, N, K, lda, ldw)) return HSD_EUNSUP;
+    g_hsd_launches += gemm_tc_bf16((const bf16*)A, lda, (const bf16*)W, ldw, C, ldc, M, N, K, accumulate != 0, st);
+  } else {
+    gemm_simt(A, lda, W, ldw, dtype == 1 ? DT_BF16 : DT_F32, C, ldc, M, N, K, accumulate != 0, st);
+    g_hsd_launches += 1;
+  }
+  return cudaGetLastError() == cudaSuccess ? HSD_OK : HSD_ECUDA;
 }
 
 hsd_status hsd_profile(hsd_ctx* ctx, int enable) {

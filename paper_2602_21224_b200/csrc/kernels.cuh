@@ -16,13 +16,21 @@ struct RowMeta {
   int t_max, anc_words;
 };
 
-// Paged KV pool of one layer: page p, kind (0=K,1=V), kv head h, slot s, dim d at
-// base + (((p*2 + kind)*Hkv + h)*page_size + s)*hd + d.
+// Paged KV pool of one layer. Block (page p, kind 0=K / 1=V, kv head h) holds
+// page_size*hd elements at ((p*2 + kind)*Hkv + h)*page_size*hd:
+//   K: element (slot, d) at slot*hd + d      ([page_size][hd], hd contiguous)
+//   V: element (slot, d) at d*page_size + slot ([hd][page_size], TRANSPOSED so that
+//      V^T tiles are K-major UMMA operands for O += P V in the tcgen05 kernel).
 struct KVLayer {
   void* base;
   const int32_t* block_table;  // [b, pages_per_req]
   int pages_per_req, page_size, kv_heads, head_dim;
 };
+
+HSD_DEV size_t kv_offset(int page, int kind, int Hkv, int h, int ps, int hd, int slot, int d) {
+  size_t blk = (((size_t)page * 2 + kind) * Hkv + h) * (size_t)ps * hd;
+  return blk + (kind == 0 ? (size_t)slot * hd + d : (size_t)d * ps + slot);
+}
 
 // init.cu
 void launch_philox_fill(void* out, DType dt, size_t count, uint32_t seed, uint32_t tid, float scale,
@@ -49,7 +57,11 @@ void launch_argmax_rows(const float* x, int M, int V, const int32_t* pos, int32_
 void launch_draft_concat(const float* Hprev, const int32_t* tok, const int32_t* pos, const void* E,
                          DType dt, int M, int n, void* out, cudaStream_t st);
 
-// attention.cu
+// attention.cu (SIMT, any precision) and attention_tc.cu (tcgen05, bf16, hd 64/128)
+bool attention_tc_supported(int hd, int page_size, DType dt);
+int launch_attention_tc(const void* q, int M, int rows_per_req, int n_req, const RowMeta& m, const KVLayer& kv,
+                        int Hq, int max_keys, void* out, float* ws, size_t ws_floats, size_t kv_layer_elems,
+                        cudaStream_t st);
 void launch_attention(const void* q, int M, int rows_per_req, int n_req, const RowMeta& m, const KVLayer& kv,
                       int Hq, DType dt, int max_keys, void* out, float* ws, size_t ws_floats,
                       cudaStream_t st);

@@ -1,27 +1,64 @@
 // layers.cu -- row-wise kernels of the Llama decoder used by draft, verify and
 // prefill passes: RMSNorm, embedding gather, RoPE + paged KV write, SwiGLU,
 // argmax, draft-input concat (reading R1).
+//
+// All are bandwidth-trivial at decode sizes (tens of rows), so they are written
+// for latency: 128-bit vector accesses, every load of a thread issued before
+// use, and grids that put (row, column-chunk) work items on many SMs.
 #include "kernels.cuh"
+
+namespace {
+template <typename T> struct Vec4;
+template <> struct Vec4<float> {
+  static HSD_DEV void store(float* p, float a, float b, float c, float d) { *(float4*)p = make_float4(a, b, c, d); }
+};
+template <> struct Vec4<bf16> {
+  static HSD_DEV void store(bf16* p, float a, float b, float c, float d) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+    uint2 u;
+    u.x = *(uint32_t*)&lo;
+    u.y = *(uint32_t*)&hi;
+    *(uint2*)p = u;
+  }
+};
+}  // namespace
 
 // ------------------------------------------------------------------ RMSNorm
 // out[r] = x[r] / sqrt(mean(x[r]^2) + eps) (gain 1). Inactive rows -> 0.
+// One CTA per row; n % 4 == 0; up to 8 float4 per thread kept in registers.
 template <typename T>
-__global__ void rmsnorm_kernel(const float* __restrict__ x, int n, float eps, T* __restrict__ out,
-                               const int32_t* __restrict__ pos) {
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, int n, float eps,
+                                                      T* __restrict__ out, const int32_t* __restrict__ pos) {
   __shared__ float red[32];
-  int r = blockIdx.x;
-  const float* xr = x + (size_t)r * n;
+  const int r = blockIdx.x;
+  const float4* xr = (const float4*)(x + (size_t)r * n);
   T* o = out + (size_t)r * n;
-  bool active = pos == nullptr || pos[r] >= 0;
-  if (!active) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) o[i] = from_f32<T>(0.f);
-    return;
-  }
+  const bool active = pos == nullptr || pos[r] >= 0;
+  const int n4 = n >> 2;
+  float4 v[8];
   float s = 0.f;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) s += xr[i] * xr[i];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    int i = threadIdx.x + j * blockDim.x;
+    v[j] = (i < n4 && active) ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
+  for (int i = threadIdx.x + 8 * blockDim.x; i < n4; i += blockDim.x) {   // n > 8192 tail
+    float4 t = active ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += t.x * t.x + t.y * t.y + t.z * t.z + t.w * t.w;
+  }
   s = block_sum(s, red);
-  float inv = 1.0f / sqrtf(s / (float)n + eps);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) o[i] = from_f32<T>(xr[i] * inv);
+  const float inv = active ? 1.0f / sqrtf(s / (float)n + eps) : 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    int i = threadIdx.x + j * blockDim.x;
+    if (i < n4) Vec4<T>::store(o + 4 * i, v[j].x * inv, v[j].y * inv, v[j].z * inv, v[j].w * inv);
+  }
+  for (int i = threadIdx.x + 8 * blockDim.x; i < n4; i += blockDim.x) {
+    float4 t = active ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    Vec4<T>::store(o + 4 * i, t.x * inv, t.y * inv, t.z * inv, t.w * inv);
+  }
 }
 
 void launch_rmsnorm(const float* x, int M, int n, float eps, void* out, DType dt, const int32_t* pos,
@@ -37,12 +74,9 @@ __global__ void embed_kernel(const T* __restrict__ E, const int32_t* __restrict_
                              const int32_t* __restrict__ pos, int n, float* __restrict__ x) {
   int r = blockIdx.x;
   float* xr = x + (size_t)r * n;
-  if (pos && pos[r] < 0) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) xr[i] = 0.f;
-    return;
-  }
-  const T* e = E + (size_t)tok[r] * n;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) xr[i] = to_f32(e[i]);
+  const bool active = !(pos && pos[r] < 0);
+  const T* e = E + (size_t)(active ? tok[r] : 0) * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xr[i] = active ? to_f32(e[i]) : 0.f;
 }
 
 void launch_embed(const void* E, DType dt, const int32_t* tok, const int32_t* pos, int M, int n, float* x,
@@ -56,45 +90,44 @@ void launch_embed(const void* E, DType dt, const int32_t* tok, const int32_t* po
 // qkv row layout: [q (Hq*hd) | k (Hkv*hd) | v (Hkv*hd)], fp32 from the GEMM.
 // Llama rotate_half convention: x' = x*cos + rotate_half(x)*sin with angle
 // pos * theta^(-2i/hd); cos/sin tables precomputed on the host in double.
+// grid (M, Hq + 2*Hkv): one CTA per (row, head); K/V go to the paged cache
+// (V transposed, see KVLayer).
 template <typename T>
 __global__ void qkv_rope_kv_kernel(const float* __restrict__ qkv, RowMeta m, const float* __restrict__ rc,
                                    const float* __restrict__ rs, int Hq, KVLayer kv, T* __restrict__ q_out) {
-  int r = blockIdx.x;
-  int hd = kv.head_dim, half = hd / 2, Hkv = kv.kv_heads;
-  int ld = (Hq + 2 * Hkv) * hd;
-  const float* row = qkv + (size_t)r * ld;
-  int p = m.pos[r];
-  T* qo = q_out + (size_t)r * Hq * hd;
-  if (p < 0) {
-    for (int i = threadIdx.x; i < Hq * hd; i += blockDim.x) qo[i] = from_f32<T>(0.f);
+  const int r = blockIdx.x, hh = blockIdx.y;
+  const int hd = kv.head_dim, half = hd / 2, Hkv = kv.kv_heads;
+  const int ld = (Hq + 2 * Hkv) * hd;
+  const float* src = qkv + (size_t)r * ld + (size_t)hh * hd;
+  const int p = m.pos[r];
+  if (hh < Hq) {
+    T* qo = q_out + ((size_t)r * Hq + hh) * hd;
+    for (int j = threadIdx.x; j < half; j += blockDim.x) {
+      if (p < 0) { qo[j] = from_f32<T>(0.f); qo[j + half] = from_f32<T>(0.f); continue; }
+      float c = rc[(size_t)p * half + j], s = rs[(size_t)p * half + j];
+      float x1 = src[j], x2 = src[j + half];
+      qo[j] = from_f32<T>(x1 * c - x2 * s);
+      qo[j + half] = from_f32<T>(x2 * c + x1 * s);
+    }
     return;
   }
-  const float* c = rc + (size_t)p * half;
-  const float* s = rs + (size_t)p * half;
-  // q heads
-  for (int i = threadIdx.x; i < Hq * half; i += blockDim.x) {
-    int h = i / half, j = i % half;
-    float x1 = row[h * hd + j], x2 = row[h * hd + j + half];
-    qo[h * hd + j] = from_f32<T>(x1 * c[j] - x2 * s[j]);
-    qo[h * hd + j + half] = from_f32<T>(x2 * c[j] + x1 * s[j]);
-  }
-  // k (rotated) and v into the paged cache at kvpos
-  int kp = m.kvpos[r];
-  int page = kv.block_table[(size_t)m.req[r] * kv.pages_per_req + kp / kv.page_size];
-  int slot = kp % kv.page_size;
+  if (p < 0) return;
+  const int kp = m.kvpos[r];
+  const int page = kv.block_table[(size_t)m.req[r] * kv.pages_per_req + kp / kv.page_size];
+  const int slot = kp % kv.page_size;
   T* base = (T*)kv.base;
-  for (int i = threadIdx.x; i < Hkv * half; i += blockDim.x) {
-    int h = i / half, j = i % half;
-    const float* kr = row + Hq * hd + h * hd;
-    float x1 = kr[j], x2 = kr[j + half];
-    size_t off = ((((size_t)page * 2 + 0) * Hkv + h) * kv.page_size + slot) * hd;
-    base[off + j] = from_f32<T>(x1 * c[j] - x2 * s[j]);
-    base[off + j + half] = from_f32<T>(x2 * c[j] + x1 * s[j]);
-  }
-  for (int i = threadIdx.x; i < Hkv * hd; i += blockDim.x) {
-    int h = i / hd, j = i % hd;
-    size_t off = ((((size_t)page * 2 + 1) * Hkv + h) * kv.page_size + slot) * hd;
-    base[off + j] = from_f32<T>(row[(Hq + Hkv) * hd + i]);
+  if (hh < Hq + Hkv) {
+    const int h = hh - Hq;
+    for (int j = threadIdx.x; j < half; j += blockDim.x) {
+      float c = rc[(size_t)p * half + j], s = rs[(size_t)p * half + j];
+      float x1 = src[j], x2 = src[j + half];
+      base[kv_offset(page, 0, Hkv, h, kv.page_size, hd, slot, j)] = from_f32<T>(x1 * c - x2 * s);
+      base[kv_offset(page, 0, Hkv, h, kv.page_size, hd, slot, j + half)] = from_f32<T>(x2 * c + x1 * s);
+    }
+  } else {
+    const int h = hh - Hq - Hkv;
+    for (int d = threadIdx.x; d < hd; d += blockDim.x)
+      base[kv_offset(page, 1, Hkv, h, kv.page_size, hd, slot, d)] = from_f32<T>(src[d]);
   }
 }
 
@@ -102,31 +135,35 @@ void launch_qkv_rope_kv(const float* qkv, int M, const RowMeta& m, const float* 
                         const float* rope_sin, int Hq, const KVLayer& kv, void* q_out, DType dt,
                         cudaStream_t st) {
   if (M <= 0) return;
+  dim3 grid(M, Hq + 2 * kv.kv_heads);
+  int thr = kv.head_dim >= 128 ? 64 : 32;
   if (dt == DT_F32)
-    qkv_rope_kv_kernel<float><<<M, 128, 0, st>>>(qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out);
+    qkv_rope_kv_kernel<float><<<grid, thr, 0, st>>>(qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out);
   else
-    qkv_rope_kv_kernel<bf16><<<M, 128, 0, st>>>(qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out);
+    qkv_rope_kv_kernel<bf16><<<grid, thr, 0, st>>>(qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out);
 }
 
 // ------------------------------------------------------------------ SwiGLU
-// gu row = [gate (f) | up (f)] -> silu(gate) * up
+// gu row = [gate (f) | up (f)] -> silu(gate) * up; grid (M, f/4/256 chunks), f % 4 == 0
 template <typename T>
 __global__ void swiglu_kernel(const float* __restrict__ gu, int f, T* __restrict__ out,
                               const int32_t* __restrict__ pos) {
-  int r = blockIdx.x;
-  const float* g = gu + (size_t)r * 2 * f;
-  T* o = out + (size_t)r * f;
-  bool active = pos == nullptr || pos[r] >= 0;
-  for (int i = threadIdx.x; i < f; i += blockDim.x) {
-    float a = g[i], u = g[f + i];
-    o[i] = from_f32<T>(active ? (a / (1.0f + expf(-a))) * u : 0.f);
-  }
+  const int r = blockIdx.x;
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;   // float4 index
+  if (4 * i >= f) return;
+  const float4 a = ((const float4*)(gu + (size_t)r * 2 * f))[i];
+  const float4 u = ((const float4*)(gu + (size_t)r * 2 * f + f))[i];
+  const bool active = pos == nullptr || pos[r] >= 0;
+  auto sl = [](float x) { return x / (1.0f + expf(-x)); };
+  if (active) Vec4<T>::store(out + (size_t)r * f + 4 * i, sl(a.x) * u.x, sl(a.y) * u.y, sl(a.z) * u.z, sl(a.w) * u.w);
+  else Vec4<T>::store(out + (size_t)r * f + 4 * i, 0.f, 0.f, 0.f, 0.f);
 }
 
 void launch_swiglu(const float* gu, int M, int f, void* out, DType dt, const int32_t* pos, cudaStream_t st) {
   if (M <= 0) return;
-  if (dt == DT_F32) swiglu_kernel<float><<<M, 256, 0, st>>>(gu, f, (float*)out, pos);
-  else swiglu_kernel<bf16><<<M, 256, 0, st>>>(gu, f, (bf16*)out, pos);
+  dim3 grid(M, (f / 4 + 255) / 256);
+  if (dt == DT_F32) swiglu_kernel<float><<<grid, 256, 0, st>>>(gu, f, (float*)out, pos);
+  else swiglu_kernel<bf16><<<grid, 256, 0, st>>>(gu, f, (bf16*)out, pos);
 }
 
 // ------------------------------------------------------------------ argmax
@@ -162,7 +199,7 @@ __global__ void argmax_rows_kernel(const float* __restrict__ x, int V, const int
 
 void launch_argmax_rows(const float* x, int M, int V, const int32_t* pos, int32_t* out, cudaStream_t st) {
   if (M <= 0) return;
-  argmax_rows_kernel<<<M, 512, 0, st>>>(x, V, pos, out);
+  argmax_rows_kernel<<<M, 1024, 0, st>>>(x, V, pos, out);
 }
 
 // ------------------------------------------------------------------ draft input

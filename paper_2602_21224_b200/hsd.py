@@ -26,7 +26,7 @@ MAX_PLANT_DEPTH = 16
 EXPORTS = ["hsd_config_defaults", "hsd_init_model", "hsd_prefill", "hsd_set_plant", "hsd_build_tree",
            "hsd_force_tree", "hsd_verify_tree", "hsd_accept_and_compact", "hsd_step", "hsd_step_host",
            "hsd_sync", "hsd_get_tensor", "hsd_kernel_launches", "hsd_destroy", "hsd_last_error",
-           "hsd_profile", "hsd_profile_read"]
+           "hsd_profile", "hsd_profile_read", "hsd_debug_gemm"]
 PROFILE_CATEGORIES = ["gemm_verify", "gemm_draft", "head_verify", "head_draft", "attn_verify", "attn_draft",
                       "tree", "resample", "walk", "compact", "rowwise"]
 
@@ -86,6 +86,7 @@ def load(path: str = LIB_PATH):
         "hsd_destroy": (I32, [VP]),
         "hsd_last_error": (C.c_char_p, [VP]),
         "hsd_profile": (I32, [VP, C.c_int]),
+        "hsd_debug_gemm": (I32, [VP, I32, VP, I32, VP, I32, I32, I32, I32, I32, I32, I32, VP]),
         "hsd_profile_read": (I32, [VP, C.c_char_p, P(C.c_double), P(I64), P(C.c_double), P(C.c_double)]),
     }
     for name, (res, args) in sig.items():
@@ -249,6 +250,21 @@ class Context:
             self.destroy()
         except Exception:
             pass
+
+
+def debug_gemm(A, W, C, accumulate=False, use_tc=False, stream=0):
+    """C (+)= A @ W^T with the library's GEMM kernels (torch CUDA tensors;
+    marshalling only). A, W: bf16 or fp32, row-major; C: fp32."""
+    import torch
+    lib = load()
+    dtype = 1 if A.dtype == torch.bfloat16 else 0
+    M, K = A.shape
+    N = W.shape[0]
+    s = lib.hsd_debug_gemm(A.data_ptr(), A.stride(0), W.data_ptr(),
+                           W.stride(0), C.data_ptr(), C.stride(0), M, N, K, int(accumulate), dtype, int(use_tc),
+                           stream)
+    if s != HSD_OK:
+        raise HsdError(s, "hsd_debug_gemm")
 
 
 def init_model(model_cfg, device=0, stream=None, **kw) -> Context:

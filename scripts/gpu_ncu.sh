@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+python -m paper_2602_21224_b200.build
+mkdir -p gpurun_out
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-profile --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+tail -3 gpurun_out/ncu_launch.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s 400 -c 4 -o gpurun_out/prof_gemm python bench.py --steps 1 --warmup 1 --no-profile --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+tail -3 gpurun_out/ncu_full.log
+ls -la gpurun_out

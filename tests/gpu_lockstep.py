@@ -54,9 +54,10 @@ def kv_rows(ctx, cfg, layer, r, positions, page_size, pages_per_req):
     for pos in positions:
         page = r * pages_per_req + pos // page_size
         slot = pos % page_size
-        blk = kv[page].float().view(2, Hkv, page_size, hd)
-        out_k.append(blk[0, :, slot, :].reshape(-1).cpu().numpy())
-        out_v.append(blk[1, :, slot, :].reshape(-1).cpu().numpy())
+        blk = kv[page].float()
+        out_k.append(blk[0].view(Hkv, page_size, hd)[:, slot, :].reshape(-1).cpu().numpy())
+        # V blocks are stored transposed, [hd][page_size] per head (KVLayer)
+        out_v.append(blk[1].view(Hkv, hd, page_size)[:, :, slot].reshape(-1).cpu().numpy())
     return np.stack(out_k), np.stack(out_v)
 
 

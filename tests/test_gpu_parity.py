@@ -157,3 +157,20 @@ def test_contract_violations_are_host_checked():
         ctx.verify_tree()                             # call order
     assert e.value.status in (hsd.HSD_ESTATE,)
     ctx.destroy()
+
+
+def test_lockstep_c1_bf16_tcgen05():
+    ls, accs = run_lockstep(get_config("c1"), hsd.BF16, steps=10, tcgen05=True)
+    assert ls.max_err["verify"] <= 2e-2 and ls.max_err["L"] <= 2e-2
+
+
+@pytest.mark.parametrize("hd,q_heads,kv_heads,prompt_len", [(64, 8, 2, 32), (128, 4, 4, 150), (128, 8, 2, 200)])
+def test_lockstep_wide_bf16_tcgen05_planted(hd, q_heads, kv_heads, prompt_len):
+    """Wider models so every GEMM spans several 128-row tiles and k-blocks of the
+    tcgen05 GEMM, and the tcgen05 tree attention (hd 64/128, MHA and GQA) runs
+    over several 64-key pages and key splits."""
+    cfg = get_config("c1").replace(hidden=512, q_heads=q_heads, kv_heads=kv_heads, head_dim=hd, ffn=1024,
+                                   vocab=1024, layers=2, steps_N=5, branch_k=3, budget_B=16,
+                                   prompt_len=prompt_len)
+    ls, accs = run_lockstep(cfg, hsd.BF16, steps=6, tcgen05=True, planted=True)
+    assert ls.max_err["verify"] <= 2e-2 and max(accs) >= 2
