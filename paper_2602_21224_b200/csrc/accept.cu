@@ -68,6 +68,8 @@ HSD_DEV int gumbel_argmax(const float* x, int V, float invT, uint32_t seed, uint
 }
 
 __global__ void __launch_bounds__(WT) walk_kernel(AcceptParams P) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[32];
   __shared__ int redi[32];
   __shared__ int acc[32], m_sh, bonus_sh, cur_sh, done_sh, excl[64], n_excl;
@@ -146,6 +148,8 @@ __global__ void __launch_bounds__(WT) walk_kernel(AcceptParams P) {
 // KV compaction: grid (b, layers, 2*Hkv); thread d moves dim d of rows j=1..m.
 template <typename T>
 __global__ void compact_kernel(CompactParams P) {
+  pdl_wait();
+  pdl_trigger();
   const int req = blockIdx.x, layer = blockIdx.y, kh = blockIdx.z;
   const int kind = kh / P.kv_heads, h = kh % P.kv_heads;
   const int m = P.acc_n[req];
@@ -173,6 +177,8 @@ __global__ void compact_kernel(CompactParams P) {
 
 // state update: pending draft pairs, root, position, step counter
 __global__ void commit_kernel(CommitParams P) {
+  pdl_wait();
+  pdl_trigger();
   const int req = blockIdx.x;
   const int m = P.acc_n[req];
   const int n = P.hidden;
@@ -194,14 +200,14 @@ __global__ void commit_kernel(CommitParams P) {
 }  // namespace
 
 void launch_walk(const AcceptParams& P, int n_req, cudaStream_t st) {
-  if (n_req > 0) walk_kernel<<<n_req, WT, 0, st>>>(P);
+  if (n_req > 0) launch_k(walk_kernel, n_req, WT, 0, st, P);
 }
 void launch_compact(const CompactParams& P, int n_req, int layers, DType dt, cudaStream_t st) {
   if (n_req <= 0) return;
   dim3 grid(n_req, layers, 2 * P.kv_heads);
-  if (dt == DT_F32) compact_kernel<float><<<grid, 128, 0, st>>>(P);
-  else compact_kernel<bf16><<<grid, 128, 0, st>>>(P);
+  if (dt == DT_F32) launch_k(compact_kernel<float>, grid, 128, 0, st, P);
+  else launch_k(compact_kernel<bf16>, grid, 128, 0, st, P);
 }
 void launch_commit(const CommitParams& P, int n_req, cudaStream_t st) {
-  if (n_req > 0) commit_kernel<<<n_req, 256, 0, st>>>(P);
+  if (n_req > 0) launch_k(commit_kernel, n_req, 256, 0, st, P);
 }

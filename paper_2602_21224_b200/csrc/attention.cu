@@ -40,6 +40,8 @@ __global__ void __launch_bounds__(NW * 32) attention_kernel(const T* __restrict_
                                                             KVLayer kv, int Hq, int max_keys, int keys_per_split,
                                                             int n_qtiles, T* __restrict__ out,
                                                             float* __restrict__ ws) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float smem[];
   const int hd = kv.head_dim, Hkv = kv.kv_heads, G = Hq / Hkv;
   float* Ks = smem;                       // [CH][hd+1]
@@ -172,6 +174,8 @@ __global__ void __launch_bounds__(NW * 32) attention_kernel(const T* __restrict_
 template <typename T>
 __global__ void attention_merge_kernel(const float* __restrict__ ws, int S, int M, int Hq, int hd,
                                        T* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   int row = blockIdx.x, head = blockIdx.y;
   size_t base = (size_t)S * M * Hq * hd;
   float Mx = -INFINITY;
@@ -222,13 +226,13 @@ void launch_attention(const void* q, int M, int R, int n_req, const RowMeta& m, 
   dim3 grid(S, kv.kv_heads, n_req * n_qtiles);
   if (dt == DT_F32) {
     cudaFuncSetAttribute(attention_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attention_kernel<float><<<grid, NW * 32, smem, st>>>((const float*)q, M, R, m, kv, Hq, max_keys, kps,
+    launch_k(attention_kernel<float>, grid, NW * 32, smem, st, (const float*)q, M, R, m, kv, Hq, max_keys, kps,
                                                          n_qtiles, (float*)out, ws);
-    if (S > 1) attention_merge_kernel<float><<<dim3(M, Hq), 128, 0, st>>>(ws, S, M, Hq, hd, (float*)out);
+    if (S > 1) launch_k(attention_merge_kernel<float>, dim3(M, Hq), 128, 0, st, ws, S, M, Hq, hd, (float*)out);
   } else {
     cudaFuncSetAttribute(attention_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attention_kernel<bf16><<<grid, NW * 32, smem, st>>>((const bf16*)q, M, R, m, kv, Hq, max_keys, kps,
+    launch_k(attention_kernel<bf16>, grid, NW * 32, smem, st, (const bf16*)q, M, R, m, kv, Hq, max_keys, kps,
                                                         n_qtiles, (bf16*)out, ws);
-    if (S > 1) attention_merge_kernel<bf16><<<dim3(M, Hq), 128, 0, st>>>(ws, S, M, Hq, hd, (bf16*)out);
+    if (S > 1) launch_k(attention_merge_kernel<bf16>, dim3(M, Hq), 128, 0, st, ws, S, M, Hq, hd, (bf16*)out);
   }
 }

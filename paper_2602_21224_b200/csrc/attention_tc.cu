@@ -10,11 +10,14 @@
 //                TMEM score buffers, then O += P_j V_j (M=128, N=hd, K=64) into
 //                the TMEM output accumulator; S_{j+1} is issued before P_j is
 //                ready so softmax of page j overlaps the score MMA of page j+1.
-//  warps 2..5  : softmax -- thread t owns TMEM lane t = one (row, head): loads
-//                its 64 scores, applies the visibility test (committed range,
-//                or tree-ancestor bit, see attention.cu), online max/sum,
-//                rescales its O row in TMEM when the max grows, writes P (bf16,
-//                128B-swizzled) to shared memory for the PV MMA.
+//  warps 2..9  : softmax -- TMEM lane t = one (row, head) is owned by a PAIR of
+//                warps (same lane quarter), each taking 32 of the page's 64
+//                keys: a 32-bit visibility mask (committed range | tree-ancestor
+//                bits, see attention.cu) is built once per page, scores are
+//                log2-scaled and exponentiated with ex2.approx, the pair
+//                exchanges its row max through shared memory, rescales its half
+//                of the O row in TMEM when the max grows, and writes its half of
+//                P (bf16, 128B-swizzled) for the PV MMA.
 // Splits > 1 write (o, m, l) partials in the SIMT kernel's layout and reuse
 // its merge kernel.
 #include "kernels.cuh"
@@ -22,7 +25,7 @@
 
 namespace {
 using namespace tc;
-constexpr int NTHREADS = 192;
+constexpr int NTHREADS = 320;   // TMA, MMA, 8 softmax warps
 constexpr int PAGE = 64;
 constexpr int STAGES = 3;
 constexpr int QROWS = 128;
@@ -36,13 +39,46 @@ struct AttnParams {
   uint32_t idesc_s, idesc_o;
 };
 
-HSD_DEV bool vis(int key, int klo, int khi, int slot, int tb, int t_max, const uint64_t (&a)[4]) {
-  if (key >= klo && key < khi) return true;
-  if (slot < 0) return false;
-  int d = key - tb;
-  if (d < 0 || d >= t_max) return false;
-  return (a[d >> 6] >> (d & 63)) & 1ull;
+// bits [a, b) of a 32-bit word (a, b clamped to [0, 32])
+HSD_DEV uint32_t range32(int a, int b) {
+  a = max(0, min(32, a));
+  b = max(0, min(32, b));
+  if (b <= a) return 0u;
+  const uint32_t hi = b == 32 ? 0xffffffffu : ((1u << b) - 1u);
+  return hi & ~((1u << a) - 1u);
 }
+// bits d0 .. d0+31 of the 256-bit ancestor mask (0 outside [0, 256))
+HSD_DEV uint32_t anc32(const uint64_t (&a)[4], int d0) {
+  if (d0 >= 256 || d0 <= -32) return 0u;
+  int sh = 0;
+  if (d0 < 0) { sh = -d0; d0 = 0; }
+  const int w = d0 >> 6, o = d0 & 63;
+  uint64_t lo = 0, hi = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {       // static indexing keeps the mask in registers
+    if (i == w) lo = a[i];
+    if (i == w + 1) hi = a[i];
+  }
+  const uint64_t v = o == 0 ? lo : ((lo >> o) | (hi << (64 - o)));
+  return ((uint32_t)v) << sh;
+}
+HSD_DEV float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+HSD_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+HSD_DEV void pair_sync(int q) { asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory"); }
 
 __global__ void __launch_bounds__(NTHREADS, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -67,6 +103,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* pvdone = pfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(pvdone + 1);
   __shared__ int tile_lo, tile_hi;
+  __shared__ float red_max[2][2][QROWS];   // [chunk parity][half][row]
+  __shared__ float red_l[2][QROWS];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, h = blockIdx.y;
@@ -80,7 +118,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (threadIdx.x == 32) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(qbar, 1);
-    for (int b = 0; b < 2; ++b) { mbar_init(&sfull[b], 1); mbar_init(&pfull[b], 128); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&sfull[b], 1); mbar_init(&pfull[b], 256); }
     mbar_init(pvdone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -91,6 +129,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();      // row metadata, q and this layer's tree K/V come from upstream kernels
+  pdl_trigger();
   // softmax threads: this lane's (row, head) and its key bounds
   const int q4 = warp & 3;
   const int lane_row = q4 * 32 + lane;                // tile row-head index owned by this thread
@@ -182,60 +222,64 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else {
     // ------------------------------------------------------------ softmax warps
-    const float scale = 1.0f / sqrtf((float)hd);
-    float mrow = -INFINITY, lrow = 0.f;
+    const int half = (warp - 2) >> 2;                  // which 32 keys of the page
+    const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+    float mrow = -INFINITY, lrow = 0.f;                // log2 domain; lrow = this half's partial sum
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    uint8_t* prow_base = sP + lane_row * 128;
+    const int hcols = hd / 2;                           // this half's O columns
     for (int j = 0; j < n_chunks; ++j) {
       mbar_wait(&sfull[j & 1], (j >> 1) & 1);
       fence_after();
-      const int key0 = (c_first + j) * PAGE;
-      float s[64];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[16];
-        tmem_ld16(tS + lane_off + (uint32_t)((j & 1) * 64 + c * 16), r);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) s[c * 16 + i] = __uint_as_float(r[i]);
+      const int kb = (c_first + j) * PAGE + half * 32;
+      uint32_t r[32];
+      tmem_ld32(tS + lane_off + (uint32_t)((j & 1) * 64 + half * 32), r);
+      uint32_t vm = 0u;
+      if (valid) {
+        vm = range32(klo - kb, khi - kb);
+        if (slot >= 0) vm |= anc32(anc, kb - tb) & range32(0, m.t_max - (kb - tb));
+        vm &= range32(k_begin - kb, k_end - kb);
       }
+      float s[32];
       float mx = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const int key = key0 + i;
-        const bool ok = valid && key >= k_begin && key < k_end && vis(key, klo, khi, slot, tb, m.t_max, anc);
-        s[i] = ok ? s[i] * scale : -INFINITY;
+      for (int i = 0; i < 32; ++i) {
+        s[i] = ((vm >> i) & 1u) ? __uint_as_float(r[i]) * scale_log2 : -INFINITY;
         mx = fmaxf(mx, s[i]);
       }
+      red_max[j & 1][half][lane_row] = mx;
+      pair_sync(q4);
+      mx = fmaxf(red_max[j & 1][0][lane_row], red_max[j & 1][1][lane_row]);
       const float mnew = fmaxf(mrow, mx);
-      const float alpha = (mrow == -INFINITY) ? (mnew == -INFINITY ? 1.f : 0.f) : expf(mrow - mnew);
+      const float alpha = (mrow == -INFINITY) ? (mnew == -INFINITY ? 1.f : 0.f) : ex2(mrow - mnew);
+      // nothing visible yet for this row: P must be exactly 0 (not ex2(-inf+inf) = NaN)
+      const float msub = mnew == -INFINITY ? 0.f : mnew;
       if (j > 0) {
         mbar_wait(pvdone, (j - 1) & 1);   // O (and the P buffer being reused) are free
         fence_after();
-        const bool need = alpha != 1.f;
-        if (__any_sync(0xffffffffu, need)) {
-          for (int c = 0; c < hd; c += 16) {
-            uint32_t r[16];
-            tmem_ld16(tO + lane_off + (uint32_t)c, r);
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+          for (int c = 0; c < hcols; c += 16) {
+            uint32_t o[16];
+            tmem_ld16(tO + lane_off + (uint32_t)(half * hcols + c), o);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tmem_st16(tO + lane_off + (uint32_t)c, r);
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st16(tO + lane_off + (uint32_t)(half * hcols + c), o);
           }
           tmem_st_wait();
         }
       }
       float psum = 0.f;
-      uint8_t* prow = prow_base + (j & 1) * p_bytes;
+      uint8_t* prow = sP + (j & 1) * p_bytes + lane_row * 128;
 #pragma unroll
-      for (int c16 = 0; c16 < 8; ++c16) {
+      for (int c = 0; c < 4; ++c) {
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float p0 = s[c16 * 8 + 2 * e] == -INFINITY ? 0.f : expf(s[c16 * 8 + 2 * e] - mnew);
-          const float p1 = s[c16 * 8 + 2 * e + 1] == -INFINITY ? 0.f : expf(s[c16 * 8 + 2 * e + 1] - mnew);
+          const float p0 = ex2(s[c * 8 + 2 * e] - msub), p1 = ex2(s[c * 8 + 2 * e + 1] - msub);
           __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
           psum += __low2float(pr) + __high2float(pr);     // l sums exactly what the MMA sees
           w[e] = *(uint32_t*)&pr;
         }
+        const int c16 = half * 4 + c;
         *(uint4*)(prow + ((c16 ^ (lane_row & 7)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
       lrow = lrow * alpha + psum;
@@ -245,36 +289,39 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_arrive(&pfull[j & 1]);
     }
     // ------------------------------------------------------------ epilogue
+    red_l[half][lane_row] = lrow;
     if (n_chunks > 0) {
       mbar_wait(pvdone, (n_chunks - 1) & 1);
       fence_after();
     }
-    for (int c = 0; c < hd; c += 16) {
-      uint32_t r[16];
-      if (n_chunks > 0) tmem_ld16(tO + lane_off + (uint32_t)c, r);
+    pair_sync(q4);
+    const float ltot = red_l[0][lane_row] + red_l[1][lane_row];
+    for (int c = 0; c < hcols; c += 16) {
+      uint32_t o[16];
+      if (n_chunks > 0) tmem_ld16(tO + lane_off + (uint32_t)(half * hcols + c), o);
       else
-        for (int i = 0; i < 16; ++i) r[i] = 0u;
+        for (int i = 0; i < 16; ++i) o[i] = 0u;
       if (writable) {
+        const int d0 = half * hcols + c;
         if (P.direct) {
-          const float inv = lrow > 0.f ? 1.0f / lrow : 0.f;
-          bf16* o = P.out + ((size_t)row * P.Hq + head) * hd + c;
+          const float inv = ltot > 0.f ? 1.0f / ltot : 0.f;
+          bf16* out = P.out + ((size_t)row * P.Hq + head) * hd + d0;
 #pragma unroll
-          for (int i = 0; i < 16; i += 2) {
-            __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[i]) * inv, __uint_as_float(r[i + 1]) * inv);
-            *(__nv_bfloat162*)(o + i) = v;
-          }
+          for (int i = 0; i < 16; i += 2)
+            *(__nv_bfloat162*)(out + i) =
+                __floats2bfloat162_rn(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
         } else {
-          float* o = P.ws + (((size_t)split * P.M + row) * P.Hq + head) * hd + c;
+          float* out = P.ws + (((size_t)split * P.M + row) * P.Hq + head) * hd + d0;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) o[i] = lrow > 0.f ? __uint_as_float(r[i]) : 0.f;
+          for (int i = 0; i < 16; ++i) out[i] = ltot > 0.f ? __uint_as_float(o[i]) : 0.f;
         }
       }
     }
-    if (!P.direct && writable) {
+    if (!P.direct && writable && half == 0) {
       const size_t base_ml = (size_t)gridDim.x * P.M * P.Hq * hd;
       const size_t idx = ((size_t)split * P.M + row) * P.Hq + head;
-      P.ws[base_ml + 2 * idx] = mrow;
-      P.ws[base_ml + 2 * idx + 1] = lrow;
+      P.ws[base_ml + 2 * idx] = mrow;      // log2 domain (merge uses exp2)
+      P.ws[base_ml + 2 * idx + 1] = ltot;
     }
   }
   fence_before();
@@ -283,26 +330,37 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
 }
 
+// split merge: one warp per (row, head), lanes over hd:
+// o = sum_s e^{m_s - M} o_s / sum_s e^{m_s - M} l_s
 __global__ void attention_merge_bf16_kernel(const float* __restrict__ ws, int S, int M, int Hq, int hd,
                                             bf16* __restrict__ out) {
-  int row = blockIdx.x, head = blockIdx.y;
-  size_t base = (size_t)S * M * Hq * hd;
+  pdl_wait();
+  pdl_trigger();
+  const int pair = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (pair >= M * Hq) return;
+  const size_t base = (size_t)S * M * Hq * hd;
   float Mx = -INFINITY;
   for (int s = 0; s < S; ++s) {
-    size_t idx = ((size_t)s * M + row) * Hq + head;
+    const size_t idx = (size_t)s * M * Hq + pair;
     if (ws[base + 2 * idx + 1] > 0.f) Mx = fmaxf(Mx, ws[base + 2 * idx]);
   }
-  for (int d = threadIdx.x; d < hd; d += blockDim.x) {
-    float num = 0.f, den = 0.f;
-    for (int s = 0; s < S; ++s) {
-      size_t idx = ((size_t)s * M + row) * Hq + head;
-      float l = ws[base + 2 * idx + 1];
-      if (l <= 0.f) continue;
-      float w = expf(ws[base + 2 * idx] - Mx);
-      num = fmaf(w, ws[idx * hd + d], num);
-      den = fmaf(w, l, den);
+  float den = 0.f, num[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int s = 0; s < S; ++s) {
+    const size_t idx = (size_t)s * M * Hq + pair;
+    const float l = ws[base + 2 * idx + 1];
+    if (l <= 0.f) continue;
+    const float w = exp2f(ws[base + 2 * idx] - Mx);   // m is in log2 units
+    den = fmaf(w, l, den);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int d = lane + 32 * i;
+      if (d < hd) num[i] = fmaf(w, ws[idx * hd + d], num[i]);
     }
-    out[((size_t)row * Hq + head) * hd + d] = __float2bfloat16_rn(den > 0.f ? num / den : 0.f);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int d = lane + 32 * i;
+    if (d < hd) out[(size_t)pair * hd + d] = __float2bfloat16_rn(den > 0.f ? num[i] / den : 0.f);
   }
 }
 }  // namespace
@@ -325,7 +383,8 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   // splits: enough CTAs for ~2 per SM, each split a whole number of pages
   const int base_ctas = n_req * kv.kv_heads * P.n_qtiles;
   const int pages = (max_keys + PAGE - 1) / PAGE;
-  int S = (2 * num_sms() + base_ctas - 1) / base_ctas;
+  // one wave: the kernel holds ~160 KB of shared memory, so one CTA per SM
+  int S = num_sms() / base_ctas;
   if (S > pages) S = pages;
   if (S > 32) S = 32;
   if (S < 1) S = 1;
@@ -361,10 +420,10 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
     attr = smem;
   }
   dim3 grid(S, kv.kv_heads, n_req * P.n_qtiles);
-  attention_tc_kernel<<<grid, NTHREADS, smem, st>>>(mq, mk, mv, P);
+  launch_k(attention_tc_kernel, grid, dim3(NTHREADS), smem, st, mq, mk, mv, P);
   int launched = 1;
   if (S > 1) {
-    attention_merge_bf16_kernel<<<dim3(M, Hq), 128, 0, st>>>(ws, S, M, Hq, hd, (bf16*)out);
+    launch_k(attention_merge_bf16_kernel, (M * Hq + 7) / 8, 256, 0, st, ws, S, M, Hq, hd, (bf16*)out);
     launched++;
   }
   return launched;

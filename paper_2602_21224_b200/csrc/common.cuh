@@ -99,6 +99,34 @@ HSD_DEV void warp_argmax(float& v, int& i) {
   }
 }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel may start
+// while its predecessor is still running. Every kernel therefore executes
+// pdl_wait() (griddepcontrol.wait: all prerequisite grids complete, memory
+// visible) before touching data produced upstream, and pdl_trigger() to let
+// its own dependents start their prologue early.
+HSD_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+HSD_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+extern bool g_hsd_pdl;   // engine.cu; HSD_PDL=0 disables (A/B testing)
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_hsd_pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---------------------------------------------------------------- error word
 #define DEV_ERR_BAD_TREE 1
 #define DEV_ERR_BAD_TOKEN 2

@@ -20,6 +20,14 @@
 #include "gemm_tc.cuh"
 
 int64_t g_hsd_launches = 0;
+static bool g_attn_tc = [] {
+  const char* e = getenv("HSD_ATTN_TC");
+  return e == nullptr || atoi(e) != 0;
+}();
+bool g_hsd_pdl = [] {
+  const char* e = getenv("HSD_PDL");
+  return e == nullptr || atoi(e) != 0;
+}();
 
 namespace {
 constexpr int PREFILL_CHUNK = 1024;
@@ -40,6 +48,8 @@ struct MetaBuf {
 // stored at p + s; sees the committed cache [0, p) plus its tree ancestors.
 __global__ void meta_verify_kernel(MetaBuf mb, int T, const int32_t* t_n, const int32_t* t_tok,
                                    const int32_t* t_depth, const int32_t* p) {
+  pdl_wait();
+  pdl_trigger();
   int r = blockIdx.x, s = threadIdx.x;
   if (s >= T) return;
   int row = r * T + s;
@@ -57,6 +67,8 @@ __global__ void meta_verify_kernel(MetaBuf mb, int T, const int32_t* t_n, const 
 // causal over the draft KV positions [1, pos] (reading R1/R2).
 __global__ void meta_dprefill_kernel(MetaBuf mb, int R, const int32_t* n_pend, const int32_t* pend_tok,
                                      const int32_t* p) {
+  pdl_wait();
+  pdl_trigger();
   int r = blockIdx.x, j = threadIdx.x;
   if (j >= R) return;
   int row = r * R + j;
@@ -74,6 +86,8 @@ __global__ void meta_dprefill_kernel(MetaBuf mb, int R, const int32_t* n_pend, c
 
 // chain step i: row r at position p + i, causal over draft KV [1, p + i]
 __global__ void meta_chain_kernel(MetaBuf mb, int b, int i, const int32_t* p) {
+  pdl_wait();
+  pdl_trigger();
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= b) return;
   int pos = p[r] + i;
@@ -84,6 +98,8 @@ __global__ void meta_chain_kernel(MetaBuf mb, int b, int i, const int32_t* p) {
 // h_1 = draft output at the last pending row -> xw[r] and chain[r][0]
 __global__ void gather_last_kernel(const float* x, int R, const int32_t* n_pend, int n, float* xw, float* chain,
                                    int N) {
+  pdl_wait();
+  pdl_trigger();
   int r = blockIdx.x;
   const float* src = x + ((size_t)r * R + n_pend[r] - 1) * n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -93,6 +109,8 @@ __global__ void gather_last_kernel(const float* x, int R, const int32_t* n_pend,
 }
 
 __global__ void copy_chain_kernel(const float* xw, int n, float* chain, int N, int i) {
+  pdl_wait();
+  pdl_trigger();
   int r = blockIdx.x;
   for (int c = threadIdx.x; c < n; c += blockDim.x) chain[((size_t)r * N + i) * n + c] = xw[(size_t)r * n + c];
 }
@@ -103,6 +121,8 @@ __global__ void first_token_kernel(const float* logits, int V, int mode, float i
                                    int r, const float* Hlast, int n, int P0, int N, float* pend_H,
                                    int32_t* pend_tok, int32_t* n_pend, int32_t* root_tok, int32_t* p,
                                    int32_t* d_first) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float sv[32];
   __shared__ int si[32];
   float bv = -INFINITY;
@@ -317,12 +337,12 @@ static void* dalloc(hsd_ctx* c, size_t bytes) {
 // GEMM dispatch: C[M,N] (+)= A[M,K] W[N,K]^T. Algorithmic bytes: W once, A once,
 // C written once (read too when accumulating).
 static void gemm(hsd_ctx* c, const void* A, int lda, const void* Wt, int ldw, float* C, int ldc, int M, int N,
-                 int K, bool acc, int cat = -1) {
+                 int K, bool acc, int cat = -1, bool c_zeroed = false) {
   if (cat < 0) cat = c->pass_verify ? P_GEMM_VERIFY : P_GEMM_DRAFT;
   Prof pf(c, cat, (double)N * K * c->esz + (double)M * K * c->esz + (double)M * N * 4 * (acc ? 2 : 1),
           2.0 * M * N * K);
   if (c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, N, K, lda, ldw)) {
-    g_hsd_launches += gemm_tc_bf16((const bf16*)A, lda, (const bf16*)Wt, ldw, C, ldc, M, N, K, acc, c->st);
+    g_hsd_launches += gemm_tc_bf16((const bf16*)A, lda, (const bf16*)Wt, ldw, C, ldc, M, N, K, acc, c->st, c_zeroed);
   } else {
     gemm_simt(A, lda, Wt, ldw, c->dt, C, ldc, M, N, K, acc, c->st);
     g_hsd_launches += 1;
@@ -346,7 +366,9 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
                           const KVLayer& kv, int max_keys) {
   const int n = c->n;
   { Prof pf(c, P_ROWWISE); launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st); }
-  gemm(c, c->a, n, w.wqkv, n, c->big, c->qkvd, M, c->qkvd, n, false);
+  // c->big is kept zero outside a GEMM -> consumer window (qkv_rope_kv and
+  // swiglu re-zero what they read), so these GEMMs accumulate without a memset
+  gemm(c, c->a, n, w.wqkv, n, c->big, c->qkvd, M, c->qkvd, n, false, -1, true);
   { Prof pf(c, P_ROWWISE);
     launch_qkv_rope_kv(c->big, M, m, c->rope_cos, c->rope_sin, c->Hq, kv, c->qb, c->dt, c->st); }
   {
@@ -355,7 +377,7 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
     // host uses the capacity-free estimate recorded by hsd_profile_read callers.
     Prof pf(c, c->pass_verify ? P_ATTN_VERIFY : P_ATTN_DRAFT, c->attn_bytes);
     int tc_launched = -1;
-    if (c->use_tc && attention_tc_supported(c->hd, c->page_size, c->dt))
+    if (c->use_tc && g_attn_tc && attention_tc_supported(c->hd, c->page_size, c->dt))
       tc_launched = launch_attention_tc(c->qb, M, R, n_req, m, kv, c->Hq, max_keys, c->ob, c->attn_ws,
                                         c->attn_ws_floats, c->kv_layer_elems, c->st);
     if (tc_launched < 0)
@@ -364,7 +386,7 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
   }
   gemm(c, c->ob, c->qd, w.wo, c->qd, x, n, M, n, c->qd, true);
   { Prof pf(c, P_ROWWISE); launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st); }
-  gemm(c, c->a, n, w.wgu, n, c->big, 2 * c->f, M, 2 * c->f, n, false);
+  gemm(c, c->a, n, w.wgu, n, c->big, 2 * c->f, M, 2 * c->f, n, false, -1, true);
   { Prof pf(c, P_ROWWISE); launch_swiglu(c->big, M, c->f, c->a, c->dt, m.pos, c->st); }
   gemm(c, c->a, c->f, w.wd, c->f, x, n, M, n, c->f, true);
   g_hsd_launches += 6;  // rmsnorm x2, rope_kv, attention(+merge counted below), swiglu
@@ -375,21 +397,21 @@ static void stage_build(hsd_ctx* c) {
   const int b = c->b, N = c->N, n = c->n, R = N + 1;
   const int kvmax = c->max_pos;
   // S0 (1): draft prefill of the pending pairs x_j = W_fc [H_{j-1}; E(t_j)] (R1)
-  meta_dprefill_kernel<<<b, 32 * ((R + 31) / 32), 0, c->st>>>(c->md, R, c->n_pend, c->pend_tok, c->p);
+  launch_k(meta_dprefill_kernel, b, 32 * ((R + 31) / 32), 0, c->st, c->md, R, c->n_pend, c->pend_tok, c->p);
   RowMeta mdv = c->md.view(nullptr, nullptr, 0, 0);
   c->attn_bytes = attn_bytes_for(c, 1, 0);
   launch_draft_concat(c->pend_H, c->md.tok, c->md.pos, c->embed, c->dt, b * R, n, c->a, c->st);
   gemm(c, c->a, 2 * n, c->fc, 2 * n, c->x_d, n, b * R, n, 2 * n, false);
   layer_forward(c, c->draft, c->x_d, b * R, R, b, mdv, kv_layer(c, c->kv_d, 0), kvmax);
-  gather_last_kernel<<<b, 256, 0, c->st>>>(c->x_d, R, c->n_pend, n, c->xw, c->chain, N);
+  launch_k(gather_last_kernel, b, 256, 0, c->st, c->x_d, R, c->n_pend, n, c->xw, c->chain, N);
   g_hsd_launches += 3;
   // S0 (2): chain h_{i+1} = TL(h_i) at positions p + i (R2)
   RowMeta mcv = c->mc.view(nullptr, nullptr, 0, 0);
   for (int i = 1; i < N; ++i) {
-    meta_chain_kernel<<<(b + 127) / 128, 128, 0, c->st>>>(c->mc, b, i, c->p);
+    launch_k(meta_chain_kernel, (b + 127) / 128, 128, 0, c->st, c->mc, b, i, c->p);
     c->attn_bytes = attn_bytes_for(c, 2, i);
     layer_forward(c, c->draft, c->xw, b, 1, b, mcv, kv_layer(c, c->kv_d, 0), kvmax);
-    copy_chain_kernel<<<b, 256, 0, c->st>>>(c->xw, n, c->chain, N, i);
+    launch_k(copy_chain_kernel, b, 256, 0, c->st, c->xw, n, c->chain, N, i);
     g_hsd_launches += 2;
   }
   // S1a: one-pass logits L = RMSNorm_f(H_chain) W_head^T, rank order
@@ -419,7 +441,7 @@ static void stage_build(hsd_ctx* c) {
 
 static void stage_verify(hsd_ctx* c) {
   const int b = c->b, T = c->T, n = c->n, M = b * T;
-  meta_verify_kernel<<<b, 32 * ((T + 31) / 32), 0, c->st>>>(c->mv, T, c->t_n, c->t_tok, c->t_depth, c->p);
+  launch_k(meta_verify_kernel, b, 32 * ((T + 31) / 32), 0, c->st, c->mv, T, c->t_n, c->t_tok, c->t_depth, c->p);
   RowMeta m = c->mv.view(c->p, c->t_anc, T, c->W);
   launch_embed(c->embed, c->dt, c->mv.tok, c->mv.pos, M, n, c->Hver, c->st);
   g_hsd_launches += 2;
@@ -778,7 +800,7 @@ hsd_status hsd_prefill(hsd_ctx* ctx, int32_t n_req, const int32_t* h_tokens, int
     const float* Hlast = c->H_prompt + (size_t)(P0 - 1) * n;
     launch_rmsnorm(Hlast, 1, n, c->cfg.rms_eps, c->a, c->dt, nullptr, c->st);
     gemm(c, c->a, n, c->head, n, c->logits, c->V, 1, c->V, n, false);
-    first_token_kernel<<<1, 512, 0, c->st>>>(c->logits, c->V, c->cfg.accept_mode == HSD_STOCHASTIC ? 1 : 0,
+    launch_k(first_token_kernel, 1, 512, 0, c->st, c->logits, c->V, c->cfg.accept_mode == HSD_STOCHASTIC ? 1 : 0,
                                              1.0f / c->cfg.temperature, (uint32_t)c->cfg.seed,
                                              c->cfg.req_offset + r, r, Hlast, n, P0, N, c->pend_H, c->pend_tok,
                                              c->n_pend, c->root_tok, c->p, d_first);

@@ -13,6 +13,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const T* __restrict__ A,
                                                         const T* __restrict__ W, int ldw,
                                                         float* __restrict__ C, int ldc, int M, int N, int K,
                                                         int accumulate) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float As[BK][BM + 4];
   __shared__ float Ws[BK][BN + 4];
   int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -62,9 +64,9 @@ void gemm_simt(const void* A, int lda, const void* W, int ldw, DType dt, float* 
   if (M <= 0 || N <= 0) return;
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
   if (dt == DT_F32)
-    gemm_simt_kernel<float><<<grid, 256, 0, st>>>((const float*)A, lda, (const float*)W, ldw, C, ldc, M, N, K,
+    launch_k(gemm_simt_kernel<float>, grid, 256, 0, st, (const float*)A, lda, (const float*)W, ldw, C, ldc, M, N, K,
                                                   accumulate);
   else
-    gemm_simt_kernel<bf16><<<grid, 256, 0, st>>>((const bf16*)A, lda, (const bf16*)W, ldw, C, ldc, M, N, K,
+    launch_k(gemm_simt_kernel<bf16>, grid, 256, 0, st, (const bf16*)A, lda, (const bf16*)W, ldw, C, ldc, M, N, K,
                                                  accumulate);
 }

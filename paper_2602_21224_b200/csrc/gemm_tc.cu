@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
 
   if (warp == 0) {
     // ---------------- TMA producer
@@ -78,9 +79,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
       const uint64_t pw = policy_evict_first(), px = policy_evict_last();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (long u = u0; u < u1; ++u) {
+      // PDL: the weight tiles of the first ring stages do not depend on the
+      // previous kernel -- stream them before griddepcontrol.wait, so the ring
+      // fills while the predecessor drains; token tiles only after the wait.
+      const long npre = (u1 - u0) < P.stages ? (u1 - u0) : P.stages;
+      for (long i = 0; i < npre; ++i) {
+        const long u = u0 + i;
+        const int t = (int)(u / P.n_kb), kb = (int)(u % P.n_kb);
+        mbar_expect_tx(&full[i], A_BYTES + b_bytes);
+        tma_load_2d(&tmW, &full[i], sA + (size_t)i * A_BYTES, kb * BK, (t / P.n_tiles_t) * BM, pw);
+      }
+      pdl_wait();
+      for (long i = 0; i < npre; ++i) {
+        const long u = u0 + i;
+        const int t = (int)(u / P.n_kb), kb = (int)(u % P.n_kb);
+        tma_load_2d(&tmX, &full[i], sB + (size_t)i * b_bytes, kb * BK, (t % P.n_tiles_t) * P.ntile, px);
+      }
+      int stage = (int)(npre % P.stages);
+      uint32_t phase = npre == P.stages ? 1u : 0u;
+      for (long u = u0 + npre; u < u1; ++u) {
         const int t = (int)(u / P.n_kb), kb = (int)(u % P.n_kb);
         const int tn = t / P.n_tiles_t, tt = t % P.n_tiles_t;
         mbar_wait(&empty[stage], phase ^ 1);
@@ -92,6 +109,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread)
+    pdl_wait();
     if (lane == 0) {
       int stage = 0, buf = 0;
       uint32_t phase = 0, aphase = 0;
@@ -122,6 +140,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else {
     // ---------------- epilogue: 4 warps = 128 TMEM lanes (lane quarter = warp % 4)
+    pdl_wait();
     const int q = warp & 3;
     int buf = 0;
     uint32_t aphase = 0;
@@ -219,9 +238,9 @@ bool gemm_tc_supported(int M, int N, int K, int lda, int ldw) {
 }
 
 int gemm_tc_bf16(const bf16* A, int lda, const bf16* W, int ldw, float* C, int ldc, int M, int N, int K,
-                 bool accumulate, cudaStream_t st) {
+                 bool accumulate, cudaStream_t st, bool c_zeroed) {
   int launched = 0;
-  if (!accumulate) {
+  if (!accumulate && !c_zeroed) {
     cudaMemset2DAsync(C, (size_t)ldc * 4, 0, (size_t)N * 4, M, st);
   }
   TcParams P;
@@ -254,7 +273,7 @@ int gemm_tc_bf16(const bf16* A, int lda, const bf16* W, int ldw, float* C, int l
     attr_done = true;
   }
   long grid = P.units < num_sms() ? P.units : num_sms();
-  gemm_tc_kernel<<<(int)grid, NTHREADS, smem, st>>>(mw, mx, P);
+  launch_k(gemm_tc_kernel, dim3((unsigned)grid), dim3(NTHREADS), smem, st, mw, mx, P);
   launched += 1;
   return launched;
 }

@@ -49,10 +49,10 @@ void launch_rmsnorm(const float* x, int M, int n, float eps, void* out, DType dt
                     cudaStream_t st);
 void launch_embed(const void* E, DType dt, const int32_t* tok, const int32_t* pos, int M, int n, float* x,
                   cudaStream_t st);
-void launch_qkv_rope_kv(const float* qkv, int M, const RowMeta& m, const float* rope_cos,
+void launch_qkv_rope_kv(float* qkv, int M, const RowMeta& m, const float* rope_cos,
                         const float* rope_sin, int Hq, const KVLayer& kv, void* q_out, DType dt,
                         cudaStream_t st);
-void launch_swiglu(const float* gu, int M, int f, void* out, DType dt, const int32_t* pos, cudaStream_t st);
+void launch_swiglu(float* gu, int M, int f, void* out, DType dt, const int32_t* pos, cudaStream_t st);
 void launch_argmax_rows(const float* x, int M, int V, const int32_t* pos, int32_t* out, cudaStream_t st);
 void launch_draft_concat(const float* Hprev, const int32_t* tok, const int32_t* pos, const void* E,
                          DType dt, int M, int n, void* out, cudaStream_t st);

@@ -29,6 +29,8 @@ template <> struct Vec4<bf16> {
 template <typename T>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, int n, float eps,
                                                       T* __restrict__ out, const int32_t* __restrict__ pos) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[32];
   const int r = blockIdx.x;
   const float4* xr = (const float4*)(x + (size_t)r * n);
@@ -64,14 +66,16 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
 void launch_rmsnorm(const float* x, int M, int n, float eps, void* out, DType dt, const int32_t* pos,
                     cudaStream_t st) {
   if (M <= 0) return;
-  if (dt == DT_F32) rmsnorm_kernel<float><<<M, 256, 0, st>>>(x, n, eps, (float*)out, pos);
-  else rmsnorm_kernel<bf16><<<M, 256, 0, st>>>(x, n, eps, (bf16*)out, pos);
+  if (dt == DT_F32) launch_k(rmsnorm_kernel<float>, M, 256, 0, st, x, n, eps, (float*)out, pos);
+  else launch_k(rmsnorm_kernel<bf16>, M, 256, 0, st, x, n, eps, (bf16*)out, pos);
 }
 
 // ------------------------------------------------------------------ embedding
 template <typename T>
 __global__ void embed_kernel(const T* __restrict__ E, const int32_t* __restrict__ tok,
                              const int32_t* __restrict__ pos, int n, float* __restrict__ x) {
+  pdl_wait();
+  pdl_trigger();
   int r = blockIdx.x;
   float* xr = x + (size_t)r * n;
   const bool active = !(pos && pos[r] < 0);
@@ -82,8 +86,8 @@ __global__ void embed_kernel(const T* __restrict__ E, const int32_t* __restrict_
 void launch_embed(const void* E, DType dt, const int32_t* tok, const int32_t* pos, int M, int n, float* x,
                   cudaStream_t st) {
   if (M <= 0) return;
-  if (dt == DT_F32) embed_kernel<float><<<M, 256, 0, st>>>((const float*)E, tok, pos, n, x);
-  else embed_kernel<bf16><<<M, 256, 0, st>>>((const bf16*)E, tok, pos, n, x);
+  if (dt == DT_F32) launch_k(embed_kernel<float>, M, 256, 0, st, (const float*)E, tok, pos, n, x);
+  else launch_k(embed_kernel<bf16>, M, 256, 0, st, (const bf16*)E, tok, pos, n, x);
 }
 
 // ------------------------------------------------------------------ RoPE + KV write
@@ -93,13 +97,21 @@ void launch_embed(const void* E, DType dt, const int32_t* tok, const int32_t* po
 // grid (M, Hq + 2*Hkv): one CTA per (row, head); K/V go to the paged cache
 // (V transposed, see KVLayer).
 template <typename T>
-__global__ void qkv_rope_kv_kernel(const float* __restrict__ qkv, RowMeta m, const float* __restrict__ rc,
+__global__ void qkv_rope_kv_kernel(float* __restrict__ qkv, RowMeta m, const float* __restrict__ rc,
                                    const float* __restrict__ rs, int Hq, KVLayer kv, T* __restrict__ q_out) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x, hh = blockIdx.y;
   const int hd = kv.head_dim, half = hd / 2, Hkv = kv.kv_heads;
   const int ld = (Hq + 2 * Hkv) * hd;
-  const float* src = qkv + (size_t)r * ld + (size_t)hh * hd;
+  float* src = qkv + (size_t)r * ld + (size_t)hh * hd;
   const int p = m.pos[r];
+  // The qkv scratch is re-zeroed once read, so the next tcgen05 GEMM into it can
+  // accumulate (red.add) without a memset (see gemm in engine.cu).
+  struct Zero {
+    float* p; int n;
+    __device__ ~Zero() { __syncthreads(); for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0.f; }
+  } zero{src, hd};
   if (hh < Hq) {
     T* qo = q_out + ((size_t)r * Hq + hh) * hd;
     for (int j = threadIdx.x; j < half; j += blockDim.x) {
@@ -131,45 +143,52 @@ __global__ void qkv_rope_kv_kernel(const float* __restrict__ qkv, RowMeta m, con
   }
 }
 
-void launch_qkv_rope_kv(const float* qkv, int M, const RowMeta& m, const float* rope_cos,
+void launch_qkv_rope_kv(float* qkv, int M, const RowMeta& m, const float* rope_cos,
                         const float* rope_sin, int Hq, const KVLayer& kv, void* q_out, DType dt,
                         cudaStream_t st) {
   if (M <= 0) return;
   dim3 grid(M, Hq + 2 * kv.kv_heads);
   int thr = kv.head_dim >= 128 ? 64 : 32;
   if (dt == DT_F32)
-    qkv_rope_kv_kernel<float><<<grid, thr, 0, st>>>(qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out);
+    launch_k(qkv_rope_kv_kernel<float>, grid, thr, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out);
   else
-    qkv_rope_kv_kernel<bf16><<<grid, thr, 0, st>>>(qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out);
+    launch_k(qkv_rope_kv_kernel<bf16>, grid, thr, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out);
 }
 
 // ------------------------------------------------------------------ SwiGLU
 // gu row = [gate (f) | up (f)] -> silu(gate) * up; grid (M, f/4/256 chunks), f % 4 == 0
 template <typename T>
-__global__ void swiglu_kernel(const float* __restrict__ gu, int f, T* __restrict__ out,
+__global__ void swiglu_kernel(float* __restrict__ gu, int f, T* __restrict__ out,
                               const int32_t* __restrict__ pos) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const int i = blockIdx.y * blockDim.x + threadIdx.x;   // float4 index
   if (4 * i >= f) return;
-  const float4 a = ((const float4*)(gu + (size_t)r * 2 * f))[i];
-  const float4 u = ((const float4*)(gu + (size_t)r * 2 * f + f))[i];
+  float4* ga = (float4*)(gu + (size_t)r * 2 * f) + i;
+  float4* gb = (float4*)(gu + (size_t)r * 2 * f + f) + i;
+  const float4 a = *ga, u = *gb;
+  *ga = make_float4(0.f, 0.f, 0.f, 0.f);   // re-zero the GEMM scratch (see qkv_rope_kv)
+  *gb = make_float4(0.f, 0.f, 0.f, 0.f);
   const bool active = pos == nullptr || pos[r] >= 0;
   auto sl = [](float x) { return x / (1.0f + expf(-x)); };
   if (active) Vec4<T>::store(out + (size_t)r * f + 4 * i, sl(a.x) * u.x, sl(a.y) * u.y, sl(a.z) * u.z, sl(a.w) * u.w);
   else Vec4<T>::store(out + (size_t)r * f + 4 * i, 0.f, 0.f, 0.f, 0.f);
 }
 
-void launch_swiglu(const float* gu, int M, int f, void* out, DType dt, const int32_t* pos, cudaStream_t st) {
+void launch_swiglu(float* gu, int M, int f, void* out, DType dt, const int32_t* pos, cudaStream_t st) {
   if (M <= 0) return;
   dim3 grid(M, (f / 4 + 255) / 256);
-  if (dt == DT_F32) swiglu_kernel<float><<<grid, 256, 0, st>>>(gu, f, (float*)out, pos);
-  else swiglu_kernel<bf16><<<grid, 256, 0, st>>>(gu, f, (bf16*)out, pos);
+  if (dt == DT_F32) launch_k(swiglu_kernel<float>, grid, 256, 0, st, gu, f, (float*)out, pos);
+  else launch_k(swiglu_kernel<bf16>, grid, 256, 0, st, gu, f, (bf16*)out, pos);
 }
 
 // ------------------------------------------------------------------ argmax
 // lowest index among maxima (reading R8)
 __global__ void argmax_rows_kernel(const float* __restrict__ x, int V, const int32_t* __restrict__ pos,
                                    int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float sv[32];
   __shared__ int si[32];
   int r = blockIdx.x;
@@ -199,7 +218,7 @@ __global__ void argmax_rows_kernel(const float* __restrict__ x, int V, const int
 
 void launch_argmax_rows(const float* x, int M, int V, const int32_t* pos, int32_t* out, cudaStream_t st) {
   if (M <= 0) return;
-  argmax_rows_kernel<<<M, 1024, 0, st>>>(x, V, pos, out);
+  launch_k(argmax_rows_kernel, M, 1024, 0, st, x, V, pos, out);
 }
 
 // ------------------------------------------------------------------ draft input
@@ -208,6 +227,8 @@ template <typename T>
 __global__ void draft_concat_kernel(const float* __restrict__ Hprev, const int32_t* __restrict__ tok,
                                     const int32_t* __restrict__ pos, const T* __restrict__ E, int n,
                                     T* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   int r = blockIdx.x;
   T* o = out + (size_t)r * 2 * n;
   bool active = pos[r] >= 0;
@@ -223,7 +244,7 @@ void launch_draft_concat(const float* Hprev, const int32_t* tok, const int32_t* 
                          DType dt, int M, int n, void* out, cudaStream_t st) {
   if (M <= 0) return;
   if (dt == DT_F32)
-    draft_concat_kernel<float><<<M, 256, 0, st>>>(Hprev, tok, pos, (const float*)E, n, (float*)out);
+    launch_k(draft_concat_kernel<float>, M, 256, 0, st, Hprev, tok, pos, (const float*)E, n, (float*)out);
   else
-    draft_concat_kernel<bf16><<<M, 256, 0, st>>>(Hprev, tok, pos, (const bf16*)E, n, (bf16*)out);
+    launch_k(draft_concat_kernel<bf16>, M, 256, 0, st, Hprev, tok, pos, (const bf16*)E, n, (bf16*)out);
 }

@@ -12,11 +12,15 @@
 // Tie rules = DESIGN.md R8. One CTA of 1024 threads per request; every vocab
 // pass is a coalesced sweep of the logit row plus the table row with per-thread
 // online (max, sum-exp) and a per-thread top-8 list, merged warp-wise.
+#include <cooperative_groups.h>
 #include "kernels.cuh"
 #include "tree.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace {
 constexpr int NT = 1024;
+constexpr int CL = 8;       // CTAs per request (one thread-block cluster)
 constexpr int KMAX = 8;
 constexpr int MAXN = 256;
 constexpr int MAXW = MAXN / 64;
@@ -63,24 +67,30 @@ HSD_DEV void top_insert(Top& t, float v, int j, const int32_t* perm) {
   }
 }
 
-// One CTA-wide sweep: v_j = L[j] + bias[j] (bias only for hot columns j < Vh).
-// Returns (in smem) lse and the top-k (v, j) sorted by (v desc, token asc).
+// Partial result of one CTA's sweep over its vocab slice for one frontier node:
+// online (max, sum-exp) and the slice's top-k (v, j) sorted by (v desc, token asc).
+struct Partial {
+  float m, s;
+  float v[KMAX];
+  int j[KMAX];
+};
+
+// One CTA-wide sweep: v_j = L[j] + bias[j] over j in [lo, hi) (bias only for hot
+// columns j < Vh). Thread 0 returns the CTA partial in *out.
 template <typename TT>
-HSD_DEV void vocab_pass(const float* __restrict__ Lrow, const TT* __restrict__ bias, int V, int Vh, int k,
-                        const int32_t* perm, float* out_lse, float* out_v, int* out_j, float* red_f,
-                        int* red_i) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+HSD_DEV void vocab_pass(const float* __restrict__ Lrow, const TT* __restrict__ bias, int lo, int hi, int Vh, int k,
+                        const int32_t* perm, Partial* out, float* red_f, int* red_i) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = NT / 32;
   float m = -INFINITY, s = 0.f;
   Top t;
   top_init(t);
-  for (int j = threadIdx.x; j < V; j += NT) {
+  for (int j = lo + threadIdx.x; j < hi; j += NT) {
     float v = Lrow[j];
     if (bias != nullptr && j < Vh) v += to_f32(bias[j]);
     if (v > m) { s = s * expf(m - v) + 1.f; m = v; }
     else s += expf(v - m);
     top_insert(t, v, j, perm);
   }
-  // (max, sum) warp combine (butterfly: every lane ends with the same value)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
@@ -109,7 +119,6 @@ HSD_DEV void vocab_pass(const float* __restrict__ Lrow, const TT* __restrict__ b
     wv[r] = bv; wj[r] = bj;
     if (lane == bl) head++;
   }
-  // publish per-warp results
   __syncthreads();
   if (lane == 0) {
     red_f[w * 2] = m; red_f[w * 2 + 1] = s;
@@ -117,8 +126,7 @@ HSD_DEV void vocab_pass(const float* __restrict__ Lrow, const TT* __restrict__ b
   }
   __syncthreads();
   if (w == 0) {
-    // (max, sum) over warps
-    float mm = red_f[lane * 2], ss = red_f[lane * 2 + 1];
+    float mm = lane < nw ? red_f[lane * 2] : -INFINITY, ss = lane < nw ? red_f[lane * 2 + 1] : 0.f;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       float om = __shfl_xor_sync(0xffffffffu, mm, o), os = __shfl_xor_sync(0xffffffffu, ss, o);
@@ -126,11 +134,10 @@ HSD_DEV void vocab_pass(const float* __restrict__ Lrow, const TT* __restrict__ b
       ss = (mm == -INFINITY ? 0.f : ss * expf(mm - nm)) + (om == -INFINITY ? 0.f : os * expf(om - nm));
       mm = nm;
     }
-    // top-k over the 32 warp lists (lane l owns warp l's sorted list)
     int hd = 0;
     for (int r = 0; r < k; ++r) {
-      float hv = hd < k ? red_f[64 + lane * KMAX + hd] : -INFINITY;
-      int hj = hd < k ? red_i[lane * KMAX + hd] : -1;
+      float hv = (lane < nw && hd < k) ? red_f[64 + lane * KMAX + hd] : -INFINITY;
+      int hj = (lane < nw && hd < k) ? red_i[lane * KMAX + hd] : -1;
       float bv = hv;
       int bj = hj, bl = lane;
 #pragma unroll
@@ -139,74 +146,118 @@ HSD_DEV void vocab_pass(const float* __restrict__ Lrow, const TT* __restrict__ b
         int oj = __shfl_xor_sync(0xffffffffu, bj, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
         if (beats(ov, oj, ol, bv, bj, bl, perm)) { bv = ov; bj = oj; bl = ol; }
       }
-      if (lane == 0) { out_v[r] = bv; out_j[r] = bj; }
+      if (lane == 0) { out->v[r] = bv; out->j[r] = bj; }
       if (lane == bl) hd++;
     }
-    if (lane == 0) *out_lse = mm + logf(ss);
+    if (lane == 0) { out->m = mm; out->s = ss; }
   }
   __syncthreads();
 }
 
-// Alg. 1 BuildSubtree into smem nodes; rows = L rows of the steps.
+// Alg. 1 BuildSubtree on a thread-block cluster of CL CTAs: every CTA sweeps its
+// vocab slice for every frontier node and stores its Partial in the LEADER's
+// shared memory (DSMEM); the leader merges (exact (max, sum-exp) combination and
+// top-k over the CL sorted lists), appends the children in frontier order and
+// selects the next frontier (TopkByJointProb). Node arrays live in the leader.
+struct ClusterSm {
+  Partial part[KMAX][CL];
+  int Q[KMAX], Qtok[KMAX], nq;
+};
+
 HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, int root_tok, NodesSm& nd,
-                           float* red_f, int* red_i) {
-  __shared__ int Q[KMAX], nq;
-  __shared__ float tv[KMAX];
-  __shared__ int tj[KMAX];
-  __shared__ float lse;
-  if (threadIdx.x == 0) {
+                           ClusterSm& cs, float* red_f, int* red_i) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  ClusterSm* lead = cluster.map_shared_rank(&cs, 0);
+  __shared__ int qtok_local[KMAX], nq_local;
+  __shared__ Partial mine;
+  if (rank == 0 && threadIdx.x == 0) {
     nd.tok[0] = root_tok; nd.par[0] = -1; nd.depth[0] = 0; nd.lj[0] = 0.f; nd.n = 1;
-    Q[0] = 0; nq = 1;
+    cs.Q[0] = 0; cs.Qtok[0] = root_tok; cs.nq = 1;
   }
-  __syncthreads();
+  cluster.sync();
+  const int per = (P.V + CL - 1) / CL;
+  const int lo = min(P.V, rank * per), hi = min(P.V, lo + per);
   for (int i = 0; i < steps; ++i) {
+    if (threadIdx.x == 0) {
+      nq_local = lead->nq;
+      for (int q = 0; q < KMAX; ++q) qtok_local[q] = lead->Qtok[q];
+    }
+    __syncthreads();
     const float* Lrow = P.L + ((size_t)req * P.N + row0 + i) * P.V;
-    int start = nd.n;
-    for (int qi = 0; qi < nq; ++qi) {
-      int u = Q[qi];
-      int tok = nd.tok[u];
-      int rk = P.rank_of ? P.rank_of[tok] : tok;
-      bool has_bias = !P.zero_table && rk < P.Vh;
+    for (int qi = 0; qi < nq_local; ++qi) {
+      const int tok = qtok_local[qi];
+      const int rk = P.rank_of ? P.rank_of[tok] : tok;
+      const bool has_bias = !P.zero_table && rk < P.Vh;
       if (P.tdt == DT_F32)
-        vocab_pass<float>(Lrow, has_bias ? (const float*)P.table + (size_t)rk * P.Vh : nullptr, P.V, P.Vh,
-                          P.k, P.perm, &lse, tv, tj, red_f, red_i);
+        vocab_pass<float>(Lrow, has_bias ? (const float*)P.table + (size_t)rk * P.Vh : nullptr, lo, hi, P.Vh, P.k,
+                          P.perm, &mine, red_f, red_i);
       else
-        vocab_pass<bf16>(Lrow, has_bias ? (const bf16*)P.table + (size_t)rk * P.Vh : nullptr, P.V, P.Vh, P.k,
-                         P.perm, &lse, tv, tj, red_f, red_i);
-      if (threadIdx.x == 0) {
-        for (int c = 0; c < P.k; ++c) {
-          int n = nd.n;
-          if (n >= MAXN) break;
-          int j = tj[c];
+        vocab_pass<bf16>(Lrow, has_bias ? (const bf16*)P.table + (size_t)rk * P.Vh : nullptr, lo, hi, P.Vh, P.k,
+                         P.perm, &mine, red_f, red_i);
+      if (threadIdx.x == 0) lead->part[qi][rank] = mine;
+      __syncthreads();
+    }
+    cluster.sync();
+    if (rank == 0) {
+      const int start = nd.n;
+      // one thread per frontier node: merge the CL partials, append k children
+      if (threadIdx.x < cs.nq) {
+        const int qi = threadIdx.x, u = cs.Q[qi];
+        float M = -INFINITY;
+        for (int c = 0; c < CL; ++c) M = fmaxf(M, cs.part[qi][c].m);
+        float S = 0.f;
+        for (int c = 0; c < CL; ++c)
+          if (cs.part[qi][c].m != -INFINITY) S += cs.part[qi][c].s * expf(cs.part[qi][c].m - M);
+        const float lse = M + logf(S);
+        int hd[CL];
+        for (int c = 0; c < CL; ++c) hd[c] = 0;
+        for (int r = 0; r < P.k; ++r) {
+          int bc = -1;
+          for (int c = 0; c < CL; ++c) {
+            if (hd[c] >= P.k) continue;
+            const float v = cs.part[qi][c].v[hd[c]];
+            const int j = cs.part[qi][c].j[hd[c]];
+            if (j < 0) continue;
+            if (bc < 0 || better_j(v, j, cs.part[qi][bc].v[hd[bc]], cs.part[qi][bc].j[hd[bc]], P.perm)) bc = c;
+          }
+          const int n = start + qi * P.k + r;
+          const float v = cs.part[qi][bc].v[hd[bc]];
+          const int j = cs.part[qi][bc].j[hd[bc]];
+          hd[bc]++;
           nd.tok[n] = P.perm ? P.perm[j] : j;
           nd.par[n] = u;
           nd.depth[n] = nd.depth[u] + 1;
-          nd.lj[n] = nd.lj[u] + (tv[c] - lse);
-          nd.n = n + 1;
+          nd.lj[n] = nd.lj[u] + (v - lse);
         }
       }
       __syncthreads();
-    }
-    // TopkByJointProb(Q_next, k): joint desc, token asc, parent creation index asc
-    if (threadIdx.x == 0) {
-      int cnt = 0;
-      bool used[KMAX * KMAX];
-      for (int c = start; c < nd.n; ++c) used[c - start] = false;
-      for (int r = 0; r < P.k && r < nd.n - start; ++r) {
-        int best = -1;
-        for (int c = start; c < nd.n; ++c) {
-          if (used[c - start]) continue;
-          if (best < 0 || nd.lj[c] > nd.lj[best] ||
-              (nd.lj[c] == nd.lj[best] &&
-               (nd.tok[c] < nd.tok[best] || (nd.tok[c] == nd.tok[best] && nd.par[c] < nd.par[best]))))
-            best = c;
+      // TopkByJointProb(Q_next, k): joint desc, token asc, parent creation index asc
+      if (threadIdx.x == 0) {
+        const int cnt_new = cs.nq * P.k;
+        nd.n = start + cnt_new;
+        int cnt = 0;
+        bool used[KMAX * KMAX];
+        for (int c = 0; c < cnt_new; ++c) used[c] = false;
+        for (int r = 0; r < P.k && r < cnt_new; ++r) {
+          int best = -1;
+          for (int c = start; c < nd.n; ++c) {
+            if (used[c - start]) continue;
+            if (best < 0 || nd.lj[c] > nd.lj[best] ||
+                (nd.lj[c] == nd.lj[best] &&
+                 (nd.tok[c] < nd.tok[best] || (nd.tok[c] == nd.tok[best] && nd.par[c] < nd.par[best]))))
+              best = c;
+          }
+          used[best - start] = true;
+          cs.Q[cnt] = best;
+          cs.Qtok[cnt] = nd.tok[best];
+          cnt++;
         }
-        used[best - start] = true;
-        Q[cnt++] = best;
+        cs.nq = cnt;
       }
-      nq = cnt;
+      __syncthreads();
     }
-    __syncthreads();
+    cluster.sync();
   }
 }
 
@@ -255,13 +306,17 @@ HSD_DEV void prune_nodes(NodesSm& nd, int keep, NodesSm& tmp) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(NT) tree_kernel(TreeParams P, int mode) {
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(TreeParams P, int mode) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ NodesSm nd, tmp;
+  __shared__ ClusterSm cs;
   __shared__ float red_f[64 + 32 * KMAX];
   __shared__ int red_i[32 * KMAX];
   __shared__ int slot_of[MAXN], maxdepth;
   __shared__ uint64_t anc[MAXN][MAXW];
-  const int req = blockIdx.x;
+  const int req = blockIdx.x / CL;
+  const bool leader = cg::this_cluster().block_rank() == 0;
   const int Br1 = P.Br + 1;
 
   if (mode == TREE_MODE_RESAMPLE) {
@@ -270,9 +325,11 @@ __global__ void __launch_bounds__(NT) tree_kernel(TreeParams P, int mode) {
     int bonus = P.bonus[req];
     int n_remain = P.N - m - 1;
     if (P.resample && n_remain > P.r && n_remain > 0) {
-      build_subtree(P, req, m + 1, n_remain, bonus, nd, red_f, red_i);
+      build_subtree(P, req, m + 1, n_remain, bonus, nd, cs, red_f, red_i);
+      if (!leader) return;
       prune_nodes(nd, P.Br, tmp);
     } else {
+      if (!leader) return;
       if (threadIdx.x == 0) {
         nd.tok[0] = bonus; nd.par[0] = -1; nd.depth[0] = 0; nd.lj[0] = 0.f; nd.n = 1;
       }
@@ -291,7 +348,8 @@ __global__ void __launch_bounds__(NT) tree_kernel(TreeParams P, int mode) {
 
   // ---- fresh tree: Alg. 1 over all N rows from the root (last committed token)
   const int root = P.root_tok[req];
-  build_subtree(P, req, 0, P.N, root, nd, red_f, red_i);
+  build_subtree(P, req, 0, P.N, root, nd, cs, red_f, red_i);
+  if (!leader) return;
   prune_nodes(nd, P.B, tmp);
   // ---- verification fusion with the pending re-sampled tree
   int pn = P.pt_n[req];
@@ -404,5 +462,5 @@ __global__ void __launch_bounds__(NT) tree_kernel(TreeParams P, int mode) {
 
 void launch_tree(const TreeParams& P, int mode, int n_req, cudaStream_t st) {
   if (n_req <= 0) return;
-  tree_kernel<<<n_req, NT, 0, st>>>(P, mode);
+  launch_k(tree_kernel, n_req * CL, NT, 0, st, P, mode);
 }

@@ -164,7 +164,8 @@ def test_lockstep_c1_bf16_tcgen05():
     assert ls.max_err["verify"] <= 2e-2 and ls.max_err["L"] <= 2e-2
 
 
-@pytest.mark.parametrize("hd,q_heads,kv_heads,prompt_len", [(64, 8, 2, 32), (128, 4, 4, 150), (128, 8, 2, 200)])
+@pytest.mark.parametrize("hd,q_heads,kv_heads,prompt_len", [(64, 8, 2, 32), (64, 4, 4, 100), (128, 4, 4, 150),
+                                                           (128, 8, 2, 200), (128, 8, 2, 32)])
 def test_lockstep_wide_bf16_tcgen05_planted(hd, q_heads, kv_heads, prompt_len):
     """Wider models so every GEMM spans several 128-row tiles and k-blocks of the
     tcgen05 GEMM, and the tcgen05 tree attention (hd 64/128, MHA and GQA) runs
