@@ -109,75 +109,103 @@ class ClockSampler:
 # CPU oracle baseline (test infrastructure; the only other place bench.py runs oracle/)
 # ---------------------------------------------------------------------------
 
-def oracle_sample(cfg_name, seed, layers=2, prompt_len=16, steps=1):
-    """Time the oracle (as it stands) on a bounded sample of the workload: the
-    config's real widths with `layers` decoder layers, a short prompt, `steps`
-    steps. Returns dict with per-step seconds split into the layer-proportional
-    verify part and the rest, and the 32-layer (L) extrapolation."""
-    from synth import get_config, prompts
-    from oracle.model import Model
-    from oracle.table import TokenInfoTable
-    from oracle.engine import Engine
-    from threadpoolctl import threadpool_info
+class OracleRunner:
+    """The oracle (as it stands: numpy float64, all host cores) on a bounded
+    sample of the workload: the config's real widths with `layers` decoder
+    layers (verify time scaled to the full depth), a short prompt, 1 request.
+    Model construction and prefill are set-up, not timed."""
 
-    cfg = get_config(cfg_name)
-    m = Model(cfg, seed=seed, precision="bf16", layers=layers)
-    from synth import vocab_permutation
-    perm = vocab_permutation(cfg.vocab, 0) if cfg.hot_tokens else None
-    e = Engine(m, TokenInfoTable(m, hot_tokens=cfg.hot_tokens, perm=perm), cfg, seed=seed)
-    t_verify = [0.0]
-    orig = e.verify
+    def __init__(self, cfg_name, seed, layers=2, prompt_len=16):
+        from synth import get_config, prompts, vocab_permutation
+        from oracle.model import Model
+        from oracle.table import TokenInfoTable
+        from oracle.engine import Engine
+        self.cfg = get_config(cfg_name)
+        self.layers, self.prompt_len = layers, prompt_len
+        m = Model(self.cfg, seed=seed, precision="bf16", layers=layers)
+        perm = vocab_permutation(self.cfg.vocab, 0) if self.cfg.hot_tokens else None
+        self.e = Engine(m, TokenInfoTable(m, hot_tokens=self.cfg.hot_tokens, perm=perm), self.cfg, seed=seed)
+        self.t_verify = 0.0
+        orig = self.e.verify
 
-    def timed_verify(q, lin):
+        def timed_verify(q, lin):
+            t0 = time.perf_counter()
+            r = orig(q, lin)
+            self.t_verify += time.perf_counter() - t0
+            return r
+        self.e.verify = timed_verify
+        self.e.prefill(prompts(self.cfg, batch=1, length=prompt_len))
+
+    def step(self):
+        """-> (measured seconds, seconds extrapolated to the full depth, emitted tokens)"""
+        self.t_verify = 0.0
         t0 = time.perf_counter()
-        r = orig(q, lin)
-        t_verify[0] += time.perf_counter() - t0
-        return r
-    e.verify = timed_verify
-    pr = prompts(cfg, batch=1, length=prompt_len)
-    e.prefill(pr)
-    emitted = 0
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        emitted += sum(len(x) for x in e.step())
-    dt = time.perf_counter() - t0
-    per_step = dt / steps
-    v = t_verify[0] / steps
-    est = (per_step - v) + v * cfg.layers / layers
-    threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-    return {"per_step_s": per_step, "verify_s": v, "est_step_s": est, "emitted": emitted / steps,
-            "threads": threads, "layers": layers, "prompt_len": prompt_len, "steps": steps}
+        emitted = sum(len(x) for x in self.e.step())
+        dt = time.perf_counter() - t0
+        est = (dt - self.t_verify) + self.t_verify * self.cfg.layers / self.layers
+        return dt, est, emitted
+
+    def threads(self):
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+
+    def sample_text(self, steps):
+        c = self.cfg
+        return (f"oracle numpy float64, 1 request, {c.name} widths with {self.layers} of {c.layers} layers "
+                f"(verify time scaled x{c.layers / self.layers:g}), {self.prompt_len}-token prompt, {steps} step(s)")
 
 
 def reference_arm(args, cfg):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the oracle timed on the host cores (rank 0 only)."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    from synth import get_config
-    samples = []
+    t_setup = time.perf_counter()
+    run = OracleRunner(args.config, args.seed)
+    t_setup = time.perf_counter() - t_setup
     for _ in range(args.warmup):
-        pass  # the oracle has no warm-up effect worth timing; keep the K/W contract
-    t0 = time.perf_counter()
-    for k in range(args.steps):
-        samples.append(oracle_sample(args.config, args.seed + k, steps=1))
-    wall = time.perf_counter() - t0
-    est = float(np.mean([s["est_step_s"] for s in samples]))
-    emitted_per_step = float(np.mean([s["emitted"] for s in samples])) * cfg.batch
-    value = emitted_per_step / (est * cfg.batch) * cfg.batch / cfg.batch
-    sample = (f"oracle float64 numpy, {cfg.name} widths with 2 of {cfg.layers} layers, 16-token prompt, 1 request, "
-              f"1 step per sample; verify time scaled x{cfg.layers // 2} to {cfg.layers} layers")
-    line = {"impl": "reference", "metric": "accepted tokens/s per GPU", "value": value, "unit": "tokens/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": cfg.name, "global_batch": cfg.batch},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": samples[0]["threads"],
-                             "kind": "oracle", "sample": sample},
+        run.step()
+    est_total, meas_total, emitted = 0.0, 0.0, 0
+    for _ in range(args.steps):
+        dt, est, em = run.step()
+        est_total += est
+        meas_total += dt
+        emitted += em
+    value = emitted / est_total
+    line = {"impl": "reference", "metric": "accepted tokens/s per GPU (whole-job aggregate over N GPUs)",
+            "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": est_total / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "global_batch": cfg.batch},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": run.threads(), "kind": "oracle",
+                             "sample": run.sample_text(args.steps)},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "wall_s": wall}
+            "measured_s_per_step": meas_total / args.steps, "setup_s": t_setup}
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
+def plan_shard(n_requests: int, world: int, rank: int):
+    """Batch sharding: contiguous request blocks when the batch
+    has at least one request per rank, else independent full replicas."""
+    from synth import shard_requests
+    if n_requests >= world:
+        lo, hi = shard_requests(n_requests, world, rank)
+        return lo, hi, f"batch-shard x{world}"
+    return 0, n_requests, f"replicas x{world}"
+
+
+def reduce_over_ranks(ms: float, emitted: float, device="cpu"):
+    """(max device time over ranks, sum of emitted tokens over ranks)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms, emitted], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        tmax = t.clone(); dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone(); dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        return float(tmax[0]), float(tsum[1])
+    return ms, emitted
+
+
 def main():
     args = parse()
     from synth import get_config, prompts, shard_requests, vocab_permutation
@@ -198,13 +226,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    # batch sharding; batch < world -> independent replicas
-    if cfg.batch >= world:
-        lo, hi = shard_requests(cfg.batch, world, rank)
-        parallel = f"batch-shard x{world}"
-    else:
-        lo, hi = 0, cfg.batch
-        parallel = f"replicas x{world}"
+    lo, hi, parallel = plan_shard(cfg.batch, world, rank)
     b = hi - lo
     N = cfg.steps_N
     max_ctx = cfg.prompt_len + (args.warmup + args.steps + 12) * (N + 1) + 16
@@ -246,13 +268,7 @@ def main():
     launches = ctx.kernel_launches() - launches0
     ctx.sync()
     emitted = int(d_n[args.warmup:].sum().item())
-    t = torch.tensor([ms, float(emitted)], dtype=torch.float64, device=f"cuda:{local}")
-    if world > 1:
-        tmax = t.clone(); dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tsum = t.clone(); dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        ms_max, emitted_all = float(tmax[0]), float(tsum[1])
-    else:
-        ms_max, emitted_all = ms, float(emitted)
+    ms_max, emitted_all = reduce_over_ranks(ms, float(emitted), device=f"cuda:{local}")
     value = emitted_all / (ms_max / 1e3)
 
     # ---- profiled pass (eager, CUDA events per launch on the same stream)
@@ -304,12 +320,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            s = oracle_sample(args.config, args.seed, steps=1)
-            cpu = {"value": s["emitted"] / s["est_step_s"] * 1.0, "unit": "tokens/s", "cores": s["threads"],
-                   "kind": "oracle",
-                   "sample": f"1 request, {cfg.name} widths with 2 of {cfg.layers} layers, 16-token prompt, 1 step "
-                             f"({s['per_step_s']:.1f} s measured; verify {s['verify_s']:.1f} s scaled to "
-                             f"{cfg.layers} layers -> {s['est_step_s']:.1f} s/step)"}
+            run = OracleRunner(args.config, args.seed)
+            dt, est, em = run.step()
+            cpu = {"value": em / est, "unit": "tokens/s", "cores": run.threads(), "kind": "oracle",
+                   "sample": run.sample_text(1) + f" ({dt:.1f} s measured -> {est:.1f} s/step extrapolated)"}
         except Exception as ex:  # the baseline must never break the GPU line
             cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": f"failed: {ex!r}"}

@@ -1,0 +1,76 @@
+"""Multi-process (gloo, world size 2, CPU) tests of the batch-sharded path's
+host logic: request partitioning, max-over-ranks timing / summed tokens, and
+that sharding never changes a result (random streams use GLOBAL request ids)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from synth import get_config, prompts, shard_requests
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n_req, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    lo, hi, kind = bench.plan_shard(n_req, world, rank)
+    ms = 10.0 + rank            # rank 1 is the slow one
+    emitted = float(hi - lo) * 3
+    ms_max, em_sum = bench.reduce_over_ranks(ms, emitted)
+    out[rank] = (lo, hi, kind, ms_max, em_sum)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_req", [1, 5, 64])
+def test_gloo_world2_shard_and_reduce(n_req):
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), n_req, out), nprocs=world, join=True)
+    res = [out[r] for r in range(world)]
+    assert all(r[3] == 11.0 for r in res)                      # max over ranks
+    if n_req >= world:
+        covered = sorted(i for lo, hi, *_ in res for i in range(lo, hi))
+        assert covered == list(range(n_req))                   # a partition
+        assert all(r[2] == "batch-shard x2" for r in res)
+        assert all(r[4] == 3.0 * n_req for r in res)
+    else:
+        assert all((r[0], r[1]) == (0, n_req) and r[2] == "replicas x2" for r in res)
+
+
+def test_shard_requests_balanced():
+    for n in range(1, 70):
+        for w in (1, 2, 4, 8):
+            spans = [shard_requests(n, w, r) for r in range(w)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(w - 1))
+            sizes = [hi - lo for lo, hi in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_sharding_invariance_of_the_stochastic_method():
+    """The oracle on requests [0,4) in one engine == the same requests split
+    over two 'ranks' with req_offset: the Philox streams are keyed by global id."""
+    from oracle.model import Model
+    from oracle.table import TokenInfoTable
+    from oracle.engine import Engine
+    cfg = get_config("c1").replace(accept="stochastic", vocab=64, hidden=32, q_heads=2, kv_heads=1,
+                                   head_dim=16, ffn=64, layers=1, prompt_len=8, max_new=10)
+    m = Model(cfg, seed=2)
+    pr = prompts(cfg, batch=4, length=8)
+    whole = Engine(m, TokenInfoTable(m), cfg, seed=5).decode(pr, 10)
+    parts = []
+    for lo, hi in (shard_requests(4, 2, 0), shard_requests(4, 2, 1)):
+        parts += Engine(m, TokenInfoTable(m), cfg, seed=5, req_offset=lo).decode(pr[lo:hi], 10)
+    assert whole == parts
