@@ -96,3 +96,22 @@ def round_bf16(x: np.ndarray) -> np.ndarray:
     lsb = (b >> np.uint64(16)) & np.uint64(1)
     r = ((b + np.uint64(0x7FFF) + lsb) >> np.uint64(16)) << np.uint64(16)
     return (r & np.uint64(0xFFFFFFFF)).astype(np.uint32).view(np.float32)
+
+
+def uniform_rows(seed: int, tensor_id: int, cols: int, scale: np.float32, rows, precision="fp32") -> np.ndarray:
+    """Rows `rows` of the [*, cols] weight tensor (seed, tensor_id), without
+    generating the rest: element (r, c) is stream word r*cols + c. Same
+    arithmetic as uniform_weights (R23); float64 result."""
+    out = np.empty((len(rows), cols), dtype=np.float64)
+    for i, r in enumerate(rows):
+        e0 = int(r) * cols
+        b0, b1 = e0 // 4, (e0 + cols + 3) // 4
+        idx = np.arange(b0, b1, dtype=np.uint64)
+        w = np.stack(philox4x32_10(idx & MASK, idx >> np.uint64(32), 0, 0, seed & 0xFFFFFFFF, tensor_id),
+                     axis=1).reshape(-1)[e0 - 4 * b0: e0 - 4 * b0 + cols]
+        u = (w >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -24)
+        x = (np.float32(scale) * (np.float32(2.0) * u - np.float32(1.0))).astype(np.float32)
+        if precision == "bf16":
+            x = round_bf16(x)
+        out[i] = x.astype(np.float64)
+    return out

@@ -522,6 +522,7 @@ static std::string check_config(const hsd_config* c) {
   if (c->branch_k > c->vocab) return "k > |V| (contract violation)";
   if (c->budget_B < 1) return "budget_B must be >= 1 (contract violation: B < 1)";
   if (c->resample_budget_Br < 0 || c->resample_threshold_r < 0) return "B_r and r must be >= 0";
+  if (c->resample_budget_Br + 1 > 64) return "B_r + 1 must be <= 64 (pending-tree capacity)";
   long cand = 1 + c->branch_k + (long)(c->steps_N - 1) * c->branch_k * c->branch_k;
   if (cand > MAXN_TREE) return "1 + k + (N-1)k^2 candidate nodes exceed the device tree capacity (256)";
   if (c->budget_B + c->resample_budget_Br + 1 > MAXN_TREE) return "B + B_r + 1 exceeds 256 verify slots";

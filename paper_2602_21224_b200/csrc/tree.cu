@@ -84,12 +84,26 @@ HSD_DEV void vocab_pass(const float* __restrict__ Lrow, const TT* __restrict__ b
   float m = -INFINITY, s = 0.f;
   Top t;
   top_init(t);
-  for (int j = lo + threadIdx.x; j < hi; j += NT) {
-    float v = Lrow[j];
-    if (bias != nullptr && j < Vh) v += to_f32(bias[j]);
-    if (v > m) { s = s * expf(m - v) + 1.f; m = v; }
-    else s += expf(v - m);
-    top_insert(t, v, j, perm);
+  // issue U loads of the logit row and U of the table row before using any
+  // (the table row streams from HBM: one round trip per U elements, not per element)
+  constexpr int U = 4;
+  for (int base = lo + threadIdx.x; base < hi; base += NT * U) {
+    float lv[U], bv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = base + u * NT;
+      lv[u] = j < hi ? Lrow[j] : 0.f;
+      bv[u] = (bias != nullptr && j < hi && j < Vh) ? to_f32(bias[j]) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = base + u * NT;
+      if (j >= hi) break;
+      const float v = lv[u] + bv[u];
+      if (v > m) { s = s * expf(m - v) + 1.f; m = v; }
+      else s += expf(v - m);
+      top_insert(t, v, j, perm);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -200,31 +214,29 @@ HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, in
     }
     cluster.sync();
     if (rank == 0) {
-      const int start = nd.n;
-      // one thread per frontier node: merge the CL partials, append k children
-      if (threadIdx.x < cs.nq) {
-        const int qi = threadIdx.x, u = cs.Q[qi];
-        float M = -INFINITY;
-        for (int c = 0; c < CL; ++c) M = fmaxf(M, cs.part[qi][c].m);
-        float S = 0.f;
-        for (int c = 0; c < CL; ++c)
-          if (cs.part[qi][c].m != -INFINITY) S += cs.part[qi][c].s * expf(cs.part[qi][c].m - M);
-        const float lse = M + logf(S);
-        int hd[CL];
-        for (int c = 0; c < CL; ++c) hd[c] = 0;
-        for (int r = 0; r < P.k; ++r) {
-          int bc = -1;
-          for (int c = 0; c < CL; ++c) {
-            if (hd[c] >= P.k) continue;
-            const float v = cs.part[qi][c].v[hd[c]];
-            const int j = cs.part[qi][c].j[hd[c]];
-            if (j < 0) continue;
-            if (bc < 0 || better_j(v, j, cs.part[qi][bc].v[hd[bc]], cs.part[qi][bc].j[hd[bc]], P.perm)) bc = c;
+      const int start = nd.n, nq = cs.nq, K = P.k;
+      // (a) per frontier node qi, rank each of its CL*k partial candidates among
+      //     the others (value desc, token asc; ties impossible: distinct tokens);
+      //     the candidate of rank r < k becomes child r of node qi.
+      for (int t = threadIdx.x; t < nq * CL * KMAX; t += blockDim.x) {
+        const int qi = t / (CL * KMAX), c = (t / KMAX) % CL, e = t % KMAX;
+        if (e >= K) continue;
+        const float v = cs.part[qi][c].v[e];
+        const int j = cs.part[qi][c].j[e];
+        if (j < 0) continue;
+        int rnk = 0;
+        for (int c2 = 0; c2 < CL; ++c2)
+          for (int e2 = 0; e2 < K; ++e2) {
+            const int j2 = cs.part[qi][c2].j[e2];
+            if (j2 >= 0 && better_j(cs.part[qi][c2].v[e2], j2, v, j, P.perm)) ++rnk;
           }
-          const int n = start + qi * P.k + r;
-          const float v = cs.part[qi][bc].v[hd[bc]];
-          const int j = cs.part[qi][bc].j[hd[bc]];
-          hd[bc]++;
+        if (rnk < K) {
+          float M = -INFINITY, S = 0.f;
+          for (int c2 = 0; c2 < CL; ++c2) M = fmaxf(M, cs.part[qi][c2].m);
+          for (int c2 = 0; c2 < CL; ++c2)
+            if (cs.part[qi][c2].m != -INFINITY) S += cs.part[qi][c2].s * expf(cs.part[qi][c2].m - M);
+          const float lse = M + logf(S);
+          const int u = cs.Q[qi], n = start + qi * K + rnk;
           nd.tok[n] = P.perm ? P.perm[j] : j;
           nd.par[n] = u;
           nd.depth[n] = nd.depth[u] + 1;
@@ -232,28 +244,26 @@ HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, in
         }
       }
       __syncthreads();
-      // TopkByJointProb(Q_next, k): joint desc, token asc, parent creation index asc
-      if (threadIdx.x == 0) {
-        const int cnt_new = cs.nq * P.k;
-        nd.n = start + cnt_new;
-        int cnt = 0;
-        bool used[KMAX * KMAX];
-        for (int c = 0; c < cnt_new; ++c) used[c] = false;
-        for (int r = 0; r < P.k && r < cnt_new; ++r) {
-          int best = -1;
-          for (int c = start; c < nd.n; ++c) {
-            if (used[c - start]) continue;
-            if (best < 0 || nd.lj[c] > nd.lj[best] ||
-                (nd.lj[c] == nd.lj[best] &&
-                 (nd.tok[c] < nd.tok[best] || (nd.tok[c] == nd.tok[best] && nd.par[c] < nd.par[best]))))
-              best = c;
-          }
-          used[best - start] = true;
-          cs.Q[cnt] = best;
-          cs.Qtok[cnt] = nd.tok[best];
-          cnt++;
+      // (b) TopkByJointProb(Q_next, k): every candidate computes its rank under
+      //     (joint desc, token asc, parent creation index asc) in parallel.
+      const int cnt_new = nq * K;
+      __shared__ int newQ[KMAX];
+      for (int c = threadIdx.x; c < cnt_new; c += blockDim.x) {
+        const int a = start + c;
+        int rnk = 0;
+        for (int b = start; b < start + cnt_new; ++b) {
+          const bool bb = nd.lj[b] > nd.lj[a] ||
+                          (nd.lj[b] == nd.lj[a] &&
+                           (nd.tok[b] < nd.tok[a] || (nd.tok[b] == nd.tok[a] && nd.par[b] < nd.par[a])));
+          rnk += bb;
         }
-        cs.nq = cnt;
+        if (rnk < K) newQ[rnk] = a;
+      }
+      __syncthreads();
+      if (threadIdx.x < KMAX) {
+        const int q = threadIdx.x;
+        if (q < K && q < cnt_new) { cs.Q[q] = newQ[q]; cs.Qtok[q] = nd.tok[newQ[q]]; }
+        if (q == 0) { nd.n = start + cnt_new; cs.nq = K < cnt_new ? K : cnt_new; }
       }
       __syncthreads();
     }
@@ -264,41 +274,51 @@ HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, in
 // keep the top-`keep` non-root nodes (joint desc, depth asc, token asc, parent asc),
 // compacted in creation order.
 HSD_DEV void prune_nodes(NodesSm& nd, int keep, NodesSm& tmp) {
-  __shared__ int flag[MAXN], newidx[MAXN];
-  int n = nd.n;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    int f = 1;
-    if (i > 0) {
-      int c = 0;
-      for (int j = 1; j < n; ++j) {
-        bool less = nd.lj[j] > nd.lj[i] ||
-                    (nd.lj[j] == nd.lj[i] &&
-                     (nd.depth[j] < nd.depth[i] ||
-                      (nd.depth[j] == nd.depth[i] &&
-                       (nd.tok[j] < nd.tok[i] || (nd.tok[j] == nd.tok[i] && nd.par[j] < nd.par[i])))));
-        c += less;
+  __shared__ int flag[MAXN], newidx[MAXN], wsum[MAXN / 32];
+  const int n = nd.n;
+  // rank of node i among non-root nodes: 4 threads per node, each a quarter of j
+  for (int t = threadIdx.x; t < 4 * MAXN; t += blockDim.x) {
+    const int i = t >> 2, part = t & 3;
+    int c = 0;
+    if (i > 0 && i < n) {
+      const float li = nd.lj[i];
+      const int di = nd.depth[i], ti = nd.tok[i], pi = nd.par[i];
+      for (int j = 1 + part; j < n; j += 4) {
+        const float lj = nd.lj[j];
+        c += lj > li || (lj == li && (nd.depth[j] < di ||
+                                      (nd.depth[j] == di && (nd.tok[j] < ti || (nd.tok[j] == ti && nd.par[j] < pi)))));
       }
-      f = c < keep;
     }
-    flag[i] = f;
+    c += __shfl_xor_sync(0xffffffffu, c, 1);
+    c += __shfl_xor_sync(0xffffffffu, c, 2);
+    if (part == 0 && i < MAXN) flag[i] = (i < n) && (i == 0 || c < keep);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int c = 0;
-    for (int i = 0; i < n; ++i) { newidx[i] = flag[i] ? c : -1; c += flag[i]; }
-    tmp.n = c;
+  // exclusive prefix sum of flags (creation order preserved)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x < MAXN) {
+    const unsigned b = __ballot_sync(0xffffffffu, flag[threadIdx.x]);
+    if (lane == 0) wsum[w] = __popc(b);
+  }
+  __syncthreads();
+  if (threadIdx.x < MAXN) {
+    const unsigned b = __ballot_sync(0xffffffffu, flag[threadIdx.x]);
+    int off = 0;
+    for (int q = 0; q < w; ++q) off += wsum[q];
+    newidx[threadIdx.x] = flag[threadIdx.x] ? off + __popc(b & ((1u << lane) - 1u)) : -1;
+    if (threadIdx.x == MAXN - 1) tmp.n = off + __popc(b);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     if (!flag[i]) continue;
-    int t = newidx[i];
+    const int t = newidx[i];
     tmp.tok[t] = nd.tok[i];
     tmp.par[t] = nd.par[i] >= 0 ? newidx[nd.par[i]] : -1;
     tmp.depth[t] = nd.depth[i];
     tmp.lj[t] = nd.lj[i];
   }
   __syncthreads();
-  int n2 = tmp.n;
+  const int n2 = tmp.n;
   for (int i = threadIdx.x; i < n2; i += blockDim.x) {
     nd.tok[i] = tmp.tok[i]; nd.par[i] = tmp.par[i]; nd.depth[i] = tmp.depth[i]; nd.lj[i] = tmp.lj[i];
   }
@@ -354,66 +374,84 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(Tre
   // ---- verification fusion with the pending re-sampled tree
   int pn = P.pt_n[req];
   if (P.fusion && pn > 1) {
-    if (threadIdx.x == 0) {
-      int map[MAXN];
-      if (P.pt_tok[req * Br1] != root) atomicOr(P.err, DEV_ERR_BAD_TREE);
+    if (threadIdx.x < 32) {            // warp 0: pending nodes in creation order, lanes search
+      const int lane = threadIdx.x;
+      int map[HSD_MAX_BR1];
+      if (lane == 0 && P.pt_tok[req * Br1] != root) atomicOr(P.err, DEV_ERR_BAD_TREE);
       map[0] = 0;
-      for (int j = 1; j < pn && j < MAXN; ++j) {
-        int ptok = P.pt_tok[req * Br1 + j];
-        int fpar = map[P.pt_par[req * Br1 + j]];
-        float plj = P.pt_lj[req * Br1 + j];
-        int hit = -1;
-        for (int i = 1; i < nd.n; ++i)
-          if (nd.par[i] == fpar && nd.tok[i] == ptok) { hit = i; break; }
-        if (hit >= 0) {
-          if (plj > nd.lj[hit]) nd.lj[hit] = plj;
+      for (int j = 1; j < pn && j < HSD_MAX_BR1; ++j) {
+        const int ptok = P.pt_tok[req * Br1 + j];
+        const int fpar = map[P.pt_par[req * Br1 + j]];
+        const float plj = P.pt_lj[req * Br1 + j];
+        const int nn = nd.n;
+        int hit = 0x7fffffff;
+        for (int i = 1 + lane; i < nn; i += 32)
+          if (nd.par[i] == fpar && nd.tok[i] == ptok) hit = min(hit, i);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) hit = min(hit, __shfl_xor_sync(0xffffffffu, hit, o));
+        if (hit != 0x7fffffff) {
+          if (lane == 0 && plj > nd.lj[hit]) nd.lj[hit] = plj;
           map[j] = hit;
-        } else if (nd.n < MAXN) {
-          int n = nd.n;
-          nd.tok[n] = ptok; nd.par[n] = fpar; nd.depth[n] = nd.depth[fpar] + 1; nd.lj[n] = plj;
-          map[j] = n;
-          nd.n = n + 1;
+        } else {
+          if (lane == 0 && nn < MAXN) {
+            nd.tok[nn] = ptok; nd.par[nn] = fpar; nd.depth[nn] = nd.depth[fpar] + 1; nd.lj[nn] = plj;
+            nd.n = nn + 1;
+          }
+          map[j] = nn < MAXN ? nn : 0;
         }
+        __syncwarp();
       }
     }
     __syncthreads();
     prune_nodes(nd, P.B + P.Br, tmp);
   }
-  // ---- linearise: BFS, siblings by (joint desc, token asc); level by level
+  // ---- linearise: BFS, siblings by (joint desc, token asc); nodes bucketed by
+  //      depth, each ranked only among its own depth's bucket
   const int n = nd.n;
+  __shared__ int dcnt[HSD_MAX_PLANT_DEPTH_DEV + 2], doff[HSD_MAX_PLANT_DEPTH_DEV + 2], bucket[MAXN];
+  if (threadIdx.x < HSD_MAX_PLANT_DEPTH_DEV + 2) dcnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&dcnt[nd.depth[i]], 1);
+  __syncthreads();
   if (threadIdx.x == 0) {
-    int md = 0;
-    for (int i = 0; i < n; ++i) md = max(md, nd.depth[i]);
+    int acc = 0, md = 0;
+    for (int d = 0; d < HSD_MAX_PLANT_DEPTH_DEV + 2; ++d) {
+      doff[d] = acc;
+      acc += dcnt[d];
+      if (dcnt[d]) md = d;
+      dcnt[d] = 0;
+    }
     maxdepth = md;
     slot_of[0] = 0;
     for (int w = 0; w < MAXW; ++w) anc[0][w] = 0ull;
     anc[0][0] = 1ull;
   }
   __syncthreads();
-  int offset = 1;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int d = nd.depth[i];
+    bucket[doff[d] + atomicAdd(&dcnt[d], 1)] = i;
+  }
+  __syncthreads();
   for (int d = 1; d <= maxdepth; ++d) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      if (nd.depth[i] != d) continue;
+    const int b0 = doff[d], nb = dcnt[d];
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+      const int i = bucket[b0 + t];
+      const int pi = slot_of[nd.par[i]];
       int c = 0;
-      int pi = slot_of[nd.par[i]];
-      for (int j = 0; j < n; ++j) {
-        if (nd.depth[j] != d) continue;
-        int pj = slot_of[nd.par[j]];
-        bool less = pj < pi || (pj == pi && (nd.lj[j] > nd.lj[i] || (nd.lj[j] == nd.lj[i] && nd.tok[j] < nd.tok[i])));
-        c += less;
+      for (int u = 0; u < nb; ++u) {
+        const int j = bucket[b0 + u];
+        const int pj = slot_of[nd.par[j]];
+        c += pj < pi || (pj == pi && (nd.lj[j] > nd.lj[i] || (nd.lj[j] == nd.lj[i] && nd.tok[j] < nd.tok[i])));
       }
-      slot_of[i] = offset + c;
+      slot_of[i] = b0 + c;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      if (nd.depth[i] != d) continue;
-      int s = slot_of[i], ps = slot_of[nd.par[i]];
-      for (int w = 0; w < MAXW; ++w) anc[s][w] = anc[ps][w];
-      anc[s][s >> 6] |= 1ull << (s & 63);
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+      const int i = bucket[b0 + t];
+      const int sl = slot_of[i], ps = slot_of[nd.par[i]];
+      for (int w = 0; w < MAXW; ++w) anc[sl][w] = anc[ps][w];
+      anc[sl][sl >> 6] |= 1ull << (sl & 63);
     }
-    int cnt = 0;
-    for (int i = 0; i < n; ++i) cnt += nd.depth[i] == d;
-    offset += cnt;
     __syncthreads();
   }
   // ---- write the linearised tree

@@ -3,6 +3,7 @@
 #include "common.cuh"
 
 #define HSD_MAX_PLANT_DEPTH_DEV 16
+#define HSD_MAX_BR1 64     // B_r + 1 capacity of the pending tree (host-checked)
 enum { TREE_MODE_FRESH = 0, TREE_MODE_RESAMPLE = 1 };
 
 struct TreeParams {

@@ -230,9 +230,13 @@ class Context:
     def kernel_launches(self) -> int:
         return int(self.lib.hsd_kernel_launches(self.h))
 
-    def tensor(self, name):
-        """Zero-copy torch view of a named device tensor (hsd_get_tensor)."""
+    def tensor(self, name, sync=True):
+        """Zero-copy torch view of a named device tensor (hsd_get_tensor). By
+        default the context stream is synchronised first, so the view is not read
+        (e.g. by .cpu() on torch's current stream) while kernels still write it."""
         import torch
+        if sync:
+            self.sync()
         t = Tensor()
         self._check(self.lib.hsd_get_tensor(self.h, name.encode(), C.byref(t)))
         shape = [t.dims[i] for i in range(t.ndim)]

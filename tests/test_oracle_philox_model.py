@@ -131,3 +131,12 @@ def test_stochastic_engine_runs_and_is_reproducible():
     c = Engine(m, TokenInfoTable(m), cfg, seed=4).decode(pr, 12)
     assert a == b and a != c
     assert all(0 <= t < cfg.vocab for t in a[0])
+
+
+def test_uniform_rows_equals_full_tensor_rows():
+    from oracle.philox import uniform_rows
+    full = uniform_weights(3, 9, (37, 23), linear_scale(23))
+    rows = [0, 5, 36, 17]
+    np.testing.assert_array_equal(uniform_rows(3, 9, 23, linear_scale(23), rows), full[rows].astype(np.float64))
+    fb = round_bf16(full)
+    np.testing.assert_array_equal(uniform_rows(3, 9, 23, linear_scale(23), rows, "bf16"), fb[rows].astype(np.float64))
