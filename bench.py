@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--simt", action="store_true", help="disable tcgen05 GEMMs (SIMT FFMA baseline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (profiling runs)")
     ap.add_argument("--batch", type=int, default=None, help="override the config's global batch")
     return ap.parse_args()
 
@@ -304,7 +305,7 @@ def main():
 
     # ---- e2e: prefill from HOST prompts + K steps with host outputs (public API)
     e2e = None
-    if rank == 0 or world > 1:
+    if not args.no_e2e:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ctx.prefill(pr)

@@ -183,7 +183,11 @@ hsd_status hsd_profile_read(hsd_ctx* ctx, const char* category, double* total_ms
 /* Test hook: one GEMM of the library, C[M,N] (+)= A[M,K] W[N,K]^T, DEVICE
  * pointers, row-major with leading dimensions lda/ldw/ldc (elements).
  * dtype 0 = fp32 operands (SIMT FFMA kernel), 1 = bf16 operands; use_tc = 1
- * selects the tcgen05 kernel (bf16 only). C is fp32. Asynchronous on `stream`.
+ * selects the tcgen05 kernel (bf16 only); use_tc = 2 the data-parallel tcgen05
+ * kernel with SwiGLU fused in the epilogue (W rows gate/up interleaved in 64-row
+ * groups; C is then a bf16 [M, N/2] output with leading dimension ldc; only for
+ * shapes with >= 4 output tiles per SM, else HSD_EUNSUP). Otherwise C is fp32.
+ * Asynchronous on `stream`.
  * Returns HSD_EUNSUP if use_tc is requested for an unsupported shape.        */
 hsd_status hsd_debug_gemm(const void* A, int32_t lda, const void* W, int32_t ldw, float* C, int32_t ldc,
                           int32_t M, int32_t N, int32_t K, int32_t accumulate, int32_t dtype, int32_t use_tc,

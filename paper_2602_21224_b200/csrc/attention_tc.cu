@@ -27,7 +27,8 @@ namespace {
 using namespace tc;
 constexpr int NTHREADS = 320;   // TMA, MMA, 8 softmax warps
 constexpr int PAGE = 64;
-constexpr int STAGES = 3;
+constexpr int CHUNK = 128;     // keys per softmax iteration = 2 pages
+constexpr int STAGES = 2;
 constexpr int QROWS = 128;
 
 struct AttnParams {
@@ -87,14 +88,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int hd = P.hd, natom = hd / 64;
   const int q_bytes = QROWS * hd * 2;          // natom atoms of [128 rows x 128 B]
-  const int k_bytes = PAGE * hd * 2;           // natom atoms of [64 keys x 128 B]
-  const int v_bytes = hd * PAGE * 2;           // one atom column of [hd rows x 128 B]
-  const int p_bytes = QROWS * PAGE * 2;        // [128 rows x 128 B]
+  const int k_bytes = CHUNK * hd * 2;          // natom atoms of [128 keys x 128 B] (2 pages each)
+  const int v_bytes = hd * CHUNK * 2;          // 2 atom columns (pages) of [hd rows x 128 B]
+  const int p_bytes = QROWS * CHUNK * 2;       // 2 atoms (key halves) of [128 rows x 128 B]
   uint8_t* sQ = base;
   uint8_t* sK = sQ + q_bytes;
   uint8_t* sV = sK + STAGES * k_bytes;
   uint8_t* sP = sV + STAGES * v_bytes;
-  uint64_t* bars = (uint64_t*)(sP + 2 * p_bytes);
+  uint64_t* bars = (uint64_t*)(sP + p_bytes);   // one P buffer: its reuse is ordered by pvdone
   uint64_t* full = bars;                 // [STAGES]
   uint64_t* empty = bars + STAGES;       // [STAGES]
   uint64_t* qbar = bars + 2 * STAGES;
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(256)
+                 "r"(512)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -162,10 +163,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   fence_after();
   const uint32_t tmem = *tmem_slot;
   const int lo = max(k_begin, tile_lo), hi = min(k_end, tile_hi);
-  const int c_first = lo / PAGE;
-  const int n_chunks = hi > lo ? (hi + PAGE - 1) / PAGE - c_first : 0;
-  const uint32_t tS = tmem;              // 2 x 64 columns
-  const uint32_t tO = tmem + 128;        // hd columns
+  const int c_first = lo / CHUNK;
+  const int n_chunks = hi > lo ? (hi + CHUNK - 1) / CHUNK - c_first : 0;
+  const uint32_t tS = tmem;              // 2 x 128 columns (double-buffered scores)
+  const uint32_t tO = tmem + 256;        // hd columns
 
   if (warp == 0) {
     if (lane == 0 && n_chunks > 0) {
@@ -181,13 +182,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int s = j % STAGES;
         const uint32_t ph = (j / STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
-        const int page = P.kv.block_table[(size_t)req * P.kv.pages_per_req + c_first + j];
         mbar_expect_tx(&full[s], k_bytes + v_bytes);
-        const int krow = ((page * 2 + 0) * P.kv.kv_heads + h) * PAGE;
-        for (int a = 0; a < natom; ++a)
-          tma_load_2d(&tmK, &full[s], sK + (size_t)s * k_bytes + a * (PAGE * 128), a * 64, krow, pol);
-        const int vrow = ((page * 2 + 1) * P.kv.kv_heads + h) * hd;
-        tma_load_2d(&tmV, &full[s], sV + (size_t)s * v_bytes, 0, vrow, pol);
+        for (int pg = 0; pg < 2; ++pg) {
+          const int page = P.kv.block_table[(size_t)req * P.kv.pages_per_req + 2 * (c_first + j) + pg];
+          const int krow = ((page * 2 + 0) * P.kv.kv_heads + h) * PAGE;
+          for (int a = 0; a < natom; ++a)
+            tma_load_2d(&tmK, &full[s], sK + (size_t)s * k_bytes + a * (CHUNK * 128) + pg * (PAGE * 128), a * 64,
+                        krow, pol);
+          const int vrow = ((page * 2 + 1) * P.kv.kv_heads + h) * hd;
+          tma_load_2d(&tmV, &full[s], sV + (size_t)s * v_bytes + pg * (hd * 128), 0, vrow, pol);
+        }
       }
     }
   } else if (warp == 1) {
@@ -197,11 +201,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int s = j % STAGES;
         mbar_wait(&full[s], (j / STAGES) & 1);
         fence_after();
-        const uint32_t d = tS + (uint32_t)((j & 1) * 64);
+        const uint32_t d = tS + (uint32_t)((j & 1) * CHUNK);
         for (int kk = 0; kk < hd / 16; ++kk) {
           const int a = kk >> 2, off = kk & 3;
           const uint64_t ad = desc_sw128(sQ + a * (QROWS * 128)) + 2 * off;
-          const uint64_t bd = desc_sw128(sK + (size_t)s * k_bytes + a * (PAGE * 128)) + 2 * off;
+          const uint64_t bd = desc_sw128(sK + (size_t)s * k_bytes + a * (CHUNK * 128)) + 2 * off;
           mma_bf16(d, ad, bd, P.idesc_s, kk > 0 ? 1u : 0u);
         }
         mma_commit(&sfull[j & 1]);
@@ -212,10 +216,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_wait(&pfull[j & 1], (j >> 1) & 1);
         fence_after();
         const int s = j % STAGES;
-        const uint64_t pd0 = desc_sw128(sP + (j & 1) * p_bytes);
-        const uint64_t vd0 = desc_sw128(sV + (size_t)s * v_bytes);
-        for (int kk = 0; kk < PAGE / 16; ++kk)
-          mma_bf16(tO, pd0 + 2 * kk, vd0 + 2 * kk, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < CHUNK / 16; ++kk) {
+          const int ka = kk >> 2, off = kk & 3;
+          const uint64_t pd = desc_sw128(sP + ka * (QROWS * 128)) + 2 * off;
+          const uint64_t vd = desc_sw128(sV + (size_t)s * v_bytes + ka * (hd * 128)) + 2 * off;
+          mma_bf16(tO, pd, vd, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
         mma_commit(&empty[s]);
         mma_commit(pvdone);
       }
@@ -230,21 +236,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int j = 0; j < n_chunks; ++j) {
       mbar_wait(&sfull[j & 1], (j >> 1) & 1);
       fence_after();
-      const int kb = (c_first + j) * PAGE + half * 32;
-      uint32_t r[32];
-      tmem_ld32(tS + lane_off + (uint32_t)((j & 1) * 64 + half * 32), r);
-      uint32_t vm = 0u;
+      const int kb = (c_first + j) * CHUNK + half * 64;       // this half's 64 keys
+      uint32_t r0[32], r1[32];
+      tmem_ld32(tS + lane_off + (uint32_t)((j & 1) * CHUNK + half * 64), r0);
+      tmem_ld32(tS + lane_off + (uint32_t)((j & 1) * CHUNK + half * 64 + 32), r1);
+      uint32_t vm0 = 0u, vm1 = 0u;
       if (valid) {
-        vm = range32(klo - kb, khi - kb);
-        if (slot >= 0) vm |= anc32(anc, kb - tb) & range32(0, m.t_max - (kb - tb));
-        vm &= range32(k_begin - kb, k_end - kb);
+        vm0 = range32(klo - kb, khi - kb);
+        vm1 = range32(klo - kb - 32, khi - kb - 32);
+        if (slot >= 0) {
+          vm0 |= anc32(anc, kb - tb) & range32(0, m.t_max - (kb - tb));
+          vm1 |= anc32(anc, kb + 32 - tb) & range32(0, m.t_max - (kb + 32 - tb));
+        }
+        vm0 &= range32(k_begin - kb, k_end - kb);
+        vm1 &= range32(k_begin - kb - 32, k_end - kb - 32);
       }
-      float s[32];
+      float s[64];
       float mx = -INFINITY;
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        s[i] = ((vm >> i) & 1u) ? __uint_as_float(r[i]) * scale_log2 : -INFINITY;
-        mx = fmaxf(mx, s[i]);
+        s[i] = ((vm0 >> i) & 1u) ? __uint_as_float(r0[i]) * scale_log2 : -INFINITY;
+        s[32 + i] = ((vm1 >> i) & 1u) ? __uint_as_float(r1[i]) * scale_log2 : -INFINITY;
+        mx = fmaxf(mx, fmaxf(s[i], s[32 + i]));
       }
       red_max[j & 1][half][lane_row] = mx;
       pair_sync(q4);
@@ -254,7 +267,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // nothing visible yet for this row: P must be exactly 0 (not ex2(-inf+inf) = NaN)
       const float msub = mnew == -INFINITY ? 0.f : mnew;
       if (j > 0) {
-        mbar_wait(pvdone, (j - 1) & 1);   // O (and the P buffer being reused) are free
+        mbar_wait(pvdone, (j - 1) & 1);   // O and the P buffer are free
         fence_after();
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
           for (int c = 0; c < hcols; c += 16) {
@@ -268,9 +281,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
       float psum = 0.f;
-      uint8_t* prow = sP + (j & 1) * p_bytes + lane_row * 128;
+      uint8_t* prow = sP + half * (QROWS * 128) + lane_row * 128;    // key half = one swizzle atom
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 8; ++c) {
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -279,8 +292,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           psum += __low2float(pr) + __high2float(pr);     // l sums exactly what the MMA sees
           w[e] = *(uint32_t*)&pr;
         }
-        const int c16 = half * 4 + c;
-        *(uint4*)(prow + ((c16 ^ (lane_row & 7)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *(uint4*)(prow + ((c ^ (lane_row & 7)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
       lrow = lrow * alpha + psum;
       mrow = mnew;
@@ -327,7 +339,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   fence_before();
   __syncthreads();
   fence_after();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
 }
 
 // split merge: one warp per (row, head), lanes over hd:
@@ -378,19 +390,19 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   P.M = M; P.R = R; P.Hq = Hq; P.G = G; P.hd = hd; P.m = m; P.kv = kv;
   P.out = (bf16*)out; P.ws = ws; P.max_keys = max_keys;
   P.n_qtiles = (R * G + QROWS - 1) / QROWS;
-  P.idesc_s = idesc_bf16(128, PAGE);
+  P.idesc_s = idesc_bf16(128, CHUNK);
   P.idesc_o = idesc_bf16(128, hd);
   // splits: enough CTAs for ~2 per SM, each split a whole number of pages
   const int base_ctas = n_req * kv.kv_heads * P.n_qtiles;
-  const int pages = (max_keys + PAGE - 1) / PAGE;
-  // one wave: the kernel holds ~160 KB of shared memory, so one CTA per SM
+  const int pages = (max_keys + CHUNK - 1) / CHUNK;     // chunks of 2 pages
+  // one wave: the kernel holds ~190 KB of shared memory, so one CTA per SM
   int S = num_sms() / base_ctas;
   if (S > pages) S = pages;
   if (S > 32) S = 32;
   if (S < 1) S = 1;
   while (S > 1 && (size_t)S * M * Hq * (hd + 2) > ws_floats) --S;
   int pps = (pages + S - 1) / S;
-  P.keys_per_split = pps * PAGE;
+  P.keys_per_split = pps * CHUNK;
   S = (pages + pps - 1) / pps;
   P.direct = S == 1;
   // tensor maps: q [M][Hq][hd] viewed (hd, heads, rows) with the head offset in
@@ -408,8 +420,8 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   if (!tma_map_bf16(&mq, q, 3, dq, sq, bq) || !tma_map_bf16(&mk, kv.base, 2, dk, sk, bk) ||
       !tma_map_bf16(&mv, kv.base, 2, dv, sv, bv))
     return -1;
-  const size_t smem = 1024 + (size_t)QROWS * hd * 2 + STAGES * ((size_t)PAGE * hd * 2 * 2) + 2 * (size_t)QROWS * PAGE * 2 +
-                      (2 * STAGES + 7) * 8 + 64;
+  const size_t smem = 1024 + (size_t)QROWS * hd * 2 + STAGES * ((size_t)CHUNK * hd * 2 * 2) +
+                      (size_t)QROWS * CHUNK * 2 + (2 * STAGES + 7) * 8 + 64;
   static size_t attr = 0;   // (the kernel also has ~1 KB of static shared memory)
   if (smem > attr) {
     if (cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=

@@ -198,7 +198,7 @@ struct hsd_ctx {
   int maxb, b = 0;   // capacity, active requests
   bool use_tc = false;
   // weights
-  void *embed = nullptr, *head = nullptr, *head_rank = nullptr, *fc = nullptr;
+  void *embed = nullptr, *head = nullptr, *head_rank = nullptr, *fc = nullptr, *gu_tmp = nullptr;
   std::vector<LayerW> layers;
   LayerW draft{};
   void* table = nullptr;
@@ -226,7 +226,7 @@ struct hsd_ctx {
   int Mcap;
   float *x_d, *xw, *Hver, *chain, *big, *draft_logits, *logits, *x_p, *H_prompt, *attn_ws;
   size_t attn_ws_floats;
-  void *a, *qb, *ob;
+  void *a, *qb, *ob, *h;   // h: SwiGLU output [Mcap, f] (never aliases the GEMM input a)
   int32_t* argmax;
   MetaBuf mv, md, mc, mp;
   // host staging for e2e
@@ -386,9 +386,23 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
   }
   gemm(c, c->ob, c->qd, w.wo, c->qd, x, n, M, n, c->qd, true);
   { Prof pf(c, P_ROWWISE); launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st); }
-  gemm(c, c->a, n, w.wgu, n, c->big, 2 * c->f, M, 2 * c->f, n, false, -1, true);
-  { Prof pf(c, P_ROWWISE); launch_swiglu(c->big, M, c->f, c->a, c->dt, m.pos, c->st); }
-  gemm(c, c->a, c->f, w.wd, c->f, x, n, M, n, c->f, true);
+  bool fused = false;
+  if (c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, 2 * c->f, n, n, n) && gemm_tc_dp(M, 2 * c->f)) {
+    // data-parallel gate/up GEMM with SwiGLU in the epilogue, bf16 h straight to c->a
+    Prof pf(c, c->pass_verify ? P_GEMM_VERIFY : P_GEMM_DRAFT,
+            (double)2 * c->f * n * c->esz + (double)M * n * c->esz + (double)M * c->f * c->esz,
+            2.0 * M * 2 * c->f * n);
+    const int k = gemm_tc_swiglu_bf16((const bf16*)c->a, n, (const bf16*)w.wgu, n, (bf16*)c->h, c->f, M, 2 * c->f,
+                                      n, c->st);
+    g_hsd_launches += k;
+    fused = k > 0;
+  }
+  if (!fused) {
+    gemm(c, c->a, n, w.wgu, n, c->big, 2 * c->f, M, 2 * c->f, n, false, -1, true);
+    Prof pf(c, P_ROWWISE);
+    launch_swiglu(c->big, M, c->f, c->h, c->dt, m.pos, c->st);
+  }
+  gemm(c, c->h, c->f, w.wd, c->f, x, n, M, n, c->f, true);
   g_hsd_launches += 6;  // rmsnorm x2, rope_kv, attention(+merge counted below), swiglu
 }
 
@@ -451,7 +465,10 @@ static void stage_verify(hsd_ctx* c) {
   c->pass_verify = 0;
   launch_rmsnorm(c->Hver, M, n, c->cfg.rms_eps, c->a, c->dt, c->mv.pos, c->st);
   gemm(c, c->a, n, c->head, n, c->logits, c->V, M, c->V, n, false, P_HEAD_VERIFY);
-  { Prof pf(c, P_ROWWISE); launch_argmax_rows(c->logits, M, c->V, c->mv.pos, c->argmax, c->st); }
+  if (c->cfg.accept_mode == HSD_GREEDY) {   // the stochastic walk reads the logits rows itself
+    Prof pf(c, P_ROWWISE);
+    launch_argmax_rows(c->logits, M, c->V, c->mv.pos, c->argmax, c->st);
+  }
   g_hsd_launches += 2;
 }
 
@@ -597,13 +614,24 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     launch_philox_fill((char*)w.wqkv + (size_t)(c->qd + c->kd) * n * es, c->dt, (size_t)c->kd * n, seed, tid0 + 2,
                        sc(n), c->st);
     launch_philox_fill(w.wo, c->dt, (size_t)n * c->qd, seed, tid0 + 3, sc(c->qd), c->st);
-    launch_philox_fill(w.wgu, c->dt, (size_t)c->f * n, seed, tid0 + 4, sc(n), c->st);
-    launch_philox_fill((char*)w.wgu + (size_t)c->f * n * es, c->dt, (size_t)c->f * n, seed, tid0 + 5, sc(n), c->st);
+    // gate (tid+4) then up (tid+5) into a scratch, then interleaved in 64-row
+    // groups (see launch_swiglu / gemm_tc_swiglu_bf16)
+    launch_philox_fill(c->gu_tmp, c->dt, (size_t)c->f * n, seed, tid0 + 4, sc(n), c->st);
+    launch_philox_fill((char*)c->gu_tmp + (size_t)c->f * n * es, c->dt, (size_t)c->f * n, seed, tid0 + 5, sc(n),
+                       c->st);
+    launch_interleave_gu(c->gu_tmp, c->f, n, w.wgu, c->dt, c->st);
     launch_philox_fill(w.wd, c->dt, (size_t)n * c->f, seed, tid0 + 6, sc(c->f), c->st);
     return w;
   };
+  if (c->f % 64) { hsd_destroy(c); fprintf(stderr, "hsd_init_model: ffn must be a multiple of 64\n"); return HSD_EINVAL; }
+  c->gu_tmp = A((size_t)2 * c->f * n * es);
+  if (fail_alloc) { hsd_destroy(c); return HSD_ENOMEM; }
   for (int l = 0; l < c->L; ++l) c->layers.push_back(make_layer(100 + 8 * l));
   c->draft = make_layer(60);
+  CU(cudaStreamSynchronize(c->st));
+  cudaFree(c->gu_tmp);
+  c->allocs.erase(std::find(c->allocs.begin(), c->allocs.end(), c->gu_tmp));
+  c->gu_tmp = nullptr;
   if (fail_alloc) { hsd_destroy(c); return HSD_ENOMEM; }
   // ---- vocab permutation (hot set, R5)
   std::vector<int32_t> perm, rank;
@@ -663,6 +691,7 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
   }
   // ---- RoPE tables (host double precision)
   c->pages_per_req = (cfg->max_ctx + c->T + c->N + 8 + c->page_size - 1) / c->page_size;
+  c->pages_per_req += c->pages_per_req & 1;   // even: the tcgen05 attention reads pages in pairs
   c->max_pos = c->pages_per_req * c->page_size;
   {
     int half = c->hd / 2;
@@ -712,6 +741,7 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     c->a = A((size_t)Mc * wa * es);
     c->qb = A((size_t)Mc * c->qd * es);
     c->ob = A((size_t)Mc * c->qd * es);
+    c->h = A((size_t)Mc * c->f * es);
     c->big = F((size_t)Mc * std::max(c->qkvd, 2 * c->f));
     c->x_d = F((size_t)b * (N + 1) * n);
     c->xw = F((size_t)b * n);
@@ -1044,7 +1074,12 @@ hsd_status hsd_debug_gemm(const void* A, int32_t lda, const void* W, int32_t ldw
                           int32_t M, int32_t N, int32_t K, int32_t accumulate, int32_t dtype, int32_t use_tc,
                           void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (use_tc) {
+  if (use_tc == 2) {   // data-parallel gate/up GEMM with fused SwiGLU: C is bf16 H [M, N/2], ld = ldc
+    if (dtype != 1 || !gemm_tc_supported(M, N, K, lda, ldw)) return HSD_EUNSUP;
+    const int k = gemm_tc_swiglu_bf16((const bf16*)A, lda, (const bf16*)W, ldw, (bf16*)C, ldc, M, N, K, st);
+    if (k == 0) return HSD_EUNSUP;
+    g_hsd_launches += k;
+  } else if (use_tc) {
     if (dtype != 1 || !gemm_tc_supported(M, N, K, lda, ldw)) return HSD_EUNSUP;
     g_hsd_launches += gemm_tc_bf16((const bf16*)A, lda, (const bf16*)W, ldw, C, ldc, M, N, K, accumulate != 0, st);
   } else {

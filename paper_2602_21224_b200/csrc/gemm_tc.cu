@@ -26,6 +26,8 @@ constexpr int BM = 128;          // weight rows per tile (UMMA M)
 constexpr int BK = 64;           // K per stage (one 128-byte swizzle atom of bf16)
 constexpr int NTHREADS = 192;    // warp0 TMA, warp1 MMA, warps 2..5 epilogue
 constexpr int A_BYTES = BM * BK * 2;
+constexpr int EPI_LD = BM + 4;   // epilogue stage row stride (floats)
+enum { EPI_ATOMIC = 0, EPI_STORE = 1, EPI_ADD = 2, EPI_SWIGLU = 3 };
 
 struct TcParams {
   int M, N, K, ldc;
@@ -36,13 +38,30 @@ struct TcParams {
   uint32_t idesc;
   uint32_t tmem_cols;
   int vec4;                       // C rows 16-byte aligned (ldc % 4 == 0, C aligned)
+  int dp;                         // 1: data-parallel (a CTA owns whole tiles), 0: stream-K
+  int epi;                        // GemmEpi
   float* C;
+  bf16* H;                        // EPI_SWIGLU output [M, N/2] bf16
+  int ldh;
 };
+
+// The idx-th (tile, k-block) unit of this CTA. Stream-K: a contiguous range of
+// units; data-parallel: whole tiles blockIdx.x, blockIdx.x + grid, ...
+struct Sched {
+  long u0, count;
+  int dp, n_kb;
+  HSD_DEV long unit(long i) const {
+    if (!dp) return u0 + i;
+    return ((long)blockIdx.x + (i / n_kb) * (long)gridDim.x) * n_kb + i % n_kb;
+  }
+};
+
+HSD_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 __global__ void __launch_bounds__(NTHREADS, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, TcParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-byte aligned carve-up: [stages x A][stages x B][barriers]
+  // 1024-byte aligned carve-up: [stages x A][stages x B][barriers][epilogue stage]
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int b_bytes = P.ntile * BK * 2;
   uint8_t* sA = base;
@@ -53,11 +72,21 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   uint64_t* tfull = bars + 2 * P.stages;       // [2]
   uint64_t* tempty = bars + 2 * P.stages + 2;  // [2]
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * P.stages + 4);
-  float* epi_smem = (float*)(bars + 2 * P.stages + 6);    // 4 warps x [16 tokens][36]
+  float* stage_buf = (float*)(bars + 2 * P.stages + 6);   // [16 tokens][EPI_LD] fp32
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long u0 = (long)blockIdx.x * P.units / gridDim.x;
-  const long u1 = (long)(blockIdx.x + 1) * P.units / gridDim.x;
+  Sched sc;
+  sc.dp = P.dp;
+  sc.n_kb = P.n_kb;
+  if (P.dp) {
+    const long n_tiles = (long)P.n_tiles_n * P.n_tiles_t;
+    const long mine = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    sc.u0 = 0;
+    sc.count = mine * P.n_kb;
+  } else {
+    sc.u0 = (long)blockIdx.x * P.units / gridDim.x;
+    sc.count = (long)(blockIdx.x + 1) * P.units / gridDim.x - sc.u0;
+  }
 
   if (threadIdx.x == 32) {
     for (int s = 0; s < P.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -85,22 +114,23 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       // PDL: the weight tiles of the first ring stages do not depend on the
       // previous kernel -- stream them before griddepcontrol.wait, so the ring
       // fills while the predecessor drains; token tiles only after the wait.
-      const long npre = (u1 - u0) < P.stages ? (u1 - u0) : P.stages;
+      const long npre = sc.count < P.stages ? sc.count : P.stages;
       for (long i = 0; i < npre; ++i) {
-        const long u = u0 + i;
+        const long u = sc.unit(i);
         const int t = (int)(u / P.n_kb), kb = (int)(u % P.n_kb);
         mbar_expect_tx(&full[i], A_BYTES + b_bytes);
         tma_load_2d(&tmW, &full[i], sA + (size_t)i * A_BYTES, kb * BK, (t / P.n_tiles_t) * BM, pw);
       }
       pdl_wait();
       for (long i = 0; i < npre; ++i) {
-        const long u = u0 + i;
+        const long u = sc.unit(i);
         const int t = (int)(u / P.n_kb), kb = (int)(u % P.n_kb);
         tma_load_2d(&tmX, &full[i], sB + (size_t)i * b_bytes, kb * BK, (t % P.n_tiles_t) * P.ntile, px);
       }
       int stage = (int)(npre % P.stages);
       uint32_t phase = npre == P.stages ? 1u : 0u;
-      for (long u = u0 + npre; u < u1; ++u) {
+      for (long i = npre; i < sc.count; ++i) {
+        const long u = sc.unit(i);
         const int t = (int)(u / P.n_kb), kb = (int)(u % P.n_kb);
         const int tn = t / P.n_tiles_t, tt = t % P.n_tiles_t;
         mbar_wait(&empty[stage], phase ^ 1);
@@ -116,10 +146,10 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     if (lane == 0) {
       int stage = 0, buf = 0;
       uint32_t phase = 0, aphase = 0;
-      for (long u = u0; u < u1; ++u) {
-        const int kb = (int)(u % P.n_kb);
-        const bool first = (u == u0) || kb == 0;
-        const bool last = (u == u1 - 1) || kb == P.n_kb - 1;
+      for (long i = 0; i < sc.count; ++i) {
+        const int kb = (int)(sc.unit(i) % P.n_kb);
+        const bool first = (i == 0) || kb == 0;
+        const bool last = (i == sc.count - 1) || kb == P.n_kb - 1;
         if (first) {
           mbar_wait(&tempty[buf], aphase ^ 1);
           fence_after();
@@ -143,56 +173,85 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     }
   } else {
     // ---------------- epilogue: 4 warps = 128 TMEM lanes (lane quarter = warp % 4)
+    // Per 16-token chunk: TMEM -> registers (thread = output feature) -> a
+    // [16 tokens][128 features] fp32 stage in shared memory -> the 128 threads
+    // emit token-major 16-byte vectors: red.add.v4 (stream-K partial sums),
+    // st.v4 (data-parallel), ld+add+st (data-parallel residual), or SwiGLU of
+    // the interleaved gate/up rows into bf16 (data-parallel).
     pdl_wait();
-    const int q = warp & 3;
+    const int q = warp & 3, et = threadIdx.x - 64;      // 0..127
     int buf = 0;
     uint32_t aphase = 0;
-    long u = u0;
-    while (u < u1) {
+    long i = 0;
+    while (i < sc.count) {
+      const long u = sc.unit(i);
       const int t = (int)(u / P.n_kb), kb = (int)(u % P.n_kb);
-      long seg_end = u + (P.n_kb - kb);
-      if (seg_end > u1) seg_end = u1;
+      long seg = P.n_kb - kb;
+      if (i + seg > sc.count) seg = sc.count - i;
       const int tn = t / P.n_tiles_t, tt = t % P.n_tiles_t;
       mbar_wait(&tfull[buf], aphase);
       fence_after();
-      // TMEM -> registers (thread = output feature, 16 tokens) -> shared-memory
-      // transpose -> each thread adds 4 consecutive features of one token with a
-      // single 16-byte red.global.add.v4.f32 (4x fewer L2 atomics than scalar).
-      const int row0 = tn * BM + q * 32;
-      float* tp = epi_smem + (warp - 2) * (16 * 36);
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * P.ntile);
       for (int c0 = 0; c0 < P.ntile; c0 += 16) {
         uint32_t r[16];
         tmem_ld16(taddr + c0, r);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) tp[j * 36 + lane] = __uint_as_float(r[j]);
-        __syncwarp();
+        for (int j = 0; j < 16; ++j) stage_buf[j * EPI_LD + q * 32 + lane] = __uint_as_float(r[j]);
+        epi_bar();
+        if (P.epi == EPI_SWIGLU) {
+          // rows 0..63 of the tile are gate rows, 64..127 the matching up rows
+          const int tk = et >> 3, f8 = (et & 7) * 8;
+          const int tok = tt * P.ntile + c0 + tk, f0 = tn * (BM / 2) + f8;
+          if (tok < P.M && f0 < P.N / 2) {
+            const float* g = stage_buf + tk * EPI_LD + f8;
+            const float* uu = g + BM / 2;
+            uint32_t w[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int f = lane + 32 * i, tk = f >> 3, r4 = (f & 7) * 4;
-          const int tok = tt * P.ntile + c0 + tk, row = row0 + r4;
-          if (tok < P.M && row < P.N) {
-            const float4 v = *(const float4*)(tp + tk * 36 + r4);
+            for (int e = 0; e < 4; ++e) {
+              const float a0 = g[2 * e], a1 = g[2 * e + 1];
+              const __nv_bfloat162 hv = __floats2bfloat162_rn(a0 / (1.0f + expf(-a0)) * uu[2 * e],
+                                                              a1 / (1.0f + expf(-a1)) * uu[2 * e + 1]);
+              w[e] = *(const uint32_t*)&hv;
+            }
+            *(uint4*)(P.H + (size_t)tok * P.ldh + f0) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int slot = et + 128 * v, tk = slot >> 5, r4 = (slot & 31) * 4;
+            const int tok = tt * P.ntile + c0 + tk, row = tn * BM + r4;
+            if (tok >= P.M || row >= P.N) continue;
+            const float4 val = *(const float4*)(stage_buf + tk * EPI_LD + r4);
             float* dst = &P.C[(size_t)tok * P.ldc + row];
             if (row + 3 < P.N && P.vec4) {
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z),
-                           "f"(v.w)
-                           : "memory");
+              if (P.epi == EPI_ATOMIC) {
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(val.x), "f"(val.y),
+                             "f"(val.z), "f"(val.w)
+                             : "memory");
+              } else if (P.epi == EPI_ADD) {
+                float4 o = *(const float4*)dst;
+                o.x += val.x; o.y += val.y; o.z += val.z; o.w += val.w;
+                *(float4*)dst = o;
+              } else {
+                *(float4*)dst = val;
+              }
             } else {
-              atomicAdd(dst, v.x);
-              if (row + 1 < P.N) atomicAdd(dst + 1, v.y);
-              if (row + 2 < P.N) atomicAdd(dst + 2, v.z);
-              if (row + 3 < P.N) atomicAdd(dst + 3, v.w);
+              const float vv[4] = {val.x, val.y, val.z, val.w};
+              for (int e = 0; e < 4 && row + e < P.N; ++e) {
+                if (P.epi == EPI_ATOMIC) atomicAdd(dst + e, vv[e]);
+                else if (P.epi == EPI_ADD) dst[e] += vv[e];
+                else dst[e] = vv[e];
+              }
             }
           }
         }
-        __syncwarp();
+        epi_bar();
       }
       fence_before();
       mbar_arrive(&tempty[buf]);
       buf ^= 1;
       if (buf == 0) aphase ^= 1;
-      u = seg_end;
+      i += seg;
     }
   }
   fence_before();
@@ -260,21 +319,30 @@ bool gemm_tc_supported(int M, int N, int K, int lda, int ldw) {
   return M >= 1 && N >= 1 && K >= 16 && K % 8 == 0 && lda % 8 == 0 && ldw % 8 == 0 && encode_fn() != nullptr;
 }
 
-int gemm_tc_bf16(const bf16* A, int lda, const bf16* W, int ldw, float* C, int ldc, int M, int N, int K,
-                 bool accumulate, cudaStream_t st, bool c_zeroed) {
-  int launched = 0;
-  if (!accumulate && !c_zeroed) {
-    cudaMemset2DAsync(C, (size_t)ldc * 4, 0, (size_t)N * 4, M, st);
-  }
-  TcParams P;
-  P.M = M; P.N = N; P.K = K; P.ldc = ldc; P.C = C;
-  // token tile: all tokens in one tile when they fit (weights streamed once)
-  int n_tok_tiles = (M + 255) / 256;
-  int nt = (M + n_tok_tiles - 1) / n_tok_tiles;
+static void tc_tiles(int M, int& nt, int& n_tok_tiles) {
+  n_tok_tiles = (M + 255) / 256;
+  nt = (M + n_tok_tiles - 1) / n_tok_tiles;
   nt = (nt + 15) / 16 * 16;
   if (nt < 16) nt = 16;
+}
+
+// Data-parallel only with >= 4 output tiles per SM (c3's gate/up and verify
+// head): below that, whole-tile ownership leaves SMs idle or unbalanced while
+// the weights stream, and stream-K's partial-sum atomics are cheap.
+bool gemm_tc_dp(int M, int N) {
+  int nt, ntt;
+  tc_tiles(M, nt, ntt);
+  return (long)((N + BM - 1) / BM) * ntt >= 4L * num_sms();
+}
+
+static int gemm_tc_launch(const bf16* A, int lda, const bf16* W, int ldw, float* C, int ldc, int M, int N, int K,
+                          int epi, int dp, bf16* H, int ldh, cudaStream_t st) {
+  TcParams P;
+  P.M = M; P.N = N; P.K = K; P.ldc = ldc; P.C = C; P.H = H; P.ldh = ldh; P.epi = epi; P.dp = dp;
+  int nt, ntt;
+  tc_tiles(M, nt, ntt);
   P.ntile = nt;
-  P.n_tiles_t = (M + nt - 1) / nt;
+  P.n_tiles_t = ntt;
   P.n_tiles_n = (N + BM - 1) / BM;
   P.n_kb = (K + BK - 1) / BK;
   P.units = (long)P.n_tiles_n * P.n_tiles_t * P.n_kb;
@@ -293,17 +361,33 @@ int gemm_tc_bf16(const bf16* A, int lda, const bf16* W, int ldw, float* C, int l
   while (cols < (uint32_t)(2 * nt)) cols <<= 1;
   P.tmem_cols = cols;
   CUtensorMap mw, mx;
-  if (!make_map(&mw, W, N, K, ldw, BM) || !make_map(&mx, A, M, K, lda, nt)) return launched;
+  if (!make_map(&mw, W, N, K, ldw, BM) || !make_map(&mx, A, M, K, lda, nt)) return 0;
   P.vec4 = (ldc % 4 == 0) && (((uintptr_t)C & 15) == 0);
-  size_t smem = 1024 + (size_t)stages * (A_BYTES + b_bytes) + (2 * stages + 6) * 8 + 4 * 16 * 36 * 4 + 16;
+  size_t smem = 1024 + (size_t)stages * (A_BYTES + b_bytes) + (2 * stages + 6) * 8 + 16 * EPI_LD * 4 + 16;
   static bool attr_done = false;
   if (!attr_done) {
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_done = true;
   }
   const long max_ctas = (long)num_sms() * per_sm;
-  long grid = P.units < max_ctas ? P.units : max_ctas;
+  const long work = dp ? (long)P.n_tiles_n * P.n_tiles_t : P.units;
+  const long grid = work < max_ctas ? work : max_ctas;
   launch_k(gemm_tc_kernel, dim3((unsigned)grid), dim3(NTHREADS), smem, st, mw, mx, P);
-  launched += 1;
-  return launched;
+  return 1;
+}
+
+int gemm_tc_bf16(const bf16* A, int lda, const bf16* W, int ldw, float* C, int ldc, int M, int N, int K,
+                 bool accumulate, cudaStream_t st, bool c_zeroed) {
+  // data-parallel (whole tiles per CTA, plain stores / residual adds) when the
+  // output has at least one tile per SM; else stream-K with red.add partials
+  const int dp = gemm_tc_dp(M, N) ? 1 : 0;
+  if (!dp && !accumulate && !c_zeroed) cudaMemset2DAsync(C, (size_t)ldc * 4, 0, (size_t)N * 4, M, st);
+  const int epi = dp ? (accumulate ? EPI_ADD : EPI_STORE) : EPI_ATOMIC;
+  return gemm_tc_launch(A, lda, W, ldw, C, ldc, M, N, K, epi, dp, nullptr, 0, st);
+}
+
+int gemm_tc_swiglu_bf16(const bf16* A, int lda, const bf16* W, int ldw, bf16* H, int ldh, int M, int N, int K,
+                        cudaStream_t st) {
+  if (!gemm_tc_dp(M, N) || N % BM) return 0;
+  return gemm_tc_launch(A, lda, W, ldw, nullptr, 0, M, N, K, EPI_SWIGLU, 1, H, ldh, st);
 }

@@ -9,3 +9,11 @@ bool gemm_tc_supported(int M, int N, int K, int lda, int ldw);
 // their consumer kernels), which saves the memset node.
 int gemm_tc_bf16(const bf16* A, int lda, const bf16* W, int ldw, float* C, int ldc, int M, int N, int K,
                  bool accumulate, cudaStream_t st, bool c_zeroed = false);
+// true when the GEMM runs data-parallel (at least one output tile per SM)
+bool gemm_tc_dp(int M, int N);
+// data-parallel gate/up GEMM with the SwiGLU fused into the epilogue: W rows are
+// interleaved in 64-row groups (gate rows g*64.., then the matching up rows),
+// H[M, N/2] = silu(gate) * up in bf16. Returns 0 (nothing launched) when the
+// shape would not run data-parallel; the caller then uses the plain path.
+int gemm_tc_swiglu_bf16(const bf16* A, int lda, const bf16* W, int ldw, bf16* H, int ldh, int M, int N, int K,
+                        cudaStream_t st);

@@ -96,50 +96,61 @@ void launch_embed(const void* E, DType dt, const int32_t* tok, const int32_t* po
 // pos * theta^(-2i/hd); cos/sin tables precomputed on the host in double.
 // grid (M, Hq + 2*Hkv): one CTA per (row, head); K/V go to the paged cache
 // (V transposed, see KVLayer).
+// One CTA per row: thread t handles rotation pairs (head, j) strided over the
+// row's q and k heads, then the v head dims; the fp32 scratch row is re-zeroed
+// after the CTA has read it (so the next tcgen05 GEMM into it needs no memset).
 template <typename T>
-__global__ void qkv_rope_kv_kernel(float* __restrict__ qkv, RowMeta m, const float* __restrict__ rc,
-                                   const float* __restrict__ rs, int Hq, KVLayer kv, T* __restrict__ q_out) {
+__global__ void __launch_bounds__(128) qkv_rope_kv_kernel(float* __restrict__ qkv, RowMeta m,
+                                                          const float* __restrict__ rc,
+                                                          const float* __restrict__ rs, int Hq, KVLayer kv,
+                                                          T* __restrict__ q_out) {
   pdl_wait();
   pdl_trigger();
-  const int r = blockIdx.x, hh = blockIdx.y;
+  const int r = blockIdx.x, part = blockIdx.y, nparts = gridDim.y;   // row r, column chunk `part`
   const int hd = kv.head_dim, half = hd / 2, Hkv = kv.kv_heads;
   const int ld = (Hq + 2 * Hkv) * hd;
-  float* src = qkv + (size_t)r * ld + (size_t)hh * hd;
+  float* row = qkv + (size_t)r * ld;
+  const int tid = part * blockDim.x + threadIdx.x, nthr = nparts * blockDim.x;
   const int p = m.pos[r];
-  // The qkv scratch is re-zeroed once read, so the next tcgen05 GEMM into it can
-  // accumulate (red.add) without a memset (see gemm in engine.cu).
-  struct Zero {
-    float* p; int n;
-    __device__ ~Zero() { __syncthreads(); for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0.f; }
-  } zero{src, hd};
-  if (hh < Hq) {
-    T* qo = q_out + ((size_t)r * Hq + hh) * hd;
-    for (int j = threadIdx.x; j < half; j += blockDim.x) {
-      if (p < 0) { qo[j] = from_f32<T>(0.f); qo[j + half] = from_f32<T>(0.f); continue; }
-      float c = rc[(size_t)p * half + j], s = rs[(size_t)p * half + j];
-      float x1 = src[j], x2 = src[j + half];
-      qo[j] = from_f32<T>(x1 * c - x2 * s);
-      qo[j + half] = from_f32<T>(x2 * c + x1 * s);
-    }
-    return;
-  }
-  if (p < 0) return;
-  const int kp = m.kvpos[r];
-  const int page = kv.block_table[(size_t)m.req[r] * kv.pages_per_req + kp / kv.page_size];
-  const int slot = kp % kv.page_size;
-  T* base = (T*)kv.base;
-  if (hh < Hq + Hkv) {
-    const int h = hh - Hq;
-    for (int j = threadIdx.x; j < half; j += blockDim.x) {
-      float c = rc[(size_t)p * half + j], s = rs[(size_t)p * half + j];
-      float x1 = src[j], x2 = src[j + half];
-      base[kv_offset(page, 0, Hkv, h, kv.page_size, hd, slot, j)] = from_f32<T>(x1 * c - x2 * s);
-      base[kv_offset(page, 0, Hkv, h, kv.page_size, hd, slot, j + half)] = from_f32<T>(x2 * c + x1 * s);
-    }
+  T* qo = q_out + (size_t)r * Hq * hd;
+  if (p < 0) {
+    for (int i = tid; i < Hq * hd; i += nthr) qo[i] = from_f32<T>(0.f);
   } else {
-    const int h = hh - Hq - Hkv;
-    for (int d = threadIdx.x; d < hd; d += blockDim.x)
-      base[kv_offset(page, 1, Hkv, h, kv.page_size, hd, slot, d)] = from_f32<T>(src[d]);
+    const float* c = rc + (size_t)p * half;
+    const float* sn = rs + (size_t)p * half;
+    const int kp = m.kvpos[r];
+    const int page = kv.block_table[(size_t)m.req[r] * kv.pages_per_req + kp / kv.page_size];
+    const int slot = kp % kv.page_size;
+    T* base = (T*)kv.base;
+    // rotated q (Hq heads) and k (Hkv heads): (Hq + Hkv) * half rotation pairs
+    for (int i = tid; i < (Hq + Hkv) * half; i += nthr) {
+      const int h = i / half, j = i % half;
+      const float x1 = row[h * hd + j], x2 = row[h * hd + j + half];
+      const float y1 = x1 * c[j] - x2 * sn[j], y2 = x2 * c[j] + x1 * sn[j];
+      if (h < Hq) {
+        qo[h * hd + j] = from_f32<T>(y1);
+        qo[h * hd + j + half] = from_f32<T>(y2);
+      } else {
+        base[kv_offset(page, 0, Hkv, h - Hq, kv.page_size, hd, slot, j)] = from_f32<T>(y1);
+        base[kv_offset(page, 0, Hkv, h - Hq, kv.page_size, hd, slot, j + half)] = from_f32<T>(y2);
+      }
+    }
+    for (int i = tid; i < Hkv * hd; i += nthr) {
+      const int h = i / hd, d = i % hd;
+      base[kv_offset(page, 1, Hkv, h, kv.page_size, hd, slot, d)] = from_f32<T>(row[(Hq + Hkv) * hd + i]);
+    }
+  }
+  // Each element was read by exactly this thread (same tid -> same indices), so
+  // re-zeroing the scratch needs no cross-CTA barrier: zero what this thread read.
+  if (p >= 0) {
+    for (int i = tid; i < (Hq + Hkv) * half; i += nthr) {
+      const int h = i / half, j = i % half;
+      row[h * hd + j] = 0.f;
+      row[h * hd + j + half] = 0.f;
+    }
+    for (int i = tid; i < Hkv * hd; i += nthr) row[(Hq + Hkv) * hd + i] = 0.f;
+  } else {
+    for (int i = tid; i < ld; i += nthr) row[i] = 0.f;
   }
 }
 
@@ -147,16 +158,17 @@ void launch_qkv_rope_kv(float* qkv, int M, const RowMeta& m, const float* rope_c
                         const float* rope_sin, int Hq, const KVLayer& kv, void* q_out, DType dt,
                         cudaStream_t st) {
   if (M <= 0) return;
-  dim3 grid(M, Hq + 2 * kv.kv_heads);
-  int thr = kv.head_dim >= 128 ? 64 : 32;
   if (dt == DT_F32)
-    launch_k(qkv_rope_kv_kernel<float>, grid, thr, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out);
+    launch_k(qkv_rope_kv_kernel<float>, dim3(M, 8), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out);
   else
-    launch_k(qkv_rope_kv_kernel<bf16>, grid, thr, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out);
+    launch_k(qkv_rope_kv_kernel<bf16>, dim3(M, 8), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out);
 }
 
 // ------------------------------------------------------------------ SwiGLU
-// gu row = [gate (f) | up (f)] -> silu(gate) * up; grid (M, f/4/256 chunks), f % 4 == 0
+// gu row = 2f values with gate/up INTERLEAVED in 64-feature groups (weight rows
+// of W_gu are stored that way so the data-parallel tcgen05 GEMM can fuse SwiGLU
+// into its epilogue): feature i's gate is column 128*(i/64) + i%64 and its up
+// value 64 columns later. out[i] = silu(gate) * up. grid (M, f/4/256), f % 64 == 0.
 template <typename T>
 __global__ void swiglu_kernel(float* __restrict__ gu, int f, T* __restrict__ out,
                               const int32_t* __restrict__ pos) {
@@ -165,8 +177,9 @@ __global__ void swiglu_kernel(float* __restrict__ gu, int f, T* __restrict__ out
   const int r = blockIdx.x;
   const int i = blockIdx.y * blockDim.x + threadIdx.x;   // float4 index
   if (4 * i >= f) return;
-  float4* ga = (float4*)(gu + (size_t)r * 2 * f) + i;
-  float4* gb = (float4*)(gu + (size_t)r * 2 * f + f) + i;
+  const int col = 128 * ((4 * i) / 64) + (4 * i) % 64;
+  float4* ga = (float4*)(gu + (size_t)r * 2 * f + col);
+  float4* gb = (float4*)(gu + (size_t)r * 2 * f + col + 64);
   const float4 a = *ga, u = *gb;
   *ga = make_float4(0.f, 0.f, 0.f, 0.f);   // re-zero the GEMM scratch (see qkv_rope_kv)
   *gb = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -181,6 +194,20 @@ void launch_swiglu(float* gu, int M, int f, void* out, DType dt, const int32_t* 
   dim3 grid(M, (f / 4 + 255) / 256);
   if (dt == DT_F32) launch_k(swiglu_kernel<float>, grid, 256, 0, st, gu, f, (float*)out, pos);
   else launch_k(swiglu_kernel<bf16>, grid, 256, 0, st, gu, f, (bf16*)out, pos);
+}
+
+// gate rows [0,f) and up rows [f,2f) of src -> interleaved 64-row groups in dst
+template <typename T>
+__global__ void interleave_gu_kernel(const T* __restrict__ src, int f, int n, T* __restrict__ dst) {
+  const int r = blockIdx.x;                       // destination row
+  const int g = r / 128, o = r % 128;
+  const int srow = o < 64 ? g * 64 + o : f + g * 64 + (o - 64);
+  for (int c = threadIdx.x; c < n; c += blockDim.x) dst[(size_t)r * n + c] = src[(size_t)srow * n + c];
+}
+
+void launch_interleave_gu(const void* src, int f, int n, void* dst, DType dt, cudaStream_t st) {
+  if (dt == DT_F32) interleave_gu_kernel<float><<<2 * f, 256, 0, st>>>((const float*)src, f, n, (float*)dst);
+  else interleave_gu_kernel<bf16><<<2 * f, 256, 0, st>>>((const bf16*)src, f, n, (bf16*)dst);
 }
 
 // ------------------------------------------------------------------ argmax

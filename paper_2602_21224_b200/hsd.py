@@ -265,8 +265,8 @@ def debug_gemm(A, W, C, accumulate=False, use_tc=False, stream=0):
     M, K = A.shape
     N = W.shape[0]
     s = lib.hsd_debug_gemm(A.data_ptr(), A.stride(0), W.data_ptr(),
-                           W.stride(0), C.data_ptr(), C.stride(0), M, N, K, int(accumulate), dtype, int(use_tc),
-                           stream)
+                           W.stride(0), C.data_ptr(), C.stride(0), M, N, K, int(accumulate), dtype,
+                           2 if use_tc == "swiglu" else int(bool(use_tc)), stream)
     if s != HSD_OK:
         raise HsdError(s, "hsd_debug_gemm")
 
