@@ -352,7 +352,11 @@ static int gemm_tc_launch(const bf16* A, int lda, const bf16* W, int ldw, float*
   // resident while this kernel drains.
   static const int ring_kb = [] { const char* e = getenv("HSD_GEMM_RING_KB"); return e ? atoi(e) : 100; }();
   static const int per_sm = [] { const char* e = getenv("HSD_GEMM_CTAS_PER_SM"); return e ? atoi(e) : 2; }();
-  int stages = (ring_kb * 1024) / (A_BYTES + b_bytes);
+  // at least 3 stages in flight: wide token tiles (compute-bound shapes) get a
+  // bigger ring and one CTA per SM instead of two shallow ones
+  int ring = ring_kb * 1024, cps = per_sm;
+  if (ring / (A_BYTES + b_bytes) < 3) { ring = 200 * 1024; cps = 1; }
+  int stages = ring / (A_BYTES + b_bytes);
   if (stages > 16) stages = 16;
   if (stages < 2) stages = 2;
   P.stages = stages;
@@ -369,7 +373,7 @@ static int gemm_tc_launch(const bf16* A, int lda, const bf16* W, int ldw, float*
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_done = true;
   }
-  const long max_ctas = (long)num_sms() * per_sm;
+  const long max_ctas = (long)num_sms() * cps;
   const long work = dp ? (long)P.n_tiles_n * P.n_tiles_t : P.units;
   const long grid = work < max_ctas ? work : max_ctas;
   launch_k(gemm_tc_kernel, dim3((unsigned)grid), dim3(NTHREADS), smem, st, mw, mx, P);
