@@ -13,15 +13,26 @@
 #include "accept.cuh"
 
 namespace {
-constexpr int WT = 256;
+constexpr int WT = 1024;
 
 // lse of x/T over V (CTA-wide, deterministic)
 HSD_DEV float row_lse(const float* x, int V, float invT, float* red) {
   float m = -INFINITY, s = 0.f;
-  for (int j = threadIdx.x; j < V; j += blockDim.x) {
-    float v = x[j] * invT;
-    if (v > m) { s = s * expf(m - v) + 1.f; m = v; }
-    else s += expf(v - m);
+  constexpr int U = 8;   // U independent loads in flight per thread
+  for (int base = threadIdx.x; base < V; base += blockDim.x * U) {
+    float xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = base + u * blockDim.x;
+      xv[u] = j < V ? x[j] : -INFINITY;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float v = xv[u] * invT;
+      if (v == -INFINITY) continue;
+      if (v > m) { s = s * expf(m - v) + 1.f; m = v; }
+      else s += expf(v - m);
+    }
   }
   float M = block_max(m, red);
   s = (m == -INFINITY) ? 0.f : s * expf(m - M);
@@ -37,6 +48,9 @@ HSD_DEV int gumbel_argmax(const float* x, int V, float invT, uint32_t seed, uint
   for (int b4 = threadIdx.x; b4 * 4 < V; b4 += blockDim.x) {
     u32x4 c = {(uint32_t)b4, slot, step, req};
     u32x4 r = philox4x32_10(c, seed, TAG_GUMBEL);
+    float xv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) xv[q] = b4 * 4 + q < V ? x[b4 * 4 + q] : 0.f;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       int v = b4 * 4 + q;
@@ -45,7 +59,7 @@ HSD_DEV int gumbel_argmax(const float* x, int V, float invT, uint32_t seed, uint
       for (int e = 0; e < n_excl; ++e) ex |= (excl[e] == v);
       if (ex) continue;
       float u = unit_open(lane_of(r, q));
-      float z = x[v] * invT - logf(-logf(u));
+      float z = xv[q] * invT - logf(-logf(u));
       if (better(z, v, bv, bi)) { bv = z; bi = v; }
     }
   }

@@ -46,6 +46,8 @@ HSD_DEV bool beats(float v, int j, int l, float w, int i, int m, const int32_t* 
   return l < m;
 }
 
+struct TreeParamsFwd;
+#define perm_of(P) ((P).perm)
 struct Top {
   float v[KMAX];
   int j[KMAX];
@@ -168,106 +170,196 @@ HSD_DEV void vocab_pass(const float* __restrict__ Lrow, const TT* __restrict__ b
   __syncthreads();
 }
 
-// Alg. 1 BuildSubtree on a thread-block cluster of CL CTAs: every CTA sweeps its
-// vocab slice for every frontier node and stores its Partial in the LEADER's
-// shared memory (DSMEM); the leader merges (exact (max, sum-exp) combination and
-// top-k over the CL sorted lists), appends the children in frontier order and
-// selects the next frontier (TopkByJointProb). Node arrays live in the leader.
+// Alg. 1 BuildSubtree on a thread-block cluster of CL CTAs (one request).
+// Every round (one step i of Alg. 1):
+//  1. each CTA sweeps its 1/CL vocab slice for ALL frontier nodes at once: the
+//     32 warps are split into one group per frontier node; a thread keeps an
+//     online (max, sum-exp) and a top-8 of l_i + r(node.token);
+//  2. warp merges, then the group's leader warp merges its warps' lists into the
+//     (node, CTA) Partial and BROADCASTS it into every CTA's shared memory
+//     (DSMEM, double-buffered by round parity);
+//  3. one cluster barrier; then every CTA merges the CL partials of every node
+//     (exact (max, sum-exp) combination, top-k by rank), appends the children in
+//     frontier order and runs TopkByJointProb -- redundantly and identically, so
+//     no second barrier is needed to publish the frontier.
 struct ClusterSm {
-  Partial part[KMAX][CL];
+  Partial part[2][KMAX][CL];
   int Q[KMAX], Qtok[KMAX], nq;
 };
+
+HSD_DEV void merge_lists_lanes(int nlists, const float* lv, const int* lj, int k, const int32_t* perm, float* ov,
+                               int* oj) {
+  // warp-collective: lane l < nlists owns sorted list l (KMAX entries, stride KMAX)
+  const int lane = threadIdx.x & 31;
+  int hd = 0;
+  for (int r = 0; r < k; ++r) {
+    float bv = (lane < nlists && hd < k) ? lv[lane * KMAX + hd] : -INFINITY;
+    int bj = (lane < nlists && hd < k) ? lj[lane * KMAX + hd] : -1, bl = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ovv = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int ojj = __shfl_xor_sync(0xffffffffu, bj, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (beats(ovv, ojj, ol, bv, bj, bl, perm)) { bv = ovv; bj = ojj; bl = ol; }
+    }
+    if (lane == 0) { ov[r] = bv; oj[r] = bj; }
+    if (lane == bl) hd++;
+  }
+}
 
 HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, int root_tok, NodesSm& nd,
                            ClusterSm& cs, float* red_f, int* red_i) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
-  ClusterSm* lead = cluster.map_shared_rank(&cs, 0);
-  __shared__ int qtok_local[KMAX], nq_local;
-  __shared__ Partial mine;
-  if (rank == 0 && threadIdx.x == 0) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ float wv[32 * KMAX], wm[32], ws[32];
+  __shared__ int wj[32 * KMAX];
+  if (threadIdx.x == 0) {
     nd.tok[0] = root_tok; nd.par[0] = -1; nd.depth[0] = 0; nd.lj[0] = 0.f; nd.n = 1;
     cs.Q[0] = 0; cs.Qtok[0] = root_tok; cs.nq = 1;
   }
-  cluster.sync();
+  cluster.sync();   // every CTA of the cluster is running before any DSMEM store
   const int per = (P.V + CL - 1) / CL;
   const int lo = min(P.V, rank * per), hi = min(P.V, lo + per);
+  const int K = P.k;
   for (int i = 0; i < steps; ++i) {
-    if (threadIdx.x == 0) {
-      nq_local = lead->nq;
-      for (int q = 0; q < KMAX; ++q) qtok_local[q] = lead->Qtok[q];
-    }
-    __syncthreads();
+    const int par = i & 1;
+    const int nq = cs.nq;
+    const int wpn = 32 / nq;                       // warps per frontier node
+    const int qi = w / wpn, wg = w % wpn;          // this warp's node and index in its group
     const float* Lrow = P.L + ((size_t)req * P.N + row0 + i) * P.V;
-    for (int qi = 0; qi < nq_local; ++qi) {
-      const int tok = qtok_local[qi];
+    // ---- 1. sweep
+    float m = -INFINITY, sacc = 0.f;
+    Top t;
+    top_init(t);
+    if (qi < nq) {
+      const int tok = cs.Qtok[qi];
       const int rk = P.rank_of ? P.rank_of[tok] : tok;
       const bool has_bias = !P.zero_table && rk < P.Vh;
-      if (P.tdt == DT_F32)
-        vocab_pass<float>(Lrow, has_bias ? (const float*)P.table + (size_t)rk * P.Vh : nullptr, lo, hi, P.Vh, P.k,
-                          P.perm, &mine, red_f, red_i);
-      else
-        vocab_pass<bf16>(Lrow, has_bias ? (const bf16*)P.table + (size_t)rk * P.Vh : nullptr, lo, hi, P.Vh, P.k,
-                         P.perm, &mine, red_f, red_i);
-      if (threadIdx.x == 0) lead->part[qi][rank] = mine;
-      __syncthreads();
+      const int gthreads = wpn * 32, gt = wg * 32 + lane;
+      constexpr int U = 4;
+      for (int base = lo + gt; base < hi; base += gthreads * U) {
+        float lv[U], bv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = base + u * gthreads;
+          lv[u] = j < hi ? Lrow[j] : 0.f;
+          float b = 0.f;
+          if (has_bias && j < hi && j < P.Vh)
+            b = P.tdt == DT_F32 ? ((const float*)P.table)[(size_t)rk * P.Vh + j]
+                                : to_f32(((const bf16*)P.table)[(size_t)rk * P.Vh + j]);
+          bv[u] = b;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = base + u * gthreads;
+          if (j >= hi) break;
+          const float v = lv[u] + bv[u];
+          if (v > m) { sacc = sacc * expf(m - v) + 1.f; m = v; }
+          else sacc += expf(v - m);
+          top_insert(t, v, j, perm_of(P));
+        }
+      }
+    }
+    // ---- 2a. warp merge: (max, sum) butterfly and top-k of the lanes' lists
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, sacc, o);
+      const float nm = fmaxf(m, om);
+      sacc = (m == -INFINITY ? 0.f : sacc * expf(m - nm)) + (om == -INFINITY ? 0.f : os * expf(om - nm));
+      m = nm;
+    }
+    {
+      int head = 0;
+      for (int r = 0; r < K; ++r) {
+        float hv = -INFINITY;
+        int hj = -1;
+#pragma unroll
+        for (int q = 0; q < KMAX; ++q)
+          if (q == head) { hv = t.v[q]; hj = t.j[q]; }
+        float bv = hv;
+        int bj = hj, bl = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oj = __shfl_xor_sync(0xffffffffu, bj, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
+          if (beats(ov, oj, ol, bv, bj, bl, perm_of(P))) { bv = ov; bj = oj; bl = ol; }
+        }
+        if (lane == 0) { wv[w * KMAX + r] = bv; wj[w * KMAX + r] = bj; }
+        if (lane == bl) head++;
+      }
+      if (lane == 0) { wm[w] = m; ws[w] = sacc; }
+    }
+    __syncthreads();
+    // ---- 2b. group leader warps: merge the group's warps, broadcast the Partial
+    if (qi < nq && wg == 0) {
+      const int w0 = qi * wpn;
+      float mm = lane < wpn ? wm[w0 + lane] : -INFINITY, ss = lane < wpn ? ws[w0 + lane] : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, mm, o), os = __shfl_xor_sync(0xffffffffu, ss, o);
+        const float nm = fmaxf(mm, om);
+        ss = (mm == -INFINITY ? 0.f : ss * expf(mm - nm)) + (om == -INFINITY ? 0.f : os * expf(om - nm));
+        mm = nm;
+      }
+      __shared__ Partial grp[KMAX];
+      merge_lists_lanes(wpn, wv + w0 * KMAX, wj + w0 * KMAX, K, perm_of(P), grp[qi].v, grp[qi].j);
+      if (lane == 0) { grp[qi].m = mm; grp[qi].s = ss; }
+      __syncwarp();
+      if (lane < CL) {                           // lane c writes this partial into CTA c
+        Partial* dst = cluster.map_shared_rank(&cs.part[par][qi][rank], lane);
+        *dst = grp[qi];
+      }
     }
     cluster.sync();
-    if (rank == 0) {
-      const int start = nd.n, nq = cs.nq, K = P.k;
-      // (a) per frontier node qi, rank each of its CL*k partial candidates among
-      //     the others (value desc, token asc; ties impossible: distinct tokens);
-      //     the candidate of rank r < k becomes child r of node qi.
-      for (int t = threadIdx.x; t < nq * CL * KMAX; t += blockDim.x) {
-        const int qi = t / (CL * KMAX), c = (t / KMAX) % CL, e = t % KMAX;
-        if (e >= K) continue;
-        const float v = cs.part[qi][c].v[e];
-        const int j = cs.part[qi][c].j[e];
-        if (j < 0) continue;
-        int rnk = 0;
+    // ---- 3. every CTA: merge the CL partials, children, TopkByJointProb
+    const int start = nd.n;
+    for (int tt = threadIdx.x; tt < nq * CL * KMAX; tt += blockDim.x) {
+      const int q = tt / (CL * KMAX), c = (tt / KMAX) % CL, e = tt % KMAX;
+      if (e >= K) continue;
+      const Partial& pc = cs.part[par][q][c];
+      const float v = pc.v[e];
+      const int j = pc.j[e];
+      if (j < 0) continue;
+      int rnk = 0;
+      for (int c2 = 0; c2 < CL; ++c2)
+        for (int e2 = 0; e2 < K; ++e2) {
+          const int j2 = cs.part[par][q][c2].j[e2];
+          if (j2 >= 0 && better_j(cs.part[par][q][c2].v[e2], j2, v, j, perm_of(P))) ++rnk;
+        }
+      if (rnk < K) {
+        float M = -INFINITY, S = 0.f;
+        for (int c2 = 0; c2 < CL; ++c2) M = fmaxf(M, cs.part[par][q][c2].m);
         for (int c2 = 0; c2 < CL; ++c2)
-          for (int e2 = 0; e2 < K; ++e2) {
-            const int j2 = cs.part[qi][c2].j[e2];
-            if (j2 >= 0 && better_j(cs.part[qi][c2].v[e2], j2, v, j, P.perm)) ++rnk;
-          }
-        if (rnk < K) {
-          float M = -INFINITY, S = 0.f;
-          for (int c2 = 0; c2 < CL; ++c2) M = fmaxf(M, cs.part[qi][c2].m);
-          for (int c2 = 0; c2 < CL; ++c2)
-            if (cs.part[qi][c2].m != -INFINITY) S += cs.part[qi][c2].s * expf(cs.part[qi][c2].m - M);
-          const float lse = M + logf(S);
-          const int u = cs.Q[qi], n = start + qi * K + rnk;
-          nd.tok[n] = P.perm ? P.perm[j] : j;
-          nd.par[n] = u;
-          nd.depth[n] = nd.depth[u] + 1;
-          nd.lj[n] = nd.lj[u] + (v - lse);
-        }
+          if (cs.part[par][q][c2].m != -INFINITY) S += cs.part[par][q][c2].s * expf(cs.part[par][q][c2].m - M);
+        const float lse = M + logf(S);
+        const int u = cs.Q[q], n = start + q * K + rnk;
+        nd.tok[n] = P.perm ? P.perm[j] : j;
+        nd.par[n] = u;
+        nd.depth[n] = nd.depth[u] + 1;
+        nd.lj[n] = nd.lj[u] + (v - lse);
       }
-      __syncthreads();
-      // (b) TopkByJointProb(Q_next, k): every candidate computes its rank under
-      //     (joint desc, token asc, parent creation index asc) in parallel.
-      const int cnt_new = nq * K;
-      __shared__ int newQ[KMAX];
-      for (int c = threadIdx.x; c < cnt_new; c += blockDim.x) {
-        const int a = start + c;
-        int rnk = 0;
-        for (int b = start; b < start + cnt_new; ++b) {
-          const bool bb = nd.lj[b] > nd.lj[a] ||
-                          (nd.lj[b] == nd.lj[a] &&
-                           (nd.tok[b] < nd.tok[a] || (nd.tok[b] == nd.tok[a] && nd.par[b] < nd.par[a])));
-          rnk += bb;
-        }
-        if (rnk < K) newQ[rnk] = a;
-      }
-      __syncthreads();
-      if (threadIdx.x < KMAX) {
-        const int q = threadIdx.x;
-        if (q < K && q < cnt_new) { cs.Q[q] = newQ[q]; cs.Qtok[q] = nd.tok[newQ[q]]; }
-        if (q == 0) { nd.n = start + cnt_new; cs.nq = K < cnt_new ? K : cnt_new; }
-      }
-      __syncthreads();
     }
-    cluster.sync();
+    __syncthreads();
+    const int cnt_new = nq * K;
+    __shared__ int newQ[KMAX];
+    for (int c = threadIdx.x; c < cnt_new; c += blockDim.x) {
+      const int a = start + c;
+      int rnk = 0;
+      for (int b = start; b < start + cnt_new; ++b) {
+        const bool bb = nd.lj[b] > nd.lj[a] ||
+                        (nd.lj[b] == nd.lj[a] &&
+                         (nd.tok[b] < nd.tok[a] || (nd.tok[b] == nd.tok[a] && nd.par[b] < nd.par[a])));
+        rnk += bb;
+      }
+      if (rnk < K) newQ[rnk] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x < KMAX) {
+      const int q = threadIdx.x;
+      if (q < K && q < cnt_new) { cs.Q[q] = newQ[q]; cs.Qtok[q] = nd.tok[newQ[q]]; }
+      if (q == 0) { nd.n = start + cnt_new; cs.nq = K < cnt_new ? K : cnt_new; }
+    }
+    __syncthreads();
   }
 }
 

@@ -5,6 +5,5 @@ tail -3 /tmp/bench.err
 python - <<'PY'
 import json
 d = json.loads(open('/tmp/bench.json').read().strip().splitlines()[-1])
-print(d['config']['workload'], d['ms_per_step'], 'tok/s', d['value'], 'roof', d['roofline']['kernel'], d['roofline']['frac'], d['roofline']['achieved'])
-print(d['profile_ms_per_step'])
+print(d['config']['workload'], d['ms_per_step'], 'tok/s', d['value'], 'roof', d['roofline']['kernel'], d['roofline']['frac'], d['roofline']['achieved'], '|', ' '.join(f"{k}={v}" for k, v in d['profile_ms_per_step'].items()))
 PY
