@@ -46,22 +46,26 @@ HSD_DEV bool beats(float v, int j, int l, float w, int i, int m, const int32_t* 
   return l < m;
 }
 
-struct TreeParamsFwd;
 #define perm_of(P) ((P).perm)
+// per-thread top-KC list, sorted by (value desc, token asc); KC = k exactly, so
+// the admission test is against the k-th best and insertion bubbles k-1 steps
+template <int KC>
 struct Top {
-  float v[KMAX];
-  int j[KMAX];
+  float v[KC];
+  int j[KC];
 };
 
-HSD_DEV void top_init(Top& t) {
+template <int KC>
+HSD_DEV void top_init(Top<KC>& t) {
 #pragma unroll
-  for (int s = 0; s < KMAX; ++s) { t.v[s] = -INFINITY; t.j[s] = -1; }
+  for (int s = 0; s < KC; ++s) { t.v[s] = -INFINITY; t.j[s] = -1; }
 }
-HSD_DEV void top_insert(Top& t, float v, int j, const int32_t* perm) {
-  if (!better_j(v, j, t.v[KMAX - 1], t.j[KMAX - 1], perm)) return;
-  t.v[KMAX - 1] = v; t.j[KMAX - 1] = j;
+template <int KC>
+HSD_DEV void top_insert(Top<KC>& t, float v, int j, const int32_t* perm) {
+  if (!better_j(v, j, t.v[KC - 1], t.j[KC - 1], perm)) return;
+  t.v[KC - 1] = v; t.j[KC - 1] = j;
 #pragma unroll
-  for (int s = KMAX - 1; s > 0; --s) {
+  for (int s = KC - 1; s > 0; --s) {
     if (better_j(t.v[s], t.j[s], t.v[s - 1], t.j[s - 1], perm)) {
       float tv = t.v[s]; t.v[s] = t.v[s - 1]; t.v[s - 1] = tv;
       int tj = t.j[s]; t.j[s] = t.j[s - 1]; t.j[s - 1] = tj;
@@ -76,99 +80,6 @@ struct Partial {
   float v[KMAX];
   int j[KMAX];
 };
-
-// One CTA-wide sweep: v_j = L[j] + bias[j] over j in [lo, hi) (bias only for hot
-// columns j < Vh). Thread 0 returns the CTA partial in *out.
-template <typename TT>
-HSD_DEV void vocab_pass(const float* __restrict__ Lrow, const TT* __restrict__ bias, int lo, int hi, int Vh, int k,
-                        const int32_t* perm, Partial* out, float* red_f, int* red_i) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = NT / 32;
-  float m = -INFINITY, s = 0.f;
-  Top t;
-  top_init(t);
-  // issue U loads of the logit row and U of the table row before using any
-  // (the table row streams from HBM: one round trip per U elements, not per element)
-  constexpr int U = 4;
-  for (int base = lo + threadIdx.x; base < hi; base += NT * U) {
-    float lv[U], bv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = base + u * NT;
-      lv[u] = j < hi ? Lrow[j] : 0.f;
-      bv[u] = (bias != nullptr && j < hi && j < Vh) ? to_f32(bias[j]) : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = base + u * NT;
-      if (j >= hi) break;
-      const float v = lv[u] + bv[u];
-      if (v > m) { s = s * expf(m - v) + 1.f; m = v; }
-      else s += expf(v - m);
-      top_insert(t, v, j, perm);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
-    float nm = fmaxf(m, om);
-    s = (m == -INFINITY ? 0.f : s * expf(m - nm)) + (om == -INFINITY ? 0.f : os * expf(om - nm));
-    m = nm;
-  }
-  // warp top-k: k rounds of argmax over the lanes' list heads
-  int head = 0;
-  float wv[KMAX];
-  int wj[KMAX];
-  for (int r = 0; r < k; ++r) {
-    float hv = -INFINITY;
-    int hj = -1;
-#pragma unroll
-    for (int q = 0; q < KMAX; ++q)
-      if (q == head) { hv = t.v[q]; hj = t.j[q]; }
-    float bv = hv;
-    int bj = hj, bl = lane;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      int oj = __shfl_xor_sync(0xffffffffu, bj, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      if (beats(ov, oj, ol, bv, bj, bl, perm)) { bv = ov; bj = oj; bl = ol; }
-    }
-    wv[r] = bv; wj[r] = bj;
-    if (lane == bl) head++;
-  }
-  __syncthreads();
-  if (lane == 0) {
-    red_f[w * 2] = m; red_f[w * 2 + 1] = s;
-    for (int r = 0; r < k; ++r) { red_f[64 + w * KMAX + r] = wv[r]; red_i[w * KMAX + r] = wj[r]; }
-  }
-  __syncthreads();
-  if (w == 0) {
-    float mm = lane < nw ? red_f[lane * 2] : -INFINITY, ss = lane < nw ? red_f[lane * 2 + 1] : 0.f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      float om = __shfl_xor_sync(0xffffffffu, mm, o), os = __shfl_xor_sync(0xffffffffu, ss, o);
-      float nm = fmaxf(mm, om);
-      ss = (mm == -INFINITY ? 0.f : ss * expf(mm - nm)) + (om == -INFINITY ? 0.f : os * expf(om - nm));
-      mm = nm;
-    }
-    int hd = 0;
-    for (int r = 0; r < k; ++r) {
-      float hv = (lane < nw && hd < k) ? red_f[64 + lane * KMAX + hd] : -INFINITY;
-      int hj = (lane < nw && hd < k) ? red_i[lane * KMAX + hd] : -1;
-      float bv = hv;
-      int bj = hj, bl = lane;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        int oj = __shfl_xor_sync(0xffffffffu, bj, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
-        if (beats(ov, oj, ol, bv, bj, bl, perm)) { bv = ov; bj = oj; bl = ol; }
-      }
-      if (lane == 0) { out->v[r] = bv; out->j[r] = bj; }
-      if (lane == bl) hd++;
-    }
-    if (lane == 0) { out->m = mm; out->s = ss; }
-  }
-  __syncthreads();
-}
 
 // Alg. 1 BuildSubtree on a thread-block cluster of CL CTAs (one request).
 // Every round (one step i of Alg. 1):
@@ -206,8 +117,9 @@ HSD_DEV void merge_lists_lanes(int nlists, const float* lv, const int* lj, int k
   }
 }
 
+template <int KT>
 HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, int root_tok, NodesSm& nd,
-                           ClusterSm& cs, float* red_f, int* red_i) {
+                           ClusterSm& cs) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -229,7 +141,7 @@ HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, in
     const float* Lrow = P.L + ((size_t)req * P.N + row0 + i) * P.V;
     // ---- 1. sweep
     float m = -INFINITY, sacc = 0.f;
-    Top t;
+    Top<KT> t;
     top_init(t);
     if (qi < nq) {
       const int tok = cs.Qtok[qi];
@@ -274,7 +186,7 @@ HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, in
         float hv = -INFINITY;
         int hj = -1;
 #pragma unroll
-        for (int q = 0; q < KMAX; ++q)
+        for (int q = 0; q < KT; ++q)
           if (q == head) { hv = t.v[q]; hj = t.j[q]; }
         float bv = hv;
         int bj = hj, bl = lane;
@@ -418,13 +330,12 @@ HSD_DEV void prune_nodes(NodesSm& nd, int keep, NodesSm& tmp) {
   __syncthreads();
 }
 
+template <int KT>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(TreeParams P, int mode) {
   pdl_wait();
   pdl_trigger();
   __shared__ NodesSm nd, tmp;
   __shared__ ClusterSm cs;
-  __shared__ float red_f[64 + 32 * KMAX];
-  __shared__ int red_i[32 * KMAX];
   __shared__ int slot_of[MAXN], maxdepth;
   __shared__ uint64_t anc[MAXN][MAXW];
   const int req = blockIdx.x / CL;
@@ -437,7 +348,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(Tre
     int bonus = P.bonus[req];
     int n_remain = P.N - m - 1;
     if (P.resample && n_remain > P.r && n_remain > 0) {
-      build_subtree(P, req, m + 1, n_remain, bonus, nd, cs, red_f, red_i);
+      build_subtree<KT>(P, req, m + 1, n_remain, bonus, nd, cs);
       if (!leader) return;
       prune_nodes(nd, P.Br, tmp);
     } else {
@@ -460,7 +371,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(Tre
 
   // ---- fresh tree: Alg. 1 over all N rows from the root (last committed token)
   const int root = P.root_tok[req];
-  build_subtree(P, req, 0, P.N, root, nd, cs, red_f, red_i);
+  build_subtree<KT>(P, req, 0, P.N, root, nd, cs);
   if (!leader) return;
   prune_nodes(nd, P.B, tmp);
   // ---- verification fusion with the pending re-sampled tree
@@ -592,5 +503,14 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(Tre
 
 void launch_tree(const TreeParams& P, int mode, int n_req, cudaStream_t st) {
   if (n_req <= 0) return;
-  launch_k(tree_kernel, n_req * CL, NT, 0, st, P, mode);
+  switch (P.k) {
+    case 1: launch_k(tree_kernel<1>, n_req * CL, NT, 0, st, P, mode); break;
+    case 2: launch_k(tree_kernel<2>, n_req * CL, NT, 0, st, P, mode); break;
+    case 3: launch_k(tree_kernel<3>, n_req * CL, NT, 0, st, P, mode); break;
+    case 4: launch_k(tree_kernel<4>, n_req * CL, NT, 0, st, P, mode); break;
+    case 5: launch_k(tree_kernel<5>, n_req * CL, NT, 0, st, P, mode); break;
+    case 6: launch_k(tree_kernel<6>, n_req * CL, NT, 0, st, P, mode); break;
+    case 7: launch_k(tree_kernel<7>, n_req * CL, NT, 0, st, P, mode); break;
+    default: launch_k(tree_kernel<8>, n_req * CL, NT, 0, st, P, mode); break;
+  }
 }
