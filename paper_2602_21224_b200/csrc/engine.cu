@@ -20,6 +20,10 @@
 #include "gemm_tc.cuh"
 
 int64_t g_hsd_launches = 0;
+// Timing ablation (debug only, results become meaningless): HSD_ABLATE is a list
+// of kernel classes to SKIP, e.g. "attn,rms,rope,swiglu,gemm,tree,draft".
+static const char* g_ablate = getenv("HSD_ABLATE");
+static bool ablate(const char* what) { return g_ablate && strstr(g_ablate, what) != nullptr; }
 static bool g_attn_tc = [] {
   const char* e = getenv("HSD_ATTN_TC");
   return e == nullptr || atoi(e) != 0;
@@ -338,6 +342,7 @@ static void* dalloc(hsd_ctx* c, size_t bytes) {
 // C written once (read too when accumulating).
 static void gemm(hsd_ctx* c, const void* A, int lda, const void* Wt, int ldw, float* C, int ldc, int M, int N,
                  int K, bool acc, int cat = -1, bool c_zeroed = false) {
+  if (ablate("gemm")) return;
   if (cat < 0) cat = c->pass_verify ? P_GEMM_VERIFY : P_GEMM_DRAFT;
   Prof pf(c, cat, (double)N * K * c->esz + (double)M * K * c->esz + (double)M * N * 4 * (acc ? 2 : 1),
           2.0 * M * N * K);
@@ -365,13 +370,13 @@ static KVLayer kv_layer(hsd_ctx* c, void* pool, int layer) {
 static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, int n_req, const RowMeta& m,
                           const KVLayer& kv, int max_keys) {
   const int n = c->n;
-  { Prof pf(c, P_ROWWISE); launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st); }
+  if (!ablate("rms")) { Prof pf(c, P_ROWWISE); launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st); }
   // c->big is kept zero outside a GEMM -> consumer window (qkv_rope_kv and
   // swiglu re-zero what they read), so these GEMMs accumulate without a memset
   gemm(c, c->a, n, w.wqkv, n, c->big, c->qkvd, M, c->qkvd, n, false, -1, true);
-  { Prof pf(c, P_ROWWISE);
+  if (!ablate("rope")) { Prof pf(c, P_ROWWISE);
     launch_qkv_rope_kv(c->big, M, m, c->rope_cos, c->rope_sin, c->Hq, kv, c->qb, c->dt, c->st); }
-  {
+  if (!ablate("attn")) {
     // algorithmic attention bytes: the request's committed K/V rows once (per
     // kv head) + q/out rows; exact per-row key counts are device-side, so the
     // host uses the capacity-free estimate recorded by hsd_profile_read callers.
@@ -385,7 +390,7 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
                        c->st);
   }
   gemm(c, c->ob, c->qd, w.wo, c->qd, x, n, M, n, c->qd, true);
-  { Prof pf(c, P_ROWWISE); launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st); }
+  if (!ablate("rms")) { Prof pf(c, P_ROWWISE); launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st); }
   bool fused = false;
   if (c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, 2 * c->f, n, n, n) && gemm_tc_dp(M, 2 * c->f)) {
     // data-parallel gate/up GEMM with SwiGLU in the epilogue, bf16 h straight to c->a
@@ -400,7 +405,7 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
   if (!fused) {
     gemm(c, c->a, n, w.wgu, n, c->big, 2 * c->f, M, 2 * c->f, n, false, -1, true);
     Prof pf(c, P_ROWWISE);
-    launch_swiglu(c->big, M, c->f, c->h, c->dt, m.pos, c->st);
+    if (!ablate("swiglu")) launch_swiglu(c->big, M, c->f, c->h, c->dt, m.pos, c->st);
   }
   gemm(c, c->h, c->f, w.wd, c->f, x, n, M, n, c->f, true);
   g_hsd_launches += 6;  // rmsnorm x2, rope_kv, attention(+merge counted below), swiglu
@@ -449,7 +454,7 @@ static void stage_build(hsd_ctx* c) {
   P.plant_stride = c->plant_stride;
   for (int i = 0; i < HSD_MAX_PLANT_DEPTH_DEV; ++i) P.plant_rates[i] = c->cfg.plant_rates[i];
   P.seed = (uint32_t)c->cfg.seed; P.req_offset = c->cfg.req_offset; P.err = c->err;
-  { Prof pf(c, P_TREE); launch_tree(P, TREE_MODE_FRESH, b, c->st); }
+  if (!ablate("tree")) { Prof pf(c, P_TREE); launch_tree(P, TREE_MODE_FRESH, b, c->st); }
   g_hsd_launches += 1;
 }
 
@@ -498,7 +503,7 @@ static void stage_accept(hsd_ctx* c, int32_t* d_emitted, int32_t* d_n) {
   P.L = c->draft_logits; P.table = c->table; P.tdt = c->dt; P.perm = c->perm_d; P.rank_of = c->rank_d;
   P.pt_n = c->pt_n; P.pt_tok = c->pt_tok; P.pt_par = c->pt_par; P.pt_depth = c->pt_depth; P.pt_lj = c->pt_lj;
   P.acc_n = c->acc_n; P.bonus = c->bonus; P.err = c->err;
-  { Prof pf(c, P_RESAMPLE); launch_tree(P, TREE_MODE_RESAMPLE, b, c->st); }
+  if (!ablate("tree")) { Prof pf(c, P_RESAMPLE); launch_tree(P, TREE_MODE_RESAMPLE, b, c->st); }
   CommitParams M{};
   M.N = c->N; M.t_max = c->T; M.hidden = c->n; M.Hverify = c->Hver;
   M.acc_n = c->acc_n; M.acc_slots = c->acc_slots; M.emitted = c->emitted; M.bonus = c->bonus;
