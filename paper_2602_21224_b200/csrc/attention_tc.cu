@@ -23,6 +23,8 @@
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
 
+unsigned long long* g_attn_trace = nullptr;   // debug phase trace (HSD_ATTN_TRACE)
+
 namespace {
 using namespace tc;
 constexpr int NTHREADS = 320;   // TMA, MMA, 8 softmax warps
@@ -31,6 +33,13 @@ constexpr int CHUNK = 128;     // keys per softmax iteration = 2 pages
 constexpr int STAGES = 2;
 constexpr int QROWS = 128;
 
+// Debug phase trace (HSD_ATTN_TRACE env -> P.trace != null): CTA (0,0,0) records
+// %globaltimer at phase boundaries, softmax thread 64 (lane row 64) and MMA lane.
+HSD_DEV uint64_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 struct AttnParams {
   int M, R, Hq, G, hd, n_qtiles, max_keys, keys_per_split, direct;
   RowMeta m;
@@ -38,7 +47,9 @@ struct AttnParams {
   bf16* out;
   float* ws;
   uint32_t idesc_s, idesc_o;
+  unsigned long long* trace;   // [64] timestamps or null
 };
+#define TRACE(i) do { if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[(i)] = gtime(); } while (0)
 
 // bits [a, b) of a 32-bit word (a, b clamped to [0, 32])
 HSD_DEV uint32_t range32(int a, int b) {
@@ -115,7 +126,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int k_begin = split * P.keys_per_split;
   const int k_end = min(P.max_keys, k_begin + P.keys_per_split);
 
-  if (threadIdx.x == 0) { tile_lo = 0x7fffffff; tile_hi = 0; }
+  if (threadIdx.x == 0) { tile_lo = 0x7fffffff; tile_hi = 0; TRACE(0); }
   if (threadIdx.x == 32) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(qbar, 1);
@@ -130,8 +141,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   __syncthreads();
+  if (threadIdx.x == 0) TRACE(1);
   pdl_wait();      // row metadata, q and this layer's tree K/V come from upstream kernels
   pdl_trigger();
+  if (threadIdx.x == 0) TRACE(2);
   // softmax threads: this lane's (row, head) and its key bounds
   const int q4 = warp & 3;
   const int lane_row = q4 * 32 + lane;                // tile row-head index owned by this thread
@@ -197,6 +210,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp == 1) {
     if (lane == 0 && n_chunks > 0) {
       mbar_wait(qbar, 0);
+      TRACE(3);
       auto issue_s = [&](int j) {
         const int s = j % STAGES;
         mbar_wait(&full[s], (j / STAGES) & 1);
@@ -236,6 +250,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int j = 0; j < n_chunks; ++j) {
       mbar_wait(&sfull[j & 1], (j >> 1) & 1);
       fence_after();
+      if (threadIdx.x == 64 && j < 12) TRACE(8 + 4 * j);
       const int kb = (c_first + j) * CHUNK + half * 64;       // this half's 64 keys
       uint32_t r0[32], r1[32];
       tmem_ld32(tS + lane_off + (uint32_t)((j & 1) * CHUNK + half * 64), r0);
@@ -266,9 +281,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const float alpha = (mrow == -INFINITY) ? (mnew == -INFINITY ? 1.f : 0.f) : ex2(mrow - mnew);
       // nothing visible yet for this row: P must be exactly 0 (not ex2(-inf+inf) = NaN)
       const float msub = mnew == -INFINITY ? 0.f : mnew;
+      if (threadIdx.x == 64 && j < 12) TRACE(9 + 4 * j);
       if (j > 0) {
         mbar_wait(pvdone, (j - 1) & 1);   // O and the P buffer are free
         fence_after();
+        if (threadIdx.x == 64 && j < 12) TRACE(10 + 4 * j);
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
           for (int c = 0; c < hcols; c += 16) {
             uint32_t o[16];
@@ -299,6 +316,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       fence_proxy_async();
       fence_before();
       mbar_arrive(&pfull[j & 1]);
+      if (threadIdx.x == 64 && j < 12) TRACE(11 + 4 * j);
     }
     // ------------------------------------------------------------ epilogue
     red_l[half][lane_row] = lrow;
@@ -306,39 +324,66 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(pvdone, (n_chunks - 1) & 1);
       fence_after();
     }
+    if (threadIdx.x == 64) { TRACE(4); if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[7] = n_chunks; }
     pair_sync(q4);
+    if (threadIdx.x == 64) TRACE(56);
     const float ltot = red_l[0][lane_row] + red_l[1][lane_row];
+    // O half-row (hcols fp32) -> the idle K/V ring (>= 128 rows x hd fp32) ->
+    // each warp then writes its 32 rows row by row with coalesced vectors
+    float* ostage = (float*)sK;                       // [128 rows][hd + 4]
+    const int ost = hd + 4;
+    const float inv = (P.direct && ltot > 0.f) ? 1.0f / ltot : 1.0f;
     for (int c = 0; c < hcols; c += 16) {
       uint32_t o[16];
       if (n_chunks > 0) tmem_ld16(tO + lane_off + (uint32_t)(half * hcols + c), o);
       else
         for (int i = 0; i < 16; ++i) o[i] = 0u;
-      if (writable) {
-        const int d0 = half * hcols + c;
+      float* dst = ostage + lane_row * ost + half * hcols + c;
+#pragma unroll
+      for (int i = 0; i < 16; i += 4)
+        *(float4*)(dst + i) = ltot > 0.f ? make_float4(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv,
+                                                       __uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    asm volatile("bar.sync 5, 256;" ::: "memory");   // all 8 softmax warps staged their rows
+    if (threadIdx.x == 64) TRACE(57);
+    // the CTA's valid rows of one (kv head, q-tile): all 256 softmax threads write
+    // them as coalesced 16-byte vectors; split partials go to ONE contiguous block
+    // ws[split][head][row][hd] per (split, head)
+    {
+      const int st = threadIdx.x - 64;
+      const int n_rh = min(QROWS, P.R * P.G - qt * QROWS);        // valid (row, head) pairs in the tile
+      const int nv = n_rh * (hd / 4);
+      for (int v = st; v < nv; v += 256) {
+        const int lr = v / (hd / 4), d4 = (v % (hd / 4)) * 4;
+        const int rh2 = qt * QROWS + lr, rl2 = rh2 / P.G, g2 = rh2 % P.G, row2 = grp * P.R + rl2;
+        if (row2 >= P.M) continue;
+        const int head2 = h * P.G + g2;
+        const float4 x = *(const float4*)(ostage + lr * ost + d4);
         if (P.direct) {
-          const float inv = ltot > 0.f ? 1.0f / ltot : 0.f;
-          bf16* out = P.out + ((size_t)row * P.Hq + head) * hd + d0;
-#pragma unroll
-          for (int i = 0; i < 16; i += 2)
-            *(__nv_bfloat162*)(out + i) =
-                __floats2bfloat162_rn(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
+          const __nv_bfloat162 a = __floats2bfloat162_rn(x.x, x.y), b = __floats2bfloat162_rn(x.z, x.w);
+          *(uint2*)(P.out + ((size_t)row2 * P.Hq + head2) * hd + d4) = make_uint2(*(const uint32_t*)&a, *(const uint32_t*)&b);
         } else {
-          float* out = P.ws + (((size_t)split * P.M + row) * P.Hq + head) * hd + d0;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) out[i] = ltot > 0.f ? __uint_as_float(o[i]) : 0.f;
+          *(float4*)(P.ws + (((size_t)split * P.Hq + head2) * P.M + row2) * hd + d4) = x;
         }
       }
     }
+    if (threadIdx.x == 64) TRACE(58);
     if (!P.direct && writable && half == 0) {
       const size_t base_ml = (size_t)gridDim.x * P.M * P.Hq * hd;
-      const size_t idx = ((size_t)split * P.M + row) * P.Hq + head;
+      const size_t idx = ((size_t)split * P.Hq + head) * P.M + row;
       P.ws[base_ml + 2 * idx] = mrow;      // log2 domain (merge uses exp2)
       P.ws[base_ml + 2 * idx + 1] = ltot;
     }
   }
+  if (threadIdx.x == 0) TRACE(59);
+  if (threadIdx.x == 32) TRACE(60);
+  if (threadIdx.x == 64) TRACE(61);
+  if (threadIdx.x == 96) TRACE(62);
   fence_before();
   __syncthreads();
   fence_after();
+  if (threadIdx.x == 0) TRACE(5);
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
 }
 
@@ -348,17 +393,19 @@ __global__ void attention_merge_bf16_kernel(const float* __restrict__ ws, int S,
                                             bf16* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
+  // one warp per (row, head); partials are laid out ws[split][head][row][hd]
   const int pair = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (pair >= M * Hq) return;
+  const int row = pair / Hq, head = pair % Hq;
   const size_t base = (size_t)S * M * Hq * hd;
   float Mx = -INFINITY;
   for (int s = 0; s < S; ++s) {
-    const size_t idx = (size_t)s * M * Hq + pair;
+    const size_t idx = ((size_t)s * Hq + head) * M + row;
     if (ws[base + 2 * idx + 1] > 0.f) Mx = fmaxf(Mx, ws[base + 2 * idx]);
   }
   float den = 0.f, num[4] = {0.f, 0.f, 0.f, 0.f};
   for (int s = 0; s < S; ++s) {
-    const size_t idx = (size_t)s * M * Hq + pair;
+    const size_t idx = ((size_t)s * Hq + head) * M + row;
     const float l = ws[base + 2 * idx + 1];
     if (l <= 0.f) continue;
     const float w = exp2f(ws[base + 2 * idx] - Mx);   // m is in log2 units
@@ -390,6 +437,12 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   P.M = M; P.R = R; P.Hq = Hq; P.G = G; P.hd = hd; P.m = m; P.kv = kv;
   P.out = (bf16*)out; P.ws = ws; P.max_keys = max_keys;
   P.n_qtiles = (R * G + QROWS - 1) / QROWS;
+  static bool trace_init = [] {
+    if (getenv("HSD_ATTN_TRACE")) cudaMalloc(&g_attn_trace, 64 * 8);
+    return true;
+  }();
+  (void)trace_init;
+  P.trace = g_attn_trace;
   P.idesc_s = idesc_bf16(128, CHUNK);
   P.idesc_o = idesc_bf16(128, hd);
   // splits: enough CTAs for ~2 per SM, each split a whole number of pages

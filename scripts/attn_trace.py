@@ -1,0 +1,25 @@
+import os, sys; sys.path.insert(0, '.')
+os.environ["HSD_ATTN_TRACE"] = "1"
+import numpy as np, torch
+from synth import get_config, prompts
+from paper_2602_21224_b200 import hsd
+cfg = get_config("c2")
+stream = torch.cuda.Stream()
+ctx = hsd.init_model(cfg, device=0, stream=stream.cuda_stream, precision=hsd.BF16, seed=0, max_batch=1,
+                     max_ctx=cfg.prompt_len + 100, tcgen05=True)
+ctx.prefill(prompts(cfg))
+for _ in range(3): ctx.step()
+ctx.build_tree(); ctx.verify_tree()   # the trace holds the last attention launch (verify layer 31)
+t = ctx.tensor("attn_trace").cpu().numpy().astype(np.int64)
+t0 = t[0]
+names = {0: "start", 1: "barriers+tmem", 2: "pdl_wait", 3: "Q landed (mma)", 4: "last PV done", 5: "end"}
+for i in [0, 1, 2, 3]:
+    print(f"{names[i]:16s} {(t[i]-t0)/1e3:8.2f} us")
+n = int(t[7])
+print("chunks", n)
+for j in range(min(n, 12)):
+    print(f" chunk {j}: S ready {(t[8+4*j]-t0)/1e3:7.2f}  max done {(t[9+4*j]-t0)/1e3:7.2f}  pv(j-1) done {(t[10+4*j]-t0)/1e3 if j>0 else float('nan'):7.2f}  P written {(t[11+4*j]-t0)/1e3:7.2f}")
+for i, nm in [(56, "epi: l exchanged"), (57, "epi: O staged"), (58, "epi: rows written"), (59, "warp0 at end"), (60, "warp1 at end"), (61, "thr64 at end"), (62, "thr96 at end")]:
+    print(f"{nm:16s} {(t[i]-t0)/1e3:8.2f} us")
+for i in [4, 5]:
+    print(f"{names[i]:16s} {(t[i]-t0)/1e3:8.2f} us")
