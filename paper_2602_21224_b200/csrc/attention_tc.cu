@@ -448,11 +448,15 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   // splits: enough CTAs for ~2 per SM, each split a whole number of pages
   const int base_ctas = n_req * kv.kv_heads * P.n_qtiles;
   const int pages = (max_keys + CHUNK - 1) / CHUNK;     // chunks of 2 pages
-  // one wave: the kernel holds ~190 KB of shared memory, so one CTA per SM
-  int S = num_sms() / base_ctas;
-  if (S > pages) S = pages;
-  if (S > 32) S = 32;
-  if (S < 1) S = 1;
+  // key splits: the kernel holds ~190 KB of shared memory and all 512 TMEM
+  // columns (one CTA per SM) and pays ~3 chunk-times of fixed cost per CTA (PDL
+  // wait, Q load, epilogue), so extra splits only pay while the grid is under
+  // about one wave: S = round(SMs / base), measured best on c2 (S=4), c3 (S=1,
+  // monotone worse above) and c5 batch 2 (S=2) -- DESIGN.md section 7.
+  int S = max(1, (2 * num_sms() + base_ctas) / (2 * base_ctas));
+  S = min(S, max(1, pages / 2));
+  static const int s_override = [] { const char* e = getenv("HSD_ATTN_SPLITS"); return e ? atoi(e) : 0; }();
+  if (s_override > 0) S = min(s_override, pages);
   while (S > 1 && (size_t)S * M * Hq * (hd + 2) > ws_floats) --S;
   int pps = (pages + S - 1) / S;
   P.keys_per_split = pps * CHUNK;
