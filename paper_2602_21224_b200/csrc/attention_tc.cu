@@ -4,22 +4,25 @@
 //
 // One CTA = (key split, kv head h, request x q-tile of 128 (row, head) pairs).
 //  warp 0      : TMA producer -- the q tile once (3-D map: hd x G heads x rows),
-//                then per 64-key page: K [64 keys x hd] and V^T [hd x 64 keys]
-//                into a 3-stage shared-memory ring (pages via the block table).
-//  warp 1      : MMA issuer -- S_j = Q K_j^T (M=128, N=64, K=hd) into one of two
-//                TMEM score buffers, then O += P_j V_j (M=128, N=hd, K=64) into
-//                the TMEM output accumulator; S_{j+1} is issued before P_j is
-//                ready so softmax of page j overlaps the score MMA of page j+1.
+//                then per 128-key chunk (2 pages via the block table): K [128 x hd]
+//                into a 3-stage K ring (freed by the S MMA) and V^T [hd x 128] into
+//                a 2-stage V ring (freed by the P V MMA); chunks wholly below the
+//                rows this pass writes load before griddepcontrol.wait.
+//  warp 1      : MMA issuer -- S_j = Q K_j^T (M=128, N=128, K=hd) into one of two
+//                TMEM score buffers, S_{j+1} issued before P_j is ready; then
+//                O += P_j V_j (M=128, N=hd, K=128) with P_j read from TMEM (the
+//                bf16 P_j overwrites the first 64 columns of S_j's buffer).
 //  warps 2..9  : softmax -- TMEM lane t = one (row, head) is owned by a PAIR of
-//                warps (same lane quarter), each taking 32 of the page's 64
-//                keys: a 32-bit visibility mask (committed range | tree-ancestor
-//                bits, see attention.cu) is built once per page, scores are
-//                log2-scaled and exponentiated with ex2.approx, the pair
-//                exchanges its row max through shared memory, rescales its half
-//                of the O row in TMEM when the max grows, and writes its half of
-//                P (bf16, 128B-swizzled) for the PV MMA.
-// Splits > 1 write (o, m, l) partials in the SIMT kernel's layout and reuse
-// its merge kernel.
+//                warps (same lane quarter), each taking 64 of the chunk's 128 keys:
+//                a visibility mask (committed range | tree-ancestor bits, see
+//                attention.cu) per 32 keys, scores exponentiated as
+//                ex2(s * log2e/sqrt(hd) - m) in one FFMA + ex2.approx, the pair
+//                exchanging its row max through shared memory. The running max is
+//                raised lazily (only when a chunk exceeds it by > 8 in log2 units),
+//                so the O rescale -- the one step that must wait for P_{j-1} V --
+//                is rare; P_j is written with tcgen05.st and never waits for the
+//                previous PV MMA.
+// Splits > 1 write (o, m, l) partials and a merge kernel combines them.
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
 
@@ -30,7 +33,8 @@ using namespace tc;
 constexpr int NTHREADS = 320;   // TMA, MMA, 8 softmax warps
 constexpr int PAGE = 64;
 constexpr int CHUNK = 128;     // keys per softmax iteration = 2 pages
-constexpr int STAGES = 2;
+constexpr int KSTAGES = 3;     // K ring: a stage frees when its S MMA completes
+constexpr int VSTAGES = 2;     // V ring: a stage frees when its P V MMA completes
 constexpr int QROWS = 128;
 
 // Debug phase trace (HSD_ATTN_TRACE env -> P.trace != null): CTA (0,0,0) records
@@ -90,6 +94,16 @@ HSD_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+HSD_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
 HSD_DEV void pair_sync(int q) { asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory"); }
 
 __global__ void __launch_bounds__(NTHREADS, 1)
@@ -101,20 +115,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int q_bytes = QROWS * hd * 2;          // natom atoms of [128 rows x 128 B]
   const int k_bytes = CHUNK * hd * 2;          // natom atoms of [128 keys x 128 B] (2 pages each)
   const int v_bytes = hd * CHUNK * 2;          // 2 atom columns (pages) of [hd rows x 128 B]
-  const int p_bytes = QROWS * CHUNK * 2;       // 2 atoms (key halves) of [128 rows x 128 B]
   uint8_t* sQ = base;
   uint8_t* sK = sQ + q_bytes;
-  uint8_t* sV = sK + STAGES * k_bytes;
-  uint8_t* sP = sV + STAGES * v_bytes;
-  uint64_t* bars = (uint64_t*)(sP + p_bytes);   // one P buffer: its reuse is ordered by pvdone
-  uint64_t* full = bars;                 // [STAGES]
-  uint64_t* empty = bars + STAGES;       // [STAGES]
-  uint64_t* qbar = bars + 2 * STAGES;
+  uint8_t* sV = sK + KSTAGES * k_bytes;
+  uint64_t* bars = (uint64_t*)(sV + VSTAGES * v_bytes);   // P lives in TMEM over its S buffer
+  uint64_t* kfull = bars;                 // [KSTAGES]
+  uint64_t* kempty = kfull + KSTAGES;     // [KSTAGES]
+  uint64_t* vfull = kempty + KSTAGES;     // [VSTAGES]
+  uint64_t* vempty = vfull + VSTAGES;     // [VSTAGES]
+  uint64_t* qbar = vempty + VSTAGES;
   uint64_t* sfull = qbar + 1;            // [2]
   uint64_t* pfull = sfull + 2;           // [2]
-  uint64_t* pvdone = pfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(pvdone + 1);
-  __shared__ int tile_lo, tile_hi;
+  uint64_t* pvdone = pfull + 2;          // one phase per P_j V_j MMA
+  uint64_t* odone = pvdone + 1;          // after the last P V MMA
+  uint32_t* tmem_slot = (uint32_t*)(odone + 1);
+  __shared__ int tile_lo, tile_hi, safe_hi;
   __shared__ float red_max[2][2][QROWS];   // [chunk parity][half][row]
   __shared__ float red_l[2][QROWS];
 
@@ -126,12 +141,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int k_begin = split * P.keys_per_split;
   const int k_end = min(P.max_keys, k_begin + P.keys_per_split);
 
-  if (threadIdx.x == 0) { tile_lo = 0x7fffffff; tile_hi = 0; TRACE(0); }
+  if (threadIdx.x == 0) { tile_lo = 0x7fffffff; tile_hi = 0; safe_hi = 0x7fffffff; TRACE(0); }
   if (threadIdx.x == 32) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < KSTAGES; ++s) { mbar_init(&kfull[s], 1); mbar_init(&kempty[s], 1); }
+    for (int s = 0; s < VSTAGES; ++s) { mbar_init(&vfull[s], 1); mbar_init(&vempty[s], 1); }
     mbar_init(qbar, 1);
     for (int b = 0; b < 2; ++b) { mbar_init(&sfull[b], 1); mbar_init(&pfull[b], 256); }
     mbar_init(pvdone, 1);
+    mbar_init(odone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -142,9 +159,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   __syncthreads();
   if (threadIdx.x == 0) TRACE(1);
-  pdl_wait();      // row metadata, q and this layer's tree K/V come from upstream kernels
-  pdl_trigger();
-  if (threadIdx.x == 0) TRACE(2);
+  // Programmatic dependent launch: only q and the K/V rows this pass's qkv_rope_kv
+  // writes (every request row's own position) come from the kernel right before
+  // this one. Every kernel upstream of that one has completed when this grid
+  // starts (qkv_rope_kv triggers only after its own griddepcontrol.wait), so the
+  // row metadata and all keys below the request's smallest row position (the
+  // committed cache, earlier draft passes) are final: they are read -- and their
+  // first chunks TMA-loaded -- before the producer's griddepcontrol.wait.
+  pdl_trigger();   // dependents wait for this grid's completion before reading it
   // softmax threads: this lane's (row, head) and its key bounds
   const int q4 = warp & 3;
   const int lane_row = q4 * 32 + lane;                // tile row-head index owned by this thread
@@ -170,6 +192,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       if (hi > lo) { atomicMin(&tile_lo, lo); atomicMax(&tile_hi, hi); }
     }
+    int pmin = 0x7fffffff;
+    for (int r = threadIdx.x - 64; r < P.R; r += 256) {
+      const int pr = grp * P.R + r < P.M ? m.pos[grp * P.R + r] : -1;
+      if (pr >= 0) pmin = min(pmin, pr);
+    }
+    if (pmin != 0x7fffffff) atomicMin(&safe_hi, pmin);
   }
   fence_before();
   __syncthreads();
@@ -188,23 +216,42 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint64_t pol = policy_evict_first();
       const uint64_t polq = policy_evict_last();
       const int row0 = grp * P.R + qt * (QROWS / P.G);
+      auto page_of = [&](int j, int pg) {
+        return P.kv.block_table[(size_t)req * P.kv.pages_per_req + 2 * (c_first + j) + pg];
+      };
+      auto load_k = [&](int j) {
+        const int s = j % KSTAGES;
+        mbar_wait(&kempty[s], ((j / KSTAGES) & 1) ^ 1);
+        mbar_expect_tx(&kfull[s], k_bytes);
+        for (int pg = 0; pg < 2; ++pg) {
+          const int krow = ((page_of(j, pg) * 2 + 0) * P.kv.kv_heads + h) * PAGE;
+          for (int a = 0; a < natom; ++a)
+            tma_load_2d(&tmK, &kfull[s], sK + (size_t)s * k_bytes + a * (CHUNK * 128) + pg * (PAGE * 128), a * 64,
+                        krow, pol);
+        }
+      };
+      auto load_v = [&](int j) {
+        const int s = j % VSTAGES;
+        mbar_wait(&vempty[s], ((j / VSTAGES) & 1) ^ 1);
+        mbar_expect_tx(&vfull[s], v_bytes);
+        for (int pg = 0; pg < 2; ++pg) {
+          const int vrow = ((page_of(j, pg) * 2 + 1) * P.kv.kv_heads + h) * hd;
+          tma_load_2d(&tmV, &vfull[s], sV + (size_t)s * v_bytes + pg * (hd * 128), 0, vrow, pol);
+        }
+      };
+      auto safe = [&](int j) { return (c_first + j + 1) * CHUNK <= safe_hi; };
+      int kj = 0, vj = 0;
+      while (kj < n_chunks && kj < KSTAGES && safe(kj)) load_k(kj++);
+      while (vj < n_chunks && vj < VSTAGES && safe(vj)) load_v(vj++);
+      pdl_wait();
+      if (threadIdx.x == 0) TRACE(2);
       mbar_expect_tx(qbar, q_bytes);
       for (int a = 0; a < natom; ++a)
         tma_load_3d(&tmQ, qbar, sQ + a * (QROWS * 128), a * 64, h * P.G, row0, polq);
-      for (int j = 0; j < n_chunks; ++j) {
-        const int s = j % STAGES;
-        const uint32_t ph = (j / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], k_bytes + v_bytes);
-        for (int pg = 0; pg < 2; ++pg) {
-          const int page = P.kv.block_table[(size_t)req * P.kv.pages_per_req + 2 * (c_first + j) + pg];
-          const int krow = ((page * 2 + 0) * P.kv.kv_heads + h) * PAGE;
-          for (int a = 0; a < natom; ++a)
-            tma_load_2d(&tmK, &full[s], sK + (size_t)s * k_bytes + a * (CHUNK * 128) + pg * (PAGE * 128), a * 64,
-                        krow, pol);
-          const int vrow = ((page * 2 + 1) * P.kv.kv_heads + h) * hd;
-          tma_load_2d(&tmV, &full[s], sV + (size_t)s * v_bytes + pg * (hd * 128), 0, vrow, pol);
-        }
+      // K runs one chunk ahead of V: V_j waits for P_{j-2} V, K_{j+1} must not
+      while (vj < n_chunks) {
+        if (kj < n_chunks && kj <= vj + 1) load_k(kj++);
+        else load_v(vj++);
       }
     }
   } else if (warp == 1) {
@@ -212,8 +259,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(qbar, 0);
       TRACE(3);
       auto issue_s = [&](int j) {
-        const int s = j % STAGES;
-        mbar_wait(&full[s], (j / STAGES) & 1);
+        const int s = j % KSTAGES;
+        mbar_wait(&kfull[s], (j / KSTAGES) & 1);
         fence_after();
         const uint32_t d = tS + (uint32_t)((j & 1) * CHUNK);
         for (int kk = 0; kk < hd / 16; ++kk) {
@@ -223,22 +270,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mma_bf16(d, ad, bd, P.idesc_s, kk > 0 ? 1u : 0u);
         }
         mma_commit(&sfull[j & 1]);
+        mma_commit(&kempty[s]);
       };
       issue_s(0);
       for (int j = 0; j < n_chunks; ++j) {
         if (j + 1 < n_chunks) issue_s(j + 1);
         mbar_wait(&pfull[j & 1], (j >> 1) & 1);
         fence_after();
-        const int s = j % STAGES;
+        const int s = j % VSTAGES;
+        mbar_wait(&vfull[s], (j / VSTAGES) & 1);
+        // O += P_j V_j with P_j (bf16, 2 keys per column) over S_j's TMEM columns;
+        // tcgen05.mma executes in issue order, so S_{j+2} (issued later into the
+        // same columns) cannot overtake this read
+        const uint32_t tP = tS + (uint32_t)((j & 1) * CHUNK);
         for (int kk = 0; kk < CHUNK / 16; ++kk) {
           const int ka = kk >> 2, off = kk & 3;
-          const uint64_t pd = desc_sw128(sP + ka * (QROWS * 128)) + 2 * off;
           const uint64_t vd = desc_sw128(sV + (size_t)s * v_bytes + ka * (hd * 128)) + 2 * off;
-          mma_bf16(tO, pd, vd, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_bf16_ts(tO, tP + (uint32_t)(kk * 8), vd, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        mma_commit(&empty[s]);
+        mma_commit(&vempty[s]);
         mma_commit(pvdone);
       }
+      mma_commit(odone);
     }
   } else {
     // ------------------------------------------------------------ softmax warps
@@ -266,54 +319,60 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         vm0 &= range32(k_begin - kb, k_end - kb);
         vm1 &= range32(k_begin - kb - 32, k_end - kb - 32);
       }
+      // raw scores, -inf where invisible (scale_log2 > 0 keeps the order, and is
+      // folded into the exponent's FFMA below)
       float s[64];
       float mx = -INFINITY;
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        s[i] = ((vm0 >> i) & 1u) ? __uint_as_float(r0[i]) * scale_log2 : -INFINITY;
-        s[32 + i] = ((vm1 >> i) & 1u) ? __uint_as_float(r1[i]) * scale_log2 : -INFINITY;
+        s[i] = ((vm0 >> i) & 1u) ? __uint_as_float(r0[i]) : -INFINITY;
+        s[32 + i] = ((vm1 >> i) & 1u) ? __uint_as_float(r1[i]) : -INFINITY;
         mx = fmaxf(mx, fmaxf(s[i], s[32 + i]));
       }
       red_max[j & 1][half][lane_row] = mx;
       pair_sync(q4);
-      mx = fmaxf(red_max[j & 1][0][lane_row], red_max[j & 1][1][lane_row]);
-      const float mnew = fmaxf(mrow, mx);
-      const float alpha = (mrow == -INFINITY) ? (mnew == -INFINITY ? 1.f : 0.f) : ex2(mrow - mnew);
-      // nothing visible yet for this row: P must be exactly 0 (not ex2(-inf+inf) = NaN)
-      const float msub = mnew == -INFINITY ? 0.f : mnew;
+      mx = fmaxf(red_max[j & 1][0][lane_row], red_max[j & 1][1][lane_row]) * scale_log2;
+      // lazy rescale: keep the running max unless the chunk raises it by more than
+      // 2^8 (P <= 256, exact in bf16's exponent range; fp32 O and l absorb it); a
+      // row with nothing visible yet has O == 0 exactly, so it just adopts the max
+      float alpha = 1.f;
+      if (mrow == -INFINITY) {
+        mrow = mx;
+      } else if (mx > mrow + 8.f) {
+        alpha = ex2(mrow - mx);
+        mrow = mx;
+      }
+      const float msub = mrow == -INFINITY ? 0.f : mrow;   // P = 0, never ex2(-inf + inf)
       if (threadIdx.x == 64 && j < 12) TRACE(9 + 4 * j);
-      if (j > 0) {
-        mbar_wait(pvdone, (j - 1) & 1);   // O and the P buffer are free
-        fence_after();
-        if (threadIdx.x == 64 && j < 12) TRACE(10 + 4 * j);
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
-          for (int c = 0; c < hcols; c += 16) {
-            uint32_t o[16];
-            tmem_ld16(tO + lane_off + (uint32_t)(half * hcols + c), o);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16(tO + lane_off + (uint32_t)(half * hcols + c), o);
-          }
-          tmem_st_wait();
-        }
-      }
+      // P_j (bf16) over this half's 32 columns of S_j (64 keys, 2 per column)
       float psum = 0.f;
-      uint8_t* prow = sP + half * (QROWS * 128) + lane_row * 128;    // key half = one swizzle atom
+      uint32_t pw[32];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint32_t w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float p0 = ex2(s[c * 8 + 2 * e] - msub), p1 = ex2(s[c * 8 + 2 * e + 1] - msub);
-          __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
-          psum += __low2float(pr) + __high2float(pr);     // l sums exactly what the MMA sees
-          w[e] = *(uint32_t*)&pr;
-        }
-        *(uint4*)(prow + ((c ^ (lane_row & 7)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+      for (int i = 0; i < 32; ++i) {
+        const float p0 = ex2(fmaf(s[2 * i], scale_log2, -msub)), p1 = ex2(fmaf(s[2 * i + 1], scale_log2, -msub));
+        __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
+        psum += __low2float(pr) + __high2float(pr);     // l sums exactly what the MMA sees
+        pw[i] = *(uint32_t*)&pr;
       }
+      tmem_st32(tS + lane_off + (uint32_t)((j & 1) * CHUNK + half * 32), pw);
+      if (__any_sync(0xffffffffu, alpha != 1.f)) {
+        // O must hold P_{<j} V exactly once before it is scaled: S_j completing
+        // implies P_{j-2} V done, so pvdone is within one phase of j-1
+        if (j > 0) {
+          mbar_wait(pvdone, (j - 1) & 1);
+          fence_after();
+        }
+        if (threadIdx.x == 64 && j < 12) TRACE(10 + 4 * j);
+        for (int c = 0; c < hcols; c += 16) {
+          uint32_t o[16];
+          tmem_ld16(tO + lane_off + (uint32_t)(half * hcols + c), o);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st16(tO + lane_off + (uint32_t)(half * hcols + c), o);
+        }
+      }
+      tmem_st_wait();
       lrow = lrow * alpha + psum;
-      mrow = mnew;
-      fence_proxy_async();
       fence_before();
       mbar_arrive(&pfull[j & 1]);
       if (threadIdx.x == 64 && j < 12) TRACE(11 + 4 * j);
@@ -321,7 +380,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // ------------------------------------------------------------ epilogue
     red_l[half][lane_row] = lrow;
     if (n_chunks > 0) {
-      mbar_wait(pvdone, (n_chunks - 1) & 1);
+      mbar_wait(odone, 0);
       fence_after();
     }
     if (threadIdx.x == 64) { TRACE(4); if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[7] = n_chunks; }
@@ -351,21 +410,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // them as coalesced 16-byte vectors; split partials go to ONE contiguous block
     // ws[split][head][row][hd] per (split, head)
     {
-      const int st = threadIdx.x - 64;
+      // warp w takes tile rows w*rpi + lane/vpr, stepping 8*rpi; lanes cover hd
+      // as float4s; (row, head) of a tile row advance incrementally (no divides)
+      const int sw = (threadIdx.x - 64) >> 5;
       const int n_rh = min(QROWS, P.R * P.G - qt * QROWS);        // valid (row, head) pairs in the tile
-      const int nv = n_rh * (hd / 4);
-      for (int v = st; v < nv; v += 256) {
-        const int lr = v / (hd / 4), d4 = (v % (hd / 4)) * 4;
-        const int rh2 = qt * QROWS + lr, rl2 = rh2 / P.G, g2 = rh2 % P.G, row2 = grp * P.R + rl2;
-        if (row2 >= P.M) continue;
-        const int head2 = h * P.G + g2;
-        const float4 x = *(const float4*)(ostage + lr * ost + d4);
-        if (P.direct) {
-          const __nv_bfloat162 a = __floats2bfloat162_rn(x.x, x.y), b = __floats2bfloat162_rn(x.z, x.w);
-          *(uint2*)(P.out + ((size_t)row2 * P.Hq + head2) * hd + d4) = make_uint2(*(const uint32_t*)&a, *(const uint32_t*)&b);
-        } else {
-          *(float4*)(P.ws + (((size_t)split * P.Hq + head2) * P.M + row2) * hd + d4) = x;
+      const int vpr = hd / 4, rpi = 32 / vpr;
+      const int d4 = (lane % vpr) * 4;
+      const int step = 8 * rpi, step_rl = step / P.G, step_g = step % P.G;
+      int lr = sw * rpi + lane / vpr;
+      int rl2 = (qt * QROWS + lr) / P.G, g2 = (qt * QROWS + lr) % P.G;
+      for (; lr < n_rh; lr += step) {
+        const int row2 = grp * P.R + rl2, head2 = h * P.G + g2;
+        if (row2 < P.M) {
+          const float4 x = *(const float4*)(ostage + lr * ost + d4);
+          if (P.direct) {
+            const __nv_bfloat162 a = __floats2bfloat162_rn(x.x, x.y), b = __floats2bfloat162_rn(x.z, x.w);
+            *(uint2*)(P.out + ((size_t)row2 * P.Hq + head2) * hd + d4) =
+                make_uint2(*(const uint32_t*)&a, *(const uint32_t*)&b);
+          } else {
+            *(float4*)(P.ws + (((size_t)split * P.Hq + head2) * P.M + row2) * hd + d4) = x;
+          }
         }
+        rl2 += step_rl;
+        g2 += step_g;
+        if (g2 >= P.G) { g2 -= P.G; ++rl2; }
       }
     }
     if (threadIdx.x == 64) TRACE(58);
@@ -477,8 +545,8 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   if (!tma_map_bf16(&mq, q, 3, dq, sq, bq) || !tma_map_bf16(&mk, kv.base, 2, dk, sk, bk) ||
       !tma_map_bf16(&mv, kv.base, 2, dv, sv, bv))
     return -1;
-  const size_t smem = 1024 + (size_t)QROWS * hd * 2 + STAGES * ((size_t)CHUNK * hd * 2 * 2) +
-                      (size_t)QROWS * CHUNK * 2 + (2 * STAGES + 7) * 8 + 64;
+  const size_t smem = 1024 + (size_t)QROWS * hd * 2 + (KSTAGES + VSTAGES) * ((size_t)CHUNK * hd * 2) +
+                      (2 * KSTAGES + 2 * VSTAGES + 8) * 8 + 64;
   static size_t attr = 0;   // (the kernel also has ~1 KB of static shared memory)
   if (smem > attr) {
     if (cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=

@@ -66,6 +66,15 @@ HSD_DEV void mma_bf16(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t idesc, 
       "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
       : "memory");
 }
+// A operand from TMEM (lane = row of A, 32-bit column = 2 consecutive K elements,
+// low half first), B from a shared-memory descriptor
+HSD_DEV void mma_bf16_ts(uint32_t dtmem, uint32_t atmem, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dtmem),
+      "r"(atmem), "l"(bd), "r"(idesc), "r"(acc)
+      : "memory");
+}
 HSD_DEV void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");

@@ -1,13 +1,15 @@
 import os, sys; sys.path.insert(0, '.')
 os.environ["HSD_ATTN_TRACE"] = "1"
 import numpy as np, torch
-from synth import get_config, prompts
+from synth import get_config, prompts, vocab_permutation
 from paper_2602_21224_b200 import hsd
-cfg = get_config("c2")
+cfg = get_config(sys.argv[1] if len(sys.argv) > 1 else "c2")
+batch = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 stream = torch.cuda.Stream()
-ctx = hsd.init_model(cfg, device=0, stream=stream.cuda_stream, precision=hsd.BF16, seed=0, max_batch=1,
-                     max_ctx=cfg.prompt_len + 100, tcgen05=True)
-ctx.prefill(prompts(cfg))
+ctx = hsd.init_model(cfg, device=0, stream=stream.cuda_stream, precision=hsd.BF16, seed=0, max_batch=batch,
+                     max_ctx=cfg.prompt_len + 100, tcgen05=True,
+                     vocab_perm=vocab_permutation(cfg.vocab, 0) if cfg.hot_tokens else None)
+ctx.prefill(prompts(cfg, batch=batch))
 for _ in range(3): ctx.step()
 ctx.build_tree(); ctx.verify_tree()   # the trace holds the last attention launch (verify layer 31)
 t = ctx.tensor("attn_trace").cpu().numpy().astype(np.int64)
@@ -17,7 +19,7 @@ for i in [0, 1, 2, 3]:
     print(f"{names[i]:16s} {(t[i]-t0)/1e3:8.2f} us")
 n = int(t[7])
 print("chunks", n)
-for j in range(min(n, 12)):
+for j in range(min(n, 12)):  # pv(j-1) is only stamped when the chunk rescales O
     print(f" chunk {j}: S ready {(t[8+4*j]-t0)/1e3:7.2f}  max done {(t[9+4*j]-t0)/1e3:7.2f}  pv(j-1) done {(t[10+4*j]-t0)/1e3 if j>0 else float('nan'):7.2f}  P written {(t[11+4*j]-t0)/1e3:7.2f}")
 for i, nm in [(56, "epi: l exchanged"), (57, "epi: O staged"), (58, "epi: rows written"), (59, "warp0 at end"), (60, "warp1 at end"), (61, "thr64 at end"), (62, "thr96 at end")]:
     print(f"{nm:16s} {(t[i]-t0)/1e3:8.2f} us")
