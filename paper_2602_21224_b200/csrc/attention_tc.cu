@@ -83,6 +83,16 @@ HSD_DEV float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+HSD_DEV void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) {   // caller issues tcgen05.wait::ld
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
 HSD_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -306,8 +316,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (threadIdx.x == 64 && j < 12) TRACE(8 + 4 * j);
       const int kb = (c_first + j) * CHUNK + half * 64;       // this half's 64 keys
       uint32_t r0[32], r1[32];
-      tmem_ld32(tS + lane_off + (uint32_t)((j & 1) * CHUNK + half * 64), r0);
-      tmem_ld32(tS + lane_off + (uint32_t)((j & 1) * CHUNK + half * 64 + 32), r1);
+      tmem_ld32_nw(tS + lane_off + (uint32_t)((j & 1) * CHUNK + half * 64), r0);
+      tmem_ld32_nw(tS + lane_off + (uint32_t)((j & 1) * CHUNK + half * 64 + 32), r1);
       uint32_t vm0 = 0u, vm1 = 0u;
       if (valid) {
         vm0 = range32(klo - kb, khi - kb);
@@ -319,16 +329,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         vm0 &= range32(k_begin - kb, k_end - kb);
         vm1 &= range32(k_begin - kb - 32, k_end - kb - 32);
       }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       // raw scores, -inf where invisible (scale_log2 > 0 keeps the order, and is
       // folded into the exponent's FFMA below)
       float s[64];
-      float mx = -INFINITY;
+      if (__all_sync(0xffffffffu, (vm0 & vm1) == 0xffffffffu)) {   // whole warp sees all 64 keys
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        s[i] = ((vm0 >> i) & 1u) ? __uint_as_float(r0[i]) : -INFINITY;
-        s[32 + i] = ((vm1 >> i) & 1u) ? __uint_as_float(r1[i]) : -INFINITY;
-        mx = fmaxf(mx, fmaxf(s[i], s[32 + i]));
+        for (int i = 0; i < 32; ++i) { s[i] = __uint_as_float(r0[i]); s[32 + i] = __uint_as_float(r1[i]); }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          s[i] = ((vm0 >> i) & 1u) ? __uint_as_float(r0[i]) : -INFINITY;
+          s[32 + i] = ((vm1 >> i) & 1u) ? __uint_as_float(r1[i]) : -INFINITY;
+        }
       }
+      // 8 independent max chains (a single chain is 64 dependent FMNMX)
+      float mxp[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mxp[k] = s[k];
+#pragma unroll
+      for (int i = 8; i < 64; ++i) mxp[i & 7] = fmaxf(mxp[i & 7], s[i]);
+      float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                       fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
       red_max[j & 1][half][lane_row] = mx;
       pair_sync(q4);
       mx = fmaxf(red_max[j & 1][0][lane_row], red_max[j & 1][1][lane_row]) * scale_log2;
@@ -345,15 +367,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const float msub = mrow == -INFINITY ? 0.f : mrow;   // P = 0, never ex2(-inf + inf)
       if (threadIdx.x == 64 && j < 12) TRACE(9 + 4 * j);
       // P_j (bf16) over this half's 32 columns of S_j (64 keys, 2 per column)
-      float psum = 0.f;
+      float ps[4] = {0.f, 0.f, 0.f, 0.f};                 // 4 independent sum chains
       uint32_t pw[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const float p0 = ex2(fmaf(s[2 * i], scale_log2, -msub)), p1 = ex2(fmaf(s[2 * i + 1], scale_log2, -msub));
         __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
-        psum += __low2float(pr) + __high2float(pr);     // l sums exactly what the MMA sees
+        ps[i & 3] += __low2float(pr) + __high2float(pr);     // l sums exactly what the MMA sees
         pw[i] = *(uint32_t*)&pr;
       }
+      const float psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
       tmem_st32(tS + lane_off + (uint32_t)((j & 1) * CHUNK + half * 32), pw);
       if (__any_sync(0xffffffffu, alpha != 1.f)) {
         // O must hold P_{<j} V exactly once before it is scaled: S_j completing
