@@ -1089,6 +1089,16 @@ hsd_status hsd_debug_gemm(const void* A, int32_t lda, const void* W, int32_t ldw
   } else if (use_tc) {
     if (dtype != 1 || !gemm_tc_supported(M, N, K, lda, ldw)) return HSD_EUNSUP;
     g_hsd_launches += gemm_tc_bf16((const bf16*)A, lda, (const bf16*)W, ldw, C, ldc, M, N, K, accumulate != 0, st);
+    extern unsigned long long* g_gemm_trace;
+    if (g_gemm_trace) {   // debug (HSD_GEMM_TRACE): phase stamps of this launch, us from CTA 0's start
+      unsigned long long t[32];
+      cudaStreamSynchronize(st);
+      cudaMemcpy(t, g_gemm_trace, sizeof(t), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "gemm_trace M=%d N=%d K=%d", M, N, K);
+      for (int i = 0; i < 32; ++i)
+        if (i % 16 < 8) fprintf(stderr, " %.2f", t[i] ? (double)(long long)(t[i] - t[0]) / 1e3 : -1.0);
+      fprintf(stderr, "\n");
+    }
   } else {
     gemm_simt(A, lda, W, ldw, dtype == 1 ? DT_BF16 : DT_F32, C, ldc, M, N, K, accumulate != 0, st);
     g_hsd_launches += 1;

@@ -20,6 +20,8 @@
 #include "gemm_tc.cuh"
 #include "tc_ptx.cuh"
 
+unsigned long long* g_gemm_trace = nullptr;   // HSD_GEMM_TRACE: last launch's phase stamps
+
 namespace {
 using namespace tc;
 constexpr int BM = 128;          // weight rows per tile (UMMA M)
@@ -43,7 +45,18 @@ struct TcParams {
   float* C;
   bf16* H;                        // EPI_SWIGLU output [M, N/2] bf16
   int ldh;
+  unsigned long long* trace;      // debug phase trace (HSD_GEMM_TRACE) or null
 };
+HSD_DEV uint64_t gtime_g() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// CTA 0 records slots 0..15, the last CTA slots 16..31: start, pre-PDL weight
+// loads issued, PDL released, first / last stage landed (MMA), epilogue start /
+// end, CTA end
+#define GTRACE(i) do { if (P.trace && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) \
+    P.trace[(blockIdx.x == 0 ? 0 : 16) + (i)] = gtime_g(); } while (0)
 
 // The idx-th (tile, k-block) unit of this CTA. Stream-K: a contiguous range of
 // units; data-parallel: whole tiles blockIdx.x, blockIdx.x + grid, ...
@@ -75,6 +88,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   float* stage_buf = (float*)(bars + 2 * P.stages + 6);   // [16 tokens][EPI_LD] fp32
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) GTRACE(0);
   Sched sc;
   sc.dp = P.dp;
   sc.n_kb = P.n_kb;
@@ -121,7 +135,9 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         mbar_expect_tx(&full[i], A_BYTES + b_bytes);
         tma_load_2d(&tmW, &full[i], sA + (size_t)i * A_BYTES, kb * BK, (t / P.n_tiles_t) * BM, pw);
       }
+      GTRACE(1);
       pdl_wait();
+      GTRACE(2);
       for (long i = 0; i < npre; ++i) {
         const long u = sc.unit(i);
         const int t = (int)(u / P.n_kb), kb = (int)(u % P.n_kb);
@@ -156,6 +172,8 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         }
         mbar_wait(&full[stage], phase);
         fence_after();
+        if (i == 0) GTRACE(3);
+        if (i == sc.count - 1) GTRACE(4);
         const uint64_t ad = desc_sw128(sA + (size_t)stage * A_BYTES);
         const uint64_t bd = desc_sw128(sB + (size_t)stage * b_bytes);
         const uint32_t dt = tmem + (uint32_t)(buf * P.ntile);
@@ -191,6 +209,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       const int tn = t / P.n_tiles_t, tt = t % P.n_tiles_t;
       mbar_wait(&tfull[buf], aphase);
       fence_after();
+      if (threadIdx.x == 64) GTRACE(5);
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * P.ntile);
       for (int c0 = 0; c0 < P.ntile; c0 += 16) {
         uint32_t r[16];
@@ -247,6 +266,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         }
         epi_bar();
       }
+      if (threadIdx.x == 64) GTRACE(6);
       fence_before();
       mbar_arrive(&tempty[buf]);
       buf ^= 1;
@@ -257,6 +277,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   fence_before();
   __syncthreads();
   fence_after();
+  if (threadIdx.x == 0) GTRACE(7);
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
 }
@@ -339,6 +360,13 @@ static int gemm_tc_launch(const bf16* A, int lda, const bf16* W, int ldw, float*
                           int epi, int dp, bf16* H, int ldh, cudaStream_t st) {
   TcParams P;
   P.M = M; P.N = N; P.K = K; P.ldc = ldc; P.C = C; P.H = H; P.ldh = ldh; P.epi = epi; P.dp = dp;
+  static unsigned long long* trace = [] {
+    unsigned long long* t = nullptr;
+    if (getenv("HSD_GEMM_TRACE")) { cudaMalloc(&t, 32 * 8); cudaMemset(t, 0, 32 * 8); }
+    return t;
+  }();
+  P.trace = trace;
+  g_gemm_trace = trace;
   int nt, ntt;
   tc_tiles(M, nt, ntt);
   P.ntile = nt;
@@ -355,7 +383,8 @@ static int gemm_tc_launch(const bf16* A, int lda, const bf16* W, int ldw, float*
   // at least 3 stages in flight: wide token tiles (compute-bound shapes) get a
   // bigger ring and one CTA per SM instead of two shallow ones
   int ring = ring_kb * 1024, cps = per_sm;
-  if (ring / (A_BYTES + b_bytes) < 3) { ring = 200 * 1024; cps = 1; }
+  static const int min_stages = [] { const char* e = getenv("HSD_GEMM_MIN_STAGES"); return e ? atoi(e) : 3; }();
+  if (ring / (A_BYTES + b_bytes) < min_stages) { ring = 200 * 1024; cps = 1; }
   int stages = ring / (A_BYTES + b_bytes);
   if (stages > 16) stages = 16;
   if (stages < 2) stages = 2;

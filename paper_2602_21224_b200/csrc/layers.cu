@@ -99,14 +99,73 @@ void launch_embed(const void* E, DType dt, const int32_t* tok, const int32_t* po
 // One CTA per row: thread t handles rotation pairs (head, j) strided over the
 // row's q and k heads, then the v head dims; the fp32 scratch row is re-zeroed
 // after the CTA has read it (so the next tcgen05 GEMM into it needs no memset).
+constexpr int ROPE_PARTS = 8;     // q/k CTAs per row
+constexpr int VROWS = 32;         // rows per V-transpose CTA
+
+// V rows -> the transposed cache V^T [hd][page_size] per (page, kv head): a CTA
+// takes a 32-row x 32-dim tile of one kv head, reads it along hd (lane = dim,
+// 128-byte rows; all 8 loads of a thread issued before its zeroing stores) into
+// shared memory and writes it along the rows (lane = row), so consecutive
+// lanes hit consecutive slots -- contiguous for a tree / prompt chunk, whose
+// rows sit at consecutive cache positions.
+template <typename T>
+__device__ void v_transpose_block(float* __restrict__ qkv, const RowMeta& m, int M, int Hq, const KVLayer& kv,
+                                  int vb) {
+  const int hd = kv.head_dim, Hkv = kv.kv_heads, ld = (Hq + 2 * Hkv) * hd;
+  const int nd = (hd + 31) / 32;
+  const int dc = vb % nd, h = (vb / nd) % Hkv, r0 = (vb / nd / Hkv) * VROWS;
+  __shared__ float tile[VROWS][33];
+  __shared__ int pg[VROWS], sl[VROWS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;   // 4 warps
+  const int nr = min(VROWS, M - r0), d = dc * 32 + lane;
+  if (threadIdx.x < VROWS) {
+    const int r = r0 + threadIdx.x;
+    int page = -1, slot = 0;
+    if (threadIdx.x < nr && m.pos[r] >= 0) {
+      const int kp = m.kvpos[r];
+      page = kv.block_table[(size_t)m.req[r] * kv.pages_per_req + kp / kv.page_size];
+      slot = kp % kv.page_size;
+    }
+    pg[threadIdx.x] = page;
+    sl[threadIdx.x] = slot;
+  }
+  float v[VROWS / 4];
+  float* src = qkv + (size_t)r0 * ld + (Hq + Hkv) * hd + h * hd + d;
+#pragma unroll
+  for (int k = 0; k < VROWS / 4; ++k) {
+    const int rr = w + 4 * k;
+    v[k] = (rr < nr && d < hd) ? src[(size_t)rr * ld] : 0.f;
+  }
+#pragma unroll
+  for (int k = 0; k < VROWS / 4; ++k) {
+    const int rr = w + 4 * k;
+    if (rr < nr && d < hd) src[(size_t)rr * ld] = 0.f;    // re-zero the GEMM scratch (see below)
+    tile[rr][lane] = v[k];
+  }
+  __syncthreads();
+  T* base = (T*)kv.base;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int dd = dc * 32 + w + 4 * k;           // lane = row
+    if (lane < nr && pg[lane] >= 0 && dd < hd)
+      base[kv_offset(pg[lane], 1, Hkv, h, kv.page_size, hd, sl[lane], dd)] = from_f32<T>(tile[lane][w + 4 * k]);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(128) qkv_rope_kv_kernel(float* __restrict__ qkv, RowMeta m,
                                                           const float* __restrict__ rc,
                                                           const float* __restrict__ rs, int Hq, KVLayer kv,
-                                                          T* __restrict__ q_out) {
+                                                          T* __restrict__ q_out, int M) {
   pdl_wait();
   pdl_trigger();
-  const int r = blockIdx.x, part = blockIdx.y, nparts = gridDim.y;   // row r, column chunk `part`
+  const int n_v = (M + VROWS - 1) / VROWS * kv.kv_heads * ((kv.head_dim + 31) / 32);
+  if ((int)blockIdx.x < n_v) {          // V-transpose CTAs first (fewer, longer), then rope
+    v_transpose_block<T>(qkv, m, M, Hq, kv, blockIdx.x);
+    return;
+  }
+  const int rb = blockIdx.x - n_v;
+  const int r = rb / ROPE_PARTS, part = rb % ROPE_PARTS, nparts = ROPE_PARTS;
   const int hd = kv.head_dim, half = hd / 2, Hkv = kv.kv_heads;
   const int ld = (Hq + 2 * Hkv) * hd;
   float* row = qkv + (size_t)r * ld;
@@ -135,10 +194,6 @@ __global__ void __launch_bounds__(128) qkv_rope_kv_kernel(float* __restrict__ qk
         base[kv_offset(page, 0, Hkv, h - Hq, kv.page_size, hd, slot, j + half)] = from_f32<T>(y2);
       }
     }
-    for (int i = tid; i < Hkv * hd; i += nthr) {
-      const int h = i / hd, d = i % hd;
-      base[kv_offset(page, 1, Hkv, h, kv.page_size, hd, slot, d)] = from_f32<T>(row[(Hq + Hkv) * hd + i]);
-    }
   }
   // Each element was read by exactly this thread (same tid -> same indices), so
   // re-zeroing the scratch needs no cross-CTA barrier: zero what this thread read.
@@ -148,9 +203,8 @@ __global__ void __launch_bounds__(128) qkv_rope_kv_kernel(float* __restrict__ qk
       row[h * hd + j] = 0.f;
       row[h * hd + j + half] = 0.f;
     }
-    for (int i = tid; i < Hkv * hd; i += nthr) row[(Hq + Hkv) * hd + i] = 0.f;
   } else {
-    for (int i = tid; i < ld; i += nthr) row[i] = 0.f;
+    for (int i = tid; i < (Hq + Hkv) * hd; i += nthr) row[i] = 0.f;   // V columns: the V CTAs
   }
 }
 
@@ -158,10 +212,11 @@ void launch_qkv_rope_kv(float* qkv, int M, const RowMeta& m, const float* rope_c
                         const float* rope_sin, int Hq, const KVLayer& kv, void* q_out, DType dt,
                         cudaStream_t st) {
   if (M <= 0) return;
+  const int grid = M * ROPE_PARTS + (M + VROWS - 1) / VROWS * kv.kv_heads * ((kv.head_dim + 31) / 32);
   if (dt == DT_F32)
-    launch_k(qkv_rope_kv_kernel<float>, dim3(M, 8), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out);
+    launch_k(qkv_rope_kv_kernel<float>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out, M);
   else
-    launch_k(qkv_rope_kv_kernel<bf16>, dim3(M, 8), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out);
+    launch_k(qkv_rope_kv_kernel<bf16>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out, M);
 }
 
 // ------------------------------------------------------------------ SwiGLU
