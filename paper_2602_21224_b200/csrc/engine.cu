@@ -385,6 +385,7 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
     if (c->use_tc && g_attn_tc && attention_tc_supported(c->hd, c->page_size, c->dt))
       tc_launched = launch_attention_tc(c->qb, M, R, n_req, m, kv, c->Hq, max_keys, c->ob, c->attn_ws,
                                         c->attn_ws_floats, c->kv_layer_elems, c->st);
+    if (tc_launched > 1) g_hsd_launches += tc_launched - 1;   // the split merge
     if (tc_launched < 0)
       launch_attention(c->qb, M, R, n_req, m, kv, c->Hq, c->dt, max_keys, c->ob, c->attn_ws, c->attn_ws_floats,
                        c->st);
@@ -405,10 +406,10 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
   if (!fused) {
     gemm(c, c->a, n, w.wgu, n, c->big, 2 * c->f, M, 2 * c->f, n, false, -1, true);
     Prof pf(c, P_ROWWISE);
-    if (!ablate("swiglu")) launch_swiglu(c->big, M, c->f, c->h, c->dt, m.pos, c->st);
+    if (!ablate("swiglu")) { launch_swiglu(c->big, M, c->f, c->h, c->dt, m.pos, c->st); g_hsd_launches += 1; }
   }
   gemm(c, c->h, c->f, w.wd, c->f, x, n, M, n, c->f, true);
-  g_hsd_launches += 6;  // rmsnorm x2, rope_kv, attention(+merge counted below), swiglu
+  g_hsd_launches += 4;  // rmsnorm x2, rope_kv, attention (merge and swiglu counted where launched)
 }
 
 // ---------------------------------------------------------------------- stages

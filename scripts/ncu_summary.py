@@ -1,6 +1,6 @@
 """Summarise `ncu --set full` reports (.ncu-rep) into a text table for profiles/.
 
-usage: python scripts/ncu_summary.py REPORT.ncu-rep [label] [--algo-bytes B1,B2,...]
+usage: python scripts/ncu_summary.py REPORT.ncu-rep [label] [--algo-bytes B1,B2,...] [--algo-flops F1,F2,...]
 """
 import csv
 import io
@@ -33,9 +33,11 @@ def load(path):
 def main():
     path = sys.argv[1]
     label = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("--") else path
-    algo = None
+    algo = flops = None
     if "--algo-bytes" in sys.argv:
         algo = [float(x) for x in sys.argv[sys.argv.index("--algo-bytes") + 1].split(",")]
+    if "--algo-flops" in sys.argv:
+        flops = [float(x) for x in sys.argv[sys.argv.index("--algo-flops") + 1].split(",")]
     h, units, rows = load(path)
     idx = {n: i for i, n in enumerate(h)}
     kcol = idx.get("Kernel Name", idx.get("Function Name"))
@@ -43,6 +45,8 @@ def main():
     cols = ["kernel"] + [m[1] for m in METRICS if any(n.endswith(m[0]) for n in h)]
     if algo:
         cols += ["algo_MB", "achieved_GB/s", "traffic/algo"]
+    if flops:
+        cols += ["algo_GFLOP", "achieved_TFLOP/s"]
     print(" | ".join(cols))
     for li, r in enumerate(rows):
         vals = [r[kcol].split("(")[0][-40:]]
@@ -61,6 +65,9 @@ def main():
             a = algo[li]
             traffic = (got.get("dram_rd_MB", 0) + got.get("dram_wr_MB", 0)) * 1e6
             vals += [f"{a / 1e6:.2f}", f"{a / (got['dur_us'] * 1e-6) / 1e9:.1f}", f"{traffic / a:.3f}"]
+        if flops and li < len(flops):
+            f = flops[li]
+            vals += [f"{f / 1e9:.1f}", f"{f / (got['dur_us'] * 1e-6) / 1e12:.1f}"]
         print(" | ".join(vals))
 
 
