@@ -1,0 +1,90 @@
+"""ablation toggles and the one-pass head, measured on B200.
+
+Ablations (c2 shapes, planted continuation R24 so that acceptance is real and
+controlled; the verify / walk / compaction kernels run unmodified):
+  full            re-sampling (Alg. 2) + verification fusion        (the method)
+  resample-off    no Alg. 2 re-sampled tree                          (P:355-375 off)
+  fusion-off      Alg. 2 tree built every step but never verified    (its cost without its benefit)
+  token-info-off  zero token-info table: Alg. 1 degenerates to a beam tree over the draft
+                  logits alone (Fig. 5a)
+Reported per variant: tau (emitted / step / request), ms / step, tokens / s, and the per-depth
+conditional acceptance P(m >= d | m >= d-1) measured from the emitted counts -- with re-sampling
+off it should reproduce the planted rates a_d (a check of the planted mechanism itself).
+
+One-pass head (NEXT-2): the draft's N lm_head rows as ONE [b*N, n] x [n, V] GEMM
+against N separate [b, n] x [n, V] GEMMs (what an iterative token-level draft pays), timed with
+CUDA events on the library's tcgen05 GEMM.
+
+usage: python scripts/ablation.py [--config c2] [--steps 30] [--warmup 5] [--out FILE.json]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np
+import torch
+import bench
+from synth import get_config, prompts, vocab_permutation
+from paper_2602_21224_b200 import hsd
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--steps", type=int, default=20)
+ap.add_argument("--warmup", type=int, default=5)
+ap.add_argument("--out", default="")
+a = ap.parse_args()
+cfg = get_config(a.config)
+N, b = cfg.steps_N, cfg.batch
+rates = bench.PLANT_RATES[:N] + [bench.PLANT_RATES[-1]] * max(0, N - len(bench.PLANT_RATES))
+VARIANTS = [("full", hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION),
+            ("resample-off", hsd.FLAG_FUSION),
+            ("fusion-off", hsd.FLAG_RESAMPLE),
+            ("token-info-off", hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | hsd.FLAG_ZERO_TABLE)]
+stream = torch.cuda.Stream()
+pr = prompts(cfg, batch=b)
+need_ctx = cfg.prompt_len + (a.steps + a.warmup + 12) * (N + 1) * 2 + 16
+rows = []
+for name, flags in VARIANTS:
+    ctx = hsd.init_model(cfg, device=0, stream=stream.cuda_stream, precision=hsd.BF16, seed=0, max_batch=b,
+                         max_ctx=need_ctx + 64 * (N + 1), tcgen05=True, flags=flags | hsd.FLAG_PLANTED,
+                         plant_rates=rates, vocab_perm=vocab_permutation(cfg.vocab, 0) if cfg.hot_tokens else None)
+    with torch.cuda.stream(stream):
+        tau, tps, ms, info, counts = bench.planted_leg(ctx, pr, cfg, b, N, a.steps, a.warmup, stream,
+                                                       return_counts=True, attempts=6)
+    m = counts.reshape(-1) - 1                      # accepted drafts per request-step
+    cond = []
+    for d in range(1, N + 1):
+        base = int((m >= d - 1).sum())
+        cond.append(round(float((m >= d).sum()) / base, 3) if base else None)
+    rows.append({"variant": name, "tau": round(tau, 3), "ms_per_step": round(ms, 3), "tokens_per_s": round(tps, 1),
+                 "cond_accept_by_depth": cond, **info})
+    print(json.dumps(rows[-1]), flush=True)
+    ctx.destroy()
+    del ctx
+    torch.cuda.empty_cache()
+
+# NEXT-2: one-pass head vs N iterative head GEMMs (weights [V, n] bf16 streamed each time)
+W = (torch.randn(cfg.vocab, cfg.hidden, device="cuda") * 0.01).to(torch.bfloat16)
+head = {}
+for label, M, reps in [("one-pass [b*N rows]", b * N, 1), ("iterative (N x [b rows])", b, N)]:
+    A = torch.randn(M, cfg.hidden, device="cuda").to(torch.bfloat16)
+    C = torch.zeros(M, cfg.vocab, device="cuda")
+    for _ in range(3):
+        hsd.debug_gemm(A, W, C, use_tc=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    it = 20
+    e0.record()
+    for _ in range(it):
+        for _ in range(reps):
+            hsd.debug_gemm(A, W, C, use_tc=True)
+    e1.record()
+    torch.cuda.synchronize()
+    head[label] = round(e0.elapsed_time(e1) * 1e3 / it, 2)
+print(json.dumps({"head_us": head, "rows": b * N, "vocab": cfg.vocab, "hidden": cfg.hidden}), flush=True)
+if a.out:
+    json.dump({"config": a.config, "planted_rates": rates, "steps": a.steps, "ablation": rows, "head_us": head},
+              open(a.out, "w"), indent=1)
