@@ -1097,7 +1097,7 @@ hsd_status hsd_debug_gemm(const void* A, int32_t lda, const void* W, int32_t ldw
       cudaMemcpy(t, g_gemm_trace, sizeof(t), cudaMemcpyDeviceToHost);
       fprintf(stderr, "gemm_trace M=%d N=%d K=%d", M, N, K);
       for (int i = 0; i < 32; ++i)
-        if (i % 16 < 8) fprintf(stderr, " %.2f", t[i] ? (double)(long long)(t[i] - t[0]) / 1e3 : -1.0);
+        if (i % 16 < 12) fprintf(stderr, " %.2f", t[i] ? (double)(long long)(t[i] - t[0]) / 1e3 : -1.0);
       fprintf(stderr, "\n");
     }
   } else {

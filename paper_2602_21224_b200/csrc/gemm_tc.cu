@@ -102,10 +102,28 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     sc.count = (long)(blockIdx.x + 1) * P.units / gridDim.x - sc.u0;
   }
 
-  if (threadIdx.x == 32) {
+  // Thread 0 initialises the barriers and, before the CTA-wide barrier, issues
+  // the first ring stages' WEIGHT loads (no kernel writes the weights, so they
+  // may precede griddepcontrol.wait): the TMA latency overlaps warp 2's TMEM
+  // allocation and the predecessor's drain. Token tiles only after the wait.
+  const long npre = sc.count < P.stages ? sc.count : P.stages;
+  uint64_t pw = 0, px = 0;
+  if (threadIdx.x == 0) {
     for (int s = 0; s < P.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 128); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+    pw = policy_evict_first();
+    px = policy_evict_last();
+    GTRACE(9);
+    for (long i = 0; i < npre; ++i) {
+      const long u = sc.unit(i);
+      const int t = (int)(u / P.n_kb), kb = (int)(u % P.n_kb);
+      mbar_expect_tx(&full[i], A_BYTES + b_bytes);
+      tma_load_2d(&tmW, &full[i], sA + (size_t)i * A_BYTES, kb * BK, (t / P.n_tiles_t) * BM, pw);
+      if (i == 0) GTRACE(11);
+    }
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -116,25 +134,13 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   fence_before();
   __syncthreads();
   fence_after();
+  if (threadIdx.x == 0) GTRACE(8);
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
 
   if (warp == 0) {
     // ---------------- TMA producer
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
-      const uint64_t pw = policy_evict_first(), px = policy_evict_last();
-      // PDL: the weight tiles of the first ring stages do not depend on the
-      // previous kernel -- stream them before griddepcontrol.wait, so the ring
-      // fills while the predecessor drains; token tiles only after the wait.
-      const long npre = sc.count < P.stages ? sc.count : P.stages;
-      for (long i = 0; i < npre; ++i) {
-        const long u = sc.unit(i);
-        const int t = (int)(u / P.n_kb), kb = (int)(u % P.n_kb);
-        mbar_expect_tx(&full[i], A_BYTES + b_bytes);
-        tma_load_2d(&tmW, &full[i], sA + (size_t)i * A_BYTES, kb * BK, (t / P.n_tiles_t) * BM, pw);
-      }
       GTRACE(1);
       pdl_wait();
       GTRACE(2);
