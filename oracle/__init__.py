@@ -17,6 +17,8 @@ Pins (tests/test_oracle_*.py):
   attention- torch scaled_dot_product_attention (float64) per root path.
   table    - PAPER.md:168 "15.3 GB" at |V|=128,256 FP8; PAPER.md:406 "1/16";
              row RMS = 1; cold rows/cols exactly 0; W_E[t]·W1·W2 by brute force.
+  fp8      - e4m3 table rows (R25): the 254 finite codes decoded bit by bit,
+             torch float8_e4m3fn cast, ties to even, saturation, row amax = 448.
   tree     - Fig. 5 worked example (PAPER.md:299, :303): 0.6, 0.3, 0.42, 0.294;
              k=1 greedy chain; zero table == beam tree; independent recursive
              brute-force builder; node-count bound.

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import numpy as np
 
+from .fp8 import quantize_row
 from .philox import round_bf16
 
 TABLE_EPS = 1e-6
@@ -34,11 +35,13 @@ class TokenInfoTable:
 
     Rows are computed on demand from the factors (the collapsed matrix is
     W_collapsed row t); `precision='bf16'` rounds stored entries to bfloat16 as
-    the GPU table stores them (SURVEY.md §8(a) init row)."""
+    the GPU table stores them (SURVEY.md §8(a) init row); `fp8=True` stores
+    them as e4m3 codes with one scale per row instead (R25)."""
 
     def __init__(self, model, hot_tokens: int = 0, perm: np.ndarray | None = None,
-                 zero: bool = False):
+                 zero: bool = False, fp8: bool = False):
         self.model = model
+        self.fp8 = fp8       # FP8 e4m3 rows with a per-row scale (reading R25, oracle/fp8.py)
         V = model.cfg.vocab
         self.V = V
         self.zero = zero
@@ -56,7 +59,9 @@ class TokenInfoTable:
             r = collapse_row(self.model, t)
             r = r / np.sqrt(np.mean(r * r) + TABLE_EPS)        # RMSNorm over the full row
             r = np.where(self.hot, r, 0.0)                     # 2-D prune: cold columns
-            if self.model.precision == "bf16":
+            if self.fp8:
+                r, _ = quantize_row(r)                         # cold columns stay exactly 0
+            elif self.model.precision == "bf16":
                 r = round_bf16(r.astype(np.float32)).astype(np.float64)
             self._cache[t] = r
         return self._cache[t]
