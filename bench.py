@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (profiling runs)")
     ap.add_argument("--no-planted", action="store_true", help="skip the planted-continuation leg")
+    ap.add_argument("--table-fp8", action="store_true",
+                    help="token-info table as e4m3 codes + per-row scale (NEXT-3, reading R25)")
     ap.add_argument("--batch", type=int, default=None, help="override the config's global batch")
     return ap.parse_args()
 
@@ -305,7 +307,8 @@ def main():
     plant_rates = PLANT_RATES[:N] + [PLANT_RATES[-1]] * max(0, N - len(PLANT_RATES))
     ctx = hsd.init_model(cfg, device=local, stream=stream.cuda_stream, precision=hsd.BF16, seed=args.seed,
                          max_batch=b, max_ctx=max_ctx + 64 * (N + 1), req_offset=lo, vocab_perm=perm,
-                         tcgen05=not args.simt, flags=hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | hsd.FLAG_PLANTED,
+                         tcgen05=not args.simt, flags=hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | hsd.FLAG_PLANTED |
+                         (hsd.FLAG_TABLE_FP8 if args.table_fp8 else 0),
                          plant_rates=plant_rates)
     pr = prompts(cfg, batch=cfg.batch)[lo:hi]
     ctx.prefill(pr)
@@ -424,7 +427,8 @@ def main():
                        "prompt_len": cfg.prompt_len, "tree": f"N{N} k{cfg.branch_k} B{cfg.budget_B} Br{cfg.resample_budget_Br}",
                        "accept": cfg.accept, "parallelism": parallel, "gemm": "simt" if args.simt else "tcgen05",
                        "l2": "no flush: every step streams >13 GB of weights (>> 126 MB L2)",
-                       "weights": "Philox random-init (no trained weights)"},
+                       "weights": "Philox random-init (no trained weights)",
+                       "table": "fp8 e4m3 + row scale" if args.table_fp8 else "bf16"},
             "tau": round(emitted_all / (args.steps * cfg.batch if cfg.batch >= world else args.steps * world * b), 4),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "tau_curve": tau_curve, "planted": planted,

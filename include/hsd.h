@@ -51,7 +51,9 @@ enum {                                               /* hsd_config.flags       *
   HSD_FLAG_FUSION = 1u << 1,    /* verification fusion             */
   HSD_FLAG_PLANTED = 1u << 2,   /* planted-continuation perf mode (DESIGN R24) */
   HSD_FLAG_ZERO_TABLE = 1u << 3,/* token info off: Alg. 1 == beam tree */
-  HSD_FLAG_TCGEN05 = 1u << 4    /* bf16 GEMMs on tcgen05 (else SIMT FFMA)       */
+  HSD_FLAG_TCGEN05 = 1u << 4,   /* bf16 GEMMs on tcgen05 (else SIMT FFMA)       */
+  HSD_FLAG_TABLE_FP8 = 1u << 5  /* token-info table as e4m3 codes + a per-row
+                                   fp32 scale (DESIGN R25)        */
 };
 
 #define HSD_MAX_PLANT_DEPTH 16
@@ -163,7 +165,8 @@ hsd_status hsd_sync(hsd_ctx* ctx);
 
 /* Debug/test access to named device tensors (e.g. "kv", "draft_logits",
  * "table", "pos", "pend_tok", "acc_slots", "bonus"). Fills a device pointer,
- * dtype code (0 f32, 1 bf16, 2 i32, 3 u64) and up to 4 dims. */
+ * dtype code (0 f32, 1 bf16, 2 i32, 3 u64, 4 u8) and up to 4 dims. With
+ * HSD_FLAG_TABLE_FP8, "table" is u8 e4m3 codes [Vh, Vh] and "table_scale" f32 [Vh]. */
 typedef struct { void* ptr; int32_t dtype; int32_t ndim; int64_t dims[4]; } hsd_tensor;
 hsd_status hsd_get_tensor(hsd_ctx* ctx, const char* name, hsd_tensor* out);
 

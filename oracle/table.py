@@ -52,13 +52,19 @@ class TokenInfoTable:
             self.hot[perm[:hot_tokens]] = True
         self._cache = {}
 
+    def fp64_row(self, t: int) -> np.ndarray:
+        """The row before storage rounding: RMSNorm over the full row, cold columns 0."""
+        if self.zero or not self.hot[t]:
+            return np.zeros(self.V)
+        r = collapse_row(self.model, t)
+        r = r / np.sqrt(np.mean(r * r) + TABLE_EPS)            # RMSNorm over the full row
+        return np.where(self.hot, r, 0.0)                      # 2-D prune: cold columns
+
     def row(self, t: int) -> np.ndarray:
         if self.zero or not self.hot[t]:
             return np.zeros(self.V)
         if t not in self._cache:
-            r = collapse_row(self.model, t)
-            r = r / np.sqrt(np.mean(r * r) + TABLE_EPS)        # RMSNorm over the full row
-            r = np.where(self.hot, r, 0.0)                     # 2-D prune: cold columns
+            r = self.fp64_row(t)
             if self.fp8:
                 r, _ = quantize_row(r)                         # cold columns stay exactly 0
             elif self.model.precision == "bf16":

@@ -206,6 +206,7 @@ struct hsd_ctx {
   std::vector<LayerW> layers;
   LayerW draft{};
   void* table = nullptr;
+  float* table_scale = nullptr;   // HSD_FLAG_TABLE_FP8: per-row e4m3 scale [Vh] (R25)
   int32_t *perm_d = nullptr, *rank_d = nullptr;
   float *rope_cos = nullptr, *rope_sin = nullptr;
   int max_pos = 0;
@@ -445,7 +446,7 @@ static void stage_build(hsd_ctx* c) {
   P.fusion = (c->cfg.flags & HSD_FLAG_FUSION) ? 1 : 0;
   P.resample = (c->cfg.flags & HSD_FLAG_RESAMPLE) ? 1 : 0;
   P.zero_table = (c->cfg.flags & HSD_FLAG_ZERO_TABLE) ? 1 : 0;
-  P.L = c->draft_logits; P.table = c->table; P.tdt = c->dt; P.perm = c->perm_d; P.rank_of = c->rank_d;
+  P.L = c->draft_logits; P.table = c->table; P.tdt = c->dt; P.tscale = c->table_scale; P.perm = c->perm_d; P.rank_of = c->rank_d;
   P.root_tok = c->root_tok;
   P.pt_n = c->pt_n; P.pt_tok = c->pt_tok; P.pt_par = c->pt_par; P.pt_depth = c->pt_depth; P.pt_lj = c->pt_lj;
   P.t_n = c->t_n; P.t_tok = c->t_tok; P.t_par = c->t_par; P.t_depth = c->t_depth; P.t_lj = c->t_lj;
@@ -501,7 +502,7 @@ static void stage_accept(hsd_ctx* c, int32_t* d_emitted, int32_t* d_n) {
   P.fusion = (c->cfg.flags & HSD_FLAG_FUSION) ? 1 : 0;
   P.resample = (c->cfg.flags & HSD_FLAG_RESAMPLE) ? 1 : 0;
   P.zero_table = (c->cfg.flags & HSD_FLAG_ZERO_TABLE) ? 1 : 0;
-  P.L = c->draft_logits; P.table = c->table; P.tdt = c->dt; P.perm = c->perm_d; P.rank_of = c->rank_d;
+  P.L = c->draft_logits; P.table = c->table; P.tdt = c->dt; P.tscale = c->table_scale; P.perm = c->perm_d; P.rank_of = c->rank_d;
   P.pt_n = c->pt_n; P.pt_tok = c->pt_tok; P.pt_par = c->pt_par; P.pt_depth = c->pt_depth; P.pt_lj = c->pt_lj;
   P.acc_n = c->acc_n; P.bonus = c->bonus; P.err = c->err;
   if (!ablate("tree")) { Prof pf(c, P_RESAMPLE); launch_tree(P, TREE_MODE_RESAMPLE, b, c->st); }
@@ -676,7 +677,10 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     float* C1 = (float*)A((size_t)Vh * d * 4);
     int chunk = (int)std::max<size_t>(1, std::min<size_t>(Vh, (size_t)(512u << 20) / ((size_t)V * 4)));
     float* C2 = (float*)A((size_t)chunk * V * 4);
-    c->table = A((size_t)Vh * Vh * es);
+    const bool fp8 = (cfg->flags & HSD_FLAG_TABLE_FP8) != 0;
+    const size_t tes = fp8 ? 1 : es;               // e4m3 codes + a per-row scale (R25)
+    c->table = A((size_t)Vh * Vh * tes);
+    if (fp8) c->table_scale = (float*)A((size_t)Vh * 4);
     if (fail_alloc) { hsd_destroy(c); return HSD_ENOMEM; }
     launch_philox_fill(w1, c->dt, (size_t)d * n, seed, 3, sc(n), c->st);
     launch_philox_fill(w2, c->dt, (size_t)V * d, seed, 4, sc(d), c->st);
@@ -687,7 +691,10 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     for (int r0 = 0; r0 < Vh; r0 += chunk) {
       int rows = std::min(chunk, Vh - r0);
       gemm_simt(C1 + (size_t)r0 * d, d, W2f, d, DT_F32, C2, V, rows, V, d, false, c->st);
-      launch_table_rows(C2, rows, V, Vh, nullptr, (char*)c->table + (size_t)r0 * Vh * es, c->dt, c->st);
+      if (fp8)
+        launch_table_rows_fp8(C2, rows, V, Vh, (char*)c->table + (size_t)r0 * Vh, c->table_scale + r0, c->st);
+      else
+        launch_table_rows(C2, rows, V, Vh, nullptr, (char*)c->table + (size_t)r0 * Vh * es, c->dt, c->st);
     }
     CU(cudaStreamSynchronize(c->st));
     for (void* p : {w1, w2, (void*)Esel, (void*)W1f, (void*)W2f, (void*)C1, (void*)C2}) {
@@ -1067,7 +1074,8 @@ hsd_status hsd_get_tensor(hsd_ctx* ctx, const char* name, hsd_tensor* out) {
   if (s == "bonus") return set(c->bonus, 2, {b});
   if (s == "emitted") return set(c->emitted, 2, {b, N + 1});
   if (s == "n_emitted") return set(c->n_emitted, 2, {b});
-  if (s == "table") return set(c->table, adt, {c->Vh, c->Vh});
+  if (s == "table") return set(c->table, c->table_scale ? 4 : adt, {c->Vh, c->Vh});
+  if (s == "table_scale" && c->table_scale) return set(c->table_scale, 0, {c->Vh});
   if (s == "embed") return set(c->embed, adt, {c->V, n});
   if (s == "head") return set(c->head, adt, {c->V, n});
   if (s == "kv") return set(c->kv_t, adt, {std::max(1, c->L), c->maxb * c->pages_per_req, 2, (int64_t)c->Hkv * c->page_size * c->hd});

@@ -49,6 +49,38 @@ __global__ void table_rows_kernel(const float* __restrict__ E, int V, int Vh, T*
   for (int i = threadIdx.x; i < Vh; i += blockDim.x) o[i] = from_f32<T>(e[i] * inv);
 }
 
+// FP8 variant (reading R25): the same RMSNorm row, then one scale per row
+// s = max_j |row[j]| / 448 over the stored (hot) columns and e4m3 codes
+// RNE(row / s) with saturation (cvt.rn.satfinite.e4m3x2.f32).
+__global__ void table_rows_fp8_kernel(const float* __restrict__ E, int V, int Vh, __nv_fp8_storage_t* __restrict__ table,
+                                      float* __restrict__ scale) {
+  __shared__ float red[32];
+  __shared__ float s_sc;
+  int r = blockIdx.x;
+  const float* e = E + (size_t)r * V;
+  float s = 0.f;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) s += e[i] * e[i];
+  s = block_sum(s, red);
+  const float inv = 1.0f / sqrtf(s / (float)V + 1e-6f);
+  float amax = 0.f;
+  for (int i = threadIdx.x; i < Vh; i += blockDim.x) amax = fmaxf(amax, fabsf(e[i] * inv));
+  amax = block_max(amax, red);
+  if (threadIdx.x == 0) {
+    s_sc = amax > 0.f ? amax / 448.0f : 1.0f;
+    scale[r] = s_sc;
+  }
+  __syncthreads();
+  const float sc = s_sc;
+  __nv_fp8_storage_t* o = table + (size_t)r * Vh;
+  for (int i = threadIdx.x; i < Vh; i += blockDim.x)
+    o[i] = __nv_cvt_float_to_fp8(__fdiv_rn(e[i] * inv, sc), __NV_SATFINITE, __NV_E4M3);
+}
+
+void launch_table_rows_fp8(const float* E, int rows, int V, int Vh, void* table, float* scale, cudaStream_t st) {
+  if (rows <= 0) return;
+  table_rows_fp8_kernel<<<rows, 512, 0, st>>>(E, V, Vh, (__nv_fp8_storage_t*)table, scale);
+}
+
 void launch_table_rows(const float* E, int rows, int V, int Vh, const int32_t* /*unused*/, void* table,
                        DType dt, cudaStream_t st) {
   if (rows <= 0) return;

@@ -35,6 +35,7 @@ HSD_DEV size_t kv_offset(int page, int kind, int Hkv, int h, int ps, int hd, int
 // init.cu
 void launch_philox_fill(void* out, DType dt, size_t count, uint32_t seed, uint32_t tid, float scale,
                         cudaStream_t st);
+void launch_table_rows_fp8(const float* E, int rows, int V, int Vh, void* table, float* scale, cudaStream_t st);
 void launch_table_rows(const float* E, int rows, int V, int Vh, const int32_t* col_of_rank,
                        void* table, DType dt, cudaStream_t st);
 void launch_gather_rows_f32(const void* src, DType dt, const int32_t* idx, int rows, int n, float* dst,

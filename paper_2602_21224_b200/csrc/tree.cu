@@ -156,9 +156,15 @@ HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, in
           const int j = base + u * gthreads;
           lv[u] = j < hi ? Lrow[j] : 0.f;
           float b = 0.f;
-          if (has_bias && j < hi && j < P.Vh)
-            b = P.tdt == DT_F32 ? ((const float*)P.table)[(size_t)rk * P.Vh + j]
-                                : to_f32(((const bf16*)P.table)[(size_t)rk * P.Vh + j]);
+          if (has_bias && j < hi && j < P.Vh) {
+            const size_t ix = (size_t)rk * P.Vh + j;
+            if (P.tscale) {
+              const __half_raw hr = __nv_cvt_fp8_to_halfraw(((const __nv_fp8_storage_t*)P.table)[ix], __NV_E4M3);
+              b = __half2float(__half(hr)) * P.tscale[rk];
+            } else {
+              b = P.tdt == DT_F32 ? ((const float*)P.table)[ix] : to_f32(((const bf16*)P.table)[ix]);
+            }
+          }
           bv[u] = b;
         }
 #pragma unroll

@@ -12,6 +12,7 @@ struct TreeParams {
   const float* L;            // [b, N, V] draft logits, columns in rank order
   const void* table;         // [Vh, Vh] token-info bias, rank-indexed
   DType tdt;
+  const float* tscale;       // non-null: table holds e4m3 codes, row r scaled by tscale[r] (R25)
   const int32_t* perm;       // [V] rank -> token (null = identity)
   const int32_t* rank_of;    // [V] token -> rank (null = identity)
   const int32_t* root_tok;   // [b] last committed token

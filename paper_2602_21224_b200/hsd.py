@@ -20,7 +20,7 @@ HSD_OK, HSD_EINVAL, HSD_ENOMEM, HSD_ECUDA, HSD_ENCCL, HSD_ESTATE, HSD_EUNSUP, HS
 STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ESTATE", -6: "EUNSUP", -7: "EDEVICE"}
 FP32_VERIFY, BF16 = 0, 1
 GREEDY, STOCHASTIC = 0, 1
-FLAG_RESAMPLE, FLAG_FUSION, FLAG_PLANTED, FLAG_ZERO_TABLE, FLAG_TCGEN05 = 1, 2, 4, 8, 16
+FLAG_RESAMPLE, FLAG_FUSION, FLAG_PLANTED, FLAG_ZERO_TABLE, FLAG_TCGEN05, FLAG_TABLE_FP8 = 1, 2, 4, 8, 16, 32
 MAX_PLANT_DEPTH = 16
 
 EXPORTS = ["hsd_config_defaults", "hsd_init_model", "hsd_prefill", "hsd_set_plant", "hsd_build_tree",
@@ -240,7 +240,7 @@ class Context:
         t = Tensor()
         self._check(self.lib.hsd_get_tensor(self.h, name.encode(), C.byref(t)))
         shape = [t.dims[i] for i in range(t.ndim)]
-        typestr = {0: "<f4", 1: "<i2", 2: "<i4", 3: "<u8"}[t.dtype]
+        typestr = {0: "<f4", 1: "<i2", 2: "<i4", 3: "<u8", 4: "|u1"}[t.dtype]
         x = torch.as_tensor(_CAI(t.ptr, shape, typestr), device=f"cuda:{self.device}")
         return x.view(torch.bfloat16) if t.dtype == 1 else x
 

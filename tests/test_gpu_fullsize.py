@@ -47,8 +47,9 @@ class GpuTableRows:
     the Alg. 1 check. The rows themselves are checked against the oracle's
     table separately (test below), so the chain stays independent."""
 
-    def __init__(self, ctx, cfg, perm):
+    def __init__(self, ctx, cfg, perm, fp8=False):
         self.t = ctx.tensor("table")
+        self.scale = ctx.tensor("table_scale").cpu().numpy().astype(np.float64) if fp8 else None
         self.V, self.perm = cfg.vocab, perm
         self.Vh = self.t.shape[0]
         self.rank = None
@@ -62,7 +63,10 @@ class GpuTableRows:
             rk = tok if self.rank is None else int(self.rank[tok])
             out = np.zeros(self.V)
             if rk < self.Vh:
-                vals = self.t[rk].float().cpu().numpy().astype(np.float64)
+                if self.scale is not None:    # e4m3 codes x the row's scale (R25)
+                    vals = self.t[rk].view(torch.float8_e4m3fn).to(torch.float64).cpu().numpy() * self.scale[rk]
+                else:
+                    vals = self.t[rk].float().cpu().numpy().astype(np.float64)
                 cols = np.arange(self.Vh) if self.perm is None else self.perm[:self.Vh]
                 out[cols] = vals
             self._c[tok] = out
@@ -117,26 +121,30 @@ def _margins_ok(margins, kinds, thr):
     return all(mg >= thr for kind, mg in margins if kind in kinds)
 
 
-def run_fullsize(name, n_steps_graph=2, n_checked=2, check_reqs=None):
+def run_fullsize(name, n_steps_graph=2, n_checked=2, check_reqs=None, table_fp8=False):
     cfg = get_config(name)
     seed = 0
     perm = vocab_permutation(cfg.vocab, 0) if cfg.hot_tokens else None
     stream = torch.cuda.Stream()
     max_ctx = cfg.prompt_len + (n_steps_graph + n_checked + 4) * (cfg.steps_N + 1) + 16
     ctx = hsd.init_model(cfg, device=0, stream=stream.cuda_stream, precision=hsd.BF16, seed=seed,
-                         max_batch=cfg.batch, max_ctx=max_ctx, vocab_perm=perm, tcgen05=True)
+                         max_batch=cfg.batch, max_ctx=max_ctx, vocab_perm=perm, tcgen05=True,
+                         flags=hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | (hsd.FLAG_TABLE_FP8 if table_fp8 else 0))
     ctx.prefill(prompts(cfg))
     for _ in range(n_steps_graph):
         ctx.step()                                   # bench configuration: graph replay
     ctx.sync()
-    table = GpuTableRows(ctx, cfg, perm)
+    table = GpuTableRows(ctx, cfg, perm, fp8=table_fp8)
     # the GPU table rows themselves vs the oracle's W_E[t] W1 W2 + RMSNorm (+ 2-D hot prune)
-    otable = TokenInfoTable(TableModel(cfg, seed), hot_tokens=cfg.hot_tokens, perm=perm)
+    otable = TokenInfoTable(TableModel(cfg, seed), hot_tokens=cfg.hot_tokens, perm=perm, fp8=table_fp8)
+    # bf16: rounding of the stored entry; fp8: one e4m3 step at the row maximum (32 / 448 of
+    # max|row|) -- the GPU's fp32 row and the oracle's fp64 row may straddle a rounding midpoint
+    row_tol = 32.0 / 448.0 if table_fp8 else 1e-2
     sample = [int(t) for t in ctx.tensor("root_tok").cpu().numpy()[:4]] + \
         [int(t) for t in (perm[:3] if perm is not None else [0, 1, 2])]
     for t in sample:
         ref, got = otable.row(t), table.row(t)
-        assert np.max(np.abs(got - ref)) <= 1e-2 * np.max(np.abs(ref)) + 1e-6, f"table row {t}"
+        assert np.max(np.abs(got - ref)) <= row_tol * np.max(np.abs(ref)) + 1e-6, f"table row {t}"
     reqs = list(range(cfg.batch)) if check_reqs is None else check_reqs
     N, k, B, Br, r_thr = cfg.steps_N, cfg.branch_k, cfg.budget_B, cfg.resample_budget_Br, cfg.resample_threshold_r
     ppr = ctx.tensor("kv").shape[1] // cfg.batch
@@ -236,6 +244,12 @@ def run_fullsize(name, n_steps_graph=2, n_checked=2, check_reqs=None):
 def test_fullsize_c2_greedy():
     st = run_fullsize("c2", n_steps_graph=2, n_checked=3)
     assert st["tree"] + st["flags"] == 3 and st["walk"] >= 2 and st["kv"] >= 6
+
+
+def test_fullsize_c3_fp8_table():
+    """NEXT-3: the c3 step with the FP8 (e4m3, per-row scale) token-info table."""
+    st = run_fullsize("c3", n_steps_graph=1, n_checked=1, check_reqs=list(range(0, 32, 8)), table_fp8=True)
+    assert st["tree"] >= 3 and st["walk"] >= 3
 
 
 def test_fullsize_c3_stochastic_hot_batch32():

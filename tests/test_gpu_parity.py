@@ -13,6 +13,7 @@ from synth import get_config, prompts, vocab_permutation
 from oracle.model import Model, layer_tid
 from oracle.table import TokenInfoTable
 from oracle.engine import greedy_decode
+from oracle.fp8 import round_e4m3
 from tests.gpu_lockstep import Lockstep
 
 pytestmark = pytest.mark.gpu
@@ -55,13 +56,60 @@ def test_token_info_table(precision, hot):
     ctx.destroy()
 
 
+def e4m3_step(q):
+    """Spacing of e4m3 values around |q| (3 mantissa bits; 2^-9 in the subnormal range)."""
+    a = np.abs(q)
+    return np.where(a < 2.0 ** -6, 2.0 ** -9, 2.0 ** (np.floor(np.log2(np.maximum(a, 2.0 ** -6))) - 3))
+
+
+@pytest.mark.parametrize("precision,hot", [(hsd.FP32_VERIFY, 0), (hsd.BF16, 0), (hsd.BF16, 128)])
+def test_token_info_table_fp8(precision, hot):
+    """FP8 table (R25): per-row scale = max|row| / 448 and e4m3 codes. The GPU row
+    (fp32) and the oracle row (fp64) may straddle a rounding midpoint, so codes are
+    compared to within one e4m3 step and must agree almost everywhere."""
+    cfg = get_config("c1").replace(vocab=512 if hot else 256, hot_tokens=hot)
+    perm = vocab_permutation(cfg.vocab, 0)
+    ctx = ctx_for(cfg, precision, seed=3, vocab_perm=perm if hot else None,
+                  flags=hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | hsd.FLAG_TABLE_FP8)
+    codes = ctx.tensor("table")
+    assert codes.dtype == torch.uint8
+    q = codes.view(torch.float8_e4m3fn).to(torch.float64).cpu().numpy()
+    sc = ctx.tensor("table_scale").cpu().numpy().astype(np.float64)
+    m = Model(cfg, seed=3, precision="fp32" if precision == hsd.FP32_VERIFY else "bf16", layers=0)
+    o8 = TokenInfoTable(m, hot_tokens=hot, perm=perm if hot else None, fp8=True)
+    Vh = hot or cfg.vocab
+    rank_tok = perm[:Vh] if hot else np.arange(cfg.vocab)
+    same = total = 0
+    for rk in range(0, Vh, max(1, Vh // 16)):
+        tok = int(rank_tok[rk])
+        r64 = o8.fp64_row(tok)[rank_tok]
+        s_ref = np.abs(r64).max() / 448.0
+        assert sc[rk] == pytest.approx(s_ref, rel=1e-5)
+        qref = round_e4m3(r64 / s_ref)                     # the oracle's codes (R25)
+        assert np.allclose(o8.row(tok)[rank_tok], qref * s_ref, rtol=1e-15, atol=0)
+        assert np.all(np.abs(q[rk] - qref) <= e4m3_step(np.maximum(np.abs(q[rk]), np.abs(qref))) + 1e-12)
+        assert np.max(np.abs(q[rk])) == 448.0
+        same += int(np.sum(q[rk] == qref)); total += qref.size
+    assert same / total > 0.99, same / total
+    ctx.destroy()
+
+
+def test_lockstep_c1_fp8_table():
+    """The whole step with the FP8 table in fp32-verify mode: the oracle's Alg. 1
+    uses its own e4m3 rows; output stays the plain greedy decode (lossless)."""
+    ls, accs = run_lockstep(get_config("c1"), hsd.FP32_VERIFY, steps=12, seed=1, table_fp8=True)
+    assert ls.checked["tree"] == 12 and ls.checked["accept"] == 12
+
+
 def run_lockstep(cfg, precision, steps, seed=0, batch=1, planted=False, accept="greedy", hot=0, tol=None,
-                 flag=None, expect_no_flags=False, tcgen05=False):
+                 flag=None, expect_no_flags=False, tcgen05=False, table_fp8=False):
     perm = vocab_permutation(cfg.vocab, 0) if hot else None
     pr = prompts(cfg, batch=batch)
     m = Model(cfg, seed=seed, precision="fp32" if precision == hsd.FP32_VERIFY else "bf16")
-    table = TokenInfoTable(m, hot_tokens=hot, perm=perm)
+    table = TokenInfoTable(m, hot_tokens=hot, perm=perm, fp8=table_fp8)
     plant, rates, flags = None, None, hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION
+    if table_fp8:
+        flags |= hsd.FLAG_TABLE_FP8
     ref = [greedy_decode(m, p, steps * (cfg.steps_N + 1) + cfg.steps_N + 4)[0] for p in pr] \
         if (planted or accept == "greedy") else None
     if planted:
