@@ -23,8 +23,10 @@
 //                is rare; P_j is written with tcgen05.st and never waits for the
 //                previous PV MMA.
 // Splits > 1 write (o, m, l) partials and a merge kernel combines them.
+#include <cooperative_groups.h>
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
+namespace cg = cooperative_groups;
 
 unsigned long long* g_attn_trace = nullptr;   // debug phase trace (HSD_ATTN_TRACE)
 
@@ -46,6 +48,7 @@ HSD_DEV uint64_t gtime() {
 }
 struct AttnParams {
   int M, R, Hq, G, hd, n_qtiles, max_keys, keys_per_split, direct;
+  int cluster;                 // 1: the S key-split CTAs form a cluster and reduce over DSMEM
   RowMeta m;
   KVLayer kv;
   bf16* out;
@@ -142,6 +145,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __shared__ int tile_lo, tile_hi, safe_hi;
   __shared__ float red_max[2][2][QROWS];   // [chunk parity][half][row]
   __shared__ float red_l[2][QROWS];
+  __shared__ float fin_m[QROWS], fin_l[QROWS];   // cluster mode: this split's (m, l) per tile row
+  __shared__ float wts[QROWS][8];                // cluster mode: merge weight of each split, per row
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, h = blockIdx.y;
@@ -427,8 +432,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                                        __uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv)
                                          : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    if (P.cluster && half == 0) { fin_m[lane_row] = mrow; fin_l[lane_row] = ltot; }
     asm volatile("bar.sync 5, 256;" ::: "memory");   // all 8 softmax warps staged their rows
     if (threadIdx.x == 64) TRACE(57);
+    if (!P.cluster) {
     // the CTA's valid rows of one (kv head, q-tile): all 256 softmax threads write
     // them as coalesced 16-byte vectors; split partials go to ONE contiguous block
     // ws[split][head][row][hd] per (split, head)
@@ -466,6 +473,52 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       P.ws[base_ml + 2 * idx] = mrow;      // log2 domain (merge uses exp2)
       P.ws[base_ml + 2 * idx + 1] = ltot;
     }
+    }
+  }
+  if (P.cluster) {
+    // split merge inside the cluster: every CTA staged its unnormalised O rows
+    // and (m, l) in shared memory; CTA r combines tile rows [r n/S, (r+1) n/S)
+    // over the S peers (DSMEM) -- o = sum_s 2^(m_s - M) o_s / sum_s 2^(m_s - M) l_s
+    // -- and writes them as bf16. No global partials, no merge kernel.
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const int S = gridDim.x, r = (int)cl.block_rank();
+    const int n_rh = min(QROWS, P.R * P.G - qt * QROWS);
+    const int r0 = r * n_rh / S, r1 = (r + 1) * n_rh / S;
+    const int ost = hd + 4;
+    if ((int)threadIdx.x < r1 - r0) {
+      const int lr = r0 + threadIdx.x;
+      float mp[8], lp[8], mm = -INFINITY;
+      for (int p = 0; p < S; ++p) {
+        mp[p] = *cl.map_shared_rank(&fin_m[lr], p);
+        lp[p] = *cl.map_shared_rank(&fin_l[lr], p);
+        if (lp[p] > 0.f) mm = fmaxf(mm, mp[p]);
+      }
+      float l = 0.f;
+      for (int p = 0; p < S; ++p) l += lp[p] > 0.f ? lp[p] * ex2(mp[p] - mm) : 0.f;
+      const float inv = l > 0.f ? 1.0f / l : 0.f;
+      for (int p = 0; p < S; ++p) wts[lr][p] = lp[p] > 0.f ? ex2(mp[p] - mm) * inv : 0.f;
+    }
+    __syncthreads();
+    const float* peer[8];
+    for (int p = 0; p < S; ++p) peer[p] = cl.map_shared_rank((const float*)sK, p);
+    const int vpr = hd / 4;
+    for (int e = threadIdx.x; e < (r1 - r0) * vpr; e += NTHREADS) {
+      const int lr = r0 + e / vpr, d4 = (e % vpr) * 4;
+      const int rh2 = qt * QROWS + lr, rl2 = rh2 / P.G, g2 = rh2 % P.G, row2 = grp * P.R + rl2;
+      if (row2 >= P.M) continue;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int p = 0; p < S; ++p) {
+        const float w = wts[lr][p];
+        if (w == 0.f) continue;                 // a split that saw nothing may hold stale rows
+        const float4 v = *(const float4*)(peer[p] + lr * ost + d4);
+        acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
+      }
+      const __nv_bfloat162 a = __floats2bfloat162_rn(acc.x, acc.y), b = __floats2bfloat162_rn(acc.z, acc.w);
+      *(uint2*)(P.out + ((size_t)row2 * P.Hq + h * P.G + g2) * hd + d4) =
+          make_uint2(*(const uint32_t*)&a, *(const uint32_t*)&b);
+    }
+    cl.sync();   // no CTA leaves while a peer still reads its shared memory
   }
   if (threadIdx.x == 0) TRACE(59);
   if (threadIdx.x == 32) TRACE(60);
@@ -548,10 +601,20 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   S = min(S, max(1, pages / 2));
   static const int s_override = [] { const char* e = getenv("HSD_ATTN_SPLITS"); return e ? atoi(e) : 0; }();
   if (s_override > 0) S = min(s_override, pages);
-  while (S > 1 && (size_t)S * M * Hq * (hd + 2) > ws_floats) --S;
+  // two splits reduce inside a 2-CTA cluster over DSMEM (no workspace, no merge
+  // kernel): c5 (b = 2) attention 6.8-7.3 -> 6.5 ms. Wider clusters measured
+  // slower (c2, S = 4: step 4.95 -> 5.38 ms) -- a 2-CTA cluster fits one TPC's SM
+  // pair, 4+ need GPC-wide co-scheduling against the PDL-overlapped predecessor.
+  // HSD_ATTN_CLUSTER_MAX raises the limit (<= 8) for experiments.
+  static const int cluster_max = [] {
+    const char* e = getenv("HSD_ATTN_CLUSTER_MAX");
+    return e ? atoi(e) : 2;
+  }();
+  P.cluster = (S >= 2 && S <= cluster_max && S <= 8) ? 1 : 0;
+  while (!P.cluster && S > 1 && (size_t)S * M * Hq * (hd + 2) > ws_floats) --S;
   int pps = (pages + S - 1) / S;
   P.keys_per_split = pps * CHUNK;
-  S = (pages + pps - 1) / pps;
+  if (!P.cluster) S = (pages + pps - 1) / pps;   // cluster mode keeps S (empty splits contribute 0)
   P.direct = S == 1;
   // tensor maps: q [M][Hq][hd] viewed (hd, heads, rows) with the head offset in
   // the coordinate; K pool rows of hd; V^T pool rows of page_size.
@@ -580,6 +643,10 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
     attr = smem;
   }
   dim3 grid(S, kv.kv_heads, n_req * P.n_qtiles);
+  if (P.cluster) {
+    launch_k_cluster(attention_tc_kernel, grid, dim3(NTHREADS), smem, st, S, mq, mk, mv, P);
+    return 1;
+  }
   launch_k(attention_tc_kernel, grid, dim3(NTHREADS), smem, st, mq, mk, mv, P);
   int launched = 1;
   if (S > 1) {

@@ -223,3 +223,16 @@ def test_lockstep_wide_bf16_tcgen05_planted(hd, q_heads, kv_heads, prompt_len):
                                    prompt_len=prompt_len)
     ls, accs = run_lockstep(cfg, hsd.BF16, steps=6, tcgen05=True, planted=True)
     assert ls.max_err["verify"] <= 2e-2 and max(accs) >= 2
+
+
+def test_attention_cluster_reduction_all_widths():
+    """Key splits merged inside a thread-block cluster over DSMEM (attention_tc.cu):
+    by default only S = 2 takes that path, so re-run the multi-split tcgen05
+    lockstep cases in a fresh process with clusters of up to 8 CTAs."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, HSD_ATTN_CLUSTER_MAX="8")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k", "tcgen05 and not cluster"],
+                       env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
