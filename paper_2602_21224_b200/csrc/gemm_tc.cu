@@ -288,6 +288,185 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
 }
 
+// ------------------------------------------------------------------ CTA-pair kernel
+// Data-parallel GEMM on a CTA pair (cluster of 2 on one TPC): one tile = 256
+// weight rows x ntile tokens, computed by tcgen05.mma.cta_group::2 (M = 256)
+// issued by the leader (rank 0). CTA r stages weight rows [r*128, +128) and
+// tokens [r*ntile/2, +ntile/2) of every k-block (the UMMA 2x1SM operand split),
+// so each SM ingests (128 + ntile/2) x 64 x 2 bytes per k-block instead of
+// (128 + ntile) x 64 x 2 -- the single-CTA kernel's limit at large M. Each CTA's
+// TMEM holds its 128 rows of the accumulator; the epilogue is the data-parallel
+// one of gemm_tc_kernel on that 128-row half.
+__global__ void __launch_bounds__(NTHREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, TcParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int half_nt = P.ntile / 2;
+  const int bh = half_nt * BK * 2;                     // this CTA's token half per stage
+  uint8_t* sA = base;
+  uint8_t* sB = base + (size_t)P.stages * A_BYTES;
+  uint64_t* bars = (uint64_t*)(sB + (size_t)P.stages * bh);
+  uint64_t* full = bars;                       // [stages] (the leader's count both CTAs' bytes)
+  uint64_t* empty = bars + P.stages;           // [stages]
+  uint64_t* tfull = bars + 2 * P.stages;       // [2]
+  uint64_t* tempty = bars + 2 * P.stages + 2;  // [2] (leader: one arrival per CTA)
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * P.stages + 4);
+  float* stage_buf = (float*)(bars + 2 * P.stages + 6);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)(blockIdx.x & 1);
+  const bool leader = rank == 0;
+  const long pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int n_tm = (P.N + 2 * BM - 1) / (2 * BM);
+  const long n_tiles = (long)n_tm * P.n_tiles_t;
+  const long my_tiles = pair < n_tiles ? (n_tiles - 1 - pair) / n_pairs + 1 : 0;
+  const long count = my_tiles * P.n_kb;
+  auto tile_of = [&](long i) { return pair + (i / P.n_kb) * n_pairs; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 2); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(P.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  const uint32_t full0 = mapa_u32(&full[0], 0);        // the leader's full barriers
+  const uint32_t tempty0 = mapa_u32(&tempty[0], 0);    // the leader's accumulator-empty barriers
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs: each stages its operand halves)
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+      const uint64_t pw = policy_evict_first(), px = policy_evict_last();
+      pdl_wait();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long i = 0; i < count; ++i) {
+        const long t = tile_of(i);
+        const int kb = (int)(i % P.n_kb);
+        const int tm = (int)(t / P.n_tiles_t), tt = (int)(t % P.n_tiles_t);
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (leader) mbar_expect_tx(&full[stage], 2u * (A_BYTES + bh));
+        tma_load_2d_2sm(&tmW, full0 + 8u * stage, sA + (size_t)stage * A_BYTES, kb * BK, (2 * tm + rank) * BM, pw);
+        tma_load_2d_2sm(&tmX, full0 + 8u * stage, sB + (size_t)stage * bh, kb * BK, tt * P.ntile + rank * half_nt,
+                        px);
+        if (++stage == P.stages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: the leader's lane 0 issues for the pair
+    pdl_wait();
+    if (leader && lane == 0) {
+      int stage = 0, buf = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (long i = 0; i < count; ++i) {
+        const int kb = (int)(i % P.n_kb);
+        const bool first = kb == 0, last = kb == P.n_kb - 1;
+        if (first) {
+          mbar_wait(&tempty[buf], aphase ^ 1);
+          fence_after();
+        }
+        mbar_wait(&full[stage], phase);
+        fence_after();
+        const uint64_t ad = desc_sw128(sA + (size_t)stage * A_BYTES);
+        const uint64_t bd = desc_sw128(sB + (size_t)stage * bh);
+        const uint32_t dt = tmem + (uint32_t)(buf * P.ntile);
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk)
+          mma_bf16_2sm(dt, ad + 2 * kk, bd + 2 * kk, P.idesc, (first && kk == 0) ? 0u : 1u);
+        mma_commit_2sm(&empty[stage], 3);
+        if (last) {
+          mma_commit_2sm(&tfull[buf], 3);
+          buf ^= 1;
+          if (buf == 0) aphase ^= 1;
+        }
+        if (++stage == P.stages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    // ---------------- epilogue: this CTA's 128 accumulator rows (output features)
+    pdl_wait();
+    const int q = warp & 3, et = threadIdx.x - 64;
+    int buf = 0;
+    uint32_t aphase = 0;
+    for (long ti = 0; ti < my_tiles; ++ti) {
+      const long t = pair + ti * n_pairs;
+      const int tm = (int)(t / P.n_tiles_t), tt = (int)(t % P.n_tiles_t);
+      const int tn = 2 * tm + rank;                   // this CTA's 128-row weight tile
+      mbar_wait(&tfull[buf], aphase);
+      fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * P.ntile);
+      for (int c0 = 0; c0 < P.ntile; c0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(taddr + c0, r);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) stage_buf[j * EPI_LD + q * 32 + lane] = __uint_as_float(r[j]);
+        epi_bar();
+        if (P.epi == EPI_SWIGLU) {
+          const int tk = et >> 3, f8 = (et & 7) * 8;
+          const int tok = tt * P.ntile + c0 + tk, f0 = tn * (BM / 2) + f8;
+          if (tok < P.M && f0 < P.N / 2) {
+            const float* g = stage_buf + tk * EPI_LD + f8;
+            const float* uu = g + BM / 2;
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float a0 = g[2 * e], a1 = g[2 * e + 1];
+              const __nv_bfloat162 hv = __floats2bfloat162_rn(a0 / (1.0f + expf(-a0)) * uu[2 * e],
+                                                              a1 / (1.0f + expf(-a1)) * uu[2 * e + 1]);
+              w[e] = *(const uint32_t*)&hv;
+            }
+            *(uint4*)(P.H + (size_t)tok * P.ldh + f0) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int slot = et + 128 * v, tk = slot >> 5, r4 = (slot & 31) * 4;
+            const int tok = tt * P.ntile + c0 + tk, row = tn * BM + r4;
+            if (tok >= P.M || row >= P.N) continue;
+            const float4 val = *(const float4*)(stage_buf + tk * EPI_LD + r4);
+            float* dst = &P.C[(size_t)tok * P.ldc + row];
+            if (row + 3 < P.N && P.vec4) {
+              if (P.epi == EPI_ADD) {
+                float4 o = *(const float4*)dst;
+                o.x += val.x; o.y += val.y; o.z += val.z; o.w += val.w;
+                *(float4*)dst = o;
+              } else {
+                *(float4*)dst = val;
+              }
+            } else {
+              const float vv[4] = {val.x, val.y, val.z, val.w};
+              for (int e = 0; e < 4 && row + e < P.N; ++e) dst[e] = (P.epi == EPI_ADD ? dst[e] : 0.f) + vv[e];
+            }
+          }
+        }
+        epi_bar();
+      }
+      // this CTA has read its half of the accumulator: one arrival on the leader
+      fence_before();
+      if (et == 0) mbar_arrive_cluster(tempty0 + 8u * buf);
+      buf ^= 1;
+      if (buf == 0) aphase ^= 1;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
+}
+
 // ------------------------------------------------------------------ host side
 }  // namespace
 
@@ -347,7 +526,8 @@ bool gemm_tc_supported(int M, int N, int K, int lda, int ldw) {
 }
 
 static void tc_tiles(int M, int& nt, int& n_tok_tiles) {
-  n_tok_tiles = (M + 255) / 256;
+  static const int max_nt = [] { const char* e = getenv("HSD_GEMM_MAX_NT"); return e ? atoi(e) : 256; }();
+  n_tok_tiles = (M + max_nt - 1) / max_nt;
   nt = (M + n_tok_tiles - 1) / n_tok_tiles;
   nt = (nt + 15) / 16 * 16;
   if (nt < 16) nt = 16;
@@ -362,10 +542,49 @@ bool gemm_tc_dp(int M, int N) {
   return (long)((N + BM - 1) / BM) * ntt >= 4L * num_sms();
 }
 
+static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float* C, int ldc, int M, int N, int K,
+                           int epi, bf16* H, int ldh, cudaStream_t st) {
+  TcParams P;
+  P.M = M; P.N = N; P.K = K; P.ldc = ldc; P.C = C; P.H = H; P.ldh = ldh; P.epi = epi; P.dp = 1;
+  P.trace = nullptr;
+  int nt, ntt;
+  tc_tiles(M, nt, ntt);
+  P.ntile = nt;
+  P.n_tiles_t = ntt;
+  P.n_tiles_n = (N + BM - 1) / BM;
+  P.n_kb = (K + BK - 1) / BK;
+  P.units = 0;
+  const int bh = (nt / 2) * BK * 2;
+  int stages = (200 * 1024) / (A_BYTES + bh);
+  if (stages > 16) stages = 16;
+  P.stages = stages;
+  P.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nt >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * nt)) cols <<= 1;
+  P.tmem_cols = cols;
+  CUtensorMap mw, mx;
+  if (!make_map(&mw, W, N, K, ldw, BM) || !make_map(&mx, A, M, K, lda, nt / 2)) return 0;
+  P.vec4 = (ldc % 4 == 0) && (((uintptr_t)C & 15) == 0);
+  const size_t smem = 1024 + (size_t)stages * (A_BYTES + bh) + (2 * stages + 6) * 8 + 16 * EPI_LD * 4 + 16;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_done = true;
+  }
+  const long pairs = (long)((N + 2 * BM - 1) / (2 * BM)) * ntt;
+  const long max_pairs = num_sms() / 2;
+  const long grid = 2 * (pairs < max_pairs ? pairs : max_pairs);
+  launch_k_cluster(gemm_tc2_kernel, dim3((unsigned)grid), dim3(NTHREADS), smem, st, 2, mw, mx, P);
+  return 1;
+}
+
 static int gemm_tc_launch(const bf16* A, int lda, const bf16* W, int ldw, float* C, int ldc, int M, int N, int K,
                           int epi, int dp, bf16* H, int ldh, cudaStream_t st) {
   TcParams P;
   P.M = M; P.N = N; P.K = K; P.ldc = ldc; P.C = C; P.H = H; P.ldh = ldh; P.epi = epi; P.dp = dp;
+  // data-parallel shapes (large M: c3/c4/c5 verify) run on CTA pairs (2-SM UMMA)
+  static const bool pair_on = [] { const char* e = getenv("HSD_GEMM_2SM"); return !(e && atoi(e) == 0); }();
+  if (dp && pair_on && num_sms() >= 2) return gemm_tc2_launch(A, lda, W, ldw, C, ldc, M, N, K, epi, H, ldh, st);
   static unsigned long long* trace = [] {
     unsigned long long* t = nullptr;
     if (getenv("HSD_GEMM_TRACE")) { cudaMalloc(&t, 32 * 8); cudaMemset(t, 0, 32 * 8); }
