@@ -63,14 +63,31 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML (pynvml)
+    every 2 ms from a thread, so even a ~100 ms region gets dozens of samples;
+    falls back to `nvidia-smi -lms 100` when NVML is unavailable."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []        # (sm_mhz, sm_max_mhz, reason names)
         self.proc = None
+        self.stop = threading.Event()
+        self.nvml = None
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = (pynvml, h)
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -84,13 +101,30 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv, h = self.nvml
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), float(mx), [k for k, b in self.REASONS.items() if rs & b]))
+            except Exception:
+                pass
+            self.stop.wait(0.002)
+
     def _read(self):
+        names = list(self.REASONS)
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 7:
-                self.rows.append(parts)
+            if len(parts) >= 7 and parts[0].replace(".", "").isdigit():
+                self.rows.append((float(parts[0]), float(parts[1]) if parts[1].replace(".", "").isdigit() else None,
+                                  [names[i] for i in range(4) if parts[3 + i].lower() == "active"]))
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml:
+            self.t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -101,12 +135,11 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        mx = [r[1] for r in self.rows if r[1]]
+        reasons = sorted({x for r in self.rows for x in r[2]})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
@@ -331,16 +364,35 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # one event between consecutive graph replays: per-step latency distribution
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for i in range(args.warmup, args.warmup + args.steps):
+            evs[i - args.warmup].record(stream)
             do_step(i)
+        evs[-1].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
+    step_ms = np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)])
     launches = ctx.kernel_launches() - launches0
+    # S2 (target tree verify) alone: staged calls, CUDA events around hsd_verify_tree
+    verify_ms = []
+    if not args.no_profile:
+        with torch.cuda.stream(stream):
+            for _ in range(min(args.steps, 8)):
+                a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ctx.build_tree()
+                a.record(stream)
+                ctx.verify_tree()
+                z.record(stream)
+                ctx.accept_and_compact()
+                stream.synchronize()
+                verify_ms.append(a.elapsed_time(z))
+    ctx.sync()
     ctx.sync()
     emitted = int(d_n[args.warmup:].sum().item())
     ms_max, emitted_all = reduce_over_ranks(ms, float(emitted), device=f"cuda:{local}")
@@ -432,6 +484,14 @@ def main():
             "tau": round(emitted_all / (args.steps * cfg.batch if cfg.batch >= world else args.steps * world * b), 4),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "tau_curve": tau_curve, "planted": planted,
+            "step_latency_ms": {"median": round(float(np.median(step_ms)), 4),
+                                "p90": round(float(np.percentile(step_ms, 90)), 4),
+                                "min": round(float(step_ms.min()), 4), "max": round(float(step_ms.max()), 4),
+                                "what": "S0-S4, one graph-replayed hsd_step, CUDA events between replays"},
+            "verify_latency_ms": ({"median": round(float(np.median(verify_ms)), 4),
+                                   "p90": round(float(np.percentile(verify_ms, 90)), 4), "n": len(verify_ms),
+                                   "what": "S2 alone: hsd_verify_tree (staged call) on the ctx stream"}
+                                  if verify_ms else None),
             "clocks": clk.summary(), "init_s": round(t_init, 2),
             "profile_ms_per_step": {k: round(v[0] / min(args.steps, 4), 4) for k, v in (prof or {}).items()},
         }

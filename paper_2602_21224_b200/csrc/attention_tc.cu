@@ -55,6 +55,7 @@ struct AttnParams {
   float* ws;
   uint32_t idesc_s, idesc_o;
   unsigned long long* trace;   // [64] timestamps or null
+  L2Pf pf;                     // weights of a later GEMM to prefetch into L2 (common.cuh)
 };
 #define TRACE(i) do { if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[(i)] = gtime(); } while (0)
 
@@ -225,6 +226,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t tO = tmem + 256;        // hd columns
 
   if (warp == 0) {
+    if (lane == 0 && n_chunks == 0) { l2pf_issue(P.pf); l2pf_issue(P.pf, 1); }
     if (lane == 0 && n_chunks > 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
@@ -259,10 +261,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       while (kj < n_chunks && kj < KSTAGES && safe(kj)) load_k(kj++);
       while (vj < n_chunks && vj < VSTAGES && safe(vj)) load_v(vj++);
       pdl_wait();
+      if (P.pf.late) l2pf_issue(P.pf, 1);   // (the late variant goes ahead of q)
       if (threadIdx.x == 0) TRACE(2);
       mbar_expect_tx(qbar, q_bytes);
       for (int a = 0; a < natom; ++a)
         tma_load_3d(&tmQ, qbar, sQ + a * (QROWS * 128), a * 64, h * P.G, row0, polq);
+      l2pf_issue(P.pf);   // behind this CTA's first K/V/Q loads in the TMA queue
       // K runs one chunk ahead of V: V_j waits for P_{j-2} V, K_{j+1} must not
       while (vj < n_chunks) {
         if (kj < n_chunks && kj <= vj + 1) load_k(kj++);
@@ -534,8 +538,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // split merge: one warp per (row, head), lanes over hd:
 // o = sum_s e^{m_s - M} o_s / sum_s e^{m_s - M} l_s
 __global__ void attention_merge_bf16_kernel(const float* __restrict__ ws, int S, int M, int Hq, int hd,
-                                            bf16* __restrict__ out) {
+                                            bf16* __restrict__ out, L2Pf pf) {
+  l2pf_issue(pf);
   pdl_wait();
+  l2pf_issue(pf, 1);
   pdl_trigger();
   // one warp per (row, head); partials are laid out ws[split][head][row][hd]
   const int pair = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -578,6 +584,7 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   const int hd = kv.head_dim, G = Hq / kv.kv_heads;
   if (QROWS % G) return -1;
   AttnParams P;
+  P.pf = take_l2pf();
   P.M = M; P.R = R; P.Hq = Hq; P.G = G; P.hd = hd; P.m = m; P.kv = kv;
   P.out = (bf16*)out; P.ws = ws; P.max_keys = max_keys;
   P.n_qtiles = (R * G + QROWS - 1) / QROWS;
@@ -650,7 +657,8 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   launch_k(attention_tc_kernel, grid, dim3(NTHREADS), smem, st, mq, mk, mv, P);
   int launched = 1;
   if (S > 1) {
-    launch_k(attention_merge_bf16_kernel, (M * Hq + 7) / 8, 256, 0, st, ws, S, M, Hq, hd, (bf16*)out);
+    launch_k(attention_merge_bf16_kernel, (M * Hq + 7) / 8, 256, 0, st, ws, S, M, Hq, hd, (bf16*)out,
+             take_l2pf());
     launched++;
   }
   return launched;

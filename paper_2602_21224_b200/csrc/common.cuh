@@ -111,6 +111,35 @@ HSD_DEV void warp_argmax(float& v, int& i) {
 HSD_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 HSD_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// ---------------------------------------------------------------- L2 weight prefetch
+// Kernels that leave HBM idle (row kernels, attention, K-TREE) carry the byte range
+// of weights a LATER GEMM will stream; thread 0 of every CTA issues its share as
+// cp.async.bulk.prefetch.L2 (fire and forget, no completion tracking) before the
+// PDL wait -- weights are never written after init. The engine sets g_l2pf right
+// before a launch; the launcher consumes it (take_l2pf) into the kernel argument.
+struct L2Pf {
+  const char* p;
+  unsigned long long bytes;
+  int late;   // 1: issue after the PDL wait (only inside the idle window), 0: before it
+};
+extern L2Pf g_l2pf;
+inline L2Pf take_l2pf() {
+  L2Pf r = g_l2pf;
+  g_l2pf = L2Pf{nullptr, 0ull, 0};
+  return r;
+}
+HSD_DEV void l2pf_issue(const L2Pf& pf, int late = 0) {
+  if (pf.bytes == 0 || pf.late != late || threadIdx.x != 0 || threadIdx.y != 0) return;
+  const unsigned long long nb = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+  const unsigned long long b = blockIdx.x + (unsigned long long)gridDim.x * (blockIdx.y + (unsigned long long)gridDim.y * blockIdx.z);
+  const unsigned long long per = (((pf.bytes + nb - 1) / nb) + 4095ull) & ~4095ull;
+  const unsigned long long lo = b * per, hi = lo + per < pf.bytes ? lo + per : pf.bytes;
+  for (unsigned long long o = lo; o < hi; o += 65536ull) {
+    const unsigned sz = (unsigned)((hi - o) < 65536ull ? (hi - o) : 65536ull) & ~15u;
+    if (sz) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf.p + o), "r"(sz) : "memory");
+  }
+}
+
 extern bool g_hsd_pdl;   // engine.cu; HSD_PDL=0 disables (A/B testing)
 
 template <typename... KArgs, typename... Args>

@@ -182,6 +182,28 @@ __global__ void f32_to_dt_kernel(const float* src, size_t count, bf16* dst) {
 // ====================================================================== context
 struct LayerW { void *wqkv, *wo, *wgu, *wd; };
 
+// L2 weight prefetch (common.cuh L2Pf): kernels that leave HBM idle carry a byte
+// range of the weights the NEXT GEMM(s) will stream. HSD_L2PF_MB (default 48, 0 =
+// off) caps the range handed to a long idle window (qkv_rope + attention, SwiGLU,
+// K-TREE); short windows (an RMSNorm right before its GEMM) get a third of it.
+L2Pf g_l2pf = {nullptr, 0ull, 0};
+// HSD_L2PF_WHERE: bitmask of the windows that prefetch (default 4 = attention only:
+// the others measured flat or slower on c2; 1 rmsnorm-1, 2 qkv_rope,
+// 4 attention, 8 rmsnorm-2, 16 SwiGLU, 32 K-TREE); HSD_L2PF_LATE=1 issues after the PDL wait
+static const int g_l2pf_where = [] { const char* e = getenv("HSD_L2PF_WHERE"); return e ? atoi(e) : 4; }();
+static const int g_l2pf_late = [] { const char* e = getenv("HSD_L2PF_LATE"); return e ? atoi(e) : 0; }();
+static const size_t g_l2pf_cap = [] {
+  const char* e = getenv("HSD_L2PF_MB");
+  return (size_t)(e ? atof(e) : 48.0) * (size_t)(1 << 20);
+}();
+struct PfScope {   // the next launch inside this scope carries [p + off, p + off + min(bytes, cap))
+  PfScope(const void* p, size_t total, size_t off, size_t cap, int where) {
+    if (g_l2pf_cap == 0 || p == nullptr || off >= total || !(g_l2pf_where & where)) return;
+    g_l2pf = L2Pf{(const char*)p + off, (unsigned long long)(std::min(total - off, cap) & ~(size_t)15), g_l2pf_late};
+  }
+  ~PfScope() { g_l2pf = L2Pf{nullptr, 0ull, 0}; }
+};
+
 // Kernel categories for hsd_profile (CUDA events around each launch; eager only).
 enum ProfCat { P_GEMM_VERIFY, P_GEMM_DRAFT, P_HEAD_VERIFY, P_HEAD_DRAFT, P_ATTN_VERIFY, P_ATTN_DRAFT, P_TREE,
                P_RESAMPLE, P_WALK, P_COMPACT, P_ROWWISE, P_NCAT };
@@ -239,6 +261,9 @@ struct hsd_ctx {
   // graph
   cudaGraphExec_t graph = nullptr;
   int64_t graph_kernels = 0;
+  // staged calls (build / verify / accept) replay their own per-stage graphs
+  cudaGraphExec_t sgraph[3] = {nullptr, nullptr, nullptr};
+  int64_t sgraph_kernels[3] = {0, 0, 0}, sgraph_replays[3] = {0, 0, 0};
   int stage = 0;       // 0 idle, 1 tree built, 2 verified
   int64_t launches0 = 0, graph_replays = 0;
   std::vector<void*> allocs;
@@ -371,11 +396,18 @@ static KVLayer kv_layer(hsd_ctx* c, void* pool, int layer) {
 static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, int n_req, const RowMeta& m,
                           const KVLayer& kv, int max_keys) {
   const int n = c->n;
-  if (!ablate("rms")) { Prof pf(c, P_ROWWISE); launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st); }
+  const size_t es = c->esz, b_qkv = (size_t)c->qkvd * n * es, b_o = (size_t)n * c->qd * es,
+               b_gu = (size_t)2 * c->f * n * es, b_d = (size_t)n * c->f * es, cap = g_l2pf_cap;
+  if (!ablate("rms")) {
+    Prof pf(c, P_ROWWISE);
+    PfScope l2(w.wqkv, b_qkv, 0, cap / 3, 1);
+    launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st);
+  }
   // c->big is kept zero outside a GEMM -> consumer window (qkv_rope_kv and
   // swiglu re-zero what they read), so these GEMMs accumulate without a memset
   gemm(c, c->a, n, w.wqkv, n, c->big, c->qkvd, M, c->qkvd, n, false, -1, true);
   if (!ablate("rope")) { Prof pf(c, P_ROWWISE);
+    PfScope l2(w.wo, b_o, 0, std::max(cap, b_o), 2);
     launch_qkv_rope_kv(c->big, M, m, c->rope_cos, c->rope_sin, c->Hq, kv, c->qb, c->dt, c->st); }
   if (!ablate("attn")) {
     // algorithmic attention bytes: the request's committed K/V rows once (per
@@ -383,6 +415,7 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
     // host uses the capacity-free estimate recorded by hsd_profile_read callers.
     Prof pf(c, c->pass_verify ? P_ATTN_VERIFY : P_ATTN_DRAFT, c->attn_bytes);
     int tc_launched = -1;
+    PfScope l2(w.wgu, b_gu, 0, cap, 4);
     if (c->use_tc && g_attn_tc && attention_tc_supported(c->hd, c->page_size, c->dt))
       tc_launched = launch_attention_tc(c->qb, M, R, n_req, m, kv, c->Hq, max_keys, c->ob, c->attn_ws,
                                         c->attn_ws_floats, c->kv_layer_elems, c->st);
@@ -392,7 +425,11 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
                        c->st);
   }
   gemm(c, c->ob, c->qd, w.wo, c->qd, x, n, M, n, c->qd, true);
-  if (!ablate("rms")) { Prof pf(c, P_ROWWISE); launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st); }
+  if (!ablate("rms")) {
+    Prof pf(c, P_ROWWISE);
+    PfScope l2(w.wgu, b_gu, cap, cap / 3, 8);
+    launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st);
+  }
   bool fused = false;
   if (c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, 2 * c->f, n, n, n) && gemm_tc_dp(M, 2 * c->f)) {
     // data-parallel gate/up GEMM with SwiGLU in the epilogue, bf16 h straight to c->a
@@ -407,6 +444,7 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
   if (!fused) {
     gemm(c, c->a, n, w.wgu, n, c->big, 2 * c->f, M, 2 * c->f, n, false, -1, true);
     Prof pf(c, P_ROWWISE);
+    PfScope l2(w.wd, b_d, 0, cap, 16);
     if (!ablate("swiglu")) { launch_swiglu(c->big, M, c->f, c->h, c->dt, m.pos, c->st); g_hsd_launches += 1; }
   }
   gemm(c, c->h, c->f, w.wd, c->f, x, n, M, n, c->f, true);
@@ -456,6 +494,11 @@ static void stage_build(hsd_ctx* c) {
   P.plant_stride = c->plant_stride;
   for (int i = 0; i < HSD_MAX_PLANT_DEPTH_DEV; ++i) P.plant_rates[i] = c->cfg.plant_rates[i];
   P.seed = (uint32_t)c->cfg.seed; P.req_offset = c->cfg.req_offset; P.err = c->err;
+  P.pf = L2Pf{nullptr, 0ull, 0};
+  if (g_l2pf_cap && !c->layers.empty()) {   // verify layer 0's QKV weights stream next
+    PfScope l2(c->layers[0].wqkv, (size_t)c->qkvd * n * c->esz, 0, g_l2pf_cap, 32);
+    P.pf = take_l2pf();
+  }
   if (!ablate("tree")) { Prof pf(c, P_TREE); launch_tree(P, TREE_MODE_FRESH, b, c->st); }
   g_hsd_launches += 1;
 }
@@ -505,6 +548,11 @@ static void stage_accept(hsd_ctx* c, int32_t* d_emitted, int32_t* d_n) {
   P.L = c->draft_logits; P.table = c->table; P.tdt = c->dt; P.tscale = c->table_scale; P.perm = c->perm_d; P.rank_of = c->rank_d;
   P.pt_n = c->pt_n; P.pt_tok = c->pt_tok; P.pt_par = c->pt_par; P.pt_depth = c->pt_depth; P.pt_lj = c->pt_lj;
   P.acc_n = c->acc_n; P.bonus = c->bonus; P.err = c->err;
+  P.pf = L2Pf{nullptr, 0ull, 0};
+  if (g_l2pf_cap) {   // the next step's draft prefill GEMM streams W_fc first
+    PfScope l2(c->fc, (size_t)2 * c->n * c->n * c->esz, 0, g_l2pf_cap, 32);
+    P.pf = take_l2pf();
+  }
   if (!ablate("tree")) { Prof pf(c, P_RESAMPLE); launch_tree(P, TREE_MODE_RESAMPLE, b, c->st); }
   CommitParams M{};
   M.N = c->N; M.t_max = c->T; M.hidden = c->n; M.Hverify = c->Hver;
@@ -515,6 +563,42 @@ static void stage_accept(hsd_ctx* c, int32_t* d_emitted, int32_t* d_n) {
   g_hsd_launches += 4;
   if (d_emitted) cudaMemcpyAsync(d_emitted, c->emitted, sizeof(int32_t) * b * (c->N + 1), cudaMemcpyDeviceToDevice, c->st);
   if (d_n) cudaMemcpyAsync(d_n, c->n_emitted, sizeof(int32_t) * b, cudaMemcpyDeviceToDevice, c->st);
+}
+
+static void drop_graphs(hsd_ctx* c) {
+  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+  for (int i = 0; i < 3; ++i)
+    if (c->sgraph[i]) { cudaGraphExecDestroy(c->sgraph[i]); c->sgraph[i] = nullptr; }
+}
+
+// Run one stage of a staged step. With a non-legacy stream and profiling off, the
+// stage is captured once into its own CUDA graph and replayed (the same launches,
+// same order, as inside hsd_step's graph), so staged latencies match the step's.
+static bool g_stage_graphs = [] { const char* e = getenv("HSD_STAGE_GRAPHS"); return !(e && e[0] == '0'); }();
+template <typename F>
+static hsd_status run_stage(hsd_ctx* ctx, int idx, F&& body) {
+  hsd_ctx* c = ctx;
+  if (c->prof_on || c->st == nullptr || !g_stage_graphs) {
+    body();
+    CU(cudaGetLastError());
+    return HSD_OK;
+  }
+  if (!c->sgraph[idx]) {
+    int64_t before = g_hsd_launches;
+    cudaGraph_t g;
+    CU(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+    c->capturing = true;
+    body();
+    c->capturing = false;
+    CU(cudaStreamEndCapture(c->st, &g));
+    c->sgraph_kernels[idx] = g_hsd_launches - before;
+    g_hsd_launches = before;
+    CU(cudaGraphInstantiate(&c->sgraph[idx], g, 0));
+    cudaGraphDestroy(g);
+  }
+  CU(cudaGraphLaunch(c->sgraph[idx], c->st));
+  c->sgraph_replays[idx]++;
+  return HSD_OK;
 }
 
 // ====================================================================== C ABI
@@ -532,7 +616,10 @@ void hsd_config_defaults(hsd_config* c) {
 const char* hsd_last_error(const hsd_ctx* ctx) { return ctx ? ctx->errmsg.c_str() : "null context"; }
 
 int64_t hsd_kernel_launches(const hsd_ctx* ctx) {
-  return ctx ? (g_hsd_launches - ctx->launches0) + ctx->graph_replays * ctx->graph_kernels : 0;
+  if (!ctx) return 0;
+  int64_t n = (g_hsd_launches - ctx->launches0) + ctx->graph_replays * ctx->graph_kernels;
+  for (int i = 0; i < 3; ++i) n += ctx->sgraph_replays[i] * ctx->sgraph_kernels[i];
+  return n;
 }
 
 static std::string check_config(const hsd_config* c) {
@@ -797,7 +884,7 @@ hsd_status hsd_prefill(hsd_ctx* ctx, int32_t n_req, const int32_t* h_tokens, int
       if (h_tokens[(size_t)r * stride + i] < 0 || h_tokens[(size_t)r * stride + i] >= c->V)
         return fail(c, HSD_EINVAL, "token outside [0, V) (contract violation)");
   }
-  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+  drop_graphs(c);
   c->b = n_req;
   const int n = c->n, N = c->N;
   CU(cudaMemsetAsync(c->step, 0, 4, c->st));
@@ -892,7 +979,7 @@ hsd_status hsd_set_plant(hsd_ctx* ctx, const int32_t* h_plant, int32_t stride) {
   c->plant_stride = stride;
   CU(cudaMemcpyAsync(c->plant, h_plant, sizeof(int32_t) * (size_t)c->b * stride, cudaMemcpyHostToDevice, c->st));
   CU(cudaStreamSynchronize(c->st));
-  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+  drop_graphs(c);
   return HSD_OK;
 }
 
@@ -910,8 +997,7 @@ static void fill_verify_view(hsd_ctx* c, hsd_verify_view* v) {
 hsd_status hsd_build_tree(hsd_ctx* ctx, hsd_tree_view* out) {
   if (!ctx) return HSD_EINVAL;
   if (ctx->b < 1) return fail(ctx, HSD_ESTATE, "hsd_build_tree before hsd_prefill");
-  stage_build(ctx);
-  CU(cudaGetLastError());
+  { const hsd_status s = run_stage(ctx, 0, [&] { stage_build(ctx); }); if (s != HSD_OK) return s; }
   ctx->stage = 1;
   fill_tree_view(ctx, out);
   return HSD_OK;
@@ -948,8 +1034,7 @@ hsd_status hsd_force_tree(hsd_ctx* ctx, const int32_t* h_tok, const int32_t* h_p
 hsd_status hsd_verify_tree(hsd_ctx* ctx, hsd_verify_view* out) {
   if (!ctx) return HSD_EINVAL;
   if (ctx->stage != 1) return fail(ctx, HSD_ESTATE, "hsd_verify_tree requires hsd_build_tree");
-  stage_verify(ctx);
-  CU(cudaGetLastError());
+  { const hsd_status s = run_stage(ctx, 1, [&] { stage_verify(ctx); }); if (s != HSD_OK) return s; }
   ctx->stage = 2;
   fill_verify_view(ctx, out);
   return HSD_OK;
@@ -958,8 +1043,10 @@ hsd_status hsd_verify_tree(hsd_ctx* ctx, hsd_verify_view* out) {
 hsd_status hsd_accept_and_compact(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n_emitted) {
   if (!ctx) return HSD_EINVAL;
   if (ctx->stage != 2) return fail(ctx, HSD_ESTATE, "hsd_accept_and_compact requires hsd_verify_tree");
-  stage_accept(ctx, d_emitted, d_n_emitted);
-  CU(cudaGetLastError());
+  { const hsd_status s = run_stage(ctx, 2, [&] { stage_accept(ctx, nullptr, nullptr); }); if (s != HSD_OK) return s; }
+  if (d_emitted)
+    CU(cudaMemcpyAsync(d_emitted, ctx->emitted, sizeof(int32_t) * ctx->b * (ctx->N + 1), cudaMemcpyDeviceToDevice, ctx->st));
+  if (d_n_emitted) CU(cudaMemcpyAsync(d_n_emitted, ctx->n_emitted, sizeof(int32_t) * ctx->b, cudaMemcpyDeviceToDevice, ctx->st));
   ctx->stage = 0;
   return HSD_OK;
 }
@@ -1145,7 +1232,7 @@ hsd_status hsd_destroy(hsd_ctx* ctx) {
   if (!ctx) return HSD_EINVAL;
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   else cudaDeviceSynchronize();
-  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+  drop_graphs(ctx);
   prof_collect(ctx);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (void* p : ctx->allocs) cudaFree(p);

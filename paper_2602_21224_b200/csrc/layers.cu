@@ -28,8 +28,11 @@ template <> struct Vec4<bf16> {
 // One CTA per row; n % 4 == 0; up to 8 float4 per thread kept in registers.
 template <typename T>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, int n, float eps,
-                                                      T* __restrict__ out, const int32_t* __restrict__ pos) {
+                                                      T* __restrict__ out, const int32_t* __restrict__ pos,
+                                                      L2Pf pf) {
+  l2pf_issue(pf);
   pdl_wait();
+  l2pf_issue(pf, 1);
   pdl_trigger();
   __shared__ float red[32];
   const int r = blockIdx.x;
@@ -65,9 +68,10 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
 
 void launch_rmsnorm(const float* x, int M, int n, float eps, void* out, DType dt, const int32_t* pos,
                     cudaStream_t st) {
+  const L2Pf pf = take_l2pf();
   if (M <= 0) return;
-  if (dt == DT_F32) launch_k(rmsnorm_kernel<float>, M, 256, 0, st, x, n, eps, (float*)out, pos);
-  else launch_k(rmsnorm_kernel<bf16>, M, 256, 0, st, x, n, eps, (bf16*)out, pos);
+  if (dt == DT_F32) launch_k(rmsnorm_kernel<float>, M, 256, 0, st, x, n, eps, (float*)out, pos, pf);
+  else launch_k(rmsnorm_kernel<bf16>, M, 256, 0, st, x, n, eps, (bf16*)out, pos, pf);
 }
 
 // ------------------------------------------------------------------ embedding
@@ -156,8 +160,10 @@ template <typename T>
 __global__ void __launch_bounds__(128) qkv_rope_kv_kernel(float* __restrict__ qkv, RowMeta m,
                                                           const float* __restrict__ rc,
                                                           const float* __restrict__ rs, int Hq, KVLayer kv,
-                                                          T* __restrict__ q_out, int M) {
+                                                          T* __restrict__ q_out, int M, L2Pf pf) {
+  l2pf_issue(pf);
   pdl_wait();
+  l2pf_issue(pf, 1);
   pdl_trigger();
   const int n_v = (M + VROWS - 1) / VROWS * kv.kv_heads * ((kv.head_dim + 31) / 32);
   if ((int)blockIdx.x < n_v) {          // V-transpose CTAs first (fewer, longer), then rope
@@ -211,12 +217,13 @@ __global__ void __launch_bounds__(128) qkv_rope_kv_kernel(float* __restrict__ qk
 void launch_qkv_rope_kv(float* qkv, int M, const RowMeta& m, const float* rope_cos,
                         const float* rope_sin, int Hq, const KVLayer& kv, void* q_out, DType dt,
                         cudaStream_t st) {
+  const L2Pf pf = take_l2pf();
   if (M <= 0) return;
   const int grid = M * ROPE_PARTS + (M + VROWS - 1) / VROWS * kv.kv_heads * ((kv.head_dim + 31) / 32);
   if (dt == DT_F32)
-    launch_k(qkv_rope_kv_kernel<float>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out, M);
+    launch_k(qkv_rope_kv_kernel<float>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out, M, pf);
   else
-    launch_k(qkv_rope_kv_kernel<bf16>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out, M);
+    launch_k(qkv_rope_kv_kernel<bf16>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out, M, pf);
 }
 
 // ------------------------------------------------------------------ SwiGLU
@@ -226,8 +233,10 @@ void launch_qkv_rope_kv(float* qkv, int M, const RowMeta& m, const float* rope_c
 // value 64 columns later. out[i] = silu(gate) * up. grid (M, f/4/256), f % 64 == 0.
 template <typename T>
 __global__ void swiglu_kernel(float* __restrict__ gu, int f, T* __restrict__ out,
-                              const int32_t* __restrict__ pos) {
+                              const int32_t* __restrict__ pos, L2Pf pf) {
+  l2pf_issue(pf);
   pdl_wait();
+  l2pf_issue(pf, 1);
   pdl_trigger();
   const int r = blockIdx.x;
   const int i = blockIdx.y * blockDim.x + threadIdx.x;   // float4 index
@@ -245,10 +254,11 @@ __global__ void swiglu_kernel(float* __restrict__ gu, int f, T* __restrict__ out
 }
 
 void launch_swiglu(float* gu, int M, int f, void* out, DType dt, const int32_t* pos, cudaStream_t st) {
+  const L2Pf pf = take_l2pf();
   if (M <= 0) return;
   dim3 grid(M, (f / 4 + 255) / 256);
-  if (dt == DT_F32) launch_k(swiglu_kernel<float>, grid, 256, 0, st, gu, f, (float*)out, pos);
-  else launch_k(swiglu_kernel<bf16>, grid, 256, 0, st, gu, f, (bf16*)out, pos);
+  if (dt == DT_F32) launch_k(swiglu_kernel<float>, grid, 256, 0, st, gu, f, (float*)out, pos, pf);
+  else launch_k(swiglu_kernel<bf16>, grid, 256, 0, st, gu, f, (bf16*)out, pos, pf);
 }
 
 // gate rows [0,f) and up rows [f,2f) of src -> interleaved 64-row groups in dst

@@ -338,7 +338,9 @@ HSD_DEV void prune_nodes(NodesSm& nd, int keep, NodesSm& tmp) {
 
 template <int KT>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(TreeParams P, int mode) {
+  l2pf_issue(P.pf);
   pdl_wait();
+  l2pf_issue(P.pf, 1);
   pdl_trigger();
   __shared__ NodesSm nd, tmp;
   __shared__ ClusterSm cs;

@@ -31,6 +31,7 @@ struct TreeParams {
   uint32_t seed;
   int req_offset;
   int* err;
+  L2Pf pf;                   // weights of a later GEMM to prefetch into L2 (common.cuh)
 };
 
 void launch_tree(const TreeParams& P, int mode, int n_req, cudaStream_t st);

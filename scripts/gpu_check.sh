@@ -1,0 +1,9 @@
+# Round re-entry check: build, GPU tests, smoke, default bench line.
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+python -m paper_2602_21224_b200.build > /dev/null
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/tests_gpu.log 2>&1; echo "tests rc=$?"
+tail -5 gpurun_out/tests_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke.log
+(time timeout 900 python bench.py) > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
+tail -3 gpurun_out/bench_c2.err; tail -c 2500 gpurun_out/bench_c2.json
