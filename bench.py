@@ -51,6 +51,10 @@ def parse():
     ap.add_argument("--table-fp8", action="store_true",
                     help="token-info table as e4m3 codes + per-row scale (NEXT-3, reading R25)")
     ap.add_argument("--batch", type=int, default=None, help="override the config's global batch")
+    ap.add_argument("--vocab-shard", action="store_true",
+                    help="vocab-sharded lm_head (SURVEY 8(e), greedy): NCCL over the N ranks; on one GPU the "
+                         "simulated mode with --shards column shards")
+    ap.add_argument("--shards", type=int, default=8, help="shard count of the simulated --vocab-shard mode")
     return ap.parse_args()
 
 
@@ -334,6 +338,15 @@ def main():
     max_ctx = cfg.prompt_len + (args.warmup + args.steps + 12) * (N + 1) + 16
     stream = torch.cuda.Stream(device=local)
     perm = vocab_permutation(cfg.vocab, 0) if cfg.hot_tokens else None
+    shard_kw, shard_desc = {}, "replicated"
+    if args.vocab_shard:
+        if world > 1:
+            shard_kw = dict(shard_mode=hsd.SHARD_NCCL, vocab_shards=world, shard_rank=rank,
+                            nccl_id=hsd.shard_nccl_id())
+            shard_desc = f"vocab-sharded x{world} (NCCL all-gather + partial-argmax merge / all-to-all)"
+        else:
+            shard_kw = dict(shard_mode=hsd.SHARD_SIM, vocab_shards=args.shards)
+            shard_desc = f"vocab-sharded x{args.shards} simulated on one GPU (all shards computed locally)"
     t_init = time.perf_counter()
     # PLANTED flag set but no plant array until the planted leg: the timed run is
     # the plain method (the tree kernel plants only when a plant array exists)
@@ -342,7 +355,7 @@ def main():
                          max_batch=b, max_ctx=max_ctx + 64 * (N + 1), req_offset=lo, vocab_perm=perm,
                          tcgen05=not args.simt, flags=hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | hsd.FLAG_PLANTED |
                          (hsd.FLAG_TABLE_FP8 if args.table_fp8 else 0),
-                         plant_rates=plant_rates)
+                         plant_rates=plant_rates, **shard_kw)
     pr = prompts(cfg, batch=cfg.batch)[lo:hi]
     ctx.prefill(pr)
     t_init = time.perf_counter() - t_init
@@ -480,7 +493,8 @@ def main():
                        "accept": cfg.accept, "parallelism": parallel, "gemm": "simt" if args.simt else "tcgen05",
                        "l2": "no flush: every step streams >13 GB of weights (>> 126 MB L2)",
                        "weights": "Philox random-init (no trained weights)",
-                       "table": "fp8 e4m3 + row scale" if args.table_fp8 else "bf16"},
+                       "table": "fp8 e4m3 + row scale" if args.table_fp8 else "bf16",
+                       "lm_head": shard_desc},
             "tau": round(emitted_all / (args.steps * cfg.batch if cfg.batch >= world else args.steps * world * b), 4),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "tau_curve": tau_curve, "planted": planted,

@@ -81,7 +81,38 @@ typedef struct {
   const int32_t* vocab_perm;
   /* planted mode: acceptance rates a_1..a_N (R24)                            */
   float plant_rates[HSD_MAX_PLANT_DEPTH];
+  /* Vocab-sharded lm_head (BASELINE configs[4]). GREEDY only
+   * (stochastic + sharding -> HSD_EUNSUP). shard_mode != HSD_SHARD_NONE splits
+   * the two per-step heads -- the draft one-pass logits (S1a) and the
+   * verify head (S2) -- by vocabulary column: shard s owns columns
+   * [lo_s, lo_{s+1}), lo_s = floor(s*V/G / 128) * 128, lo_G = V, G =
+   * vocab_shards. Verify: every shard computes its columns for ALL rows, a
+   * per-row partial argmax (max value, lowest token id) over its columns, and
+   * the partials are merged exactly (the global argmax is the best partial).
+   * Draft: every shard computes its columns for all rows and an all-to-all
+   * returns each row owner its full fp32 logits rows (bit-identical columns).
+   *  HSD_SHARD_NCCL: G = number of processes (one per GPU), shard_rank = this
+   *    process; normalised rows are all-gathered and partials / logits slices
+   *    exchanged with NCCL (nccl_id = hsd_nccl_unique_id() bytes of shard 0,
+   *    broadcast by the caller). Every shard must prefill the same number of
+   *    requests. Each process keeps the full W_head (prefill's first-token
+   *    head stays local).
+   *  HSD_SHARD_SIM: one process computes all G column slices itself and runs
+   *    the same partial / merge / scatter kernels, the collectives replaced by
+   *    the buffers they would fill -- the single-GPU test of the sharded
+   *    arithmetic. shard_rank must be 0.
+   * In sharded mode hsd_verify_view.logits is NULL (no full logits rows).     */
+  int32_t vocab_shards, shard_rank, shard_mode;
+  uint8_t nccl_id[128];
 } hsd_config;
+
+enum { HSD_SHARD_NONE = 0, HSD_SHARD_NCCL = 1, HSD_SHARD_SIM = 2 };   /* hsd_config.shard_mode */
+
+/* Write a fresh NCCL unique id (128 bytes, HOST buffer `out`) for the shard
+ * group; call on shard 0 only and broadcast the bytes to the other shards.
+ * NCCL is loaded at run time (dlopen "libnccl.so.2"): HSD_ENCCL if it cannot
+ * be loaded or the call fails. Synchronous, no device work.                 */
+hsd_status hsd_nccl_unique_id(uint8_t* out);
 
 /* Fill *cfg with neutral defaults (flags RESAMPLE|FUSION, B_r 4, r 1, page 64). */
 void hsd_config_defaults(hsd_config* cfg);

@@ -266,12 +266,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_expect_tx(qbar, q_bytes);
       for (int a = 0; a < natom; ++a)
         tma_load_3d(&tmQ, qbar, sQ + a * (QROWS * 128), a * 64, h * P.G, row0, polq);
-      l2pf_issue(P.pf);   // behind this CTA's first K/V/Q loads in the TMA queue
       // K runs one chunk ahead of V: V_j waits for P_{j-2} V, K_{j+1} must not
       while (vj < n_chunks) {
         if (kj < n_chunks && kj <= vj + 1) load_k(kj++);
         else load_v(vj++);
       }
+      l2pf_issue(P.pf);   // after this CTA's last K/V load: the bulk prefetch queues behind them in TMA
     }
   } else if (warp == 1) {
     if (lane == 0 && n_chunks > 0) {

@@ -256,6 +256,16 @@ struct hsd_ctx {
   void *a, *qb, *ob, *h;   // h: SwiGLU output [Mcap, f] (never aliases the GEMM input a)
   int32_t* argmax;
   MetaBuf mv, md, mc, mp;
+  // vocab-sharded lm_head (shard.cu): G column shards, this one = srank
+  int shard_mode = HSD_SHARD_NONE, G = 1, srank = 0, shard_rows = 0, shard_wmax = 0;
+  int shard_lo[HSD_MAX_SHARDS + 1] = {};
+  void* comm = nullptr;
+  void* a_all = nullptr;         // [G * rows, n] all-gathered normalised rows (NCCL)
+  float* lslice = nullptr;       // [G * rows, w] this shard's logits columns
+  float* lrecv = nullptr;        // [G][rows][wmax] draft-logit column slices (all-to-all target)
+  float *pv_loc = nullptr, *pv_all = nullptr;     // partial argmax values [G*rows], [G][G*rows]
+  int32_t *pi_loc = nullptr, *pi_all = nullptr;   // partial argmax token ids
+  std::string nccl_err;          // first collective failure (surfaced as HSD_ENCCL)
   // host staging for e2e
   int32_t *h_pinned = nullptr;
   // graph
@@ -451,6 +461,63 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
   g_hsd_launches += 4;  // rmsnorm x2, rope_kv, attention (merge and swiglu counted where launched)
 }
 
+// ------------------------------------------------------- vocab-sharded lm_head
+// shard s owns head columns [lo_s, lo_{s+1}). c->a holds the M
+// normalised rows. SIM computes every shard's columns itself; NCCL computes its
+// own columns for the all-gathered rows of all G ranks (rank r's rows at r*M).
+static void shard_head_verify(hsd_ctx* c, int M) {
+  const size_t es = c->esz;
+  const int n = c->n, G = c->G, r = c->srank;
+  const int* lo = c->shard_lo;
+  if (c->shard_mode == HSD_SHARD_SIM) {
+    for (int s = 0; s < G; ++s) {
+      const int w = lo[s + 1] - lo[s];
+      gemm(c, c->a, n, (const char*)c->head + (size_t)lo[s] * n * es, n, c->lslice, w, M, w, n, false, P_HEAD_VERIFY);
+      { Prof pf(c, P_ROWWISE); launch_argmax_part(c->lslice, M, w, w, lo[s], c->pv_all + (size_t)s * M, c->pi_all + (size_t)s * M, c->st); }
+    }
+    { Prof pf(c, P_ROWWISE); launch_argmax_merge(c->pv_all, c->pi_all, G, M, 0, M, c->mv.pos, c->argmax, c->st); }
+    g_hsd_launches += G + 1;
+    return;
+  }
+  const int w = lo[r + 1] - lo[r];
+  if (!shard_allgather(c->a, c->a_all, (size_t)M * n * es, c->comm, c->st, c->nccl_err)) return;
+  gemm(c, c->a_all, n, (const char*)c->head + (size_t)lo[r] * n * es, n, c->lslice, w, G * M, w, n, false,
+       P_HEAD_VERIFY);
+  { Prof pf(c, P_ROWWISE); launch_argmax_part(c->lslice, G * M, w, w, lo[r], c->pv_loc, c->pi_loc, c->st); }
+  if (!shard_allgather(c->pv_loc, c->pv_all, (size_t)G * M * 4, c->comm, c->st, c->nccl_err)) return;
+  if (!shard_allgather(c->pi_loc, c->pi_all, (size_t)G * M * 4, c->comm, c->st, c->nccl_err)) return;
+  { Prof pf(c, P_ROWWISE); launch_argmax_merge(c->pv_all, c->pi_all, G, G * M, r * M, M, c->mv.pos, c->argmax, c->st); }
+  g_hsd_launches += 2;
+}
+
+// draft one-pass logits, sharded: full fp32 rows reassembled for the row owner
+static void shard_head_draft(hsd_ctx* c, int R) {
+  const size_t es = c->esz;
+  const int n = c->n, G = c->G, r = c->srank, wmax = c->shard_wmax;
+  const int* lo = c->shard_lo;
+  if (c->shard_mode == HSD_SHARD_SIM) {
+    for (int s = 0; s < G; ++s) {
+      const int w = lo[s + 1] - lo[s];
+      gemm(c, c->a, n, (const char*)c->head_rank + (size_t)lo[s] * n * es, n, c->lrecv + (size_t)s * R * wmax, w, R,
+           w, n, false, P_HEAD_DRAFT);
+    }
+  } else {
+    const int w = lo[r + 1] - lo[r];
+    if (!shard_allgather(c->a, c->a_all, (size_t)R * n * es, c->comm, c->st, c->nccl_err)) return;
+    gemm(c, c->a_all, n, (const char*)c->head_rank + (size_t)lo[r] * n * es, n, c->lslice, w, G * R, w, n, false,
+         P_HEAD_DRAFT);
+    size_t so[HSD_MAX_SHARDS], sb[HSD_MAX_SHARDS], ro[HSD_MAX_SHARDS], rb[HSD_MAX_SHARDS];
+    for (int p = 0; p < G; ++p) {
+      so[p] = (size_t)p * R * w * 4; sb[p] = (size_t)R * w * 4;
+      ro[p] = (size_t)p * R * wmax * 4; rb[p] = (size_t)R * (lo[p + 1] - lo[p]) * 4;
+    }
+    if (!shard_alltoallv((const char*)c->lslice, so, sb, (char*)c->lrecv, ro, rb, G, c->comm, c->st, c->nccl_err))
+      return;
+  }
+  { Prof pf(c, P_ROWWISE); launch_scatter_cols(c->lrecv, (size_t)R * wmax, R, G, lo, c->draft_logits, c->V, c->st); }
+  g_hsd_launches += 1;
+}
+
 // ---------------------------------------------------------------------- stages
 static void stage_build(hsd_ctx* c) {
   const int b = c->b, N = c->N, n = c->n, R = N + 1;
@@ -475,7 +542,8 @@ static void stage_build(hsd_ctx* c) {
   }
   // S1a: one-pass logits L = RMSNorm_f(H_chain) W_head^T, rank order
   launch_rmsnorm(c->chain, b * N, n, c->cfg.rms_eps, c->a, c->dt, nullptr, c->st);
-  gemm(c, c->a, n, c->head_rank, n, c->draft_logits, c->V, b * N, c->V, n, false, P_HEAD_DRAFT);
+  if (c->shard_mode != HSD_SHARD_NONE) shard_head_draft(c, b * N);
+  else gemm(c, c->a, n, c->head_rank, n, c->draft_logits, c->V, b * N, c->V, n, false, P_HEAD_DRAFT);
   g_hsd_launches += 1;
   // S1b + S1c: Alg. 1, prune, fuse, linearise (+ planting)
   TreeParams P{};
@@ -514,8 +582,12 @@ static void stage_verify(hsd_ctx* c) {
   for (int l = 0; l < c->L; ++l) layer_forward(c, c->layers[l], c->Hver, M, T, b, m, kv_layer(c, c->kv_t, l), c->max_pos);
   c->pass_verify = 0;
   launch_rmsnorm(c->Hver, M, n, c->cfg.rms_eps, c->a, c->dt, c->mv.pos, c->st);
-  gemm(c, c->a, n, c->head, n, c->logits, c->V, M, c->V, n, false, P_HEAD_VERIFY);
-  if (c->cfg.accept_mode == HSD_GREEDY) {   // the stochastic walk reads the logits rows itself
+  if (c->shard_mode != HSD_SHARD_NONE) {   // greedy only (checked at init)
+    shard_head_verify(c, M);
+  } else {
+    gemm(c, c->a, n, c->head, n, c->logits, c->V, M, c->V, n, false, P_HEAD_VERIFY);
+  }
+  if (c->cfg.accept_mode == HSD_GREEDY && c->shard_mode == HSD_SHARD_NONE) {   // the stochastic walk reads the logits rows itself
     Prof pf(c, P_ROWWISE);
     launch_argmax_rows(c->logits, M, c->V, c->mv.pos, c->argmax, c->st);
   }
@@ -581,6 +653,7 @@ static hsd_status run_stage(hsd_ctx* ctx, int idx, F&& body) {
   if (c->prof_on || c->st == nullptr || !g_stage_graphs) {
     body();
     CU(cudaGetLastError());
+    if (!c->nccl_err.empty()) return fail(c, HSD_ENCCL, c->nccl_err);
     return HSD_OK;
   }
   if (!c->sgraph[idx]) {
@@ -591,6 +664,7 @@ static hsd_status run_stage(hsd_ctx* ctx, int idx, F&& body) {
     body();
     c->capturing = false;
     CU(cudaStreamEndCapture(c->st, &g));
+    if (!c->nccl_err.empty()) return fail(c, HSD_ENCCL, c->nccl_err);
     c->sgraph_kernels[idx] = g_hsd_launches - before;
     g_hsd_launches = before;
     CU(cudaGraphInstantiate(&c->sgraph[idx], g, 0));
@@ -614,6 +688,16 @@ void hsd_config_defaults(hsd_config* c) {
 }
 
 const char* hsd_last_error(const hsd_ctx* ctx) { return ctx ? ctx->errmsg.c_str() : "null context"; }
+
+hsd_status hsd_nccl_unique_id(uint8_t* out) {
+  if (!out) return HSD_EINVAL;
+  std::string err;
+  if (!shard_nccl_unique_id(out, err)) {
+    fprintf(stderr, "hsd_nccl_unique_id: %s\n", err.c_str());
+    return HSD_ENCCL;
+  }
+  return HSD_OK;
+}
 
 int64_t hsd_kernel_launches(const hsd_ctx* ctx) {
   if (!ctx) return 0;
@@ -644,6 +728,13 @@ static std::string check_config(const hsd_config* c) {
   if (c->precision != HSD_FP32_VERIFY && c->precision != HSD_BF16) return "precision must be FP32_VERIFY or BF16";
   if (c->accept_mode != HSD_GREEDY && c->accept_mode != HSD_STOCHASTIC) return "bad accept_mode";
   if (c->accept_mode == HSD_STOCHASTIC && !(c->temperature > 0.f)) return "temperature must be > 0";
+  if (c->shard_mode != HSD_SHARD_NONE) {
+    if (c->shard_mode != HSD_SHARD_NCCL && c->shard_mode != HSD_SHARD_SIM) return "bad shard_mode";
+    if (c->vocab_shards < 1 || c->vocab_shards > HSD_MAX_SHARDS) return "vocab_shards must be in [1, 16]";
+    if (c->vocab < 128 * c->vocab_shards) return "vocab_shards > V / 128 (each shard owns >= 128 columns)";
+    if (c->shard_mode == HSD_SHARD_SIM && c->shard_rank != 0) return "HSD_SHARD_SIM requires shard_rank 0";
+    if (c->shard_rank < 0 || c->shard_rank >= c->vocab_shards) return "shard_rank must be in [0, vocab_shards)";
+  }
   return "";
 }
 
@@ -657,6 +748,10 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     last = why;
     fprintf(stderr, "hsd_init_model: %s\n", why.c_str());
     return HSD_EINVAL;
+  }
+  if (cfg->shard_mode != HSD_SHARD_NONE && cfg->accept_mode != HSD_GREEDY) {
+    fprintf(stderr, "hsd_init_model: the vocab-sharded lm_head supports greedy acceptance only\n");
+    return HSD_EUNSUP;
   }
   hsd_ctx* ctx = new hsd_ctx();
   ctx->cfg = *cfg;
@@ -862,11 +957,36 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     meta(c->md, (size_t)b * (N + 1));
     meta(c->mc, (size_t)b);
     meta(c->mp, (size_t)PREFILL_CHUNK);
+    if (cfg->shard_mode != HSD_SHARD_NONE) {
+      c->shard_mode = cfg->shard_mode;
+      c->G = cfg->vocab_shards;
+      c->srank = cfg->shard_rank;
+      for (int s = 0; s < c->G; ++s) c->shard_lo[s] = (int)(((long)s * V / c->G) / 128 * 128);
+      c->shard_lo[c->G] = V;
+      c->shard_wmax = 0;
+      for (int s = 0; s < c->G; ++s) c->shard_wmax = std::max(c->shard_wmax, c->shard_lo[s + 1] - c->shard_lo[s]);
+      const int rows = std::max(b * T, b * N), G = c->G, wmax = c->shard_wmax;
+      c->shard_rows = rows;
+      const int grows = c->shard_mode == HSD_SHARD_NCCL ? G * rows : rows;
+      c->lslice = F((size_t)grows * wmax);
+      c->lrecv = F((size_t)G * rows * wmax);
+      c->pv_loc = F((size_t)G * rows); c->pi_loc = I((size_t)G * rows);
+      c->pv_all = F((size_t)G * G * rows); c->pi_all = I((size_t)G * G * rows);
+      if (c->shard_mode == HSD_SHARD_NCCL) c->a_all = A((size_t)G * rows * n * es);
+    }
     if (fail_alloc) { hsd_destroy(c); return HSD_ENOMEM; }
     if (cudaMallocHost(&c->h_pinned, sizeof(int32_t) * (size_t)b * (N + 2)) != cudaSuccess) c->h_pinned = nullptr;
   }
   CU(cudaStreamSynchronize(c->st));
   CU(cudaGetLastError());
+  if (c->shard_mode == HSD_SHARD_NCCL) {
+    std::string err;
+    if (!shard_nccl_init(&c->comm, c->G, cfg->nccl_id, c->srank, err)) {
+      fprintf(stderr, "hsd_init_model: %s\n", err.c_str());
+      hsd_destroy(c);
+      return HSD_ENCCL;
+    }
+  }
   *out = c;
   return HSD_OK;
 }
@@ -990,7 +1110,8 @@ static void fill_tree_view(hsd_ctx* c, hsd_tree_view* v) {
 }
 static void fill_verify_view(hsd_ctx* c, hsd_verify_view* v) {
   if (!v) return;
-  v->logits = c->logits; v->argmax = c->argmax; v->hidden = c->Hver;
+  v->logits = c->shard_mode != HSD_SHARD_NONE ? nullptr : c->logits;   // sharded: no full rows
+  v->argmax = c->argmax; v->hidden = c->Hver;
   v->batch = c->b; v->t_max = c->T; v->vocab = c->V; v->hidden_dim = c->n;
 }
 
@@ -1060,6 +1181,7 @@ hsd_status hsd_step(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n_emitted) {
     // profiled steps run eagerly so every launch is bracketed by CUDA events
     stage_build(c); stage_verify(c); stage_accept(c, d_emitted, d_n_emitted);
     CU(cudaGetLastError());
+    if (!c->nccl_err.empty()) return fail(c, HSD_ENCCL, c->nccl_err);
     return HSD_OK;
   }
   if (!c->graph) {
@@ -1067,6 +1189,7 @@ hsd_status hsd_step(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n_emitted) {
       // graphs cannot capture the legacy stream: run eagerly
       stage_build(c); stage_verify(c); stage_accept(c, nullptr, nullptr);
       CU(cudaGetLastError());
+      if (!c->nccl_err.empty()) return fail(c, HSD_ENCCL, c->nccl_err);
     } else {
       int64_t before = g_hsd_launches;
       cudaGraph_t g;
@@ -1075,6 +1198,7 @@ hsd_status hsd_step(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n_emitted) {
       stage_build(c); stage_verify(c); stage_accept(c, nullptr, nullptr);
       c->capturing = false;
       CU(cudaStreamEndCapture(c->st, &g));
+      if (!c->nccl_err.empty()) return fail(c, HSD_ENCCL, c->nccl_err);
       c->graph_kernels = g_hsd_launches - before;
       g_hsd_launches = before;  // counted per replay instead
       CU(cudaGraphInstantiate(&c->graph, g, 0));
@@ -1234,6 +1358,7 @@ hsd_status hsd_destroy(hsd_ctx* ctx) {
   else cudaDeviceSynchronize();
   drop_graphs(ctx);
   prof_collect(ctx);
+  shard_nccl_destroy(ctx->comm);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);

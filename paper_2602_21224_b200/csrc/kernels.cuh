@@ -1,5 +1,6 @@
 // kernels.cuh -- launcher declarations shared by the engine (product side).
 #pragma once
+#include <string>
 #include "common.cuh"
 
 // Per-row metadata of one forward pass (rows are padded; pos < 0 = inactive).
@@ -68,3 +69,20 @@ void launch_attention(const void* q, int M, int rows_per_req, int n_req, const R
                       int Hq, DType dt, int max_keys, void* out, float* ws, size_t ws_floats,
                       cudaStream_t st);
 size_t attention_ws_floats(int M, int Hq, int hd, int max_splits);
+
+// shard.cu: vocab-sharded lm_head -- partial argmax / merge /
+// column scatter kernels and the run-time-loaded NCCL entry points
+#define HSD_MAX_SHARDS 16
+void launch_argmax_part(const float* x, int rows, int ld, int w, int col0, float* outv, int32_t* outi,
+                        cudaStream_t st);
+void launch_argmax_merge(const float* pv, const int32_t* pi, int S, int stride, int row0, int M,
+                         const int32_t* pos, int32_t* out, cudaStream_t st);
+void launch_scatter_cols(const float* src, size_t src_stride, int rows, int S, const int* lo, float* dst, int ld,
+                         cudaStream_t st);
+bool shard_nccl_unique_id(uint8_t* out, std::string& err);
+bool shard_nccl_init(void** comm, int nranks, const uint8_t* id_bytes, int rank, std::string& err);
+void shard_nccl_destroy(void* comm);
+bool shard_allgather(const void* send, void* recv, size_t bytes, void* comm, cudaStream_t st, std::string& err);
+bool shard_alltoallv(const char* send, const size_t* send_off, const size_t* send_bytes, char* recv,
+                     const size_t* recv_off, const size_t* recv_bytes, int nranks, void* comm, cudaStream_t st,
+                     std::string& err);

@@ -22,11 +22,12 @@ FP32_VERIFY, BF16 = 0, 1
 GREEDY, STOCHASTIC = 0, 1
 FLAG_RESAMPLE, FLAG_FUSION, FLAG_PLANTED, FLAG_ZERO_TABLE, FLAG_TCGEN05, FLAG_TABLE_FP8 = 1, 2, 4, 8, 16, 32
 MAX_PLANT_DEPTH = 16
+SHARD_NONE, SHARD_NCCL, SHARD_SIM = 0, 1, 2
 
 EXPORTS = ["hsd_config_defaults", "hsd_init_model", "hsd_prefill", "hsd_set_plant", "hsd_build_tree",
            "hsd_force_tree", "hsd_verify_tree", "hsd_accept_and_compact", "hsd_step", "hsd_step_host",
            "hsd_sync", "hsd_get_tensor", "hsd_kernel_launches", "hsd_destroy", "hsd_last_error",
-           "hsd_profile", "hsd_profile_read", "hsd_debug_gemm"]
+           "hsd_profile", "hsd_profile_read", "hsd_debug_gemm", "hsd_nccl_unique_id"]
 PROFILE_CATEGORIES = ["gemm_verify", "gemm_draft", "head_verify", "head_draft", "attn_verify", "attn_draft",
                       "tree", "resample", "walk", "compact", "rowwise"]
 
@@ -38,7 +39,9 @@ class HsdConfig(C.Structure):
                                    "hot_tokens", "table_rank", "max_batch", "max_ctx", "page_size", "precision",
                                    "accept_mode")] + \
         [("temperature", C.c_float), ("seed", C.c_uint64), ("flags", C.c_uint32), ("req_offset", C.c_int32),
-         ("vocab_perm", C.POINTER(C.c_int32)), ("plant_rates", C.c_float * MAX_PLANT_DEPTH)]
+         ("vocab_perm", C.POINTER(C.c_int32)), ("plant_rates", C.c_float * MAX_PLANT_DEPTH),
+         ("vocab_shards", C.c_int32), ("shard_rank", C.c_int32), ("shard_mode", C.c_int32),
+         ("nccl_id", C.c_uint8 * 128)]
 
 
 class TreeView(C.Structure):
@@ -88,6 +91,7 @@ def load(path: str = LIB_PATH):
         "hsd_profile": (I32, [VP, C.c_int]),
         "hsd_debug_gemm": (I32, [VP, I32, VP, I32, VP, I32, I32, I32, I32, I32, I32, I32, VP]),
         "hsd_profile_read": (I32, [VP, C.c_char_p, P(C.c_double), P(I64), P(C.c_double), P(C.c_double)]),
+        "hsd_nccl_unique_id": (I32, [P(C.c_uint8)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -109,7 +113,7 @@ def _i32(a):
 
 def make_config(model_cfg, *, precision=BF16, max_batch=None, max_ctx=None, seed=0, flags=None,
                 accept=None, temperature=None, req_offset=0, vocab_perm=None, plant_rates=None,
-                page_size=64, tcgen05=False):
+                page_size=64, tcgen05=False, vocab_shards=1, shard_rank=0, shard_mode=SHARD_NONE, nccl_id=None):
     """Build an HsdConfig from a shape description (any object with the
     attributes of synth.Config). Returns (config, keepalive)."""
     lib = load()
@@ -131,6 +135,12 @@ def make_config(model_cfg, *, precision=BF16, max_batch=None, max_ctx=None, seed
     c.seed = int(seed)
     c.flags = int(flags if flags is not None else (FLAG_RESAMPLE | FLAG_FUSION)) | (FLAG_TCGEN05 if tcgen05 else 0)
     c.req_offset = int(req_offset)
+    c.vocab_shards, c.shard_rank, c.shard_mode = int(vocab_shards), int(shard_rank), int(shard_mode)
+    if nccl_id is not None:
+        b = bytes(nccl_id)
+        if len(b) != 128:
+            raise ValueError("nccl_id must be 128 bytes (hsd_nccl_unique_id)")
+        C.memmove(c.nccl_id, b, 128)
     keep = []
     if vocab_perm is not None:
         arr, ptr = _i32(vocab_perm)
@@ -269,6 +279,31 @@ def debug_gemm(A, W, C, accumulate=False, use_tc=False, stream=0):
                            2 if use_tc == "swiglu" else int(bool(use_tc)), stream)
     if s != HSD_OK:
         raise HsdError(s, "hsd_debug_gemm")
+
+
+def nccl_unique_id() -> bytes:
+    """hsd_nccl_unique_id: 128 bytes on shard 0, to broadcast to the other shards."""
+    buf = (C.c_uint8 * 128)()
+    s = load().hsd_nccl_unique_id(buf)
+    if s != HSD_OK:
+        raise HsdError(s, "hsd_nccl_unique_id (libnccl.so.2 not loadable?)")
+    return bytes(buf)
+
+
+def shard_nccl_id(group=None) -> bytes:
+    """Bootstrap of the vocab-shard NCCL group over an initialised
+    torch.distributed process group (any backend): shard 0 creates the id
+    (hsd_nccl_unique_id), every rank receives the same 128 bytes."""
+    import torch.distributed as dist
+    obj = [nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return obj[0]
+
+
+def vocab_shard_bounds(V: int, G: int):
+    """Column bounds lo_0..lo_G of the G vocab shards (include/hsd.h): lo_s =
+    floor(s*V/G / 128) * 128, lo_G = V. Host-side mirror for tests/planning."""
+    return [(s * V // G) // 128 * 128 for s in range(G)] + [V]
 
 
 def init_model(model_cfg, device=0, stream=None, **kw) -> Context:

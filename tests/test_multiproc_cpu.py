@@ -74,3 +74,28 @@ def test_sharding_invariance_of_the_stochastic_method():
     for lo, hi in (shard_requests(4, 2, 0), shard_requests(4, 2, 1)):
         parts += Engine(m, TokenInfoTable(m), cfg, seed=5, req_offset=lo).decode(pr[lo:hi], 10)
     assert whole == parts
+
+
+def _shard_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2602_21224_b200 import hsd
+    nid = hsd.shard_nccl_id()
+    cfg = get_config("c1")
+    c, _ = hsd.make_config(cfg, shard_mode=hsd.SHARD_NCCL, vocab_shards=world, shard_rank=rank, nccl_id=nid)
+    out[rank] = (bytes(c.nccl_id), c.shard_rank, c.vocab_shards, c.shard_mode)
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_vocab_shard_bootstrap():
+    """Vocab-sharded lm_head bootstrap: shard 0's NCCL unique id
+    reaches every rank intact through the process group, and each rank's config
+    names its own shard of the same G-shard group."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_shard_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    ids = [out[r][0] for r in range(world)]
+    assert len(ids[0]) == 128 and ids[0] == ids[1] and any(ids[0])
+    assert [out[r][1] for r in range(world)] == [0, 1]
+    assert all(out[r][2] == world and out[r][3] == 1 for r in range(world))
