@@ -32,7 +32,9 @@ unsigned long long* g_attn_trace = nullptr;   // debug phase trace (HSD_ATTN_TRA
 
 namespace {
 using namespace tc;
-constexpr int NTHREADS = 320;   // TMA, MMA, 8 softmax warps
+// softmax warps per TMEM lane quarter (SW): each owns CHUNK / SW keys of a chunk;
+// the CTA has 64 + 128 * SW threads (TMA warp, MMA warp, 4 * SW softmax warps)
+template <int SW> constexpr int nthreads() { return 64 + 128 * SW; }
 constexpr int PAGE = 64;
 constexpr int CHUNK = 128;     // keys per softmax iteration = 2 pages
 constexpr int KSTAGES = 3;     // K ring: a stage frees when its S MMA completes
@@ -118,9 +120,12 @@ HSD_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
-HSD_DEV void pair_sync(int q) { asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory"); }
+// the SW softmax warps of lane quarter q (named barrier 1 + q)
+template <int SW>
+HSD_DEV void quad_sync(int q) { asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * SW) : "memory"); }
 
-__global__ void __launch_bounds__(NTHREADS, 1)
+template <int SW>
+__global__ void __launch_bounds__(nthreads<SW>(), 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, AttnParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -144,8 +149,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* odone = pvdone + 1;          // after the last P V MMA
   uint32_t* tmem_slot = (uint32_t*)(odone + 1);
   __shared__ int tile_lo, tile_hi, safe_hi;
-  __shared__ float red_max[2][2][QROWS];   // [chunk parity][half][row]
-  __shared__ float red_l[2][QROWS];
+  constexpr int NTHREADS = nthreads<SW>();
+  constexpr int KPW = CHUNK / SW;          // keys per softmax warp per chunk (64 or 32)
+  constexpr int NSM = 128 * SW;            // softmax threads
+  __shared__ float red_max[2][SW][QROWS];   // [chunk parity][key part][row]
+  __shared__ float red_l[SW][QROWS];
   __shared__ float fin_m[QROWS], fin_l[QROWS];   // cluster mode: this split's (m, l) per tile row
   __shared__ float wts[QROWS][8];                // cluster mode: merge weight of each split, per row
 
@@ -162,7 +170,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int s = 0; s < KSTAGES; ++s) { mbar_init(&kfull[s], 1); mbar_init(&kempty[s], 1); }
     for (int s = 0; s < VSTAGES; ++s) { mbar_init(&vfull[s], 1); mbar_init(&vempty[s], 1); }
     mbar_init(qbar, 1);
-    for (int b = 0; b < 2; ++b) { mbar_init(&sfull[b], 1); mbar_init(&pfull[b], 256); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&sfull[b], 1); mbar_init(&pfull[b], NSM); }
     mbar_init(pvdone, 1);
     mbar_init(odone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -209,7 +217,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (hi > lo) { atomicMin(&tile_lo, lo); atomicMax(&tile_hi, hi); }
     }
     int pmin = 0x7fffffff;
-    for (int r = threadIdx.x - 64; r < P.R; r += 256) {
+    for (int r = threadIdx.x - 64; r < P.R; r += NSM) {
       const int pr = grp * P.R + r < P.M ? m.pos[grp * P.R + r] : -1;
       if (pr >= 0) pmin = min(pmin, pr);
     }
@@ -314,55 +322,60 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else {
     // ------------------------------------------------------------ softmax warps
-    const int half = (warp - 2) >> 2;                  // which 32 keys of the page
+    const int part = (warp - 2) >> 2;                  // which KPW keys of the chunk
     const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
-    float mrow = -INFINITY, lrow = 0.f;                // log2 domain; lrow = this half's partial sum
+    float mrow = -INFINITY, lrow = 0.f;                // log2 domain; lrow = this part's partial sum
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    const int hcols = hd / 2;                           // this half's O columns
+    const int hcols = hd / SW;                          // this part's O columns
     for (int j = 0; j < n_chunks; ++j) {
       mbar_wait(&sfull[j & 1], (j >> 1) & 1);
       fence_after();
       if (threadIdx.x == 64 && j < 12) TRACE(8 + 4 * j);
-      const int kb = (c_first + j) * CHUNK + half * 64;       // this half's 64 keys
+      const int kb = (c_first + j) * CHUNK + part * KPW;       // this part's keys
       uint32_t r0[32], r1[32];
-      tmem_ld32_nw(tS + lane_off + (uint32_t)((j & 1) * CHUNK + half * 64), r0);
-      tmem_ld32_nw(tS + lane_off + (uint32_t)((j & 1) * CHUNK + half * 64 + 32), r1);
-      uint32_t vm0 = 0u, vm1 = 0u;
+      tmem_ld32_nw(tS + lane_off + (uint32_t)((j & 1) * CHUNK + part * KPW), r0);
+      if constexpr (KPW == 64) tmem_ld32_nw(tS + lane_off + (uint32_t)((j & 1) * CHUNK + part * KPW + 32), r1);
+      uint32_t vm0 = 0u, vm1 = 0xffffffffu;
       if (valid) {
         vm0 = range32(klo - kb, khi - kb);
-        vm1 = range32(klo - kb - 32, khi - kb - 32);
-        if (slot >= 0) {
-          vm0 |= anc32(anc, kb - tb) & range32(0, m.t_max - (kb - tb));
-          vm1 |= anc32(anc, kb + 32 - tb) & range32(0, m.t_max - (kb + 32 - tb));
-        }
+        if (slot >= 0) vm0 |= anc32(anc, kb - tb) & range32(0, m.t_max - (kb - tb));
         vm0 &= range32(k_begin - kb, k_end - kb);
-        vm1 &= range32(k_begin - kb - 32, k_end - kb - 32);
+        if constexpr (KPW == 64) {
+          vm1 = range32(klo - kb - 32, khi - kb - 32);
+          if (slot >= 0) vm1 |= anc32(anc, kb + 32 - tb) & range32(0, m.t_max - (kb + 32 - tb));
+          vm1 &= range32(k_begin - kb - 32, k_end - kb - 32);
+        }
       }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       // raw scores, -inf where invisible (scale_log2 > 0 keeps the order, and is
       // folded into the exponent's FFMA below)
-      float s[64];
-      if (__all_sync(0xffffffffu, (vm0 & vm1) == 0xffffffffu)) {   // whole warp sees all 64 keys
+      float s[KPW];
+      if (__all_sync(0xffffffffu, (vm0 & vm1) == 0xffffffffu)) {   // whole warp sees all its keys
 #pragma unroll
-        for (int i = 0; i < 32; ++i) { s[i] = __uint_as_float(r0[i]); s[32 + i] = __uint_as_float(r1[i]); }
+        for (int i = 0; i < 32; ++i) {
+          s[i] = __uint_as_float(r0[i]);
+          if constexpr (KPW == 64) s[32 + i] = __uint_as_float(r1[i]);
+        }
       } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           s[i] = ((vm0 >> i) & 1u) ? __uint_as_float(r0[i]) : -INFINITY;
-          s[32 + i] = ((vm1 >> i) & 1u) ? __uint_as_float(r1[i]) : -INFINITY;
+          if constexpr (KPW == 64) s[32 + i] = ((vm1 >> i) & 1u) ? __uint_as_float(r1[i]) : -INFINITY;
         }
       }
-      // 8 independent max chains (a single chain is 64 dependent FMNMX)
+      // 8 independent max chains (a single chain is KPW dependent FMNMX)
       float mxp[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) mxp[k] = s[k];
 #pragma unroll
-      for (int i = 8; i < 64; ++i) mxp[i & 7] = fmaxf(mxp[i & 7], s[i]);
+      for (int i = 8; i < KPW; ++i) mxp[i & 7] = fmaxf(mxp[i & 7], s[i]);
       float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
                        fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
-      red_max[j & 1][half][lane_row] = mx;
-      pair_sync(q4);
-      mx = fmaxf(red_max[j & 1][0][lane_row], red_max[j & 1][1][lane_row]) * scale_log2;
+      red_max[j & 1][part][lane_row] = mx;
+      quad_sync<SW>(q4);
+#pragma unroll
+      for (int p2 = 0; p2 < SW; ++p2) mx = fmaxf(mx, red_max[j & 1][p2][lane_row]);
+      mx *= scale_log2;
       // lazy rescale: keep the running max unless the chunk raises it by more than
       // 2^8 (P <= 256, exact in bf16's exponent range; fp32 O and l absorb it); a
       // row with nothing visible yet has O == 0 exactly, so it just adopts the max
@@ -375,18 +388,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       const float msub = mrow == -INFINITY ? 0.f : mrow;   // P = 0, never ex2(-inf + inf)
       if (threadIdx.x == 64 && j < 12) TRACE(9 + 4 * j);
-      // P_j (bf16) over this half's 32 columns of S_j (64 keys, 2 per column)
+      // P_j (bf16) over this part's KPW/2 columns of S_j (KPW keys, 2 per column)
       float ps[4] = {0.f, 0.f, 0.f, 0.f};                 // 4 independent sum chains
       uint32_t pw[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < KPW / 2; ++i) {
         const float p0 = ex2(fmaf(s[2 * i], scale_log2, -msub)), p1 = ex2(fmaf(s[2 * i + 1], scale_log2, -msub));
         __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
         ps[i & 3] += __low2float(pr) + __high2float(pr);     // l sums exactly what the MMA sees
         pw[i] = *(uint32_t*)&pr;
       }
       const float psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
-      tmem_st32(tS + lane_off + (uint32_t)((j & 1) * CHUNK + half * 32), pw);
+      if constexpr (KPW == 64) {
+        tmem_st32(tS + lane_off + (uint32_t)((j & 1) * CHUNK + part * 32), pw);
+      } else {
+        uint32_t pw16[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pw16[i] = pw[i];
+        tmem_st16(tS + lane_off + (uint32_t)((j & 1) * CHUNK + part * 16), pw16);
+      }
       if (__any_sync(0xffffffffu, alpha != 1.f)) {
         // O must hold P_{<j} V exactly once before it is scaled: S_j completing
         // implies P_{j-2} V done, so pvdone is within one phase of j-1
@@ -397,10 +417,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (threadIdx.x == 64 && j < 12) TRACE(10 + 4 * j);
         for (int c = 0; c < hcols; c += 16) {
           uint32_t o[16];
-          tmem_ld16(tO + lane_off + (uint32_t)(half * hcols + c), o);
+          tmem_ld16(tO + lane_off + (uint32_t)(part * hcols + c), o);
 #pragma unroll
           for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st16(tO + lane_off + (uint32_t)(half * hcols + c), o);
+          tmem_st16(tO + lane_off + (uint32_t)(part * hcols + c), o);
         }
       }
       tmem_st_wait();
@@ -410,15 +430,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (threadIdx.x == 64 && j < 12) TRACE(11 + 4 * j);
     }
     // ------------------------------------------------------------ epilogue
-    red_l[half][lane_row] = lrow;
+    red_l[part][lane_row] = lrow;
     if (n_chunks > 0) {
       mbar_wait(odone, 0);
       fence_after();
     }
     if (threadIdx.x == 64) { TRACE(4); if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[7] = n_chunks; }
-    pair_sync(q4);
+    quad_sync<SW>(q4);
     if (threadIdx.x == 64) TRACE(56);
-    const float ltot = red_l[0][lane_row] + red_l[1][lane_row];
+    float ltot = 0.f;
+#pragma unroll
+    for (int p2 = 0; p2 < SW; ++p2) ltot += red_l[p2][lane_row];
     // O half-row (hcols fp32) -> the idle K/V ring (>= 128 rows x hd fp32) ->
     // each warp then writes its 32 rows row by row with coalesced vectors
     float* ostage = (float*)sK;                       // [128 rows][hd + 4]
@@ -426,18 +448,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const float inv = (P.direct && ltot > 0.f) ? 1.0f / ltot : 1.0f;
     for (int c = 0; c < hcols; c += 16) {
       uint32_t o[16];
-      if (n_chunks > 0) tmem_ld16(tO + lane_off + (uint32_t)(half * hcols + c), o);
+      if (n_chunks > 0) tmem_ld16(tO + lane_off + (uint32_t)(part * hcols + c), o);
       else
         for (int i = 0; i < 16; ++i) o[i] = 0u;
-      float* dst = ostage + lane_row * ost + half * hcols + c;
+      float* dst = ostage + lane_row * ost + part * hcols + c;
 #pragma unroll
       for (int i = 0; i < 16; i += 4)
         *(float4*)(dst + i) = ltot > 0.f ? make_float4(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv,
                                                        __uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv)
                                          : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    if (P.cluster && half == 0) { fin_m[lane_row] = mrow; fin_l[lane_row] = ltot; }
-    asm volatile("bar.sync 5, 256;" ::: "memory");   // all 8 softmax warps staged their rows
+    if (P.cluster && part == 0) { fin_m[lane_row] = mrow; fin_l[lane_row] = ltot; }
+    asm volatile("bar.sync 5, %0;" ::"r"(NSM) : "memory");   // all softmax warps staged their rows
     if (threadIdx.x == 64) TRACE(57);
     if (!P.cluster) {
     // the CTA's valid rows of one (kv head, q-tile): all 256 softmax threads write
@@ -450,7 +472,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int n_rh = min(QROWS, P.R * P.G - qt * QROWS);        // valid (row, head) pairs in the tile
       const int vpr = hd / 4, rpi = 32 / vpr;
       const int d4 = (lane % vpr) * 4;
-      const int step = 8 * rpi, step_rl = step / P.G, step_g = step % P.G;
+      const int step = 4 * SW * rpi, step_rl = step / P.G, step_g = step % P.G;
       int lr = sw * rpi + lane / vpr;
       int rl2 = (qt * QROWS + lr) / P.G, g2 = (qt * QROWS + lr) % P.G;
       for (; lr < n_rh; lr += step) {
@@ -471,7 +493,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
     if (threadIdx.x == 64) TRACE(58);
-    if (!P.direct && writable && half == 0) {
+    if (!P.direct && writable && part == 0) {
       const size_t base_ml = (size_t)gridDim.x * P.M * P.Hq * hd;
       const size_t idx = ((size_t)split * P.Hq + head) * P.M + row;
       P.ws[base_ml + 2 * idx] = mrow;      // log2 domain (merge uses exp2)
@@ -640,21 +662,31 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
     return -1;
   const size_t smem = 1024 + (size_t)QROWS * hd * 2 + (KSTAGES + VSTAGES) * ((size_t)CHUNK * hd * 2) +
                       (2 * KSTAGES + 2 * VSTAGES + 8) * 8 + 64;
-  static size_t attr = 0;   // (the kernel also has ~1 KB of static shared memory)
-  if (smem > attr) {
-    if (cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess) {
-      cudaGetLastError();
-      return -1;
+  // softmax warps per lane quarter: 2 (8 softmax warps, 64 keys each) or 4 (16 warps,
+  // 32 keys each: shorter per-thread chains, more warps to hide TMEM/barrier latency).
+  // Measured: c3 (768 CTAs, many waves) attention 11.6 -> 11.1
+  // ms with 4; c2 (<= 1 wave) 1.05 -> 1.08 ms. So 4 when the grid spans > 2 waves.
+  // HSD_ATTN_SW=2|4 forces one.
+  static const int sw_env = [] { const char* e = getenv("HSD_ATTN_SW"); return e ? atoi(e) : 0; }();
+  const int sw = sw_env == 2 || sw_env == 4 ? sw_env : ((size_t)S * base_ctas > 2 * (size_t)num_sms() ? 4 : 2);
+  static size_t attr[2] = {0, 0};   // (the kernel also has ~1-3 KB of static shared memory)
+  auto launch = [&](auto kern, int nthr, size_t& at) {
+    if (smem > at) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      at = smem;
     }
-    attr = smem;
-  }
-  dim3 grid(S, kv.kv_heads, n_req * P.n_qtiles);
-  if (P.cluster) {
-    launch_k_cluster(attention_tc_kernel, grid, dim3(NTHREADS), smem, st, S, mq, mk, mv, P);
-    return 1;
-  }
-  launch_k(attention_tc_kernel, grid, dim3(NTHREADS), smem, st, mq, mk, mv, P);
+    dim3 grid(S, kv.kv_heads, n_req * P.n_qtiles);
+    if (P.cluster) launch_k_cluster(kern, grid, dim3(nthr), smem, st, S, mq, mk, mv, P);
+    else launch_k(kern, grid, dim3(nthr), smem, st, mq, mk, mv, P);
+    return true;
+  };
+  const bool ok = sw == 4 ? launch(attention_tc_kernel<4>, nthreads<4>(), attr[1])
+                          : launch(attention_tc_kernel<2>, nthreads<2>(), attr[0]);
+  if (!ok) return -1;
+  if (P.cluster) return 1;
   int launched = 1;
   if (S > 1) {
     launch_k(attention_merge_bf16_kernel, (M * Hq + 7) / 8, 256, 0, st, ws, S, M, Hq, hd, (bf16*)out,
