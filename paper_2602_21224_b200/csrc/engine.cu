@@ -759,6 +759,7 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
   ctx->launches0 = g_hsd_launches;
   CU(cudaSetDevice(device));
   ctx->st = (cudaStream_t)cuda_stream;
+  tree_trace_init();
   hsd_ctx* c = ctx;
   c->dt = cfg->precision == HSD_BF16 ? DT_BF16 : DT_F32;
   c->esz = c->dt == DT_BF16 ? 2 : 4;
@@ -1293,6 +1294,8 @@ hsd_status hsd_get_tensor(hsd_ctx* ctx, const char* name, hsd_tensor* out) {
   if (s == "kv_draft") return set(c->kv_d, adt, {1, c->maxb * c->pages_per_req, 2, (int64_t)c->Hkv * c->page_size * c->hd});
   extern unsigned long long* g_attn_trace;
   if (s == "attn_trace" && g_attn_trace) return set(g_attn_trace, 3, {64});
+  extern unsigned long long* g_tree_trace;
+  if (s == "tree_trace" && g_tree_trace) return set(g_tree_trace, 3, {64});
   if (s == "layer0_wqkv" && c->L > 0) return set(c->layers[0].wqkv, adt, {c->qkvd, n});
   return fail(c, HSD_EINVAL, "unknown tensor name " + s);
 }

@@ -18,8 +18,19 @@
 
 namespace cg = cooperative_groups;
 
+unsigned long long* g_tree_trace = nullptr;   // debug phase trace (HSD_TREE_TRACE)
+
 namespace {
 constexpr int NT = 1024;
+// Debug phase trace: thread 0 of request 0's leader CTA stamps %globaltimer
+#define TTRACE(i)                                                                                   \
+  do {                                                                                              \
+    if (P.trace && threadIdx.x == 0 && blockIdx.x == 0) {                                           \
+      uint64_t t_;                                                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                        \
+      P.trace[(i)] = t_;                                                                            \
+    }                                                                                               \
+  } while (0)
 constexpr int CL = 8;       // CTAs per request (one thread-block cluster)
 constexpr int KMAX = 8;
 constexpr int MAXN = 256;
@@ -47,32 +58,11 @@ HSD_DEV bool beats(float v, int j, int l, float w, int i, int m, const int32_t* 
 }
 
 #define perm_of(P) ((P).perm)
-// per-thread top-KC list, sorted by (value desc, token asc); KC = k exactly, so
-// the admission test is against the k-th best and insertion bubbles k-1 steps
-template <int KC>
-struct Top {
-  float v[KC];
-  int j[KC];
-};
-
-template <int KC>
-HSD_DEV void top_init(Top<KC>& t) {
-#pragma unroll
-  for (int s = 0; s < KC; ++s) { t.v[s] = -INFINITY; t.j[s] = -1; }
+HSD_DEV float ex2f_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
-template <int KC>
-HSD_DEV void top_insert(Top<KC>& t, float v, int j, const int32_t* perm) {
-  if (!better_j(v, j, t.v[KC - 1], t.j[KC - 1], perm)) return;
-  t.v[KC - 1] = v; t.j[KC - 1] = j;
-#pragma unroll
-  for (int s = KC - 1; s > 0; --s) {
-    if (better_j(t.v[s], t.j[s], t.v[s - 1], t.j[s - 1], perm)) {
-      float tv = t.v[s]; t.v[s] = t.v[s - 1]; t.v[s - 1] = tv;
-      int tj = t.j[s]; t.j[s] = t.j[s - 1]; t.j[s - 1] = tj;
-    }
-  }
-}
-
 // Partial result of one CTA's sweep over its vocab slice for one frontier node:
 // online (max, sum-exp) and the slice's top-k (v, j) sorted by (v desc, token asc).
 struct Partial {
@@ -139,21 +129,29 @@ HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, in
     const int wpn = 32 / nq;                       // warps per frontier node
     const int qi = w / wpn, wg = w % wpn;          // this warp's node and index in its group
     const float* Lrow = P.L + ((size_t)req * P.N + row0 + i) * P.V;
-    // ---- 1. sweep
+    // ---- 1. sweep. Each thread keeps an online (max, sum-exp); each WARP keeps
+    //      one top-k list distributed over lanes 0..k-1 (sorted, R8 order). A
+    //      batch of 32 candidates (one per lane) is tested against the warp's
+    //      k-th best with one ballot; only the (few) winners are inserted, one
+    //      warp-wide shift each. (Per-thread lists inserted ~half of all
+    //      elements at ~16 elements per thread -- the sweep was issue-bound on
+    //      the insertion bubble, HSD_TREE_TRACE + ncu source counters.)
     float m = -INFINITY, sacc = 0.f;
-    Top<KT> t;
-    top_init(t);
+    float ev = -INFINITY;   // lane < K: this lane's entry of the warp's top-k
+    int ej = -1;
     if (qi < nq) {
       const int tok = cs.Qtok[qi];
       const int rk = P.rank_of ? P.rank_of[tok] : tok;
       const bool has_bias = !P.zero_table && rk < P.Vh;
-      const int gthreads = wpn * 32, gt = wg * 32 + lane;
+      const int gthreads = wpn * 32;
+      float tv = -INFINITY;   // the warp's current k-th best (v, j)
+      int tj = -1;
       constexpr int U = 4;
-      for (int base = lo + gt; base < hi; base += gthreads * U) {
+      for (int wbase = lo + wg * 32; wbase < hi; wbase += gthreads * U) {   // warp-uniform trip count
         float lv[U], bv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int j = base + u * gthreads;
+          const int j = wbase + lane + u * gthreads;
           lv[u] = j < hi ? Lrow[j] : 0.f;
           float b = 0.f;
           if (has_bias && j < hi && j < P.Vh) {
@@ -167,18 +165,46 @@ HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, in
           }
           bv[u] = b;
         }
+        // branch-free online (max, sum-exp) per batch of U: one rescale of the
+        // running sum per batch, exponentials as ex2.approx of log2e-scaled differences
+        float v[U], mb = m;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int j = base + u * gthreads;
-          if (j >= hi) break;
-          const float v = lv[u] + bv[u];
-          if (v > m) { sacc = sacc * expf(m - v) + 1.f; m = v; }
-          else sacc += expf(v - m);
-          top_insert(t, v, j, perm_of(P));
+          const int j = wbase + lane + u * gthreads;
+          v[u] = j < hi ? lv[u] + bv[u] : -INFINITY;
+          mb = fmaxf(mb, v[u]);
+        }
+        constexpr float LOG2E = 1.4426950408889634f;
+        float add = 0.f;
+#pragma unroll
+        for (int u = 0; u < U; ++u) add += ex2f_approx((v[u] - mb) * LOG2E);   // -inf -> 0
+        sacc = (m == -INFINITY ? 0.f : sacc * ex2f_approx((m - mb) * LOG2E)) + add;
+        m = mb;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = wbase + lane + u * gthreads;
+          unsigned cand = __ballot_sync(0xffffffffu, j < hi && better_j(v[u], j, tv, tj, perm_of(P)));
+          while (cand) {
+            const int src = __ffs(cand) - 1;
+            cand &= cand - 1;
+            const float xv = __shfl_sync(0xffffffffu, v[u], src);
+            const int xj = __shfl_sync(0xffffffffu, j, src);
+            if (!better_j(xv, xj, tv, tj, perm_of(P))) continue;    // the k-th best rose meanwhile
+            const int pos = __popc(__ballot_sync(0xffffffffu, lane < K && better_j(ev, ej, xv, xj, perm_of(P))));
+            const float upv = __shfl_up_sync(0xffffffffu, ev, 1);
+            const int upj = __shfl_up_sync(0xffffffffu, ej, 1);
+            if (lane < K) {
+              if (lane == pos) { ev = xv; ej = xj; }
+              else if (lane > pos) { ev = upv; ej = upj; }
+            }
+            tv = __shfl_sync(0xffffffffu, ev, K - 1);
+            tj = __shfl_sync(0xffffffffu, ej, K - 1);
+          }
         }
       }
     }
-    // ---- 2a. warp merge: (max, sum) butterfly and top-k of the lanes' lists
+    TTRACE(2 + 4 * i);
+    // ---- 2a. warp merge: (max, sum) butterfly; the top-k is already warp-wide
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, sacc, o);
@@ -187,27 +213,11 @@ HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, in
       m = nm;
     }
     {
-      int head = 0;
-      for (int r = 0; r < K; ++r) {
-        float hv = -INFINITY;
-        int hj = -1;
-#pragma unroll
-        for (int q = 0; q < KT; ++q)
-          if (q == head) { hv = t.v[q]; hj = t.j[q]; }
-        float bv = hv;
-        int bj = hj, bl = lane;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int oj = __shfl_xor_sync(0xffffffffu, bj, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
-          if (beats(ov, oj, ol, bv, bj, bl, perm_of(P))) { bv = ov; bj = oj; bl = ol; }
-        }
-        if (lane == 0) { wv[w * KMAX + r] = bv; wj[w * KMAX + r] = bj; }
-        if (lane == bl) head++;
-      }
+      if (lane < K) { wv[w * KMAX + lane] = ev; wj[w * KMAX + lane] = ej; }
       if (lane == 0) { wm[w] = m; ws[w] = sacc; }
     }
     __syncthreads();
+    TTRACE(3 + 4 * i);
     // ---- 2b. group leader warps: merge the group's warps, broadcast the Partial
     if (qi < nq && wg == 0) {
       const int w0 = qi * wpn;
@@ -229,6 +239,7 @@ HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, in
       }
     }
     cluster.sync();
+    TTRACE(4 + 4 * i);
     // ---- 3. every CTA: merge the CL partials, children, TopkByJointProb
     const int start = nd.n;
     for (int tt = threadIdx.x; tt < nq * CL * KMAX; tt += blockDim.x) {
@@ -278,6 +289,7 @@ HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, in
       if (q == 0) { nd.n = start + cnt_new; cs.nq = K < cnt_new ? K : cnt_new; }
     }
     __syncthreads();
+    TTRACE(5 + 4 * i);
   }
 }
 
@@ -338,8 +350,10 @@ HSD_DEV void prune_nodes(NodesSm& nd, int keep, NodesSm& tmp) {
 
 template <int KT>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(TreeParams P, int mode) {
+  TTRACE(0);
   l2pf_issue(P.pf);
   pdl_wait();
+  TTRACE(1);
   l2pf_issue(P.pf, 1);
   pdl_trigger();
   __shared__ NodesSm nd, tmp;
@@ -381,7 +395,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(Tre
   const int root = P.root_tok[req];
   build_subtree<KT>(P, req, 0, P.N, root, nd, cs);
   if (!leader) return;
+  TTRACE(40);
   prune_nodes(nd, P.B, tmp);
+  TTRACE(41);
   // ---- verification fusion with the pending re-sampled tree
   int pn = P.pt_n[req];
   if (P.fusion && pn > 1) {
@@ -414,8 +430,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(Tre
       }
     }
     __syncthreads();
+    TTRACE(42);
     prune_nodes(nd, P.B + P.Br, tmp);
   }
+  TTRACE(43);
   // ---- linearise: BFS, siblings by (joint desc, token asc); nodes bucketed by
   //      depth, each ranked only among its own depth's bucket
   const int n = nd.n;
@@ -484,6 +502,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(Tre
   }
   if (threadIdx.x == 0) P.t_n[req] = n;
   __syncthreads();
+  TTRACE(44);
   // ---- planted-continuation perf mode (reading R24), after linearisation
   if (P.plant != nullptr && threadIdx.x == 0) {
     int p = P.p[req];
@@ -509,8 +528,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(Tre
 }
 }  // namespace
 
-void launch_tree(const TreeParams& P, int mode, int n_req, cudaStream_t st) {
+// called by hsd_init_model (outside any graph capture)
+void tree_trace_init() {
+  if (getenv("HSD_TREE_TRACE") && !g_tree_trace) cudaMalloc(&g_tree_trace, 64 * 8);
+}
+
+void launch_tree(const TreeParams& P0, int mode, int n_req, cudaStream_t st) {
   if (n_req <= 0) return;
+  TreeParams P = P0;
+  P.trace = mode == TREE_MODE_FRESH ? g_tree_trace : nullptr;   // (never mutate the kernel's P: a local copy)
   switch (P.k) {
     case 1: launch_k(tree_kernel<1>, n_req * CL, NT, 0, st, P, mode); break;
     case 2: launch_k(tree_kernel<2>, n_req * CL, NT, 0, st, P, mode); break;

@@ -32,6 +32,8 @@ struct TreeParams {
   int req_offset;
   int* err;
   L2Pf pf;                   // weights of a later GEMM to prefetch into L2 (common.cuh)
+  unsigned long long* trace; // debug phase trace (HSD_TREE_TRACE) or null
 };
 
 void launch_tree(const TreeParams& P, int mode, int n_req, cudaStream_t st);
+void tree_trace_init();   // debug: HSD_TREE_TRACE phase trace buffer
