@@ -134,6 +134,18 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
 hsd_status hsd_prefill(hsd_ctx* ctx, int32_t n_req, const int32_t* h_tokens, int32_t stride,
                        const int32_t* h_lens, int32_t* d_first);
 
+/* Continuous batching (the serving layer around the path,
+ * P:428): replace the request in batch slot `slot` (0 <= slot < the prefilled
+ * n_req) by a new prompt h_tokens (HOST [len] int32, 2 <= len <= max_ctx,
+ * ragged: any length per slot) while the other slots keep their state. Runs the
+ * same per-request prefill as hsd_prefill (target KV + H, first token, draft
+ * prefill) for that slot only and clears its pending re-sampled tree; the step
+ * graph stays valid (no shape change). d_first: DEVICE [n_req] int32 or NULL
+ * (entry `slot` written). Synchronous. HSD_ESTATE before hsd_prefill or inside a
+ * staged step; HSD_EUNSUP with the NCCL vocab-sharded head (every shard would have
+ * to admit in lockstep).                                                      */
+hsd_status hsd_admit(hsd_ctx* ctx, int32_t slot, const int32_t* h_tokens, int32_t len, int32_t* d_first);
+
 /* Planted mode only: HOST row-major [n_req, stride] greedy continuation tokens
  * indexed by absolute position (R24). Copied. */
 hsd_status hsd_set_plant(hsd_ctx* ctx, const int32_t* h_plant, int32_t stride);

@@ -675,6 +675,75 @@ static hsd_status run_stage(hsd_ctx* ctx, int idx, F&& body) {
   return HSD_OK;
 }
 
+// Prefill of ONE request slot r (PAPER.md:184 setting; R1, R22): target causal
+// forward over the prompt (KV + H), first token, draft prefill over the prompt's
+// (H_{j-1}, t_j) pairs. Touches only slot r's state, so it also admits a new request
+// into a live batch (hsd_admit, continuous batching).
+static hsd_status prefill_one(hsd_ctx* ctx, int r, const int32_t* pt, int P0, int32_t* d_first) {
+  hsd_ctx* c = ctx;
+  const int n = c->n, N = c->N;
+  std::vector<int32_t> tok, pos, kvpos, req, klo, khi, slot;
+  // target causal forward over the prompt, chunked
+  for (int s0 = 0; s0 < P0; s0 += PREFILL_CHUNK) {
+    int M = std::min(PREFILL_CHUNK, P0 - s0);
+    tok.resize(M); pos.resize(M); kvpos.resize(M); req.resize(M); klo.resize(M); khi.resize(M); slot.resize(M);
+    for (int i = 0; i < M; ++i) {
+      tok[i] = pt[s0 + i]; pos[i] = s0 + i; kvpos[i] = s0 + i; req[i] = r; klo[i] = 0; khi[i] = s0 + i + 1;
+      slot[i] = -1;
+    }
+    CU(cudaMemcpyAsync(c->mp.tok, tok.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mp.pos, pos.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mp.kvpos, kvpos.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mp.req, req.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mp.klo, klo.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mp.khi, khi.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mp.slot, slot.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    RowMeta m = c->mp.view(nullptr, nullptr, 0, 0);
+    // rows of this chunk belong to request r: pass them as one "request" with
+    // the block table row r by offsetting the row->request map (req[] = r).
+    launch_embed(c->embed, c->dt, c->mp.tok, c->mp.pos, M, n, c->x_p, c->st);
+    g_hsd_launches += 1;
+    for (int l = 0; l < c->L; ++l)
+      layer_forward(c, c->layers[l], c->x_p, M, M, 1, m, kv_layer(c, c->kv_t, l), s0 + M);
+    CU(cudaMemcpyAsync(c->H_prompt + (size_t)s0 * n, c->x_p, sizeof(float) * M * n, cudaMemcpyDeviceToDevice, c->st));
+    CU(cudaStreamSynchronize(c->st));
+  }
+  // logits of the last prompt position -> first token (R22)
+  const float* Hlast = c->H_prompt + (size_t)(P0 - 1) * n;
+  launch_rmsnorm(Hlast, 1, n, c->cfg.rms_eps, c->a, c->dt, nullptr, c->st);
+  gemm(c, c->a, n, c->head, n, c->logits, c->V, 1, c->V, n, false);
+  launch_k(first_token_kernel, 1, 512, 0, c->st, c->logits, c->V, c->cfg.accept_mode == HSD_STOCHASTIC ? 1 : 0,
+                                           1.0f / c->cfg.temperature, (uint32_t)c->cfg.seed,
+                                           c->cfg.req_offset + r, r, Hlast, n, P0, N, c->pend_H, c->pend_tok,
+                                           c->n_pend, c->root_tok, c->p, d_first);
+  g_hsd_launches += 2;
+  // draft prefill over pairs j = 1..P0-1: x_j = W_fc [H_{j-1}; E(t_j)] (R1)
+  for (int j0 = 1; j0 < P0; j0 += PREFILL_CHUNK) {
+    int M = std::min(PREFILL_CHUNK, P0 - j0);
+    tok.resize(M); pos.resize(M); kvpos.resize(M); req.resize(M); klo.resize(M); khi.resize(M); slot.resize(M);
+    for (int i = 0; i < M; ++i) {
+      int j = j0 + i;
+      tok[i] = pt[j]; pos[i] = j; kvpos[i] = j; req[i] = r; klo[i] = 1; khi[i] = j + 1; slot[i] = -1;
+    }
+    CU(cudaMemcpyAsync(c->mp.tok, tok.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mp.pos, pos.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mp.kvpos, kvpos.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mp.req, req.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mp.klo, klo.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mp.khi, khi.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    CU(cudaMemcpyAsync(c->mp.slot, slot.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
+    RowMeta m = c->mp.view(nullptr, nullptr, 0, 0);
+    launch_draft_concat(c->H_prompt + (size_t)(j0 - 1) * n, c->mp.tok, c->mp.pos, c->embed, c->dt, M, n, c->a,
+                        c->st);
+    gemm(c, c->a, 2 * n, c->fc, 2 * n, c->x_p, n, M, n, 2 * n, false);
+    layer_forward(c, c->draft, c->x_p, M, M, 1, m, kv_layer(c, c->kv_d, 0), j0 + M);
+    g_hsd_launches += 1;
+    CU(cudaStreamSynchronize(c->st));
+  }
+
+  return HSD_OK;
+}
+
 // ====================================================================== C ABI
 extern "C" {
 
@@ -1019,71 +1088,33 @@ hsd_status hsd_prefill(hsd_ctx* ctx, int32_t n_req, const int32_t* h_tokens, int
   std::vector<int32_t> ones(c->maxb, 1);
   CU(cudaMemcpyAsync(c->pt_n, ones.data(), 4 * n_req, cudaMemcpyHostToDevice, c->st));
   CU(cudaStreamSynchronize(c->st));
-  std::vector<int32_t> tok, pos, kvpos, req, klo, khi, slot;
   for (int r = 0; r < n_req; ++r) {
-    const int P0 = h_lens[r];
-    const int32_t* pt = h_tokens + (size_t)r * stride;
-    // target causal forward over the prompt, chunked
-    for (int s0 = 0; s0 < P0; s0 += PREFILL_CHUNK) {
-      int M = std::min(PREFILL_CHUNK, P0 - s0);
-      tok.resize(M); pos.resize(M); kvpos.resize(M); req.resize(M); klo.resize(M); khi.resize(M); slot.resize(M);
-      for (int i = 0; i < M; ++i) {
-        tok[i] = pt[s0 + i]; pos[i] = s0 + i; kvpos[i] = s0 + i; req[i] = r; klo[i] = 0; khi[i] = s0 + i + 1;
-        slot[i] = -1;
-      }
-      CU(cudaMemcpyAsync(c->mp.tok, tok.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      CU(cudaMemcpyAsync(c->mp.pos, pos.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      CU(cudaMemcpyAsync(c->mp.kvpos, kvpos.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      CU(cudaMemcpyAsync(c->mp.req, req.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      CU(cudaMemcpyAsync(c->mp.klo, klo.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      CU(cudaMemcpyAsync(c->mp.khi, khi.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      CU(cudaMemcpyAsync(c->mp.slot, slot.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      RowMeta m = c->mp.view(nullptr, nullptr, 0, 0);
-      // rows of this chunk belong to request r: pass them as one "request" with
-      // the block table row r by offsetting the row->request map (req[] = r).
-      launch_embed(c->embed, c->dt, c->mp.tok, c->mp.pos, M, n, c->x_p, c->st);
-      g_hsd_launches += 1;
-      for (int l = 0; l < c->L; ++l)
-        layer_forward(c, c->layers[l], c->x_p, M, M, 1, m, kv_layer(c, c->kv_t, l), s0 + M);
-      CU(cudaMemcpyAsync(c->H_prompt + (size_t)s0 * n, c->x_p, sizeof(float) * M * n, cudaMemcpyDeviceToDevice, c->st));
-      CU(cudaStreamSynchronize(c->st));
-    }
-    // logits of the last prompt position -> first token (R22)
-    const float* Hlast = c->H_prompt + (size_t)(P0 - 1) * n;
-    launch_rmsnorm(Hlast, 1, n, c->cfg.rms_eps, c->a, c->dt, nullptr, c->st);
-    gemm(c, c->a, n, c->head, n, c->logits, c->V, 1, c->V, n, false);
-    launch_k(first_token_kernel, 1, 512, 0, c->st, c->logits, c->V, c->cfg.accept_mode == HSD_STOCHASTIC ? 1 : 0,
-                                             1.0f / c->cfg.temperature, (uint32_t)c->cfg.seed,
-                                             c->cfg.req_offset + r, r, Hlast, n, P0, N, c->pend_H, c->pend_tok,
-                                             c->n_pend, c->root_tok, c->p, d_first);
-    g_hsd_launches += 2;
-    // draft prefill over pairs j = 1..P0-1: x_j = W_fc [H_{j-1}; E(t_j)] (R1)
-    for (int j0 = 1; j0 < P0; j0 += PREFILL_CHUNK) {
-      int M = std::min(PREFILL_CHUNK, P0 - j0);
-      tok.resize(M); pos.resize(M); kvpos.resize(M); req.resize(M); klo.resize(M); khi.resize(M); slot.resize(M);
-      for (int i = 0; i < M; ++i) {
-        int j = j0 + i;
-        tok[i] = pt[j]; pos[i] = j; kvpos[i] = j; req[i] = r; klo[i] = 1; khi[i] = j + 1; slot[i] = -1;
-      }
-      CU(cudaMemcpyAsync(c->mp.tok, tok.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      CU(cudaMemcpyAsync(c->mp.pos, pos.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      CU(cudaMemcpyAsync(c->mp.kvpos, kvpos.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      CU(cudaMemcpyAsync(c->mp.req, req.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      CU(cudaMemcpyAsync(c->mp.klo, klo.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      CU(cudaMemcpyAsync(c->mp.khi, khi.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      CU(cudaMemcpyAsync(c->mp.slot, slot.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
-      RowMeta m = c->mp.view(nullptr, nullptr, 0, 0);
-      launch_draft_concat(c->H_prompt + (size_t)(j0 - 1) * n, c->mp.tok, c->mp.pos, c->embed, c->dt, M, n, c->a,
-                          c->st);
-      gemm(c, c->a, 2 * n, c->fc, 2 * n, c->x_p, n, M, n, 2 * n, false);
-      layer_forward(c, c->draft, c->x_p, M, M, 1, m, kv_layer(c, c->kv_d, 0), j0 + M);
-      g_hsd_launches += 1;
-      CU(cudaStreamSynchronize(c->st));
-    }
+    const hsd_status st = prefill_one(c, r, h_tokens + (size_t)r * stride, h_lens[r], d_first);
+    if (st != HSD_OK) return st;
   }
   CU(cudaStreamSynchronize(c->st));
   CU(cudaGetLastError());
   c->stage = 0;
+  return HSD_OK;
+}
+
+hsd_status hsd_admit(hsd_ctx* ctx, int32_t slot, const int32_t* h_tokens, int32_t len, int32_t* d_first) {
+  if (!ctx) return HSD_EINVAL;
+  hsd_ctx* c = ctx;
+  if (c->b < 1) return fail(c, HSD_ESTATE, "hsd_admit before hsd_prefill");
+  if (c->stage != 0) return fail(c, HSD_ESTATE, "hsd_admit in the middle of a staged step");
+  if (slot < 0 || slot >= c->b) return fail(c, HSD_EINVAL, "slot must be in [0, batch)");
+  if (!h_tokens || len < 2 || len > c->cfg.max_ctx) return fail(c, HSD_EINVAL, "prompt length must be in [2, max_ctx]");
+  if (c->shard_mode == HSD_SHARD_NCCL) return fail(c, HSD_EUNSUP, "hsd_admit with the NCCL vocab-sharded head");
+  for (int i = 0; i < len; ++i)
+    if (h_tokens[i] < 0 || h_tokens[i] >= c->V) return fail(c, HSD_EINVAL, "token outside [0, V) (contract violation)");
+  const int32_t one = 1;   // no pending re-sampled tree for the new request
+  CU(cudaMemcpyAsync(c->pt_n + slot, &one, 4, cudaMemcpyHostToDevice, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  const hsd_status st = prefill_one(c, slot, h_tokens, len, d_first);
+  if (st != HSD_OK) return st;
+  CU(cudaStreamSynchronize(c->st));
+  CU(cudaGetLastError());
   return HSD_OK;
 }
 

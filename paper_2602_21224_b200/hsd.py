@@ -27,7 +27,7 @@ SHARD_NONE, SHARD_NCCL, SHARD_SIM = 0, 1, 2
 EXPORTS = ["hsd_config_defaults", "hsd_init_model", "hsd_prefill", "hsd_set_plant", "hsd_build_tree",
            "hsd_force_tree", "hsd_verify_tree", "hsd_accept_and_compact", "hsd_step", "hsd_step_host",
            "hsd_sync", "hsd_get_tensor", "hsd_kernel_launches", "hsd_destroy", "hsd_last_error",
-           "hsd_profile", "hsd_profile_read", "hsd_debug_gemm", "hsd_nccl_unique_id"]
+           "hsd_profile", "hsd_profile_read", "hsd_debug_gemm", "hsd_nccl_unique_id", "hsd_admit"]
 PROFILE_CATEGORIES = ["gemm_verify", "gemm_draft", "head_verify", "head_draft", "attn_verify", "attn_draft",
                       "tree", "resample", "walk", "compact", "rowwise"]
 
@@ -92,6 +92,7 @@ def load(path: str = LIB_PATH):
         "hsd_debug_gemm": (I32, [VP, I32, VP, I32, VP, I32, I32, I32, I32, I32, I32, I32, VP]),
         "hsd_profile_read": (I32, [VP, C.c_char_p, P(C.c_double), P(I64), P(C.c_double), P(C.c_double)]),
         "hsd_nccl_unique_id": (I32, [P(C.c_uint8)]),
+        "hsd_admit": (I32, [VP, I32, P(I32), I32, VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -187,6 +188,12 @@ class Context:
         self._check(self.lib.hsd_prefill(self.h, tokens.shape[0], tp, tokens.shape[1], lp,
                                          C.c_void_p(d_first or 0)))
         self.batch = tokens.shape[0]
+
+    def admit(self, slot, tokens, d_first=None):
+        """hsd_admit: a new (ragged-length) prompt into batch slot `slot`; the
+        other slots keep decoding (continuous batching)."""
+        t, tp = _i32(np.asarray(tokens, dtype=np.int32).ravel())
+        self._check(self.lib.hsd_admit(self.h, int(slot), tp, t.size, C.c_void_p(d_first or 0)))
 
     def set_plant(self, plant):
         plant = np.atleast_2d(np.asarray(plant, dtype=np.int32))
