@@ -536,10 +536,28 @@ static void tc_tiles(int M, int& nt, int& n_tok_tiles) {
 // Data-parallel only with >= 4 output tiles per SM (c3's gate/up and verify
 // head): below that, whole-tile ownership leaves SMs idle or unbalanced while
 // the weights stream, and stream-K's partial-sum atomics are cheap.
+//
+// Below that, the CTA-pair kernel (256-row weight tiles, num_sms/2 pairs) still
+// owns whole tiles efficiently when its pair-tile count spans >= 1.5 waves and
+// fills >= 90 % of the last one: c3's QKV (216 pair tiles = 2.92 waves), O and
+// down (144 = 1.95 waves) at M = 2080. Batch-1 / small-M shapes (c2, c5 b = 2,
+// the draft GEMMs) stay stream-K. HSD_GEMM_DP_WAVE=0 restores the 4-tiles rule.
 bool gemm_tc_dp(int M, int N) {
   int nt, ntt;
   tc_tiles(M, nt, ntt);
-  return (long)((N + BM - 1) / BM) * ntt >= 4L * num_sms();
+  if ((long)((N + BM - 1) / BM) * ntt >= 4L * num_sms()) return true;
+  static const bool wave_rule = [] {
+    const char* e = getenv("HSD_GEMM_DP_WAVE");
+    const char* p = getenv("HSD_GEMM_2SM");
+    return !(e && atoi(e) == 0) && !(p && atoi(p) == 0);
+  }();
+  const long pairs = num_sms() / 2;
+  if (!wave_rule || pairs < 1) return false;
+  const long ptiles = (long)((N + 2 * BM - 1) / (2 * BM)) * ntt;
+  const long full = ptiles / pairs, rem = ptiles % pairs;
+  const double waves = (double)ptiles / (double)pairs;
+  const double eff = waves / (double)(full + (rem ? 1 : 0));
+  return waves >= 1.5 && eff >= 0.9;
 }
 
 static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float* C, int ldc, int M, int N, int K,
