@@ -252,6 +252,7 @@ struct hsd_ctx {
   // workspace
   int Mcap;
   float *x_d, *xw, *Hver, *chain, *big, *draft_logits, *logits, *x_p, *H_prompt, *attn_ws;
+  float* big_dp = nullptr;   // QKV output of a data-parallel (storing) GEMM: no re-zeroing needed
   size_t attn_ws_floats;
   void *a, *qb, *ob, *h;   // h: SwiGLU output [Mcap, f] (never aliases the GEMM input a)
   int32_t* argmax;
@@ -415,10 +416,15 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
   }
   // c->big is kept zero outside a GEMM -> consumer window (qkv_rope_kv and
   // swiglu re-zero what they read), so these GEMMs accumulate without a memset
-  gemm(c, c->a, n, w.wqkv, n, c->big, c->qkvd, M, c->qkvd, n, false, -1, true);
+  // a data-parallel QKV GEMM STORES its output (into big_dp), so qkv_rope need not
+  // re-zero it; the stream-K one accumulates into the zero-kept scratch big
+  const bool qkv_dp = c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, c->qkvd, n, n, n) &&
+                      gemm_tc_dp(M, c->qkvd);
+  float* qkv = qkv_dp ? c->big_dp : c->big;
+  gemm(c, c->a, n, w.wqkv, n, qkv, c->qkvd, M, c->qkvd, n, false, -1, true);
   if (!ablate("rope")) { Prof pf(c, P_ROWWISE);
     PfScope l2(w.wo, b_o, 0, std::max(cap, b_o), 2);
-    launch_qkv_rope_kv(c->big, M, m, c->rope_cos, c->rope_sin, c->Hq, kv, c->qb, c->dt, c->st); }
+    launch_qkv_rope_kv(qkv, M, m, c->rope_cos, c->rope_sin, c->Hq, kv, c->qb, c->dt, c->st, !qkv_dp); }
   if (!ablate("attn")) {
     // algorithmic attention bytes: the request's committed K/V rows once (per
     // kv head) + q/out rows; exact per-row key counts are device-side, so the
@@ -1008,6 +1014,7 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     c->ob = A((size_t)Mc * c->qd * es);
     c->h = A((size_t)Mc * c->f * es);
     c->big = F((size_t)Mc * std::max(c->qkvd, 2 * c->f));
+    c->big_dp = F((size_t)Mc * c->qkvd);
     c->x_d = F((size_t)b * (N + 1) * n);
     c->xw = F((size_t)b * n);
     c->Hver = F((size_t)b * T * n);

@@ -51,9 +51,11 @@ void launch_rmsnorm(const float* x, int M, int n, float eps, void* out, DType dt
                     cudaStream_t st);
 void launch_embed(const void* E, DType dt, const int32_t* tok, const int32_t* pos, int M, int n, float* x,
                   cudaStream_t st);
+// zero: re-zero the fp32 scratch rows after reading them (the stream-K GEMMs
+// accumulate into a zero scratch); false when a data-parallel GEMM stored them
 void launch_qkv_rope_kv(float* qkv, int M, const RowMeta& m, const float* rope_cos,
                         const float* rope_sin, int Hq, const KVLayer& kv, void* q_out, DType dt,
-                        cudaStream_t st);
+                        cudaStream_t st, bool zero = true);
 void launch_swiglu(float* gu, int M, int f, void* out, DType dt, const int32_t* pos, cudaStream_t st);
 void launch_interleave_gu(const void* src, int f, int n, void* dst, DType dt, cudaStream_t st);
 void launch_argmax_rows(const float* x, int M, int V, const int32_t* pos, int32_t* out, cudaStream_t st);

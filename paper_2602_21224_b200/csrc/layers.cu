@@ -114,7 +114,7 @@ constexpr int VROWS = 32;         // rows per V-transpose CTA
 // rows sit at consecutive cache positions.
 template <typename T>
 __device__ void v_transpose_block(float* __restrict__ qkv, const RowMeta& m, int M, int Hq, const KVLayer& kv,
-                                  int vb) {
+                                  int vb, int zero) {
   const int hd = kv.head_dim, Hkv = kv.kv_heads, ld = (Hq + 2 * Hkv) * hd;
   const int nd = (hd + 31) / 32;
   const int dc = vb % nd, h = (vb / nd) % Hkv, r0 = (vb / nd / Hkv) * VROWS;
@@ -143,7 +143,7 @@ __device__ void v_transpose_block(float* __restrict__ qkv, const RowMeta& m, int
 #pragma unroll
   for (int k = 0; k < VROWS / 4; ++k) {
     const int rr = w + 4 * k;
-    if (rr < nr && d < hd) src[(size_t)rr * ld] = 0.f;    // re-zero the GEMM scratch (see below)
+    if (zero && rr < nr && d < hd) src[(size_t)rr * ld] = 0.f;    // re-zero the GEMM scratch (see below)
     tile[rr][lane] = v[k];
   }
   __syncthreads();
@@ -160,14 +160,14 @@ template <typename T>
 __global__ void __launch_bounds__(128) qkv_rope_kv_kernel(float* __restrict__ qkv, RowMeta m,
                                                           const float* __restrict__ rc,
                                                           const float* __restrict__ rs, int Hq, KVLayer kv,
-                                                          T* __restrict__ q_out, int M, L2Pf pf) {
+                                                          T* __restrict__ q_out, int M, int zero, L2Pf pf) {
   l2pf_issue(pf);
   pdl_wait();
   l2pf_issue(pf, 1);
   pdl_trigger();
   const int n_v = (M + VROWS - 1) / VROWS * kv.kv_heads * ((kv.head_dim + 31) / 32);
   if ((int)blockIdx.x < n_v) {          // V-transpose CTAs first (fewer, longer), then rope
-    v_transpose_block<T>(qkv, m, M, Hq, kv, blockIdx.x);
+    v_transpose_block<T>(qkv, m, M, Hq, kv, blockIdx.x, zero);
     return;
   }
   const int rb = blockIdx.x - n_v;
@@ -187,22 +187,45 @@ __global__ void __launch_bounds__(128) qkv_rope_kv_kernel(float* __restrict__ qk
     const int page = kv.block_table[(size_t)m.req[r] * kv.pages_per_req + kp / kv.page_size];
     const int slot = kp % kv.page_size;
     T* base = (T*)kv.base;
-    // rotated q (Hq heads) and k (Hkv heads): (Hq + Hkv) * half rotation pairs
-    for (int i = tid; i < (Hq + Hkv) * half; i += nthr) {
-      const int h = i / half, j = i % half;
-      const float x1 = row[h * hd + j], x2 = row[h * hd + j + half];
-      const float y1 = x1 * c[j] - x2 * sn[j], y2 = x2 * c[j] + x1 * sn[j];
-      if (h < Hq) {
-        qo[h * hd + j] = from_f32<T>(y1);
-        qo[h * hd + j + half] = from_f32<T>(y2);
-      } else {
-        base[kv_offset(page, 0, Hkv, h - Hq, kv.page_size, hd, slot, j)] = from_f32<T>(y1);
-        base[kv_offset(page, 0, Hkv, h - Hq, kv.page_size, hd, slot, j + half)] = from_f32<T>(y2);
+    // rotated q (Hq heads) and k (Hkv heads): (Hq + Hkv) * half rotation pairs.
+    // All of a thread's loads are issued before its first store (up to RP pairs per
+    // pass): the stores go through pointers the compiler cannot prove disjoint from
+    // the scratch row, so an interleaved loop serialised one memory round trip per
+    // pair (c4: 5 pairs per thread, qkv_rope ~1 ms per layer in the launch list)
+    constexpr int RP = 8;
+    const int npairs = (Hq + Hkv) * half;
+    for (int i0 = tid; i0 < npairs; i0 += RP * nthr) {
+      float x1[RP], x2[RP], cc[RP], ss[RP];
+#pragma unroll
+      for (int u = 0; u < RP; ++u) {
+        const int i = i0 + u * nthr;
+        if (i < npairs) {
+          const int h = i / half, j = i % half;
+          x1[u] = row[h * hd + j];
+          x2[u] = row[h * hd + j + half];
+          cc[u] = c[j];
+          ss[u] = sn[j];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < RP; ++u) {
+        const int i = i0 + u * nthr;
+        if (i >= npairs) break;
+        const int h = i / half, j = i % half;
+        const float y1 = x1[u] * cc[u] - x2[u] * ss[u], y2 = x2[u] * cc[u] + x1[u] * ss[u];
+        if (h < Hq) {
+          qo[h * hd + j] = from_f32<T>(y1);
+          qo[h * hd + j + half] = from_f32<T>(y2);
+        } else {
+          base[kv_offset(page, 0, Hkv, h - Hq, kv.page_size, hd, slot, j)] = from_f32<T>(y1);
+          base[kv_offset(page, 0, Hkv, h - Hq, kv.page_size, hd, slot, j + half)] = from_f32<T>(y2);
+        }
       }
     }
   }
   // Each element was read by exactly this thread (same tid -> same indices), so
   // re-zeroing the scratch needs no cross-CTA barrier: zero what this thread read.
+  if (!zero) return;   // a data-parallel GEMM stored (not accumulated) this scratch
   if (p >= 0) {
     for (int i = tid; i < (Hq + Hkv) * half; i += nthr) {
       const int h = i / half, j = i % half;
@@ -216,14 +239,14 @@ __global__ void __launch_bounds__(128) qkv_rope_kv_kernel(float* __restrict__ qk
 
 void launch_qkv_rope_kv(float* qkv, int M, const RowMeta& m, const float* rope_cos,
                         const float* rope_sin, int Hq, const KVLayer& kv, void* q_out, DType dt,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool zero) {
   const L2Pf pf = take_l2pf();
   if (M <= 0) return;
   const int grid = M * ROPE_PARTS + (M + VROWS - 1) / VROWS * kv.kv_heads * ((kv.head_dim + 31) / 32);
   if (dt == DT_F32)
-    launch_k(qkv_rope_kv_kernel<float>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out, M, pf);
+    launch_k(qkv_rope_kv_kernel<float>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out, M, zero ? 1 : 0, pf);
   else
-    launch_k(qkv_rope_kv_kernel<bf16>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out, M, pf);
+    launch_k(qkv_rope_kv_kernel<bf16>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out, M, zero ? 1 : 0, pf);
 }
 
 // ------------------------------------------------------------------ SwiGLU
