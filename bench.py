@@ -290,6 +290,66 @@ def planted_leg(ctx, pr, cfg, b, N, steps, warmup, stream, return_counts=False, 
     return out + (n_h[warmup:],) if return_counts else out
 
 
+def gemm_chain(ctx, cfg, b, local, gbs, tfl, bound, reps=3):
+    """The step's verify GEMMs (every target layer's QKV, O, gate/up, down at M =
+    b*T rows) launched back to back through hsd_debug_gemm on one stream, timed with
+    CUDA events around the whole chain: algorithmic bytes (or flops) / time."""
+    import torch
+    from paper_2602_21224_b200 import hsd
+    T = cfg.budget_B + cfg.resample_budget_Br + 1
+    M, n, f = b * T, cfg.hidden, cfg.ffn
+    dev = f"cuda:{local}"
+    qd = cfg.q_heads * cfg.head_dim
+    A_n = torch.randn(M, n, device=dev).to(torch.bfloat16)
+    A_q = torch.randn(M, qd, device=dev).to(torch.bfloat16)
+    A_f = torch.randn(M, f, device=dev).to(torch.bfloat16)
+    qkvd = qd + 2 * cfg.kv_heads * cfg.head_dim
+    C = torch.zeros(M, max(qkvd, 2 * f), device=dev)
+    H = torch.zeros(M, f, device=dev, dtype=torch.bfloat16)
+    st = torch.cuda.Stream(device=local)
+    W = [[ctx.tensor(f"layer{l}_{p}") for p in ("wqkv", "wo", "wgu", "wd")] for l in range(cfg.layers)]
+    byts = fl = 0.0
+
+    def chain():
+        nonlocal byts, fl
+        byts = fl = 0.0
+        for wq, wo, wgu, wd in W:
+            for A, Wt, N, K, mode in ((A_n, wq, qkvd, n, 1), (A_q, wo, n, qd, 1), (A_n, wgu, 2 * f, n, 2),
+                                      (A_f, wd, n, f, 1)):
+                if mode == 2:
+                    try:
+                        hsd.debug_gemm(A, Wt, H, use_tc="swiglu", stream=st.cuda_stream)
+                        byts += N * K * 2 + M * K * 2 + M * (N // 2) * 2
+                        fl += 2.0 * M * N * K
+                        continue
+                    except hsd.HsdError:
+                        pass
+                hsd.debug_gemm(A, Wt, C[:, :N] if N < C.shape[1] else C, accumulate=True, use_tc=True,
+                               stream=st.cuda_stream)
+                byts += N * K * 2 + M * K * 2 + M * N * 8
+                fl += 2.0 * M * N * K
+    with torch.cuda.stream(st):
+        chain()
+        st.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            chain()
+        e1.record(st)
+        st.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    launches = 4 * cfg.layers
+    if bound == "hbm":
+        ach = byts / (ms / 1e3) / 1e9
+        return {"chain": {"achieved": round(ach, 1), "frac": round(ach / gbs, 4), "unit": "GB/s",
+                          "us_per_launch": round(ms * 1e3 / launches, 2), "launches": launches,
+                          "what": "verify GEMMs back to back (PDL chain, no events between launches)"}}
+    ach = fl / (ms / 1e3) / 1e12
+    return {"chain": {"achieved": round(ach, 2), "frac": round(ach / tfl, 4), "unit": "TFLOP/s",
+                      "us_per_launch": round(ms * 1e3 / launches, 2), "launches": launches,
+                      "what": "verify GEMMs back to back (PDL chain, no events between launches)"}}
+
+
 def plan_shard(n_requests: int, world: int, rank: int):
     """Batch sharding: contiguous request blocks when the batch
     has at least one request per rank, else independent full replicas."""
@@ -441,6 +501,16 @@ def main():
                     "frac": round(ach / tfl, 4), "traffic": traffic}
         roof.update({"kernel": cat, "launches_per_step": pn / kp, "share_of_step": round(pms / total_prof, 4),
                      "peak_source": src, "algorithmic_bytes_per_launch": pby / max(pn, 1)})
+
+    # ---- supplementary: the verify GEMMs as a back-to-back PDL chain (the same
+    # kernels, shapes and weights as the step's L layers x {QKV, O, gate/up, down},
+    # launched in a row with no event between launches): per-launch duration when
+    # nothing but GEMMs stream, vs the event-bracketed eager pass above
+    if roof is not None and roof.get("kernel") == "gemm_verify" and not args.no_profile:
+        try:
+            roof.update(gemm_chain(ctx, cfg, b, local, gbs, tfl, roof["bound"]))
+        except Exception as ex:  # supplementary only
+            roof["chain"] = {"error": repr(ex)}
 
     # ---- e2e: prefill from HOST prompts + K steps with host outputs (public API)
     e2e = None

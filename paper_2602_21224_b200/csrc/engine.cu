@@ -1335,6 +1335,22 @@ hsd_status hsd_get_tensor(hsd_ctx* ctx, const char* name, hsd_tensor* out) {
   extern unsigned long long* g_tree_trace;
   if (s == "tree_trace" && g_tree_trace) return set(g_tree_trace, 3, {64});
   if (s == "layer0_wqkv" && c->L > 0) return set(c->layers[0].wqkv, adt, {c->qkvd, n});
+  // target layer weights by name, e.g. "layer7_wo" ([out, in] row-major, nn.Linear layout;
+  // gate/up rows interleaved in 64-row groups, see launch_swiglu)
+  if (s.rfind("layer", 0) == 0) {
+    const size_t us = s.find('_');
+    if (us != std::string::npos) {
+      const int l = atoi(s.substr(5, us - 5).c_str());
+      const std::string part = s.substr(us + 1);
+      if (l >= 0 && l < c->L) {
+        const LayerW& w = c->layers[l];
+        if (part == "wqkv") return set(w.wqkv, adt, {c->qkvd, n});
+        if (part == "wo") return set(w.wo, adt, {n, c->qd});
+        if (part == "wgu") return set(w.wgu, adt, {2 * (int64_t)c->f, n});
+        if (part == "wd") return set(w.wd, adt, {n, c->f});
+      }
+    }
+  }
   return fail(c, HSD_EINVAL, "unknown tensor name " + s);
 }
 
