@@ -50,6 +50,7 @@ HSD_DEV uint64_t gtime() {
 }
 struct AttnParams {
   int M, R, Hq, G, hd, n_qtiles, max_keys, keys_per_split, direct;
+  int dyn;                     // 1: key splits divide the CTA's VISIBLE chunks (device-side), not max_keys
   int cluster;                 // 1: the S key-split CTAs form a cluster and reduce over DSMEM
   RowMeta m;
   KVLayer kv;
@@ -162,8 +163,6 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   const int grp = blockIdx.z / P.n_qtiles, qt = blockIdx.z % P.n_qtiles;
   const RowMeta& m = P.m;
   const int req = m.req[grp * P.R];
-  const int k_begin = split * P.keys_per_split;
-  const int k_end = min(P.max_keys, k_begin + P.keys_per_split);
 
   if (threadIdx.x == 0) { tile_lo = 0x7fffffff; tile_hi = 0; safe_hi = 0x7fffffff; TRACE(0); }
   if (threadIdx.x == 32) {
@@ -227,6 +226,20 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  // key range of this split: with P.dyn the S splits divide the chunks this tile
+  // actually sees ([tile_lo, tile_hi), known only on the device) evenly, so a
+  // context far below the capacity max_keys does not leave splits idle while
+  // others take several chunks; identical in every split CTA of the tile
+  int k_begin, k_end;
+  if (P.dyn) {
+    const int c0 = tile_lo / CHUNK, c1 = (tile_hi + CHUNK - 1) / CHUNK;
+    const int cps = c1 > c0 ? (c1 - c0 + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    k_begin = (c0 + split * cps) * CHUNK;
+    k_end = k_begin + cps * CHUNK;
+  } else {
+    k_begin = split * P.keys_per_split;
+    k_end = min(P.max_keys, k_begin + P.keys_per_split);
+  }
   const int lo = max(k_begin, tile_lo), hi = min(k_end, tile_hi);
   const int c_first = lo / CHUNK;
   const int n_chunks = hi > lo ? (hi + CHUNK - 1) / CHUNK - c_first : 0;
@@ -628,6 +641,17 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   // monotone worse above) and c5 batch 2 (S=2) -- DESIGN.md section 7.
   int S = max(1, (2 * num_sms() + base_ctas) / (2 * base_ctas));
   S = min(S, max(1, pages / 2));
+  // Latency-bound regime (a few chunks per split CTA, c2): one CTA per SM (all TMEM
+  // columns, ~190 KB of shared memory), so a second wave of split CTAs adds a whole
+  // CTA latency -- cap S at one wave (c2: S 5 -> 4) and divide the chunks each tile
+  // really sees evenly on the device (c2 step 4.95 -> 4.73 ms). With many chunks
+  // per split (c5, b = 2: 70 chunks) the per-SM K/V stream is the limit and
+  // spreading over every SM wins even past one wave (cap there: 46.1 -> 48.8 ms).
+  // HSD_ATTN_DYNSPLIT: 0 off, 1 cap + device ranges (default), 2 cap only.
+  static const int dyn = [] { const char* e = getenv("HSD_ATTN_DYNSPLIT"); return e ? atoi(e) : 1; }();
+  const bool latency_bound = (pages + S - 1) / S <= 4;
+  if (dyn && latency_bound) S = min(S, max(1, num_sms() / base_ctas));
+  P.dyn = dyn == 1 && latency_bound;
   static const int s_override = [] { const char* e = getenv("HSD_ATTN_SPLITS"); return e ? atoi(e) : 0; }();
   if (s_override > 0) S = min(s_override, pages);
   // two splits reduce inside a 2-CTA cluster over DSMEM (no workspace, no merge
@@ -643,7 +667,7 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   while (!P.cluster && S > 1 && (size_t)S * M * Hq * (hd + 2) > ws_floats) --S;
   int pps = (pages + S - 1) / S;
   P.keys_per_split = pps * CHUNK;
-  if (!P.cluster) S = (pages + pps - 1) / pps;   // cluster mode keeps S (empty splits contribute 0)
+  if (!P.cluster && !P.dyn) S = (pages + pps - 1) / pps;   // cluster / dynamic modes keep S (empty splits contribute 0)
   P.direct = S == 1;
   // tensor maps: q [M][Hq][hd] viewed (hd, heads, rows) with the head offset in
   // the coordinate; K pool rows of hd; V^T pool rows of page_size.

@@ -13,6 +13,6 @@ timeout 600 $NF -k regex:attention_tc_kernel -c 1 -o $O/r01_attn_c2 python scrip
 timeout 600 $NF -k regex:tree_kernel -c 2 -o $O/r01_tree_c2 python scripts/profile_step.py c2 --stage step > $O/ncu_tree_c2.log 2>&1
 # c3 (batch 32): launch list of one profiled step, verify layer-0 GEMMs + attention
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/r01_launches_c3.csv python scripts/profile_step.py c3 --stage step > $O/ncu_launch_c3.log 2>&1
-timeout 900 $NF -k regex:gemm_tc_kernel -c 4 -o $O/r01_gemm_c3 python scripts/profile_step.py c3 > $O/ncu_gemm_c3.log 2>&1
+timeout 900 $NF -k regex:gemm_tc -c 4 -o $O/r01_gemm_c3 python scripts/profile_step.py c3 > $O/ncu_gemm_c3.log 2>&1
 timeout 900 $NF -k regex:attention_tc_kernel -c 1 -o $O/r01_attn_c3 python scripts/profile_step.py c3 > $O/ncu_attn_c3.log 2>&1
 ls -la $O | tail -12
