@@ -419,7 +419,7 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
   // a data-parallel QKV GEMM STORES its output (into big_dp), so qkv_rope need not
   // re-zero it; the stream-K one accumulates into the zero-kept scratch big
   const bool qkv_dp = c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, c->qkvd, n, n, n) &&
-                      gemm_tc_dp(M, c->qkvd);
+                      gemm_tc_dp(M, c->qkvd, n, false);
   float* qkv = qkv_dp ? c->big_dp : c->big;
   gemm(c, c->a, n, w.wqkv, n, qkv, c->qkvd, M, c->qkvd, n, false, -1, true);
   if (!ablate("rope")) { Prof pf(c, P_ROWWISE);
@@ -447,7 +447,7 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
     launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st);
   }
   bool fused = false;
-  if (c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, 2 * c->f, n, n, n) && gemm_tc_dp(M, 2 * c->f)) {
+  if (c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, 2 * c->f, n, n, n) && gemm_tc_dp(M, 2 * c->f, n, false)) {
     // data-parallel gate/up GEMM with SwiGLU in the epilogue, bf16 h straight to c->a
     Prof pf(c, c->pass_verify ? P_GEMM_VERIFY : P_GEMM_DRAFT,
             (double)2 * c->f * n * c->esz + (double)M * n * c->esz + (double)M * c->f * c->esz,
