@@ -447,7 +447,7 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
     launch_rmsnorm(x, M, n, c->cfg.rms_eps, c->a, c->dt, m.pos, c->st);
   }
   bool fused = false;
-  if (c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, 2 * c->f, n, n, n) && gemm_tc_dp(M, 2 * c->f, n, false)) {
+  if (c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, 2 * c->f, n, n, n) && gemm_tc_swiglu_ok(M, 2 * c->f, n)) {
     // data-parallel gate/up GEMM with SwiGLU in the epilogue, bf16 h straight to c->a
     Prof pf(c, c->pass_verify ? P_GEMM_VERIFY : P_GEMM_DRAFT,
             (double)2 * c->f * n * c->esz + (double)M * n * c->esz + (double)M * c->f * c->esz,

@@ -603,12 +603,12 @@ static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float
 }
 
 static int gemm_tc_launch(const bf16* A, int lda, const bf16* W, int ldw, float* C, int ldc, int M, int N, int K,
-                          int epi, int dp, bf16* H, int ldh, cudaStream_t st) {
+                          int epi, int dp, bf16* H, int ldh, cudaStream_t st, bool allow_pair = true) {
   TcParams P;
   P.M = M; P.N = N; P.K = K; P.ldc = ldc; P.C = C; P.H = H; P.ldh = ldh; P.epi = epi; P.dp = dp;
   // data-parallel shapes (large M: c3/c4/c5 verify) run on CTA pairs (2-SM UMMA)
   static const bool pair_on = [] { const char* e = getenv("HSD_GEMM_2SM"); return !(e && atoi(e) == 0); }();
-  if (dp && pair_on && num_sms() >= 2) return gemm_tc2_launch(A, lda, W, ldw, C, ldc, M, N, K, epi, H, ldh, st);
+  if (dp && allow_pair && pair_on && num_sms() >= 2) return gemm_tc2_launch(A, lda, W, ldw, C, ldc, M, N, K, epi, H, ldh, st);
   static unsigned long long* trace = [] {
     unsigned long long* t = nullptr;
     if (getenv("HSD_GEMM_TRACE")) { cudaMalloc(&t, 32 * 8); cudaMemset(t, 0, 32 * 8); }
@@ -668,8 +668,30 @@ int gemm_tc_bf16(const bf16* A, int lda, const bf16* W, int ldw, float* C, int l
   return gemm_tc_launch(A, lda, W, ldw, C, ldc, M, N, K, epi, dp, nullptr, 0, st);
 }
 
+// Decode-size gate/up (one token tile, >= one 128-row weight tile per SM: c2's
+// 172 tiles at M <= 256) CAN run data-parallel on single CTAs with SwiGLU in the
+// epilogue (whole tiles per CTA in one wave, no stream-K partials, no separate
+// SwiGLU launch) -- measured slower on c2 (step 4.73 -> 5.19 ms: one CTA cannot
+// pull a 1.4 MB weight tile at its share of HBM bandwidth), so it is opt-in
+// (HSD_GEMM_SWIGLU_1CTA=1) for experiments.
+static bool swiglu_1cta(int M, int N) {
+  static const bool on = [] { const char* e = getenv("HSD_GEMM_SWIGLU_1CTA"); return e && atoi(e) == 1; }();
+  int nt, ntt;
+  tc_tiles(M, nt, ntt);
+  const long tiles = (long)((N + BM - 1) / BM) * ntt;
+  return on && ntt == 1 && tiles >= num_sms() && tiles <= 2L * num_sms();
+}
+
+bool gemm_tc_swiglu_ok(int M, int N, int K) {
+  if (N % BM) return false;
+  return gemm_tc_dp(M, N, K, false) || swiglu_1cta(M, N);
+}
+
 int gemm_tc_swiglu_bf16(const bf16* A, int lda, const bf16* W, int ldw, bf16* H, int ldh, int M, int N, int K,
                         cudaStream_t st) {
-  if (!gemm_tc_dp(M, N, K, false) || N % BM) return 0;
-  return gemm_tc_launch(A, lda, W, ldw, nullptr, 0, M, N, K, EPI_SWIGLU, 1, H, ldh, st);
+  if (N % BM) return 0;
+  if (gemm_tc_dp(M, N, K, false)) return gemm_tc_launch(A, lda, W, ldw, nullptr, 0, M, N, K, EPI_SWIGLU, 1, H, ldh, st);
+  if (swiglu_1cta(M, N))
+    return gemm_tc_launch(A, lda, W, ldw, nullptr, 0, M, N, K, EPI_SWIGLU, 1, H, ldh, st, /*allow_pair=*/false);
+  return 0;
 }

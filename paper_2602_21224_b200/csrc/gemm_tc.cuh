@@ -12,6 +12,8 @@ int gemm_tc_bf16(const bf16* A, int lda, const bf16* W, int ldw, float* C, int l
 // true when the GEMM runs data-parallel (at least one output tile per SM)
 // K / accumulate: 0 / false when unknown (store epilogue)
 bool gemm_tc_dp(int M, int N, int K = 0, bool accumulate = false);
+// the gate/up GEMM can fuse SwiGLU into its epilogue (data-parallel shapes)
+bool gemm_tc_swiglu_ok(int M, int N, int K);
 // data-parallel gate/up GEMM with the SwiGLU fused into the epilogue: W rows are
 // interleaved in 64-row groups (gate rows g*64.., then the matching up rows),
 // H[M, N/2] = silu(gate) * up in bf16. Returns 0 (nothing launched) when the
