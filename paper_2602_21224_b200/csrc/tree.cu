@@ -146,6 +146,7 @@ HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, in
       const int gthreads = wpn * 32;
       float tv = -INFINITY;   // the warp's current k-th best (v, j)
       int tj = -1;
+      bool seeded = false;    // warp-uniform: the list holds the first batch's top-k
       constexpr int U = 4;
       for (int wbase = lo + wg * 32; wbase < hi; wbase += gthreads * U) {   // warp-uniform trip count
         float lv[U], bv[U];
@@ -183,6 +184,29 @@ HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, in
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int j = wbase + lane + u * gthreads;
+          if (!seeded) {
+            // the warp's list is still empty (first batch of the round): every lane
+            // would be a candidate, so seed it with a warp bitonic sort of the
+            // batch (R8 order, empty slots last) instead of 32 serial insertions
+            float sv = j < hi ? v[u] : -INFINITY;
+            int sj = j < hi ? j : -1;
+#pragma unroll
+            for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+              for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, sv, jj);
+                const int oj = __shfl_xor_sync(0xffffffffu, sj, jj);
+                const bool want_better = ((lane & jj) == 0) == ((lane & kk) == 0);
+                const bool other_better = better_j(ov, oj, sv, sj, perm_of(P));
+                if (want_better == other_better) { sv = ov; sj = oj; }
+              }
+            }
+            if (lane < K) { ev = sv; ej = sj; }
+            tv = __shfl_sync(0xffffffffu, sv, K - 1);
+            tj = __shfl_sync(0xffffffffu, sj, K - 1);
+            seeded = true;
+            continue;
+          }
           unsigned cand = __ballot_sync(0xffffffffu, j < hi && better_j(v[u], j, tv, tj, perm_of(P)));
           while (cand) {
             const int src = __ffs(cand) - 1;
