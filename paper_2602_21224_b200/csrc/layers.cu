@@ -5,6 +5,7 @@
 // All are bandwidth-trivial at decode sizes (tens of rows), so they are written
 // for latency: 128-bit vector accesses, every load of a thread issued before
 // use, and grids that put (row, column-chunk) work items on many SMs.
+#include <algorithm>
 #include "kernels.cuh"
 
 namespace {
@@ -103,7 +104,8 @@ void launch_embed(const void* E, DType dt, const int32_t* tok, const int32_t* po
 // One CTA per row: thread t handles rotation pairs (head, j) strided over the
 // row's q and k heads, then the v head dims; the fp32 scratch row is re-zeroed
 // after the CTA has read it (so the next tcgen05 GEMM into it needs no memset).
-constexpr int ROPE_PARTS = 8;     // q/k CTAs per row
+int num_sms();   // gemm_tc.cu (cached device SM count)
+constexpr int ROPE_PARTS = 8;     // max q/k CTAs per row (fewer when M is large, see the launcher)
 constexpr int VROWS = 32;         // rows per V-transpose CTA
 
 // V rows -> the transposed cache V^T [hd][page_size] per (page, kv head): a CTA
@@ -160,7 +162,8 @@ template <typename T>
 __global__ void __launch_bounds__(128) qkv_rope_kv_kernel(float* __restrict__ qkv, RowMeta m,
                                                           const float* __restrict__ rc,
                                                           const float* __restrict__ rs, int Hq, KVLayer kv,
-                                                          T* __restrict__ q_out, int M, int zero, L2Pf pf) {
+                                                          T* __restrict__ q_out, int M, int zero, int nparts_,
+                                                          L2Pf pf) {
   l2pf_issue(pf);
   pdl_wait();
   l2pf_issue(pf, 1);
@@ -171,7 +174,7 @@ __global__ void __launch_bounds__(128) qkv_rope_kv_kernel(float* __restrict__ qk
     return;
   }
   const int rb = blockIdx.x - n_v;
-  const int r = rb / ROPE_PARTS, part = rb % ROPE_PARTS, nparts = ROPE_PARTS;
+  const int nparts = nparts_, r = rb / nparts, part = rb % nparts;
   const int hd = kv.head_dim, half = hd / 2, Hkv = kv.kv_heads;
   const int ld = (Hq + 2 * Hkv) * hd;
   float* row = qkv + (size_t)r * ld;
@@ -242,11 +245,17 @@ void launch_qkv_rope_kv(float* qkv, int M, const RowMeta& m, const float* rope_c
                         cudaStream_t st, bool zero) {
   const L2Pf pf = take_l2pf();
   if (M <= 0) return;
-  const int grid = M * ROPE_PARTS + (M + VROWS - 1) / VROWS * kv.kv_heads * ((kv.head_dim + 31) / 32);
+  // q/k CTAs per row: 8 at decode sizes (c2: M = 65, latency-bound, spread wide);
+  // at large M a row per CTA -- c3's 2080 x 8 tiny CTAs spent more time in CTA
+  // turnaround and the per-CTA metadata chain than in their 2.5 pairs per thread
+  static const int parts_env = [] { const char* e = getenv("HSD_ROPE_PARTS"); return e ? atoi(e) : 0; }();
+  const int nparts = parts_env > 0 ? std::min(parts_env, ROPE_PARTS)
+                                   : std::max(1, std::min(ROPE_PARTS, (num_sms() * 8) / std::max(M, 1)));
+  const int grid = M * nparts + (M + VROWS - 1) / VROWS * kv.kv_heads * ((kv.head_dim + 31) / 32);
   if (dt == DT_F32)
-    launch_k(qkv_rope_kv_kernel<float>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out, M, zero ? 1 : 0, pf);
+    launch_k(qkv_rope_kv_kernel<float>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (float*)q_out, M, zero ? 1 : 0, nparts, pf);
   else
-    launch_k(qkv_rope_kv_kernel<bf16>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out, M, zero ? 1 : 0, pf);
+    launch_k(qkv_rope_kv_kernel<bf16>, dim3(grid), 128, 0, st, qkv, m, rope_cos, rope_sin, Hq, kv, (bf16*)q_out, M, zero ? 1 : 0, nparts, pf);
 }
 
 // ------------------------------------------------------------------ SwiGLU
