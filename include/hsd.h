@@ -242,6 +242,21 @@ hsd_status hsd_debug_gemm(const void* A, int32_t lda, const void* W, int32_t ldw
 /* Number of this library's kernels launched on the ctx since creation. */
 int64_t hsd_kernel_launches(const hsd_ctx* ctx);
 
+/* Measurement: per-launch device time of the verify GEMMs INSIDE graph-replayed
+ * steps (no events between launches). enable != 0: the next hsd_step recaptures
+ * its graph with every verify GEMM launch stamping %globaltimer at CTA entry
+ * (minimum over CTAs) and exit (maximum) into a device buffer indexed by (step
+ * counter mod 64, launch); enable == 0 drops the stamped graph. Synchronous.
+ * HSD_ESTATE inside a staged step.                                           */
+hsd_status hsd_kstamp(hsd_ctx* ctx, int enable);
+/* Read the stamps (synchronous): *avg_us = mean (exit - entry) over every stamped
+ * launch of every stamped replay still in the buffer, *samples their count,
+ * *bytes_per_launch / *flops_per_launch the mean algorithmic bytes / flops of one
+ * stamped launch (the same accounting as hsd_profile). HOST outputs, may be NULL.
+ * HSD_ESTATE if no stamped graph ran.                                         */
+hsd_status hsd_kstamp_read(hsd_ctx* ctx, double* avg_us, int64_t* samples, double* bytes_per_launch,
+                           double* flops_per_launch);
+
 hsd_status hsd_destroy(hsd_ctx* ctx);
 const char* hsd_last_error(const hsd_ctx* ctx);
 

@@ -140,6 +140,23 @@ HSD_DEV void l2pf_issue(const L2Pf& pf, int late = 0) {
   }
 }
 
+// ---------------------------------------------------------------- kernel stamps
+// hsd_kstamp: the engine hands the NEXT GEMM launch a stamp slot (like L2Pf);
+// kernels fold per-CTA %globaltimer entry / exit times into [slot][id] arrays.
+constexpr int KST_SLOTS = 64;     // replays kept (step counter mod 64)
+constexpr int KST_MAXID = 512;    // stamped launches per step
+struct KStamp {
+  unsigned long long* buf;        // [2][KST_SLOTS][KST_MAXID]: entry minima, then exit maxima
+  int id;
+  const int* step;                // device step counter (slot = step mod KST_SLOTS)
+};
+extern KStamp g_kstamp;
+inline KStamp take_kstamp() {
+  KStamp r = g_kstamp;
+  g_kstamp = KStamp{nullptr, 0, nullptr};
+  return r;
+}
+
 extern bool g_hsd_pdl;   // engine.cu; HSD_PDL=0 disables (A/B testing)
 
 template <typename... KArgs, typename... Args>

@@ -187,6 +187,7 @@ struct LayerW { void *wqkv, *wo, *wgu, *wd; };
 // off) caps the range handed to a long idle window (qkv_rope + attention, SwiGLU,
 // K-TREE); short windows (an RMSNorm right before its GEMM) get a third of it.
 L2Pf g_l2pf = {nullptr, 0ull, 0};
+KStamp g_kstamp = {nullptr, 0, nullptr};
 // HSD_L2PF_WHERE: bitmask of the windows that prefetch (default 4 = attention only:
 // the others measured flat or slower on c2; 1 rmsnorm-1, 2 qkv_rope,
 // 4 attention, 8 rmsnorm-2, 16 SwiGLU, 32 K-TREE); HSD_L2PF_LATE=1 issues after the PDL wait
@@ -267,6 +268,11 @@ struct hsd_ctx {
   float *pv_loc = nullptr, *pv_all = nullptr;     // partial argmax values [G*rows], [G][G*rows]
   int32_t *pi_loc = nullptr, *pi_all = nullptr;   // partial argmax token ids
   std::string nccl_err;          // first collective failure (surfaced as HSD_ENCCL)
+  // hsd_kstamp: per-launch %globaltimer stamps of the verify GEMMs inside graph replays
+  unsigned long long* kst_buf = nullptr;
+  bool kst_on = false;
+  int kst_n = 0;
+  std::vector<double> kst_bytes, kst_flops;
   // host staging for e2e
   int32_t *h_pinned = nullptr;
   // graph
@@ -375,6 +381,15 @@ static void* dalloc(hsd_ctx* c, size_t bytes) {
   return p;
 }
 
+// hsd_kstamp: while a stamped graph is captured, the next verify GEMM launch gets
+// stamp slot id kst_n (its algorithmic bytes / flops recorded for hsd_kstamp_read)
+static void kstamp_next(hsd_ctx* c, int cat, double bytes, double flops) {
+  if (!c->kst_on || !c->capturing || cat != P_GEMM_VERIFY || c->kst_n >= KST_MAXID) return;
+  g_kstamp = KStamp{c->kst_buf, c->kst_n++, c->step};
+  c->kst_bytes.push_back(bytes);
+  c->kst_flops.push_back(flops);
+}
+
 // GEMM dispatch: C[M,N] (+)= A[M,K] W[N,K]^T. Algorithmic bytes: W once, A once,
 // C written once (read too when accumulating).
 static void gemm(hsd_ctx* c, const void* A, int lda, const void* Wt, int ldw, float* C, int ldc, int M, int N,
@@ -384,6 +399,8 @@ static void gemm(hsd_ctx* c, const void* A, int lda, const void* Wt, int ldw, fl
   Prof pf(c, cat, (double)N * K * c->esz + (double)M * K * c->esz + (double)M * N * 4 * (acc ? 2 : 1),
           2.0 * M * N * K);
   if (c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, N, K, lda, ldw)) {
+    kstamp_next(c, cat, (double)N * K * c->esz + (double)M * K * c->esz + (double)M * N * 4 * (acc ? 2 : 1),
+                2.0 * M * N * K);
     g_hsd_launches += gemm_tc_bf16((const bf16*)A, lda, (const bf16*)Wt, ldw, C, ldc, M, N, K, acc, c->st, c_zeroed);
   } else {
     gemm_simt(A, lda, Wt, ldw, c->dt, C, ldc, M, N, K, acc, c->st);
@@ -452,6 +469,9 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
     Prof pf(c, c->pass_verify ? P_GEMM_VERIFY : P_GEMM_DRAFT,
             (double)2 * c->f * n * c->esz + (double)M * n * c->esz + (double)M * c->f * c->esz,
             2.0 * M * 2 * c->f * n);
+    kstamp_next(c, c->pass_verify ? P_GEMM_VERIFY : P_GEMM_DRAFT,
+                (double)2 * c->f * n * c->esz + (double)M * n * c->esz + (double)M * c->f * c->esz,
+                2.0 * M * 2 * c->f * n);
     const int k = gemm_tc_swiglu_bf16((const bf16*)c->a, n, (const bf16*)w.wgu, n, (bf16*)c->h, c->f, M, 2 * c->f,
                                       n, c->st);
     g_hsd_launches += k;
@@ -1407,6 +1427,66 @@ hsd_status hsd_profile_read(hsd_ctx* ctx, const char* category, double* total_ms
     }
   }
   return fail(ctx, HSD_EINVAL, std::string("unknown profile category ") + category);
+}
+
+hsd_status hsd_kstamp(hsd_ctx* ctx, int enable) {
+  if (!ctx) return HSD_EINVAL;
+  hsd_ctx* c = ctx;
+  if (c->stage != 0) return fail(c, HSD_ESTATE, "hsd_kstamp in the middle of a staged step");
+  const size_t n = (size_t)2 * KST_SLOTS * KST_MAXID;
+  if (enable && !c->kst_buf) {
+    c->kst_buf = (unsigned long long*)dalloc(c, n * 8);
+    if (!c->kst_buf) return fail(c, HSD_ENOMEM, "kstamp buffer");
+  }
+  if (enable) {
+    CU(cudaMemsetAsync(c->kst_buf, 0xff, n / 2 * 8, c->st));            // entry minima
+    CU(cudaMemsetAsync(c->kst_buf + n / 2, 0, n / 2 * 8, c->st));       // exit maxima
+    CU(cudaStreamSynchronize(c->st));
+  }
+  c->kst_on = enable != 0;
+  c->kst_n = 0;
+  c->kst_bytes.clear();
+  c->kst_flops.clear();
+  drop_graphs(c);   // the next hsd_step recaptures (with or without stamps)
+  return HSD_OK;
+}
+
+hsd_status hsd_kstamp_read(hsd_ctx* ctx, double* avg_us, int64_t* samples, double* bytes_per_launch,
+                           double* flops_per_launch) {
+  if (!ctx) return HSD_EINVAL;
+  hsd_ctx* c = ctx;
+  if (!c->kst_buf || c->kst_n == 0) return fail(c, HSD_ESTATE, "hsd_kstamp_read: no stamped replay");
+  CU(cudaStreamSynchronize(c->st));
+  const size_t n = (size_t)KST_SLOTS * KST_MAXID;
+  std::vector<unsigned long long> h(2 * n);
+  CU(cudaMemcpy(h.data(), c->kst_buf, 2 * n * 8, cudaMemcpyDeviceToHost));
+  double sum = 0.0;
+  int64_t cnt = 0;
+  for (size_t slot = 0; slot < (size_t)KST_SLOTS; ++slot)
+    for (int id = 0; id < c->kst_n; ++id) {
+      const unsigned long long a = h[slot * KST_MAXID + id], b = h[n + slot * KST_MAXID + id];
+      if (a != ~0ull && b != 0ull && b > a) { sum += (double)(b - a); ++cnt; }
+    }
+  if (getenv("HSD_KST_DUMP")) {   // debug: per-launch durations of the first stamped slot
+    for (size_t slot = 0; slot < (size_t)KST_SLOTS; ++slot) {
+      if (h[slot * KST_MAXID] == ~0ull) continue;
+      fprintf(stderr, "kstamp slot %zu:", slot);
+      for (int id = 0; id < c->kst_n && id < 16; ++id) {
+        const unsigned long long a = h[slot * KST_MAXID + id], b = h[n + slot * KST_MAXID + id];
+        fprintf(stderr, " %d:%.1f(+%.1f)", id, a != ~0ull && b ? (double)(long long)(b - a) / 1e3 : -1.0,
+                id > 0 && a != ~0ull ? (double)(long long)(a - h[slot * KST_MAXID + id - 1]) / 1e3 : 0.0);
+      }
+      fprintf(stderr, "\n");
+      break;
+    }
+  }
+  double by = 0.0, fl = 0.0;
+  for (int id = 0; id < c->kst_n; ++id) { by += c->kst_bytes[id]; fl += c->kst_flops[id]; }
+  if (avg_us) *avg_us = cnt ? sum / cnt / 1e3 : 0.0;
+  if (samples) *samples = cnt;
+  if (bytes_per_launch) *bytes_per_launch = by / c->kst_n;
+  if (flops_per_launch) *flops_per_launch = fl / c->kst_n;
+  return HSD_OK;
 }
 
 hsd_status hsd_destroy(hsd_ctx* ctx) {

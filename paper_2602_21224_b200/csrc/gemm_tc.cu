@@ -46,11 +46,30 @@ struct TcParams {
   bf16* H;                        // EPI_SWIGLU output [M, N/2] bf16
   int ldh;
   unsigned long long* trace;      // debug phase trace (HSD_GEMM_TRACE) or null
+  KStamp kst;                     // per-launch %globaltimer stamps (hsd_kstamp) or kst.buf == null
 };
 HSD_DEV uint64_t gtime_g() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+// launch duration inside graph replays: every CTA's thread 0 folds its entry time
+// (atomicMin) and exit time (atomicMax) into the slot (step mod KST_SLOTS, launch id)
+// entry = the first return from griddepcontrol.wait in the CTA (inputs ready); the
+// pre-wait weight prefetch overlaps the predecessor and is not counted
+HSD_DEV void kstamp_wait(const KStamp& k) {
+  // one thread per CTA (thread 0 = the TMA producer's lane): every waiting thread
+  // hitting one address serialised ~50k atomics per launch in L2
+  if (k.buf == nullptr || threadIdx.x != 0) return;
+  const size_t e = (size_t)((*k.step) & (KST_SLOTS - 1)) * KST_MAXID + k.id;
+  atomicMin(k.buf + e, (unsigned long long)gtime_g());
+}
+HSD_DEV void kstamp(const KStamp& k, bool end) {
+  if (k.buf == nullptr || threadIdx.x != 0) return;
+  const size_t e = (size_t)((*k.step) & (KST_SLOTS - 1)) * KST_MAXID + k.id;
+  const unsigned long long t = gtime_g();
+  if (end) atomicMax(k.buf + (size_t)KST_SLOTS * KST_MAXID + e, t);
+  else atomicMin(k.buf + e, t);
 }
 // CTA 0 records slots 0..15, the last CTA slots 16..31: start, pre-PDL weight
 // loads issued, PDL released, first / last stage landed (MMA), epilogue start /
@@ -143,6 +162,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     if (lane == 0) {
       GTRACE(1);
       pdl_wait();
+    kstamp_wait(P.kst);
       GTRACE(2);
       for (long i = 0; i < npre; ++i) {
         const long u = sc.unit(i);
@@ -165,6 +185,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread)
     pdl_wait();
+    kstamp_wait(P.kst);
     if (lane == 0) {
       int stage = 0, buf = 0;
       uint32_t phase = 0, aphase = 0;
@@ -203,6 +224,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     // st.v4 (data-parallel), ld+add+st (data-parallel residual), or SwiGLU of
     // the interleaved gate/up rows into bf16 (data-parallel).
     pdl_wait();
+    kstamp_wait(P.kst);
     const int q = warp & 3, et = threadIdx.x - 64;      // 0..127
     int buf = 0;
     uint32_t aphase = 0;
@@ -284,6 +306,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   __syncthreads();
   fence_after();
   if (threadIdx.x == 0) GTRACE(7);
+  kstamp(P.kst, true);
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
 }
@@ -349,6 +372,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
       const uint64_t pw = policy_evict_first(), px = policy_evict_last();
       pdl_wait();
+    kstamp_wait(P.kst);
       int stage = 0;
       uint32_t phase = 0;
       for (long i = 0; i < count; ++i) {
@@ -366,6 +390,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer: the leader's lane 0 issues for the pair
     pdl_wait();
+    kstamp_wait(P.kst);
     if (leader && lane == 0) {
       int stage = 0, buf = 0;
       uint32_t phase = 0, aphase = 0;
@@ -396,6 +421,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else {
     // ---------------- epilogue: this CTA's 128 accumulator rows (output features)
     pdl_wait();
+    kstamp_wait(P.kst);
     const int q = warp & 3, et = threadIdx.x - 64;
     int buf = 0;
     uint32_t aphase = 0;
@@ -463,6 +489,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   fence_after();
+  kstamp(P.kst, true);
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols) : "memory");
 }
@@ -567,10 +594,11 @@ bool gemm_tc_dp(int M, int N, int K, bool accumulate) {
 }
 
 static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float* C, int ldc, int M, int N, int K,
-                           int epi, bf16* H, int ldh, cudaStream_t st) {
+                           int epi, bf16* H, int ldh, cudaStream_t st, KStamp ks) {
   TcParams P;
   P.M = M; P.N = N; P.K = K; P.ldc = ldc; P.C = C; P.H = H; P.ldh = ldh; P.epi = epi; P.dp = 1;
   P.trace = nullptr;
+  P.kst = ks;
   int nt, ntt;
   tc_tiles(M, nt, ntt);
   P.ntile = nt;
@@ -606,9 +634,10 @@ static int gemm_tc_launch(const bf16* A, int lda, const bf16* W, int ldw, float*
                           int epi, int dp, bf16* H, int ldh, cudaStream_t st, bool allow_pair = true) {
   TcParams P;
   P.M = M; P.N = N; P.K = K; P.ldc = ldc; P.C = C; P.H = H; P.ldh = ldh; P.epi = epi; P.dp = dp;
+  P.kst = take_kstamp();
   // data-parallel shapes (large M: c3/c4/c5 verify) run on CTA pairs (2-SM UMMA)
   static const bool pair_on = [] { const char* e = getenv("HSD_GEMM_2SM"); return !(e && atoi(e) == 0); }();
-  if (dp && allow_pair && pair_on && num_sms() >= 2) return gemm_tc2_launch(A, lda, W, ldw, C, ldc, M, N, K, epi, H, ldh, st);
+  if (dp && allow_pair && pair_on && num_sms() >= 2) return gemm_tc2_launch(A, lda, W, ldw, C, ldc, M, N, K, epi, H, ldh, st, P.kst);
   static unsigned long long* trace = [] {
     unsigned long long* t = nullptr;
     if (getenv("HSD_GEMM_TRACE")) { cudaMalloc(&t, 32 * 8); cudaMemset(t, 0, 32 * 8); }

@@ -27,7 +27,7 @@ SHARD_NONE, SHARD_NCCL, SHARD_SIM = 0, 1, 2
 EXPORTS = ["hsd_config_defaults", "hsd_init_model", "hsd_prefill", "hsd_set_plant", "hsd_build_tree",
            "hsd_force_tree", "hsd_verify_tree", "hsd_accept_and_compact", "hsd_step", "hsd_step_host",
            "hsd_sync", "hsd_get_tensor", "hsd_kernel_launches", "hsd_destroy", "hsd_last_error",
-           "hsd_profile", "hsd_profile_read", "hsd_debug_gemm", "hsd_nccl_unique_id", "hsd_admit"]
+           "hsd_profile", "hsd_profile_read", "hsd_debug_gemm", "hsd_nccl_unique_id", "hsd_admit", "hsd_kstamp", "hsd_kstamp_read"]
 PROFILE_CATEGORIES = ["gemm_verify", "gemm_draft", "head_verify", "head_draft", "attn_verify", "attn_draft",
                       "tree", "resample", "walk", "compact", "rowwise"]
 
@@ -93,6 +93,8 @@ def load(path: str = LIB_PATH):
         "hsd_profile_read": (I32, [VP, C.c_char_p, P(C.c_double), P(I64), P(C.c_double), P(C.c_double)]),
         "hsd_nccl_unique_id": (I32, [P(C.c_uint8)]),
         "hsd_admit": (I32, [VP, I32, P(I32), I32, VP]),
+        "hsd_kstamp": (I32, [VP, C.c_int]),
+        "hsd_kstamp_read": (I32, [VP, P(C.c_double), P(I64), P(C.c_double), P(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -243,6 +245,15 @@ class Context:
                                                   C.byref(fl)))
             out[cat] = (ms.value, n.value, by.value, fl.value)
         return out
+
+    def kstamp(self, enable: bool):
+        self._check(self.lib.hsd_kstamp(self.h, 1 if enable else 0))
+
+    def kstamp_read(self):
+        """(avg us per stamped verify-GEMM launch, samples, bytes / launch, flops / launch)"""
+        us, n, by, fl = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+        self._check(self.lib.hsd_kstamp_read(self.h, C.byref(us), C.byref(n), C.byref(by), C.byref(fl)))
+        return us.value, n.value, by.value, fl.value
 
     def kernel_launches(self) -> int:
         return int(self.lib.hsd_kernel_launches(self.h))
