@@ -499,8 +499,20 @@ def main():
             ach = pfl / (pms / 1e3) / 1e12
             roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": tfl, "unit": "TFLOP/s",
                     "frac": round(ach / tfl, 4), "traffic": traffic}
+        # the other HBM-side kernels of the step against the same peak (eager pass,
+        # algorithmic bytes: attention = the visible K/V rows once per kv head + q/out rows)
+        roof_other = {}
+        for oc in ("attn_verify", "attn_draft", "compact"):
+            oms, on, oby, ofl = prof.get(oc, (0.0, 0, 0.0, 0.0))
+            if oms > 0 and oby > 0:
+                oa = oby / (oms / 1e3) / 1e9
+                roof_other[oc] = {"achieved": round(oa, 1), "frac": round(oa / gbs, 4), "unit": "GB/s",
+                                  "us_per_launch": round(oms * 1e3 / max(on, 1), 2),
+                                  "algorithmic_bytes_per_launch": oby / max(on, 1),
+                                  "flop_per_byte": round(ofl / oby, 1) if ofl else None}
         roof.update({"kernel": cat, "launches_per_step": pn / kp, "share_of_step": round(pms / total_prof, 4),
-                     "peak_source": src, "algorithmic_bytes_per_launch": pby / max(pn, 1)})
+                     "peak_source": src, "algorithmic_bytes_per_launch": pby / max(pn, 1),
+                     "other_kernels_eager": roof_other})
 
     # ---- the dominant kernel's launch duration INSIDE graph-replayed steps: every
     # verify GEMM launch stamps %globaltimer at CTA entry / exit (hsd_kstamp), so
