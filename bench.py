@@ -525,6 +525,19 @@ def main():
                     ctx.step()
             stream.synchronize()
             k_us, k_n, k_by, k_fl = ctx.kstamp_read()
+            try:
+                a_us, a_n = ctx.kstamp_read_attention()
+                ao = roof.get("other_kernels_eager", {}).get("attn_verify")
+                if ao and a_us > 0:
+                    ach = ao["algorithmic_bytes_per_launch"] / (a_us * 1e-6) / 1e9
+                    roof["attn_verify_in_graph"] = {
+                        "achieved": round(ach, 1), "frac": round(ach / gbs, 4), "unit": "GB/s",
+                        "us_per_launch": round(a_us, 2), "stamped_launches": a_n,
+                        "what": "tree attention (+ split merge) per launch in graph-replayed steps, "
+                                "first return from griddepcontrol.wait to last CTA exit; algorithmic "
+                                "bytes as in other_kernels_eager"}
+            except Exception:
+                pass
             ctx.kstamp(False)
             eager = {k: roof[k] for k in ("achieved", "frac")}
             eager["what"] = "CUDA events around each launch on the ctx stream, eager (un-graphed) step"

@@ -256,6 +256,10 @@ hsd_status hsd_kstamp(hsd_ctx* ctx, int enable);
  * HSD_ESTATE if no stamped graph ran.                                         */
 hsd_status hsd_kstamp_read(hsd_ctx* ctx, double* avg_us, int64_t* samples, double* bytes_per_launch,
                            double* flops_per_launch);
+/* The same for the verify tree-attention launches (the tcgen05 kernel plus its
+ * split merge when there is one): *avg_us from the first return from
+ * griddepcontrol.wait to the last CTA exit of the merge, *samples as above.   */
+hsd_status hsd_kstamp_read_attention(hsd_ctx* ctx, double* avg_us, int64_t* samples);
 
 hsd_status hsd_destroy(hsd_ctx* ctx);
 const char* hsd_last_error(const hsd_ctx* ctx);

@@ -59,6 +59,7 @@ struct AttnParams {
   uint32_t idesc_s, idesc_o;
   unsigned long long* trace;   // [64] timestamps or null
   L2Pf pf;                     // weights of a later GEMM to prefetch into L2 (common.cuh)
+  KStamp kst;                  // per-launch stamps (hsd_kstamp) or kst.buf == null
 };
 #define TRACE(i) do { if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[(i)] = gtime(); } while (0)
 
@@ -282,6 +283,7 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
       while (kj < n_chunks && kj < KSTAGES && safe(kj)) load_k(kj++);
       while (vj < n_chunks && vj < VSTAGES && safe(vj)) load_v(vj++);
       pdl_wait();
+      kst_enter(P.kst);
       if (P.pf.late) l2pf_issue(P.pf, 1);   // (the late variant goes ahead of q)
       if (threadIdx.x == 0) TRACE(2);
       mbar_expect_tx(qbar, q_bytes);
@@ -567,13 +569,14 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   __syncthreads();
   fence_after();
   if (threadIdx.x == 0) TRACE(5);
+  kst_exit(P.kst);
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
 }
 
 // split merge: one warp per (row, head), lanes over hd:
 // o = sum_s e^{m_s - M} o_s / sum_s e^{m_s - M} l_s
 __global__ void attention_merge_bf16_kernel(const float* __restrict__ ws, int S, int M, int Hq, int hd,
-                                            bf16* __restrict__ out, L2Pf pf) {
+                                            bf16* __restrict__ out, L2Pf pf, KStamp kst) {
   l2pf_issue(pf);
   pdl_wait();
   l2pf_issue(pf, 1);
@@ -606,6 +609,7 @@ __global__ void attention_merge_bf16_kernel(const float* __restrict__ ws, int S,
     const int d = lane + 32 * i;
     if (d < hd) out[(size_t)pair * hd + d] = __float2bfloat16_rn(den > 0.f ? num[i] / den : 0.f);
   }
+  kst_exit(kst);   // the split merge ends the attention launch
 }
 }  // namespace
 
@@ -620,6 +624,7 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   if (QROWS % G) return -1;
   AttnParams P;
   P.pf = take_l2pf();
+  P.kst = take_kstamp();
   P.M = M; P.R = R; P.Hq = Hq; P.G = G; P.hd = hd; P.m = m; P.kv = kv;
   P.out = (bf16*)out; P.ws = ws; P.max_keys = max_keys;
   P.n_qtiles = (R * G + QROWS - 1) / QROWS;
@@ -714,7 +719,7 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   int launched = 1;
   if (S > 1) {
     launch_k(attention_merge_bf16_kernel, (M * Hq + 7) / 8, 256, 0, st, ws, S, M, Hq, hd, (bf16*)out,
-             take_l2pf());
+             take_l2pf(), P.kst);
     launched++;
   }
   return launched;

@@ -156,6 +156,20 @@ inline KStamp take_kstamp() {
   g_kstamp = KStamp{nullptr, 0, nullptr};
   return r;
 }
+// entry = the first return from griddepcontrol.wait (call from thread 0 only, right
+// after its pdl_wait); exit = the last CTA's exit (thread 0 at the very end)
+HSD_DEV void kst_enter(const KStamp& k) {
+  if (k.buf == nullptr || threadIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  atomicMin(k.buf + (size_t)((*k.step) & (KST_SLOTS - 1)) * KST_MAXID + k.id, t);
+}
+HSD_DEV void kst_exit(const KStamp& k) {
+  if (k.buf == nullptr || threadIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  atomicMax(k.buf + (size_t)KST_SLOTS * KST_MAXID + (size_t)((*k.step) & (KST_SLOTS - 1)) * KST_MAXID + k.id, t);
+}
 
 extern bool g_hsd_pdl;   // engine.cu; HSD_PDL=0 disables (A/B testing)
 

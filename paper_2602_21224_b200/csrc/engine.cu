@@ -273,6 +273,7 @@ struct hsd_ctx {
   bool kst_on = false;
   int kst_n = 0;
   std::vector<double> kst_bytes, kst_flops;
+  std::vector<int> kst_cat;
   // host staging for e2e
   int32_t *h_pinned = nullptr;
   // graph
@@ -384,10 +385,12 @@ static void* dalloc(hsd_ctx* c, size_t bytes) {
 // hsd_kstamp: while a stamped graph is captured, the next verify GEMM launch gets
 // stamp slot id kst_n (its algorithmic bytes / flops recorded for hsd_kstamp_read)
 static void kstamp_next(hsd_ctx* c, int cat, double bytes, double flops) {
-  if (!c->kst_on || !c->capturing || cat != P_GEMM_VERIFY || c->kst_n >= KST_MAXID) return;
+  if (!c->kst_on || !c->capturing || (cat != P_GEMM_VERIFY && cat != P_ATTN_VERIFY) || c->kst_n >= KST_MAXID)
+    return;
   g_kstamp = KStamp{c->kst_buf, c->kst_n++, c->step};
   c->kst_bytes.push_back(bytes);
   c->kst_flops.push_back(flops);
+  c->kst_cat.push_back(cat);
 }
 
 // GEMM dispatch: C[M,N] (+)= A[M,K] W[N,K]^T. Algorithmic bytes: W once, A once,
@@ -449,9 +452,12 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
     Prof pf(c, c->pass_verify ? P_ATTN_VERIFY : P_ATTN_DRAFT, c->attn_bytes);
     int tc_launched = -1;
     PfScope l2(w.wgu, b_gu, 0, cap, 4);
-    if (c->use_tc && g_attn_tc && attention_tc_supported(c->hd, c->page_size, c->dt))
+    if (c->use_tc && g_attn_tc && attention_tc_supported(c->hd, c->page_size, c->dt)) {
+      kstamp_next(c, c->pass_verify ? P_ATTN_VERIFY : P_ATTN_DRAFT, 0.0, 0.0);
       tc_launched = launch_attention_tc(c->qb, M, R, n_req, m, kv, c->Hq, max_keys, c->ob, c->attn_ws,
                                         c->attn_ws_floats, c->kv_layer_elems, c->st);
+      g_kstamp = KStamp{nullptr, 0, nullptr};   // (unconsumed if the tc kernel declined)
+    }
     if (tc_launched > 1) g_hsd_launches += tc_launched - 1;   // the split merge
     if (tc_launched < 0)
       launch_attention(c->qb, M, R, n_req, m, kv, c->Hq, c->dt, max_keys, c->ob, c->attn_ws, c->attn_ws_floats,
@@ -1447,12 +1453,13 @@ hsd_status hsd_kstamp(hsd_ctx* ctx, int enable) {
   c->kst_n = 0;
   c->kst_bytes.clear();
   c->kst_flops.clear();
+  c->kst_cat.clear();
   drop_graphs(c);   // the next hsd_step recaptures (with or without stamps)
   return HSD_OK;
 }
 
-hsd_status hsd_kstamp_read(hsd_ctx* ctx, double* avg_us, int64_t* samples, double* bytes_per_launch,
-                           double* flops_per_launch) {
+static hsd_status kstamp_read_cat(hsd_ctx* ctx, int want_cat, double* avg_us, int64_t* samples,
+                                  double* bytes_per_launch, double* flops_per_launch) {
   if (!ctx) return HSD_EINVAL;
   hsd_ctx* c = ctx;
   if (!c->kst_buf || c->kst_n == 0) return fail(c, HSD_ESTATE, "hsd_kstamp_read: no stamped replay");
@@ -1464,6 +1471,7 @@ hsd_status hsd_kstamp_read(hsd_ctx* ctx, double* avg_us, int64_t* samples, doubl
   int64_t cnt = 0;
   for (size_t slot = 0; slot < (size_t)KST_SLOTS; ++slot)
     for (int id = 0; id < c->kst_n; ++id) {
+      if (c->kst_cat[id] != want_cat) continue;
       const unsigned long long a = h[slot * KST_MAXID + id], b = h[n + slot * KST_MAXID + id];
       if (a != ~0ull && b != 0ull && b > a) { sum += (double)(b - a); ++cnt; }
     }
@@ -1481,12 +1489,23 @@ hsd_status hsd_kstamp_read(hsd_ctx* ctx, double* avg_us, int64_t* samples, doubl
     }
   }
   double by = 0.0, fl = 0.0;
-  for (int id = 0; id < c->kst_n; ++id) { by += c->kst_bytes[id]; fl += c->kst_flops[id]; }
+  int nid = 0;
+  for (int id = 0; id < c->kst_n; ++id)
+    if (c->kst_cat[id] == want_cat) { by += c->kst_bytes[id]; fl += c->kst_flops[id]; ++nid; }
   if (avg_us) *avg_us = cnt ? sum / cnt / 1e3 : 0.0;
   if (samples) *samples = cnt;
-  if (bytes_per_launch) *bytes_per_launch = by / c->kst_n;
-  if (flops_per_launch) *flops_per_launch = fl / c->kst_n;
+  if (bytes_per_launch) *bytes_per_launch = nid ? by / nid : 0.0;
+  if (flops_per_launch) *flops_per_launch = nid ? fl / nid : 0.0;
   return HSD_OK;
+}
+
+hsd_status hsd_kstamp_read(hsd_ctx* ctx, double* avg_us, int64_t* samples, double* bytes_per_launch,
+                           double* flops_per_launch) {
+  return kstamp_read_cat(ctx, P_GEMM_VERIFY, avg_us, samples, bytes_per_launch, flops_per_launch);
+}
+
+hsd_status hsd_kstamp_read_attention(hsd_ctx* ctx, double* avg_us, int64_t* samples) {
+  return kstamp_read_cat(ctx, P_ATTN_VERIFY, avg_us, samples, nullptr, nullptr);
 }
 
 hsd_status hsd_destroy(hsd_ctx* ctx) {

@@ -27,7 +27,7 @@ SHARD_NONE, SHARD_NCCL, SHARD_SIM = 0, 1, 2
 EXPORTS = ["hsd_config_defaults", "hsd_init_model", "hsd_prefill", "hsd_set_plant", "hsd_build_tree",
            "hsd_force_tree", "hsd_verify_tree", "hsd_accept_and_compact", "hsd_step", "hsd_step_host",
            "hsd_sync", "hsd_get_tensor", "hsd_kernel_launches", "hsd_destroy", "hsd_last_error",
-           "hsd_profile", "hsd_profile_read", "hsd_debug_gemm", "hsd_nccl_unique_id", "hsd_admit", "hsd_kstamp", "hsd_kstamp_read"]
+           "hsd_profile", "hsd_profile_read", "hsd_debug_gemm", "hsd_nccl_unique_id", "hsd_admit", "hsd_kstamp", "hsd_kstamp_read", "hsd_kstamp_read_attention"]
 PROFILE_CATEGORIES = ["gemm_verify", "gemm_draft", "head_verify", "head_draft", "attn_verify", "attn_draft",
                       "tree", "resample", "walk", "compact", "rowwise"]
 
@@ -95,6 +95,7 @@ def load(path: str = LIB_PATH):
         "hsd_admit": (I32, [VP, I32, P(I32), I32, VP]),
         "hsd_kstamp": (I32, [VP, C.c_int]),
         "hsd_kstamp_read": (I32, [VP, P(C.c_double), P(I64), P(C.c_double), P(C.c_double)]),
+        "hsd_kstamp_read_attention": (I32, [VP, P(C.c_double), P(I64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -254,6 +255,12 @@ class Context:
         us, n, by, fl = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
         self._check(self.lib.hsd_kstamp_read(self.h, C.byref(us), C.byref(n), C.byref(by), C.byref(fl)))
         return us.value, n.value, by.value, fl.value
+
+    def kstamp_read_attention(self):
+        """(avg us per stamped verify tree-attention launch incl. its split merge, samples)"""
+        us, n = C.c_double(), C.c_int64()
+        self._check(self.lib.hsd_kstamp_read_attention(self.h, C.byref(us), C.byref(n)))
+        return us.value, n.value
 
     def kernel_launches(self) -> int:
         return int(self.lib.hsd_kernel_launches(self.h))
