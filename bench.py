@@ -483,7 +483,10 @@ def main():
         prof = ctx.profile_read()
         ctx.profile(False)
         gbs, tfl, src = peaks()
-        cat, (pms, pn, pby, pfl) = max(prof.items(), key=lambda kv: kv[1][0])
+        # the dominant kernel category with an algorithmic byte count (latency-only
+        # categories such as K-TREE carry none and cannot be placed on a roofline)
+        cands = [(k, v) for k, v in prof.items() if v[2] > 0] or list(prof.items())
+        cat, (pms, pn, pby, pfl) = max(cands, key=lambda kv: kv[1][0])
         achieved_gbs = pby / (pms / 1e3) / 1e9 if pms > 0 else 0.0
         ai = pfl / pby if pby else 0.0
         ridge = tfl * 1e12 / (gbs * 1e9)
