@@ -102,7 +102,7 @@ def test_lockstep_c1_fp8_table():
 
 
 def run_lockstep(cfg, precision, steps, seed=0, batch=1, planted=False, accept="greedy", hot=0, tol=None,
-                 flag=None, expect_no_flags=False, tcgen05=False, table_fp8=False):
+                 flag=None, expect_no_flags=False, tcgen05=False, table_fp8=False, extra_ctx=0):
     perm = vocab_permutation(cfg.vocab, 0) if hot else None
     pr = prompts(cfg, batch=batch)
     m = Model(cfg, seed=seed, precision="fp32" if precision == hsd.FP32_VERIFY else "bf16")
@@ -117,7 +117,8 @@ def run_lockstep(cfg, precision, steps, seed=0, batch=1, planted=False, accept="
         rates = [1.0, 0.9, 0.8, 0.7, 0.7, 0.7, 0.7, 0.7]
         flags |= hsd.FLAG_PLANTED
     ctx = ctx_for(cfg, precision, seed=seed, max_batch=batch, flags=flags, accept=accept, vocab_perm=perm,
-                  plant_rates=rates, max_ctx=cfg.prompt_len + steps * (cfg.steps_N + 1) + 8, tcgen05=tcgen05)
+                  plant_rates=rates, max_ctx=cfg.prompt_len + steps * (cfg.steps_N + 1) + 8 + extra_ctx,
+                  tcgen05=tcgen05)
     ls = Lockstep(ctx, cfg, m, table, pr, seed=seed, accept=accept, plant=plant, plant_rates=rates, perm=perm,
                   logit_tol=tol or (1e-4 if precision == hsd.FP32_VERIFY else 2e-2),
                   flag_margin=flag or (1e-4 if precision == hsd.FP32_VERIFY else 1e-2))
@@ -223,6 +224,18 @@ def test_lockstep_wide_bf16_tcgen05_planted(hd, q_heads, kv_heads, prompt_len):
                                    prompt_len=prompt_len)
     ls, accs = run_lockstep(cfg, hsd.BF16, steps=6, tcgen05=True, planted=True)
     assert ls.max_err["verify"] <= 2e-2 and max(accs) >= 2
+
+
+def test_lockstep_attention_capacity_far_above_context():
+    """Key splits are sized on the host from the context CAPACITY (max_ctx) but, in the
+    latency-bound regime, divide the chunks each tile really sees on the device
+    (attention_tc.cu, P.dyn): a 4k-key capacity over a ~100-key context leaves most
+    capacity splits empty. MHA hd 128 and GQA hd 64, planted acceptance."""
+    for hd, qh, kvh in [(128, 4, 4), (64, 8, 2)]:
+        cfg = get_config("c1").replace(hidden=512, q_heads=qh, kv_heads=kvh, head_dim=hd, ffn=1024, vocab=1024,
+                                       layers=2, steps_N=5, branch_k=3, budget_B=16, prompt_len=100)
+        ls, accs = run_lockstep(cfg, hsd.BF16, steps=5, tcgen05=True, planted=True, extra_ctx=4096)
+        assert ls.max_err["verify"] <= 2e-2 and max(accs) >= 2
 
 
 def test_attention_cluster_reduction_all_widths():
