@@ -121,8 +121,10 @@ def _margins_ok(margins, kinds, thr):
     return all(mg >= thr for kind, mg in margins if kind in kinds)
 
 
-def run_fullsize(name, n_steps_graph=2, n_checked=2, check_reqs=None, table_fp8=False):
+def run_fullsize(name, n_steps_graph=2, n_checked=2, check_reqs=None, table_fp8=False, batch=None):
     cfg = get_config(name)
+    if batch:
+        cfg = cfg.replace(batch=batch)
     seed = 0
     perm = vocab_permutation(cfg.vocab, 0) if cfg.hot_tokens else None
     stream = torch.cuda.Stream()
@@ -258,4 +260,20 @@ def test_fullsize_c3_fp8_table():
 
 def test_fullsize_c3_stochastic_hot_batch32():
     st = run_fullsize("c3", n_steps_graph=1, n_checked=1, check_reqs=list(range(0, 32, 4)))
+    assert st["tree"] >= 6 and st["walk"] >= 6 and st["kv"] >= 18
+
+
+def test_fullsize_c5_greedy_70b_batch2():
+    """Llama-3-70B shapes (80 layers, n 8192, GQA 64/8, V 128256 with the 2-D hot
+    table, 8k context) at b = 2 on one GPU: 5 q-tiles per (request, kv head) and the
+    2-CTA cluster key-split merge in the tree attention, stream-K GEMMs at M = 130."""
+    st = run_fullsize("c5", n_steps_graph=1, n_checked=1, batch=2)
+    assert st["tree"] >= 1 and st["walk"] >= 1 and st["kv"] >= 3
+
+
+def test_fullsize_c4_greedy_13b_batch64():
+    """Llama-2-13B shapes with the wider tree (N6 k6 B128 -> 133 verify slots), 64
+    requests on one GPU (M = 8512 verify rows: data-parallel CTA-pair GEMMs, fused
+    SwiGLU, the storing QKV GEMM without scratch re-zeroing)."""
+    st = run_fullsize("c4", n_steps_graph=1, n_checked=1, check_reqs=list(range(0, 64, 8)))
     assert st["tree"] >= 6 and st["walk"] >= 6 and st["kv"] >= 18
