@@ -182,8 +182,9 @@ __global__ void f32_to_dt_kernel(const float* src, size_t count, bf16* dst) {
 // ====================================================================== context
 struct LayerW { void *wqkv, *wo, *wgu, *wd; };
 
-// L2 weight prefetch (common.cuh L2Pf): kernels that leave HBM idle carry a byte
-// range of the weights the NEXT GEMM(s) will stream. HSD_L2PF_MB (default 48, 0 =
+// L2 weight prefetch (common.cuh L2Pf; cap swept on c2: 0 / 32 / 48 / 64 / 96 / 128 / 160 MB ->
+// 4.89 / 4.77 / 4.76 / 4.74 / 4.73 / 4.76 / 4.86 ms): kernels that leave HBM idle carry a byte
+// range of the weights the NEXT GEMM(s) will stream. HSD_L2PF_MB (default 96, 0 =
 // off) caps the range handed to a long idle window (qkv_rope + attention, SwiGLU,
 // K-TREE); short windows (an RMSNorm right before its GEMM) get a third of it.
 L2Pf g_l2pf = {nullptr, 0ull, 0};
@@ -195,7 +196,7 @@ static const int g_l2pf_where = [] { const char* e = getenv("HSD_L2PF_WHERE"); r
 static const int g_l2pf_late = [] { const char* e = getenv("HSD_L2PF_LATE"); return e ? atoi(e) : 0; }();
 static const size_t g_l2pf_cap = [] {
   const char* e = getenv("HSD_L2PF_MB");
-  return (size_t)(e ? atof(e) : 48.0) * (size_t)(1 << 20);
+  return (size_t)(e ? atof(e) : 96.0) * (size_t)(1 << 20);
 }();
 struct PfScope {   // the next launch inside this scope carries [p + off, p + off + min(bytes, cap))
   PfScope(const void* p, size_t total, size_t off, size_t cap, int where) {
