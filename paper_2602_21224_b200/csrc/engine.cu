@@ -89,22 +89,22 @@ __global__ void meta_dprefill_kernel(MetaBuf mb, int R, const int32_t* n_pend, c
 }
 
 // chain step i: row r at position p + i, causal over draft KV [1, p + i]
-__global__ void meta_chain_kernel(MetaBuf mb, int b, int i, const int32_t* p) {
-  pdl_wait();
-  pdl_trigger();
-  int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= b) return;
-  int pos = p[r] + i;
+
+// row metadata of chain step i for request r (position p + i, keys [1, p + i]): written
+// by the kernel that ends the previous chain step (no separate metadata launch)
+HSD_DEV void chain_meta(const MetaBuf& mb, int r, int i, const int32_t* p) {
+  const int pos = p[r] + i;
   mb.tok[r] = 0; mb.pos[r] = pos; mb.kvpos[r] = pos; mb.req[r] = r;
   mb.klo[r] = 1; mb.khi[r] = pos + 1; mb.slot[r] = -1;
 }
 
-// h_1 = draft output at the last pending row -> xw[r] and chain[r][0]
+// h_1 = draft output at the last pending row -> xw[r] and chain[r][0]; meta of chain step 1
 __global__ void gather_last_kernel(const float* x, int R, const int32_t* n_pend, int n, float* xw, float* chain,
-                                   int N) {
+                                   int N, MetaBuf mc, const int32_t* p) {
   pdl_wait();
   pdl_trigger();
   int r = blockIdx.x;
+  if (threadIdx.x == 0 && N > 1) chain_meta(mc, r, 1, p);
   const float* src = x + ((size_t)r * R + n_pend[r] - 1) * n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     xw[(size_t)r * n + i] = src[i];
@@ -112,10 +112,12 @@ __global__ void gather_last_kernel(const float* x, int R, const int32_t* n_pend,
   }
 }
 
-__global__ void copy_chain_kernel(const float* xw, int n, float* chain, int N, int i) {
+// chain row i -> chain[r][i]; meta of chain step i + 1
+__global__ void copy_chain_kernel(const float* xw, int n, float* chain, int N, int i, MetaBuf mc, const int32_t* p) {
   pdl_wait();
   pdl_trigger();
   int r = blockIdx.x;
+  if (threadIdx.x == 0 && i + 1 < N) chain_meta(mc, r, i + 1, p);
   for (int c = threadIdx.x; c < n; c += blockDim.x) chain[((size_t)r * N + i) * n + c] = xw[(size_t)r * n + c];
 }
 
@@ -562,16 +564,16 @@ static void stage_build(hsd_ctx* c) {
   launch_draft_concat(c->pend_H, c->md.tok, c->md.pos, c->embed, c->dt, b * R, n, c->a, c->st);
   gemm(c, c->a, 2 * n, c->fc, 2 * n, c->x_d, n, b * R, n, 2 * n, false);
   layer_forward(c, c->draft, c->x_d, b * R, R, b, mdv, kv_layer(c, c->kv_d, 0), kvmax);
-  launch_k(gather_last_kernel, b, 256, 0, c->st, c->x_d, R, c->n_pend, n, c->xw, c->chain, N);
+  launch_k(gather_last_kernel, b, 256, 0, c->st, c->x_d, R, c->n_pend, n, c->xw, c->chain, N, c->mc, c->p);
   g_hsd_launches += 3;
   // S0 (2): chain h_{i+1} = TL(h_i) at positions p + i (R2)
   RowMeta mcv = c->mc.view(nullptr, nullptr, 0, 0);
   for (int i = 1; i < N; ++i) {
-    launch_k(meta_chain_kernel, (b + 127) / 128, 128, 0, c->st, c->mc, b, i, c->p);
+    // (chain step i's row metadata was written by gather_last / the previous copy_chain)
     c->attn_bytes = attn_bytes_for(c, 2, i);
     layer_forward(c, c->draft, c->xw, b, 1, b, mcv, kv_layer(c, c->kv_d, 0), kvmax);
-    launch_k(copy_chain_kernel, b, 256, 0, c->st, c->xw, n, c->chain, N, i);
-    g_hsd_launches += 2;
+    launch_k(copy_chain_kernel, b, 256, 0, c->st, c->xw, n, c->chain, N, i, c->mc, c->p);
+    g_hsd_launches += 1;
   }
   // S1a: one-pass logits L = RMSNorm_f(H_chain) W_head^T, rank order
   launch_rmsnorm(c->chain, b * N, n, c->cfg.rms_eps, c->a, c->dt, nullptr, c->st);
