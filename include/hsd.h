@@ -239,6 +239,17 @@ hsd_status hsd_debug_gemm(const void* A, int32_t lda, const void* W, int32_t ldw
                           int32_t M, int32_t N, int32_t K, int32_t accumulate, int32_t dtype, int32_t use_tc,
                           void* stream);
 
+/* Test hook: n independent Gumbel-max draws with the stochastic walk's own device
+ * code (reading R13; PAPER.md:449 leaves T > 0 unspecified): draw i returns
+ * argmax_v (l_v / T - log(-log U_v)) over row d_row[i] of the DEVICE fp32 logits
+ * [*, ld] (v < V), with U_v the sampling uniform of the Gumbel Philox stream
+ * (seed, 0x5EED0002), counter (v/4, d_slot[i], step, req), word v%4 (DESIGN.md
+ * section 4). d_row, d_slot, d_out: DEVICE int32 [n]. Asynchronous on `stream`.
+ * HSD_EINVAL on null pointers, ld < V or temperature <= 0.                   */
+hsd_status hsd_debug_gumbel(const float* d_logits, int32_t ld, int32_t V, float temperature, uint64_t seed,
+                            int32_t req, int32_t step, int32_t n, const int32_t* d_row, const int32_t* d_slot,
+                            int32_t* d_out, void* stream);
+
 /* Number of this library's kernels launched on the ctx since creation. */
 int64_t hsd_kernel_launches(const hsd_ctx* ctx);
 

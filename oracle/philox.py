@@ -10,7 +10,9 @@ Streams used by the method (DESIGN.md §"Random streams"):
   accept  : key=(seed, 0x5EED0001), counter=(slot, rank, step, req), word 0
   gumbel  : key=(seed, 0x5EED0002), counter=(v//4, slot, step, req), word v%4
   plant   : key=(seed, 0x5EED0003), counter=(depth, step, req, 0), word 0
-  sampling uniforms are u = ((x>>8)+0.5)*2^-24 in (0,1).
+  sampling uniforms are u = ((x>>9)+0.5)*2^-23 in (0,1): 2^23 values, each exact
+  in float32 (k+0.5 < 2^23 needs 24 significant bits), so the GPU's fp32 u is
+  this float64 u bit for bit; min 2^-24, max 1-2^-24.
 """
 from __future__ import annotations
 
@@ -71,8 +73,9 @@ def linear_scale(fan_in: int) -> np.float32:
 
 
 def unit_open(x: np.ndarray) -> np.ndarray:
-    """Sampling uniform in (0,1): ((x>>8)+0.5)*2^-24, float64 (exact)."""
-    return ((x >> np.uint32(8)).astype(np.float64) + 0.5) * 2.0 ** -24
+    """Sampling uniform in (0,1): ((x>>9)+0.5)*2^-23, float64; every value is
+    exactly representable in float32 (the GPU computes the same number)."""
+    return ((x >> np.uint32(9)).astype(np.float64) + 0.5) * 2.0 ** -23
 
 
 def accept_uniform(seed: int, req: int, step: int, slot: int, rank: int) -> float:

@@ -211,7 +211,26 @@ __global__ void commit_kernel(CommitParams P) {
     if (req == 0) atomicAdd(P.step, 1);
   }
 }
+// test hook (hsd_debug_gumbel): pair i = one Gumbel-max draw over logits row row[i]
+// with the walk's own device function and Philox stream (seed, req, step, slot[i])
+__global__ void __launch_bounds__(WT) gumbel_debug_kernel(const float* logits, int ld, int V, float invT, uint32_t seed,
+                                                          uint32_t req, uint32_t step, const int32_t* row,
+                                                          const int32_t* slot, int32_t* out) {
+  __shared__ float red[32];
+  __shared__ int redi[32];
+  const int i = blockIdx.x;
+  const int b = gumbel_argmax(logits + (size_t)row[i] * ld, V, invT, seed, req, step, (uint32_t)slot[i], nullptr, 0,
+                              red, redi);
+  if (threadIdx.x == 0) out[i] = b;
+}
 }  // namespace
+
+void launch_gumbel_debug(const float* logits, int ld, int V, float temperature, uint32_t seed, int req, int step,
+                         int n, const int32_t* row, const int32_t* slot, int32_t* out, cudaStream_t st) {
+  if (n > 0)
+    gumbel_debug_kernel<<<n, WT, 0, st>>>(logits, ld, V, 1.0f / temperature, seed, (uint32_t)req, (uint32_t)step, row,
+                                          slot, out);
+}
 
 void launch_walk(const AcceptParams& P, int n_req, cudaStream_t st) {
   if (n_req > 0) launch_k(walk_kernel, n_req, WT, 0, st, P);

@@ -34,3 +34,5 @@ struct CommitParams {
 void launch_walk(const AcceptParams& P, int n_req, cudaStream_t st);
 void launch_compact(const CompactParams& P, int n_req, int layers, DType dt, cudaStream_t st);
 void launch_commit(const CommitParams& P, int n_req, cudaStream_t st);
+void launch_gumbel_debug(const float* logits, int ld, int V, float temperature, uint32_t seed, int req, int step,
+                         int n, const int32_t* row, const int32_t* slot, int32_t* out, cudaStream_t st);

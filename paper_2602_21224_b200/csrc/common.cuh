@@ -39,8 +39,11 @@ HSD_DEV u32x4 philox4x32_10(u32x4 c, uint32_t k0, uint32_t k1) {
 HSD_DEV uint32_t lane_of(const u32x4& v, int i) {
   return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
-// sampling uniform in (0,1): ((x>>8)+0.5)*2^-24 (exact in fp32)
-HSD_DEV float unit_open(uint32_t x) { return ((float)(x >> 8) + 0.5f) * 5.9604644775390625e-08f; }
+// sampling uniform in (0,1): ((x>>9)+0.5)*2^-23. k = x>>9 < 2^23, so k + 0.5 has at
+// most 24 significant bits and every step is exact in fp32: u in [2^-24, 1 - 2^-24],
+// never 0 or 1 (a 24-bit k + 0.5 would round to 2^24 at k = 2^24-1, i.e. u = 1 and
+// an infinite Gumbel score)
+HSD_DEV float unit_open(uint32_t x) { return ((float)(x >> 9) + 0.5f) * 1.1920928955078125e-07f; }
 
 #define TAG_ACCEPT 0x5EED0001u
 #define TAG_GUMBEL 0x5EED0002u

@@ -1412,6 +1412,16 @@ hsd_status hsd_debug_gemm(const void* A, int32_t lda, const void* W, int32_t ldw
   return cudaGetLastError() == cudaSuccess ? HSD_OK : HSD_ECUDA;
 }
 
+hsd_status hsd_debug_gumbel(const float* d_logits, int32_t ld, int32_t V, float temperature, uint64_t seed,
+                            int32_t req, int32_t step, int32_t n, const int32_t* d_row, const int32_t* d_slot,
+                            int32_t* d_out, void* stream) {
+  if (!d_logits || !d_row || !d_slot || !d_out || V < 1 || ld < V || n < 0 || !(temperature > 0.f)) return HSD_EINVAL;
+  launch_gumbel_debug(d_logits, ld, V, temperature, (uint32_t)seed, req, step, n, d_row, d_slot, d_out,
+                      (cudaStream_t)stream);
+  g_hsd_launches += 1;
+  return cudaGetLastError() == cudaSuccess ? HSD_OK : HSD_ECUDA;
+}
+
 hsd_status hsd_profile(hsd_ctx* ctx, int enable) {
   if (!ctx) return HSD_EINVAL;
   prof_collect(ctx);

@@ -27,7 +27,8 @@ SHARD_NONE, SHARD_NCCL, SHARD_SIM = 0, 1, 2
 EXPORTS = ["hsd_config_defaults", "hsd_init_model", "hsd_prefill", "hsd_set_plant", "hsd_build_tree",
            "hsd_force_tree", "hsd_verify_tree", "hsd_accept_and_compact", "hsd_step", "hsd_step_host",
            "hsd_sync", "hsd_get_tensor", "hsd_kernel_launches", "hsd_destroy", "hsd_last_error",
-           "hsd_profile", "hsd_profile_read", "hsd_debug_gemm", "hsd_nccl_unique_id", "hsd_admit", "hsd_kstamp", "hsd_kstamp_read", "hsd_kstamp_read_attention"]
+           "hsd_profile", "hsd_profile_read", "hsd_debug_gemm", "hsd_nccl_unique_id", "hsd_admit", "hsd_kstamp", "hsd_kstamp_read", "hsd_kstamp_read_attention",
+           "hsd_debug_gumbel"]
 PROFILE_CATEGORIES = ["gemm_verify", "gemm_draft", "head_verify", "head_draft", "attn_verify", "attn_draft",
                       "tree", "resample", "walk", "compact", "rowwise"]
 
@@ -96,6 +97,7 @@ def load(path: str = LIB_PATH):
         "hsd_kstamp": (I32, [VP, C.c_int]),
         "hsd_kstamp_read": (I32, [VP, P(C.c_double), P(I64), P(C.c_double), P(C.c_double)]),
         "hsd_kstamp_read_attention": (I32, [VP, P(C.c_double), P(I64)]),
+        "hsd_debug_gumbel": (I32, [VP, I32, I32, C.c_float, C.c_uint64, I32, I32, I32, VP, VP, VP, VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -304,6 +306,19 @@ def debug_gemm(A, W, C, accumulate=False, use_tc=False, stream=0):
                            2 if use_tc == "swiglu" else int(bool(use_tc)), stream)
     if s != HSD_OK:
         raise HsdError(s, "hsd_debug_gemm")
+
+
+def debug_gumbel(logits, rows, slots, temperature, seed, req, step, stream=0):
+    """hsd_debug_gumbel: Gumbel-max draws (the walk's device code) for logits rows
+    `rows` (torch CUDA fp32 [*, V]) with Philox slots `slots` (int32 CUDA tensors)."""
+    import torch
+    out = torch.empty(rows.numel(), dtype=torch.int32, device=logits.device)
+    s = load().hsd_debug_gumbel(logits.data_ptr(), logits.stride(0), logits.shape[1], float(temperature), int(seed),
+                                int(req), int(step), rows.numel(), rows.data_ptr(), slots.data_ptr(),
+                                out.data_ptr(), stream)
+    if s != HSD_OK:
+        raise HsdError(s, "hsd_debug_gumbel")
+    return out
 
 
 def nccl_unique_id() -> bytes:

@@ -208,10 +208,10 @@ def run_fullsize(name, n_steps_graph=2, n_checked=2, check_reqs=None, table_fp8=
             else:
                 o_acc, o_bonus = stochastic_walk(lin_g, logits, cfg.temperature, seed, r, step_no, wm)
                 # decisions the GPU takes in fp32 (R9) and the oracle in fp64: a Gumbel-perturbed
-                # score of magnitude ~10-20 carries ~1e-5 of fp32 rounding, and p_res = e^(v - lse)
-                # an lse summed over V = 128256 terms; 1e-4 is the fp32 flag margin of SURVEY
-                # 8(c.4) (1e-5 flaked: ~1 run in 6 saw an unflagged near-tie)
-                thr = 1e-4
+                # score of magnitude ~10-20 carries ~2e-6 of fp32 rounding. (A 1e-4 margin used
+                # to hide a sampling-uniform bug -- u rounded to 1 -- fixed in common.cuh and
+                # pinned by tests/test_gpu_sampling.py.)
+                thr = 1e-5
             g_acc = [int(s) for s in acc[r, :acc_n[r]]]
             if g_acc == o_acc and int(bonus[r]) == o_bonus:
                 stats["walk"] += 1

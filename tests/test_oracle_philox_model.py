@@ -140,3 +140,19 @@ def test_uniform_rows_equals_full_tensor_rows():
     np.testing.assert_array_equal(uniform_rows(3, 9, 23, linear_scale(23), rows), full[rows].astype(np.float64))
     fb = round_bf16(full)
     np.testing.assert_array_equal(uniform_rows(3, 9, 23, linear_scale(23), rows, "bf16"), fb[rows].astype(np.float64))
+
+
+def test_sampling_uniform_exact_in_fp32_and_open():
+    """unit_open over all 2^23 distinct values: strictly inside (0, 1), equal to
+    its float32 rounding (the GPU computes it in fp32), strictly increasing, and
+    -log(-log u) finite everywhere (reading R13's Gumbel-max)."""
+    from oracle.philox import unit_open
+    k = np.arange(2 ** 23, dtype=np.uint32)
+    u = unit_open(k << np.uint32(9))
+    assert u.min() > 0.0 and u.max() < 1.0
+    assert np.array_equal(u.astype(np.float32).astype(np.float64), u)
+    assert np.all(np.diff(u) > 0)
+    assert np.all(np.isfinite(-np.log(-np.log(u))))
+    # the low 9 bits of the word do not matter; extremes of the 32-bit word
+    assert unit_open(np.uint32(0xFFFFFFFF)) == 1.0 - 2.0 ** -24
+    assert unit_open(np.uint32(0)) == 2.0 ** -24
