@@ -40,7 +40,9 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3",
+                    help="BASELINE configs: c1 tiny, c2 7B b1, c3 8B b32 (default: the largest single-GPU "
+                         "config), c4 13B b64, c5 70B")
     ap.add_argument("--impl", default="hsd", choices=["hsd", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--simt", action="store_true", help="disable tcgen05 GEMMs (SIMT FFMA baseline)")
@@ -51,6 +53,11 @@ def parse():
     ap.add_argument("--table-fp8", action="store_true",
                     help="token-info table as e4m3 codes + per-row scale (NEXT-3, reading R25)")
     ap.add_argument("--batch", type=int, default=None, help="override the config's global batch")
+    ap.add_argument("--batch-per-gpu", type=int, default=None,
+                    help="weak scaling: this many requests per GPU (default: the config's batch for the "
+                         "weak-scaled configs c1/c2/c3, SURVEY 8(e))")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: split the config's global batch over the N ranks (default for c4/c5)")
     ap.add_argument("--vocab-shard", action="store_true",
                     help="vocab-sharded lm_head (SURVEY 8(e), greedy): NCCL over the N ranks; on one GPU the "
                          "simulated mode with --shards column shards")
@@ -146,6 +153,9 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
+METRIC = "accepted tokens/s per GPU and per-step verify latency at 1/2/4/8 B200"   # BASELINE.json
+
+
 # ---------------------------------------------------------------------------
 # CPU oracle baseline (test infrastructure; the only other place bench.py runs oracle/)
 # ---------------------------------------------------------------------------
@@ -156,34 +166,67 @@ class OracleRunner:
     layers (verify time scaled to the full depth), a short prompt, 1 request.
     Model construction and prefill are set-up, not timed."""
 
-    def __init__(self, cfg_name, seed, layers=2, prompt_len=16):
-        from synth import get_config, prompts, vocab_permutation
+    def __init__(self, cfg, seed, layers=2, prefill_len=16):
+        from synth import prompts, vocab_permutation
         from oracle.model import Model
         from oracle.table import TokenInfoTable
         from oracle.engine import Engine
-        self.cfg = get_config(cfg_name)
-        self.layers, self.prompt_len = layers, prompt_len
+        self.cfg = cfg
+        self.layers, self.prefill_len = layers, prefill_len
         m = Model(self.cfg, seed=seed, precision="bf16", layers=layers)
         perm = vocab_permutation(self.cfg.vocab, 0) if self.cfg.hot_tokens else None
         self.e = Engine(m, TokenInfoTable(m, hot_tokens=self.cfg.hot_tokens, perm=perm), self.cfg, seed=seed)
-        self.t_verify = 0.0
-        orig = self.e.verify
+        # verify time is split into its decoder layers (scaled to the full depth)
+        # and the lm_head products (once per slot at any depth, not scaled)
+        self.t_verify = self.t_head = 0.0
+        self.in_verify = False
+        orig, orig_logits = self.e.verify, m.logits
 
         def timed_verify(q, lin):
             t0 = time.perf_counter()
+            self.in_verify = True
             r = orig(q, lin)
+            self.in_verify = False
             self.t_verify += time.perf_counter() - t0
             return r
+
+        def timed_logits(H):
+            t0 = time.perf_counter()
+            r = orig_logits(H)
+            if self.in_verify:
+                self.t_head += time.perf_counter() - t0
+            return r
         self.e.verify = timed_verify
-        self.e.prefill(prompts(self.cfg, batch=1, length=prompt_len))
+        m.logits = timed_logits
+        # the config's own context length: the oracle prefills a short prefix (set-up,
+        # token by token) and the committed context is extended to prompt_len by
+        # tiling those K/V rows (the step's attention then reads a prompt_len-long
+        # cache; only the timing, never a value, is used)
+        C = max(self.cfg.prompt_len, prefill_len)
+        full = prompts(self.cfg, batch=1, length=C)[0]
+        self.e.prefill([full[:prefill_len]])
+        q = self.e.reqs[0]
+        P0 = prefill_len
+        first = q.tokens[P0]
+        for l in range(m.n_layers):
+            for j in range(P0, C):
+                q.kv[l][0].append(q.kv[l][0][j % P0])
+                q.kv[l][1].append(q.kv[l][1][j % P0])
+        for j in range(P0, C):
+            q.dkv[j] = q.dkv[1 + (j - 1) % (P0 - 1)]
+            q.H.append(q.H[j % P0])
+        q.tokens = [int(t) for t in full] + [first]
+        q.pend = [(q.H[C - 1], first, C)]
+        self.context = C
 
     def step(self):
         """-> (measured seconds, seconds extrapolated to the full depth, emitted tokens)"""
-        self.t_verify = 0.0
+        self.t_verify = self.t_head = 0.0
         t0 = time.perf_counter()
         emitted = sum(len(x) for x in self.e.step())
         dt = time.perf_counter() - t0
-        est = (dt - self.t_verify) + self.t_verify * self.cfg.layers / self.layers
+        t_layers = self.t_verify - self.t_head
+        est = (dt - t_layers) + t_layers * self.cfg.layers / self.layers
         return dt, est, emitted
 
     def threads(self):
@@ -193,7 +236,8 @@ class OracleRunner:
     def sample_text(self, steps):
         c = self.cfg
         return (f"oracle numpy float64, 1 request, {c.name} widths with {self.layers} of {c.layers} layers "
-                f"(verify time scaled x{c.layers / self.layers:g}), {self.prompt_len}-token prompt, {steps} step(s)")
+                f"(verify decoder-layer time scaled x{c.layers / self.layers:g}), {self.context}-token context "
+                f"({self.prefill_len} prefilled, the rest tiled K/V rows), {steps} step(s)")
 
 
 def reference_arm(args, cfg):
@@ -201,7 +245,7 @@ def reference_arm(args, cfg):
     if int(os.environ.get("RANK", "0")) != 0:
         return
     t_setup = time.perf_counter()
-    run = OracleRunner(args.config, args.seed)
+    run = OracleRunner(cfg, args.seed)
     t_setup = time.perf_counter() - t_setup
     for _ in range(args.warmup):
         run.step()
@@ -212,11 +256,14 @@ def reference_arm(args, cfg):
         meas_total += dt
         emitted += em
     value = emitted / est_total
-    line = {"impl": "reference", "metric": "accepted tokens/s per GPU (whole-job aggregate over N GPUs)",
+    _, _, gbatch, scaling, _ = plan_shard(cfg.name, cfg.batch, max(args.gpus, 1), 0, args.batch_per_gpu, args.strong)
+    line = {"impl": "reference", "metric": METRIC,
             "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": est_total / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": est_total / args.steps * 1e3, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "global_batch": cfg.batch},
+            "config": {"workload": cfg.name, "global_batch": gbatch,
+                       "oracle_sample": "one request per step (the oracle decodes requests one at a time, so its "
+                                        "throughput on the whole batch is this single-request rate)"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": run.threads(), "kind": "oracle",
                              "sample": run.sample_text(args.steps)},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -350,14 +397,26 @@ def gemm_chain(ctx, cfg, b, local, gbs, tfl, bound, reps=3):
                       "what": "verify GEMMs back to back (PDL chain, no events between launches)"}}
 
 
-def plan_shard(n_requests: int, world: int, rank: int):
-    """Batch sharding: contiguous request blocks when the batch
-    has at least one request per rank, else independent full replicas."""
+# c1/c2 (batch 1) run as independent replicas and c3 at 32 requests
+# per GPU -- weak scaling; c4 (64 global) and c5 (16 global) split a fixed batch
+# -- strong scaling
+WEAK_CONFIGS = ("c1", "c2", "c3")
+
+
+def plan_shard(cfg_name: str, batch: int, world: int, rank: int, batch_per_gpu=None, strong=False):
+    """Batch sharding: -> (lo, hi, global_batch, scaling, parallel).
+    Rank `rank` owns global requests [lo, hi) -- their prompts and their global
+    request ids (random streams) -- so no two ranks ever duplicate work.
+      weak:   batch_per_gpu requests per rank, global batch = world * batch_per_gpu
+      strong: the config's global batch split into contiguous blocks"""
     from synth import shard_requests
-    if n_requests >= world:
-        lo, hi = shard_requests(n_requests, world, rank)
-        return lo, hi, f"batch-shard x{world}"
-    return 0, n_requests, f"replicas x{world}"
+    if not strong and (batch_per_gpu or cfg_name in WEAK_CONFIGS):
+        bpg = batch_per_gpu or batch
+        return rank * bpg, (rank + 1) * bpg, world * bpg, "weak", f"batch-shard dp{world} ({bpg} requests/GPU)"
+    if batch < world:
+        raise SystemExit(f"strong scaling needs a global batch >= {world} GPUs (got {batch})")
+    lo, hi = shard_requests(batch, world, rank)
+    return lo, hi, batch, "strong", f"batch-shard dp{world} ({batch} global requests split)"
 
 
 def reduce_over_ranks(ms: float, emitted: float, device="cpu"):
@@ -392,7 +451,8 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    lo, hi, parallel = plan_shard(cfg.batch, world, rank)
+    lo, hi, gbatch, scaling, parallel = plan_shard(cfg.name, cfg.batch, world, rank, args.batch_per_gpu,
+                                                   args.strong)
     b = hi - lo
     N = cfg.steps_N
     max_ctx = cfg.prompt_len + (args.warmup + args.steps + 12) * (N + 1) + 16
@@ -416,7 +476,7 @@ def main():
                          tcgen05=not args.simt, flags=hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | hsd.FLAG_PLANTED |
                          (hsd.FLAG_TABLE_FP8 if args.table_fp8 else 0),
                          plant_rates=plant_rates, **shard_kw)
-    pr = prompts(cfg, batch=cfg.batch)[lo:hi]
+    pr = prompts(cfg, batch=gbatch)[lo:hi]
     ctx.prefill(pr)
     t_init = time.perf_counter() - t_init
 
@@ -514,7 +574,15 @@ def main():
                                   "algorithmic_bytes_per_launch": oby / max(on, 1),
                                   "flop_per_byte": round(ofl / oby, 1) if ofl else None}
         roof.update({"kernel": cat, "launches_per_step": pn / kp, "share_of_step": round(pms / total_prof, 4),
-                     "peak_source": src, "algorithmic_bytes_per_launch": pby / max(pn, 1),
+                     "peak_source": src + (" HBM copy GB/s" if ai < ridge else " sustained bf16 TFLOP/s (cuBLAS, "
+                                                                          "back to back for 4 s)"),
+                     "algorithmic_bytes_per_launch": pby / max(pn, 1),
+                     "algorithmic_flops_per_launch": pfl / max(pn, 1),
+                     "us_per_launch": round(pms * 1e3 / max(pn, 1), 2),
+                     "measured": f"CUDA events around every launch of the category on the ctx stream over {kp} "
+                                 "eager (un-graphed) steps right after the timed region; achieved = algorithmic "
+                                 "bytes (or flops) / mean launch duration",
+                     "traffic_source": f"profiles/traffic_{cfg.name}.json" if traffic else None,
                      "other_kernels_eager": roof_other})
 
     # ---- the dominant kernel's launch duration INSIDE graph-replayed steps: every
@@ -542,19 +610,22 @@ def main():
             except Exception:
                 pass
             ctx.kstamp(False)
-            eager = {k: roof[k] for k in ("achieved", "frac")}
-            eager["what"] = "CUDA events around each launch on the ctx stream, eager (un-graphed) step"
+            # supplementary only: the stamp window starts at the first return from
+            # griddepcontrol.wait, so it excludes the pre-wait weight prefetch and
+            # credits weights another kernel pulled into L2 -- an
+            # upper bound, not the reported `frac`
             if roof["bound"] == "hbm":
                 ach = k_by / (k_us * 1e-6) / 1e9
-                roof.update({"achieved": round(ach, 1), "frac": round(ach / gbs, 4)})
+                ig = {"achieved": round(ach, 1), "frac": round(ach / gbs, 4), "unit": "GB/s"}
             else:
                 ach = k_fl / (k_us * 1e-6) / 1e12
-                roof.update({"achieved": round(ach, 2), "frac": round(ach / tfl, 4)})
-            roof.update({"measured": "graph-replayed steps: per-launch %globaltimer stamps of every verify GEMM, from the first "
-                                     "return from griddepcontrol.wait (inputs ready) to the last CTA exit (hsd_kstamp); mean over launches and replays",
-                         "us_per_launch": round(k_us, 2), "stamped_launches": k_n,
-                         "algorithmic_bytes_per_launch": k_by, "eager": eager})
-        except Exception as ex:  # keep the eager numbers
+                ig = {"achieved": round(ach, 2), "frac": round(ach / tfl, 4), "unit": "TFLOP/s"}
+            ig.update({"us_per_launch": round(k_us, 2), "stamped_launches": k_n,
+                       "what": "upper bound: graph-replayed steps, per-launch %globaltimer stamps from the first "
+                               "return from griddepcontrol.wait to the last CTA exit (hsd_kstamp); excludes the "
+                               "pre-wait weight prefetch and credits L2-prefetched weights"})
+            roof["in_graph_stamps"] = ig
+        except Exception as ex:  # supplementary only
             roof["stamp_error"] = repr(ex)
 
     # ---- supplementary: the verify GEMMs as a back-to-back PDL chain (the same
@@ -570,17 +641,25 @@ def main():
     # ---- e2e: prefill from HOST prompts + K steps with host outputs (public API)
     e2e = None
     if not args.no_e2e:
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ctx.prefill(pr)
+        ctx.prefill(pr)                       # H2D: the prompts from host memory
+        t_pre = time.perf_counter()
         em_total = 0
         for _ in range(args.steps):
-            em, n = ctx.step_host()
+            em, n = ctx.step_host()           # D2H: the step's emitted tokens + counts
             em_total += int(n.sum())
-        t_e2e = time.perf_counter() - t0
-        e2e = {"value": em_total * max(world, 1) / t_e2e, "unit": "tokens/s",
+        t_end = time.perf_counter()
+        t_all, em_all = reduce_over_ranks(t_end - t0, float(em_total), device=f"cuda:{local}")
+        t_dec, _ = reduce_over_ranks(t_end - t_pre, 0.0, device=f"cuda:{local}")
+        e2e = {"value": round(em_all / t_all, 2), "unit": "tokens/s",
                "h2d_bytes_per_step": int(pr.nbytes / args.steps), "d2h_bytes_per_step": int(b * (N + 2) * 4),
-               "includes": "prefill of the prompts from host memory + K hsd_step_host calls"}
+               "includes": "host wall clock (max over ranks) of hsd_prefill from host prompts + K hsd_step_host "
+                           "calls (each a graph replay + D2H of the emitted tokens)",
+               "decode_only": round(em_all / t_dec, 2),
+               "prefill_s": round(t_all - t_dec, 3)}
 
     planted = None
     if not args.no_planted:
@@ -593,13 +672,12 @@ def main():
         except Exception as ex:
             planted = {"error": repr(ex)}
     step_s = ms_max / args.steps / 1e3
-    tau_curve = [{"tau": t, "tokens_per_s": round(cfg.batch * t / step_s if cfg.batch >= world else
-                                                   world * b * t / step_s, 1)} for t in (1.0, 2.0, 3.15, 4.0)]
+    tau_curve = [{"tau": t, "tokens_per_s": round(gbatch * t / step_s, 1)} for t in (1.0, 2.0, 3.15, 4.0)]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            run = OracleRunner(args.config, args.seed)
+            run = OracleRunner(cfg, args.seed)
             dt, est, em = run.step()
             cpu = {"value": em / est, "unit": "tokens/s", "cores": run.threads(), "kind": "oracle",
                    "sample": run.sample_text(1) + f" ({dt:.1f} s measured -> {est:.1f} s/step extrapolated)"}
@@ -609,18 +687,20 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": "accepted tokens/s per GPU (whole-job aggregate over N GPUs)",
-            "value": round(value, 2), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC,
+            "value": round(value, 2), "unit": "tokens/s",
+            "value_is": "whole-job aggregate: accepted tokens emitted by all N ranks / max-over-ranks device time",
+            "per_gpu_value": round(value / world, 2), "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": cfg.name, "global_batch": cfg.batch, "per_gpu_batch": b,
+            "scaling": scaling, "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": cfg.name, "global_batch": gbatch, "per_gpu_batch": b,
                        "prompt_len": cfg.prompt_len, "tree": f"N{N} k{cfg.branch_k} B{cfg.budget_B} Br{cfg.resample_budget_Br}",
                        "accept": cfg.accept, "parallelism": parallel, "gemm": "simt" if args.simt else "tcgen05",
                        "l2": "no flush: every step streams >13 GB of weights (>> 126 MB L2)",
                        "weights": "Philox random-init (no trained weights)",
                        "table": "fp8 e4m3 + row scale" if args.table_fp8 else "bf16",
                        "lm_head": shard_desc},
-            "tau": round(emitted_all / (args.steps * cfg.batch if cfg.batch >= world else args.steps * world * b), 4),
+            "tau": round(emitted_all / (args.steps * gbatch), 4),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "tau_curve": tau_curve, "planted": planted,
             "step_latency_ms": {"median": round(float(np.median(step_ms)), 4),

@@ -126,8 +126,13 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
 
 /* Prefill `n_req` (<= max_batch) requests. h_tokens: HOST row-major
  * [n_req, stride] int32 prompt tokens, request r uses h_tokens[r*stride ...
- * + h_lens[r]). h_lens: HOST [n_req], 2 <= len, len + max_new + N + T <=
- * max_ctx. Runs the target causally over each prompt (writes KV), picks the
+ * + h_lens[r]). h_lens: HOST [n_req], 2 <= len <= max_ctx. Capacity: the KV
+ * pool holds max_pos >= max_ctx + T + N positions per slot; a step writes KV up
+ * to p + T - 1 and commits at most N + 1 tokens, so hsd_step / hsd_build_tree
+ * return HSD_ESTATE (nothing launched) once a slot's committed length p could
+ * reach max_pos - T (the host tracks p + (N + 1) per step and re-reads the
+ * device's p when that bound gets tight). Slot r's global request id (random
+ * streams, R13 / R22 / R24) is req_offset + r. Runs the target causally over each prompt (writes KV), picks the
  * first token (argmax, or Gumbel sample in stochastic mode, R22), and runs the
  * draft layer over pairs (H_{j-1}, t_j), j = 1..len-1 (R1). d_first: DEVICE
  * [n_req] int32 output (may be NULL). Resets the step counter.              */
@@ -143,8 +148,12 @@ hsd_status hsd_prefill(hsd_ctx* ctx, int32_t n_req, const int32_t* h_tokens, int
  * graph stays valid (no shape change). d_first: DEVICE [n_req] int32 or NULL
  * (entry `slot` written). Synchronous. HSD_ESTATE before hsd_prefill or inside a
  * staged step; HSD_EUNSUP with the NCCL vocab-sharded head (every shard would have
- * to admit in lockstep).                                                      */
-hsd_status hsd_admit(hsd_ctx* ctx, int32_t slot, const int32_t* h_tokens, int32_t len, int32_t* d_first);
+ * to admit in lockstep). req_id (>= 0, else HSD_EINVAL): the admitted request's
+ * GLOBAL id for every random stream (first-token Gumbel, acceptance uniforms,
+ * planting) -- the caller gives each admitted request a fresh id, so it never
+ * reuses the noise of the slot's earlier requests.                             */
+hsd_status hsd_admit(hsd_ctx* ctx, int32_t slot, const int32_t* h_tokens, int32_t len, int32_t req_id,
+                     int32_t* d_first);
 
 /* Planted mode only: HOST row-major [n_req, stride] greedy continuation tokens
  * indexed by absolute position (R24). Copied. */

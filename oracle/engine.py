@@ -54,6 +54,7 @@ class Engine:
         self.req_offset = req_offset
         self.plant, self.plant_rates = plant, plant_rates
         self.reqs = []
+        self.req_ids = []    # global request id per slot (random streams)
         self.step_idx = 0
         self.trace = []      # per step, per request: dict of intermediate results
 
@@ -63,9 +64,25 @@ class Engine:
         first token = argmax (greedy) or a Gumbel sample (slot 0, step 0) unless
         `first_tokens` forces it (lockstep tests); then the draft layer over
         pairs j = 1..P0-1; pair P0 stays pending."""
+        self.reqs, self.req_ids = [], []
+        return [self._prefill_one(prompt, self.req_offset + r,
+                                  None if first_tokens is None else first_tokens[r])
+                for r, prompt in enumerate(prompts)]
+
+    def admit(self, slot, prompt, req_id, first_token=None):
+        """Continuous batching (the serving layer around the path): slot
+        `slot` restarts with a new prompt under the fresh global request id
+        `req_id` (its random streams); the other slots keep their state."""
+        q_old, id_old = self.reqs, self.req_ids
+        t1 = self._prefill_one(prompt, req_id, first_token)
+        q_new = self.reqs.pop()
+        self.req_ids.pop()
+        q_old[slot], id_old[slot] = q_new, req_id
+        return t1
+
+    def _prefill_one(self, prompt, req_id, first_token):
         m = self.m
-        first = []
-        for r, prompt in enumerate(prompts):
+        if True:
             q = Request(m.n_layers)
             logits = None
             for pos, t in enumerate(prompt):
@@ -74,12 +91,12 @@ class Engine:
                     q.kv[l][0].append(k); q.kv[l][1].append(v)
                 q.H.append(H)
                 q.tokens.append(int(t))
-            if first_tokens is not None:
-                t1 = int(first_tokens[r])
+            if first_token is not None:
+                t1 = int(first_token)
             elif self.accept == "greedy":
                 t1 = argmax_lowest(logits)
             else:
-                U = gumbel_uniforms(self.seed, self.req_offset + r, 0, 0, m.cfg.vocab)
+                U = gumbel_uniforms(self.seed, req_id, 0, 0, m.cfg.vocab)
                 t1 = gumbel_argmax(logits, self.T, U)[0]
             q.tokens.append(t1)
             P0 = len(prompt)
@@ -87,8 +104,8 @@ class Engine:
             self._draft_prefill(q, pairs[:-1])
             q.pend = pairs[-1:]
             self.reqs.append(q)
-            first.append(t1)
-        return first
+            self.req_ids.append(req_id)
+        return t1
 
     def _draft_prefill(self, q, pairs):
         h = None
@@ -116,15 +133,26 @@ class Engine:
             chain.append(h)
         return chain
 
-    def verify(self, q, lin):
-        """S2: per-slot plain forward of its root path over the cache."""
+    def verify(self, q, lin, slots=None):
+        """S2: per-slot plain forward of its root path over the cache. `slots`
+        (tests at full size): only those slots and their ancestors are computed;
+        the other rows of H / logits stay zero."""
         m = self.m
         p = len(q.tokens) - 1
         Tn = lin["T"]
+        need = set(range(Tn))
+        if slots is not None:
+            need = set()
+            for u in slots:
+                while u >= 0 and u not in need:
+                    need.add(u)
+                    u = int(lin["par"][u])
         path_rows = [None] * Tn
         H = np.zeros((Tn, m.cfg.hidden))
         logits = np.zeros((Tn, m.cfg.vocab))
         for u in range(Tn):
+            if u not in need:
+                continue
             par = int(lin["par"][u])
             prev = path_rows[par] if par >= 0 else [([], []) for _ in range(m.n_layers)]
             ctx = [(q.kv[l][0] + prev[l][0], q.kv[l][1] + prev[l][1]) for l in range(m.n_layers)]
@@ -149,13 +177,13 @@ class Engine:
                 tree = T.prune(T.fuse(fresh, q.pending), B + Br)
             lin = T.linearize(tree)
             if self.plant is not None:
-                plant_path(lin, self.plant[ri], p, self.plant_rates, self.seed, self.req_offset + ri,
+                plant_path(lin, self.plant[ri], p, self.plant_rates, self.seed, self.req_ids[ri],
                            self.step_idx)
             H, logits, path_rows = self.verify(q, lin)                    # S2
             if self.accept == "greedy":                                   # S3
                 acc, bonus = greedy_walk(lin, logits, mg)
             else:
-                acc, bonus = stochastic_walk(lin, logits, self.T, self.seed, self.req_offset + ri,
+                acc, bonus = stochastic_walk(lin, logits, self.T, self.seed, self.req_ids[ri],
                                              self.step_idx, mg)
             mm = len(acc)
             last = acc[-1] if acc else 0                                   # S4

@@ -20,6 +20,7 @@ then token-identical by construction when the method is lossless.
 from __future__ import annotations
 
 import math
+import os
 import numpy as np
 
 from .philox import uniform_weights, linear_scale, round_bf16
@@ -85,10 +86,22 @@ class Model:
             self.w2 = self._w(TID_W2, (V, d), linear_scale(d))      # paper W_2 = w2^T (d x |V|)
 
     def _w(self, tid, shape, scale):
-        w = uniform_weights(self.seed, tid, shape, scale)
-        if self.precision == "bf16":
-            w = round_bf16(w)
-        return w.astype(np.float64)
+        w = uniform_weights(self.seed, tid, shape, scale).reshape(-1)
+        out = np.empty(w.size, dtype=np.float64)
+
+        def conv(e0, e1):   # elementwise: bf16 rounding (bf16 mode) then exact widening
+            x = w[e0:e1]
+            out[e0:e1] = round_bf16(x) if self.precision == "bf16" else x
+        step = 1 << 22
+        ranges = [(e0, min(w.size, e0 + step)) for e0 in range(0, w.size, step)]
+        if len(ranges) <= 1:
+            for r in ranges:
+                conv(*r)
+        else:
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(max_workers=min(len(ranges), os.cpu_count() or 1)) as ex:
+                list(ex.map(lambda r: conv(*r), ranges))
+        return out.reshape(shape)
 
     def _layer(self, tid):
         c = self.cfg

@@ -57,14 +57,36 @@ def raw_stream(seed: int, tensor_id: int, count: int) -> np.ndarray:
     return words[:count]
 
 
+_CHUNK = 1 << 22      # elements per worker chunk (a multiple of 4: whole Philox blocks)
+
+
+def _uniform_chunk(seed, tensor_id, scale, e0, e1, out):
+    """Elements [e0, e1) of uniform_weights' stream into out[e0:e1] (e0 % 4 == 0)."""
+    idx = np.arange(e0 // 4, (e1 + 3) // 4, dtype=np.uint64)
+    words = np.stack(philox4x32_10(idx & MASK, idx >> np.uint64(32), 0, 0, seed & 0xFFFFFFFF, tensor_id),
+                     axis=1).reshape(-1)[:e1 - e0]
+    u = (words >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -24)
+    t = np.float32(2.0) * u - np.float32(1.0)        # exact
+    out[e0:e1] = (np.float32(scale) * t).astype(np.float32)
+
+
 def uniform_weights(seed: int, tensor_id: int, shape, scale: np.float32) -> np.ndarray:
     """w = s*(2u-1), u=(x>>8)*2^-24, every step in float32 (exact except the one
-    correctly-rounded multiply). Returned as float32."""
+    correctly-rounded multiply). Returned as float32. Large tensors are generated
+    in independent element ranges on a thread pool (numpy releases the GIL); each
+    element's value depends only on its own counter, so the result is the same."""
     count = int(np.prod(shape))
-    x = raw_stream(seed, tensor_id, count)
-    u = (x >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -24)
-    t = np.float32(2.0) * u - np.float32(1.0)        # exact
-    return (np.float32(scale) * t).astype(np.float32).reshape(shape)
+    out = np.empty(count, dtype=np.float32)
+    ranges = [(e0, min(count, e0 + _CHUNK)) for e0 in range(0, count, _CHUNK)]
+    if len(ranges) <= 1:
+        for e0, e1 in ranges:
+            _uniform_chunk(seed, tensor_id, scale, e0, e1, out)
+    else:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(len(ranges), os.cpu_count() or 1)) as ex:
+            list(ex.map(lambda r: _uniform_chunk(seed, tensor_id, scale, r[0], r[1], out), ranges))
+    return out.reshape(shape)
 
 
 def linear_scale(fan_in: int) -> np.float32:

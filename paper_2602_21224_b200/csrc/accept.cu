@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(WT) walk_kernel(AcceptParams P) {
     __syncthreads();
   } else {
     const float invT = 1.0f / P.temperature;
-    const uint32_t rq = (uint32_t)(P.req_offset + req), st = (uint32_t)(*P.step);
+    const uint32_t rq = (uint32_t)P.req_id[req], st = (uint32_t)(*P.step);
     while (true) {
       int cur = cur_sh;
       const float* x = P.logits + ((size_t)req * T + cur) * P.V;

@@ -7,7 +7,7 @@ struct AcceptParams {
   int N, t_max, V;
   float temperature;
   uint32_t seed;
-  int req_offset;
+  const int32_t* req_id;    // [b] global request id per slot (random streams)
   const int32_t *t_tok, *t_par, *t_n;
   const int32_t* argmax;    // [b, t_max] (greedy)
   const float* logits;      // [b, t_max, V] (stochastic)

@@ -243,6 +243,12 @@ struct hsd_ctx {
   int32_t* block_table = nullptr;
   // state
   int32_t *p, *root_tok, *n_pend, *pend_tok, *step;
+  int32_t* req_id = nullptr;       // [maxb] global request id per slot (random streams)
+  std::vector<int32_t> req_id_h;   // host copy
+  // host-side bound on every slot's committed length p: p grows by at most N + 1
+  // per step, and a step writes target / draft KV up to p + T - 1, so a step is
+  // refused (HSD_ESTATE) once p_hi + T would pass the KV capacity max_pos
+  std::vector<int64_t> p_hi;
   float* pend_H;
   int* err;
   int32_t *pt_n, *pt_tok, *pt_par, *pt_depth;
@@ -404,11 +410,17 @@ static void gemm(hsd_ctx* c, const void* A, int lda, const void* Wt, int ldw, fl
   if (cat < 0) cat = c->pass_verify ? P_GEMM_VERIFY : P_GEMM_DRAFT;
   Prof pf(c, cat, (double)N * K * c->esz + (double)M * K * c->esz + (double)M * N * 4 * (acc ? 2 : 1),
           2.0 * M * N * K);
-  if (c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, N, K, lda, ldw)) {
+  // TMA needs 16-byte aligned operand bases; gemm_tc_bf16 returns 0 (nothing launched)
+  // when it cannot encode a tensor map -- both fall back to the SIMT kernel
+  const bool aligned = (((uintptr_t)A | (uintptr_t)Wt) & 15) == 0;
+  int launched = 0;
+  if (c->use_tc && c->dt == DT_BF16 && aligned && gemm_tc_supported(M, N, K, lda, ldw)) {
     kstamp_next(c, cat, (double)N * K * c->esz + (double)M * K * c->esz + (double)M * N * 4 * (acc ? 2 : 1),
                 2.0 * M * N * K);
-    g_hsd_launches += gemm_tc_bf16((const bf16*)A, lda, (const bf16*)Wt, ldw, C, ldc, M, N, K, acc, c->st, c_zeroed);
-  } else {
+    launched = gemm_tc_bf16((const bf16*)A, lda, (const bf16*)Wt, ldw, C, ldc, M, N, K, acc, c->st, c_zeroed);
+    g_hsd_launches += launched;
+  }
+  if (launched == 0) {
     gemm_simt(A, lda, Wt, ldw, c->dt, C, ldc, M, N, K, acc, c->st);
     g_hsd_launches += 1;
   }
@@ -596,7 +608,7 @@ static void stage_build(hsd_ctx* c) {
   P.plant = (c->cfg.flags & HSD_FLAG_PLANTED) ? c->plant : nullptr;
   P.plant_stride = c->plant_stride;
   for (int i = 0; i < HSD_MAX_PLANT_DEPTH_DEV; ++i) P.plant_rates[i] = c->cfg.plant_rates[i];
-  P.seed = (uint32_t)c->cfg.seed; P.req_offset = c->cfg.req_offset; P.err = c->err;
+  P.seed = (uint32_t)c->cfg.seed; P.req_id = c->req_id; P.err = c->err;
   P.pf = L2Pf{nullptr, 0ull, 0};
   if (g_l2pf_cap && !c->layers.empty()) {   // verify layer 0's QKV weights stream next
     PfScope l2(c->layers[0].wqkv, (size_t)c->qkvd * n * c->esz, 0, g_l2pf_cap, 32);
@@ -634,7 +646,7 @@ static void stage_accept(hsd_ctx* c, int32_t* d_emitted, int32_t* d_n) {
   AcceptParams A{};
   A.mode = c->cfg.accept_mode == HSD_STOCHASTIC ? 1 : 0;
   A.N = c->N; A.t_max = c->T; A.V = c->V; A.temperature = c->cfg.temperature;
-  A.seed = (uint32_t)c->cfg.seed; A.req_offset = c->cfg.req_offset;
+  A.seed = (uint32_t)c->cfg.seed; A.req_id = c->req_id;
   A.t_tok = c->t_tok; A.t_par = c->t_par; A.t_n = c->t_n; A.argmax = c->argmax; A.logits = c->logits;
   A.step = c->step;
   A.acc_n = c->acc_n; A.acc_slots = c->acc_slots; A.bonus = c->bonus; A.emitted = c->emitted;
@@ -654,7 +666,7 @@ static void stage_accept(hsd_ctx* c, int32_t* d_emitted, int32_t* d_n) {
   P.zero_table = (c->cfg.flags & HSD_FLAG_ZERO_TABLE) ? 1 : 0;
   P.L = c->draft_logits; P.table = c->table; P.tdt = c->dt; P.tscale = c->table_scale; P.perm = c->perm_d; P.rank_of = c->rank_d;
   P.pt_n = c->pt_n; P.pt_tok = c->pt_tok; P.pt_par = c->pt_par; P.pt_depth = c->pt_depth; P.pt_lj = c->pt_lj;
-  P.acc_n = c->acc_n; P.bonus = c->bonus; P.err = c->err;
+  P.acc_n = c->acc_n; P.bonus = c->bonus; P.err = c->err; P.req_id = c->req_id;
   P.pf = L2Pf{nullptr, 0ull, 0};
   if (g_l2pf_cap) {   // the next step's draft prefill GEMM streams W_fc first
     PfScope l2(c->fc, (size_t)2 * c->n * c->n * c->esz, 0, g_l2pf_cap, 32);
@@ -714,8 +726,11 @@ static hsd_status run_stage(hsd_ctx* ctx, int idx, F&& body) {
 // forward over the prompt (KV + H), first token, draft prefill over the prompt's
 // (H_{j-1}, t_j) pairs. Touches only slot r's state, so it also admits a new request
 // into a live batch (hsd_admit, continuous batching).
-static hsd_status prefill_one(hsd_ctx* ctx, int r, const int32_t* pt, int P0, int32_t* d_first) {
+static hsd_status prefill_one(hsd_ctx* ctx, int r, const int32_t* pt, int P0, int32_t* d_first, int32_t req_g) {
   hsd_ctx* c = ctx;
+  c->req_id_h[r] = req_g;
+  c->p_hi[r] = P0;
+  CU(cudaMemcpyAsync(c->req_id + r, &c->req_id_h[r], 4, cudaMemcpyHostToDevice, c->st));
   const int n = c->n, N = c->N;
   std::vector<int32_t> tok, pos, kvpos, req, klo, khi, slot;
   // target causal forward over the prompt, chunked
@@ -749,7 +764,7 @@ static hsd_status prefill_one(hsd_ctx* ctx, int r, const int32_t* pt, int P0, in
   gemm(c, c->a, n, c->head, n, c->logits, c->V, 1, c->V, n, false);
   launch_k(first_token_kernel, 1, 512, 0, c->st, c->logits, c->V, c->cfg.accept_mode == HSD_STOCHASTIC ? 1 : 0,
                                            1.0f / c->cfg.temperature, (uint32_t)c->cfg.seed,
-                                           c->cfg.req_offset + r, r, Hlast, n, P0, N, c->pend_H, c->pend_tok,
+                                           req_g, r, Hlast, n, P0, N, c->pend_H, c->pend_tok,
                                            c->n_pend, c->root_tok, c->p, d_first);
   g_hsd_launches += 2;
   // draft prefill over pairs j = 1..P0-1: x_j = W_fc [H_{j-1}; E(t_j)] (R1)
@@ -1027,6 +1042,7 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     const int b = c->maxb, T = c->T, N = c->N, Br1 = c->Br + 1;
     auto I = [&](size_t cnt) { return (int32_t*)A(cnt * 4); };
     auto F = [&](size_t cnt) { return (float*)A(cnt * 4); };
+    c->req_id = I(b); c->req_id_h.assign(b, 0); c->p_hi.assign(b, 0);
     c->p = I(b); c->root_tok = I(b); c->n_pend = I(b); c->pend_tok = I((size_t)b * (N + 1)); c->step = I(1);
     c->pend_H = F((size_t)b * (N + 1) * n); c->err = (int*)I(1);
     c->pt_n = I(b); c->pt_tok = I((size_t)b * Br1); c->pt_par = I((size_t)b * Br1); c->pt_depth = I((size_t)b * Br1);
@@ -1125,7 +1141,7 @@ hsd_status hsd_prefill(hsd_ctx* ctx, int32_t n_req, const int32_t* h_tokens, int
   CU(cudaMemcpyAsync(c->pt_n, ones.data(), 4 * n_req, cudaMemcpyHostToDevice, c->st));
   CU(cudaStreamSynchronize(c->st));
   for (int r = 0; r < n_req; ++r) {
-    const hsd_status st = prefill_one(c, r, h_tokens + (size_t)r * stride, h_lens[r], d_first);
+    const hsd_status st = prefill_one(c, r, h_tokens + (size_t)r * stride, h_lens[r], d_first, c->cfg.req_offset + r);
     if (st != HSD_OK) return st;
   }
   CU(cudaStreamSynchronize(c->st));
@@ -1134,7 +1150,28 @@ hsd_status hsd_prefill(hsd_ctx* ctx, int32_t n_req, const int32_t* h_tokens, int
   return HSD_OK;
 }
 
-hsd_status hsd_admit(hsd_ctx* ctx, int32_t slot, const int32_t* h_tokens, int32_t len, int32_t* d_first) {
+// capacity contract (include/hsd.h): a step writes KV rows up to p + T - 1 and the
+// tree's RoPE positions up to p + N; p itself grows by at most N + 1 per step
+static hsd_status check_capacity(hsd_ctx* c) {
+  bool tight = false;
+  for (int r = 0; r < c->b; ++r) tight |= c->p_hi[r] + c->T > c->max_pos;
+  if (tight) {   // the bound assumes N + 1 tokens per step: refresh it from the device's p
+    std::vector<int32_t> p(c->b);
+    if (cudaStreamSynchronize(c->st) != cudaSuccess ||
+        cudaMemcpy(p.data(), c->p, 4 * c->b, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return fail(c, HSD_ECUDA, "check_capacity: reading p");
+    for (int r = 0; r < c->b; ++r) c->p_hi[r] = p[r];
+  }
+  for (int r = 0; r < c->b; ++r)
+    if (c->p_hi[r] + c->T > c->max_pos)
+      return fail(c, HSD_ESTATE, "context capacity exhausted: slot " + std::to_string(r) + " may hold " +
+                                     std::to_string(c->p_hi[r]) + " committed tokens, a step needs " +
+                                     std::to_string(c->T) + " more KV rows of " + std::to_string(c->max_pos));
+  return HSD_OK;
+}
+
+hsd_status hsd_admit(hsd_ctx* ctx, int32_t slot, const int32_t* h_tokens, int32_t len, int32_t req_id,
+                     int32_t* d_first) {
   if (!ctx) return HSD_EINVAL;
   hsd_ctx* c = ctx;
   if (c->b < 1) return fail(c, HSD_ESTATE, "hsd_admit before hsd_prefill");
@@ -1147,7 +1184,8 @@ hsd_status hsd_admit(hsd_ctx* ctx, int32_t slot, const int32_t* h_tokens, int32_
   const int32_t one = 1;   // no pending re-sampled tree for the new request
   CU(cudaMemcpyAsync(c->pt_n + slot, &one, 4, cudaMemcpyHostToDevice, c->st));
   CU(cudaStreamSynchronize(c->st));
-  const hsd_status st = prefill_one(c, slot, h_tokens, len, d_first);
+  if (req_id < 0) return fail(c, HSD_EINVAL, "req_id must be >= 0");
+  const hsd_status st = prefill_one(c, slot, h_tokens, len, d_first, req_id);
   if (st != HSD_OK) return st;
   CU(cudaStreamSynchronize(c->st));
   CU(cudaGetLastError());
@@ -1186,6 +1224,7 @@ static void fill_verify_view(hsd_ctx* c, hsd_verify_view* v) {
 hsd_status hsd_build_tree(hsd_ctx* ctx, hsd_tree_view* out) {
   if (!ctx) return HSD_EINVAL;
   if (ctx->b < 1) return fail(ctx, HSD_ESTATE, "hsd_build_tree before hsd_prefill");
+  { const hsd_status s = check_capacity(ctx); if (s != HSD_OK) return s; }
   { const hsd_status s = run_stage(ctx, 0, [&] { stage_build(ctx); }); if (s != HSD_OK) return s; }
   ctx->stage = 1;
   fill_tree_view(ctx, out);
@@ -1236,6 +1275,7 @@ hsd_status hsd_accept_and_compact(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n
   if (d_emitted)
     CU(cudaMemcpyAsync(d_emitted, ctx->emitted, sizeof(int32_t) * ctx->b * (ctx->N + 1), cudaMemcpyDeviceToDevice, ctx->st));
   if (d_n_emitted) CU(cudaMemcpyAsync(d_n_emitted, ctx->n_emitted, sizeof(int32_t) * ctx->b, cudaMemcpyDeviceToDevice, ctx->st));
+  for (int r = 0; r < ctx->b; ++r) ctx->p_hi[r] += ctx->N + 1;
   ctx->stage = 0;
   return HSD_OK;
 }
@@ -1245,6 +1285,8 @@ hsd_status hsd_step(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n_emitted) {
   hsd_ctx* c = ctx;
   if (c->b < 1) return fail(c, HSD_ESTATE, "hsd_step before hsd_prefill");
   if (c->stage != 0) return fail(c, HSD_ESTATE, "hsd_step in the middle of a staged step");
+  { const hsd_status s = check_capacity(c); if (s != HSD_OK) return s; }
+  for (int r = 0; r < c->b; ++r) c->p_hi[r] += c->N + 1;
   if (c->prof_on) {
     // profiled steps run eagerly so every launch is bracketed by CUDA events
     stage_build(c); stage_verify(c); stage_accept(c, d_emitted, d_n_emitted);

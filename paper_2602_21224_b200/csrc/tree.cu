@@ -542,7 +542,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(Tre
         if (P.t_tok[req * T + s] == want && hit < 0) hit = s;
       }
       if (first < 0) break;
-      u32x4 c = {(uint32_t)d, (uint32_t)step, (uint32_t)(P.req_offset + req), 0u};
+      u32x4 c = {(uint32_t)d, (uint32_t)step, (uint32_t)P.req_id[req], 0u};
       u32x4 r = philox4x32_10(c, P.seed, TAG_PLANT);
       if (!(unit_open(r.x) < P.plant_rates[d - 1])) break;
       cur = hit >= 0 ? hit : first;

@@ -29,7 +29,7 @@ struct TreeParams {
   int plant_stride;
   float plant_rates[HSD_MAX_PLANT_DEPTH_DEV];
   uint32_t seed;
-  int req_offset;
+  const int32_t* req_id;     // [b] global request id per slot (plant stream)
   int* err;
   L2Pf pf;                   // weights of a later GEMM to prefetch into L2 (common.cuh)
   unsigned long long* trace; // debug phase trace (HSD_TREE_TRACE) or null

@@ -93,7 +93,7 @@ def load(path: str = LIB_PATH):
         "hsd_debug_gemm": (I32, [VP, I32, VP, I32, VP, I32, I32, I32, I32, I32, I32, I32, VP]),
         "hsd_profile_read": (I32, [VP, C.c_char_p, P(C.c_double), P(I64), P(C.c_double), P(C.c_double)]),
         "hsd_nccl_unique_id": (I32, [P(C.c_uint8)]),
-        "hsd_admit": (I32, [VP, I32, P(I32), I32, VP]),
+        "hsd_admit": (I32, [VP, I32, P(I32), I32, I32, VP]),
         "hsd_kstamp": (I32, [VP, C.c_int]),
         "hsd_kstamp_read": (I32, [VP, P(C.c_double), P(I64), P(C.c_double), P(C.c_double)]),
         "hsd_kstamp_read_attention": (I32, [VP, P(C.c_double), P(I64)]),
@@ -194,11 +194,12 @@ class Context:
                                          C.c_void_p(d_first or 0)))
         self.batch = tokens.shape[0]
 
-    def admit(self, slot, tokens, d_first=None):
+    def admit(self, slot, tokens, req_id, d_first=None):
         """hsd_admit: a new (ragged-length) prompt into batch slot `slot`; the
-        other slots keep decoding (continuous batching)."""
+        other slots keep decoding (continuous batching). `req_id` is the new
+        request's global id for its random streams (must be fresh)."""
         t, tp = _i32(np.asarray(tokens, dtype=np.int32).ravel())
-        self._check(self.lib.hsd_admit(self.h, int(slot), tp, t.size, C.c_void_p(d_first or 0)))
+        self._check(self.lib.hsd_admit(self.h, int(slot), tp, t.size, int(req_id), C.c_void_p(d_first or 0)))
 
     def set_plant(self, plant):
         plant = np.atleast_2d(np.asarray(plant, dtype=np.int32))

@@ -14,8 +14,13 @@ METRICS = [   # (metric, column, scale applied to the value converted to seconds
     ("dram__bytes_read.sum", "dram_rd_MB", 1e-6),
     ("dram__bytes_write.sum", "dram_wr_MB", 1e-6),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_%", 1),
+    # tcgen05 (UTCHMMA) issue is counted by the tensor pipe's HMMA sub-pipe; the
+    # legacy tensor_% / op-path columns do not see tcgen05 MMAs on sm_100
+    ("sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed", "hmma_subpipe_%", 1),
+    ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed", "tc_pipe_%", 1),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tmem_%", 1),
+    ("sm__inst_executed_pipe_tensor_subpipe_hmma.sum", "utchmma_inst", 1),
     ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor_%", 1),
-    ("sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed", "bf16_ops_%", 1),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm_%", 1),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occ_%", 1),
     ("launch__registers_per_thread", "regs", 1),

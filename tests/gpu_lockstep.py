@@ -86,6 +86,7 @@ class Lockstep:
         self.max_err = {"L": 0.0, "verify": 0.0, "kv": 0.0}
         self.step_no = 0
         self.emitted = [[] for _ in prompts]
+        self.req_ids = list(range(len(prompts)))     # global request id per slot (ctx req_offset 0)
 
     def start(self):
         import torch
@@ -98,14 +99,31 @@ class Lockstep:
         for r in range(b):
             self.emitted[r].append(int(first[r]))
         # oracle first token (plain argmax / Gumbel sample)
-        e = self._engine(r_off=0)
+        e = Engine(self.m, self.table, self.cfg, seed=self.seed, accept=self.accept, temperature=self.T)
         ofirst = e.prefill(self.prompts)
         return first, ofirst
 
-    def _engine(self, r_off):
+    def admit(self, slot, prompt, req_id):
+        """hsd_admit a new request into `slot` under global id `req_id`; returns
+        (GPU first token, oracle first token) of the admitted request."""
+        import torch
+        d_first = torch.zeros(len(self.prompts), dtype=torch.int32, device="cuda")
+        prompt = [int(t) for t in prompt]
+        self.ctx.admit(slot, prompt, req_id, d_first=d_first.data_ptr())
+        first = int(d_first.cpu()[slot])
+        e = Engine(self.m, self.table, self.cfg, seed=self.seed, accept=self.accept, temperature=self.T)
+        e.prefill([self.prompts[0]])
+        ofirst = e.admit(0, prompt, req_id)
+        self.prompts[slot] = prompt
+        self.tokens[slot] = prompt + [first]
+        self.emitted[slot] = [first]
+        self.req_ids[slot] = req_id
+        return first, ofirst
+
+    def _engine(self, r):
         return Engine(self.m, self.table, self.cfg, seed=self.seed, accept=self.accept,
-                      temperature=self.T, resample=self.resample, fusion=self.fusion, req_offset=r_off,
-                      plant=None if self.plant is None else [self.plant[r_off]], plant_rates=self.plant_rates)
+                      temperature=self.T, resample=self.resample, fusion=self.fusion, req_offset=self.req_ids[r],
+                      plant=None if self.plant is None else [self.plant[r]], plant_rates=self.plant_rates)
 
     def _margins_ok(self, margins, kinds, scale):
         for kind, mg in margins:

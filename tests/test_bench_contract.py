@@ -43,3 +43,22 @@ def test_gpu_arm_line():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["step_latency_ms"]["median"] > 0 and d["verify_latency_ms"]["median"] > 0
+
+
+def test_plan_shard_weak_and_strong():
+    """weak-scaled configs give every rank its own fixed block of
+    requests (distinct prompts and global request ids, never duplicated work);
+    strong-scaled configs split the fixed global batch into a partition."""
+    sys.path.insert(0, ROOT)
+    from bench import plan_shard
+    for world in (1, 2, 4, 8):
+        blocks = [plan_shard("c3", 32, world, r) for r in range(world)]
+        assert all(b[2] == 32 * world and b[3] == "weak" and b[1] - b[0] == 32 for b in blocks)
+        assert sorted(x for b in blocks for x in range(b[0], b[1])) == list(range(32 * world))
+        reps = [plan_shard("c2", 1, world, r) for r in range(world)]
+        assert [(b[0], b[1]) for b in reps] == [(r, r + 1) for r in range(world)]
+        st = [plan_shard("c4", 64, world, r) for r in range(world)]
+        assert all(b[2] == 64 and b[3] == "strong" for b in st)
+        assert sorted(x for b in st for x in range(b[0], b[1])) == list(range(64))
+    assert plan_shard("c3", 32, 2, 1, batch_per_gpu=8)[:3] == (8, 16, 16)
+    assert plan_shard("c3", 32, 2, 1, strong=True)[:4] == (16, 32, 32, "strong")

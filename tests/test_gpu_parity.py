@@ -164,6 +164,35 @@ def test_lockstep_c1_stochastic():
     assert ls.checked["accept"] >= 10
 
 
+def test_lockstep_stochastic_admit_fresh_request_id():
+    """Continuous batching in stochastic mode: a request admitted into a used slot
+    draws its first token and its acceptance uniforms from its OWN global request
+    id (hsd_admit's req_id), not the slot's earlier request's noise; the oracle
+    (Engine.admit) follows the same rule, so the lockstep stays exact."""
+    cfg = get_config("c1").replace(accept="stochastic", batch=2)
+    pr = prompts(cfg, batch=2)
+    seed = 3
+    m = Model(cfg, seed=seed, precision="fp32")
+    table = TokenInfoTable(m)
+    ctx = ctx_for(cfg, hsd.FP32_VERIFY, seed=seed, max_batch=2, accept="stochastic",
+                  flags=hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION, max_ctx=cfg.prompt_len + 12 * (cfg.steps_N + 1) + 8)
+    ls = Lockstep(ctx, cfg, m, table, pr, seed=seed, accept="stochastic")
+    ls.start()
+    for _ in range(4):
+        ls.step()
+    fresh = prompts(cfg.replace(prompt_len=19), batch=6)[5]
+    firsts = []
+    for rid in (11, 12):                       # the same prompt under two fresh ids
+        g, o = ls.admit(1, fresh, rid)
+        assert g == o, f"admitted first token {g} != oracle {o} (req_id {rid})"
+        firsts.append(g)
+        for _ in range(3):
+            ls.step()
+    ctx.sync()
+    assert ls.checked["accept"] >= 14, ls.checked
+    ctx.destroy()
+
+
 def test_lockstep_hot_pruned_gqa_batch2():
     cfg = get_config("c1").replace(vocab=512, hot_tokens=64, kv_heads=2, batch=2)
     ls, accs = run_lockstep(cfg, hsd.FP32_VERIFY, steps=8, batch=2, hot=64, planted=True)

@@ -42,7 +42,7 @@ def test_ragged_batch_then_admit_is_lossless(precision):
     first = [[int(x)] for x in ctx.tensor("root_tok").cpu().numpy()]    # the first token of each slot
     got = [list(f) for f in first]
     _collect(ctx, steps, got)
-    ctx.admit(1, fresh)                                   # slot 1: new request, others continue
+    ctx.admit(1, fresh, 7)                                 # slot 1: new request, others continue
     got_admit = [int(ctx.tensor("root_tok").cpu().numpy()[1])]
     rest = [[], [], []]
     _collect(ctx, steps, rest)
@@ -65,11 +65,43 @@ def test_admit_contract():
     cfg = get_config("c1").replace(batch=2)
     ctx = hsd.init_model(cfg, device=0, precision=hsd.FP32_VERIFY, seed=0, max_batch=2, max_ctx=96)
     with pytest.raises(hsd.HsdError) as e:
-        ctx.admit(0, [1, 2, 3])                           # before prefill
+        ctx.admit(0, [1, 2, 3], 5)                         # before prefill
     assert e.value.status == hsd.HSD_ESTATE
     ctx.prefill(np.stack(prompts(cfg, batch=2)))
     for bad_slot, toks in [(2, [1, 2, 3]), (-1, [1, 2, 3]), (0, [5]), (0, [1, cfg.vocab])]:
         with pytest.raises(hsd.HsdError) as e:
-            ctx.admit(bad_slot, toks)
+            ctx.admit(bad_slot, toks, 5)
         assert e.value.status == hsd.HSD_EINVAL
+    ctx.destroy()
+
+
+def test_step_refuses_at_kv_capacity():
+    """Capacity contract (include/hsd.h, hsd_prefill): a step writes KV rows up to
+    p + T - 1, so once a slot's committed length could pass max_pos - T, hsd_step
+    returns HSD_ESTATE and launches nothing -- never writing past the slot's pages
+    into the next request's. The host bound is refreshed from the device's p, so
+    a slot is refused only when it is really full."""
+    cfg = get_config("c1").replace(batch=2)
+    ctx = hsd.init_model(cfg, device=0, precision=hsd.FP32_VERIFY, seed=0, max_batch=2, max_ctx=40)
+    ctx.prefill(np.stack(prompts(cfg, batch=2)))
+    T = cfg.budget_B + cfg.resample_budget_Br + 1
+    page = 64
+    max_pos = ctx.tensor("kv").shape[1] // 2 * page
+    refused = False
+    for _ in range(200):
+        p = ctx.tensor("p").cpu().numpy()
+        try:
+            ctx.step_host()
+        except hsd.HsdError as e:
+            assert e.status == hsd.HSD_ESTATE and "capacity" in str(e)
+            assert int(p.max()) + T > max_pos            # refused only when really full
+            refused = True
+            break
+        assert int(ctx.tensor("p").cpu().numpy().max()) <= max_pos
+    assert refused
+    # the refusal is sticky and harmless: a second call refuses again, state unchanged
+    p_before = ctx.tensor("p").cpu().numpy().copy()
+    with pytest.raises(hsd.HsdError):
+        ctx.step_host()
+    assert np.array_equal(ctx.tensor("p").cpu().numpy(), p_before)
     ctx.destroy()

@@ -167,3 +167,43 @@ def test_stochastic_low_temperature_is_greedy():
     for s in range(20):
         st = stochastic_walk(lin, lg, 1e-4, s, 0, 1)
         assert st == g
+
+
+def test_admit_is_lossless_and_uses_the_new_request_id():
+    """Engine.admit (continuous batching around the path): the admitted
+    slot decodes its new prompt losslessly while the other slot continues
+    untouched, and its random streams use the NEW global request id (stochastic
+    first token = the Gumbel-max sample under that id; a different id gives
+    independent noise)."""
+    cfg = tiny(steps_N=3, branch_k=2, budget_B=6)
+    m = Model(cfg, seed=4)
+    table = TokenInfoTable(m)
+    pr = prompts(cfg, batch=3, length=8, prompt_seed=5)
+    e = Engine(m, table, cfg)
+    e.prefill(pr[:2])
+    outs = [[q.tokens[-1]] for q in e.reqs]
+    for _ in range(3):
+        for o, new in zip(outs, e.step()):
+            o.extend(new)
+    t1 = e.admit(1, pr[2], req_id=9)
+    assert e.req_ids == [0, 9]
+    new_out = [t1]
+    for _ in range(4):
+        a, b = e.step()
+        outs[0].extend(a)
+        new_out.extend(b)
+    assert outs[0] == greedy_decode(m, pr[0], len(outs[0]))[0]
+    assert new_out == greedy_decode(m, pr[2], len(new_out))[0]
+    # stochastic: the admitted first token is the Gumbel-max sample of ITS id
+    from oracle.philox import gumbel_uniforms
+    from oracle.accept import gumbel_argmax
+    es = Engine(m, table, cfg.replace(accept="stochastic"), seed=1, accept="stochastic", temperature=1.0)
+    es.prefill(pr[:2])
+    kv = [([], []) for _ in range(m.n_layers)]          # the prompt's last-position logits, plain
+    for pos, t in enumerate(pr[2]):
+        _, logits, rows = m.target_one(int(t), pos, kv)
+        for l, (k, v) in enumerate(rows):
+            kv[l][0].append(k); kv[l][1].append(v)
+    picks = {rid: es.admit(1, pr[2], req_id=rid) for rid in (5, 6, 7, 8)}
+    for rid, t in picks.items():
+        assert t == gumbel_argmax(logits, 1.0, gumbel_uniforms(1, rid, 0, 0, cfg.vocab))[0]
