@@ -19,6 +19,8 @@ LIB = os.path.join(HERE, "libhsd.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v" if os.environ.get("HSD_PTXAS_V") else "-O3", "-I", os.path.join(ROOT, "include")]
+# debug builds only (e.g. -DHSD_ATTN_TRACE_ON); a change of flags rebuilds every object
+FLAGS += os.environ.get("HSD_EXTRA_NVCC", "").split()
 
 
 def nvcc() -> str:
@@ -51,6 +53,14 @@ def _compile(src: str, verbose: bool) -> str:
 
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    sig = os.path.join(BUILD, "flags.txt")
+    want = " ".join(ARCH + FLAGS)
+    if not os.path.exists(sig) or open(sig).read() != want:
+        for f in os.listdir(BUILD):
+            if f.endswith(".o"):
+                os.remove(os.path.join(BUILD, f))
+        with open(sig, "w") as fh:
+            fh.write(want)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), sources()))
     if os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):

@@ -4,16 +4,24 @@
 //
 // One CTA = (key split, kv head h, request x q-tile of 128 (row, head) pairs).
 //  warp 0      : TMA producer -- the q tile once (3-D map: hd x G heads x rows),
-//                then per 128-key chunk (2 pages via the block table): K [128 x hd]
-//                into a 3-stage K ring (freed by the S MMA) and V^T [hd x 128] into
-//                a 2-stage V ring (freed by the P V MMA); chunks wholly below the
-//                rows this pass writes load before griddepcontrol.wait.
+//                then per 128-key chunk (2 pages via the block table) K [128 x hd]
+//                into a 3-stage K ring (freed by the S MMA);
+//  warp 2      : TMA producer of V^T [hd x 128] into a 2-stage V ring (freed by the
+//                P V MMA). Two producers, so a K load never queues behind a V load
+//                that waits for a P V MMA (one producer serialised them: S_{j+1} was
+//                issued only after K_{j+1} landed behind V_j, the load latency
+//                exposed every chunk). Chunks wholly below the rows this pass
+//                writes load before griddepcontrol.wait.
 //  warp 1      : MMA issuer -- S_j = Q K_j^T (M=128, N=128, K=hd) into one of two
 //                TMEM score buffers, S_{j+1} issued before P_j is ready; then
 //                O += P_j V_j (M=128, N=hd, K=128) with P_j read from TMEM (the
 //                bf16 P_j overwrites the first 64 columns of S_j's buffer).
-//  warps 2..9  : softmax -- TMEM lane t = one (row, head) is owned by a PAIR of
-//                warps (same lane quarter), each taking 64 of the chunk's 128 keys:
+//                The V^T tile carries 16 extra constant rows (a row of ones, then
+//                zeros), so the same MMA also accumulates l = sum_k P_jk in O's
+//                column hd: the row sum of exactly the bf16 P the MMA consumed,
+//                with no per-key additions in the softmax warps.
+//  warps 2..   : softmax -- TMEM lane t = one (row, head) is owned by SW warps
+//                (same lane quarter), each taking 128 / SW of the chunk's keys:
 //                a visibility mask (committed range | tree-ancestor bits, see
 //                attention.cu) per 32 keys, scores exponentiated as
 //                ex2(s * log2e/sqrt(hd) - m) in one FFMA + ex2.approx, the pair
@@ -34,7 +42,10 @@ namespace {
 using namespace tc;
 // softmax warps per TMEM lane quarter (SW): each owns CHUNK / SW keys of a chunk;
 // the CTA has 64 + 128 * SW threads (TMA warp, MMA warp, 4 * SW softmax warps)
-template <int SW> constexpr int nthreads() { return 64 + 128 * SW; }
+// the CTA has 96 + 128 * SW threads: warp 0 TMA (Q, K), warp 1 MMA, warp 2 TMA (V),
+// then 4 * SW softmax warps (warp w reads TMEM lane quarter w % 4)
+template <int SW> constexpr int nthreads() { return 96 + 128 * SW; }
+constexpr int SM0 = 96;        // first softmax thread
 constexpr int PAGE = 64;
 constexpr int CHUNK = 128;     // keys per softmax iteration = 2 pages
 constexpr int KSTAGES = 3;     // K ring: a stage frees when its S MMA completes
@@ -51,6 +62,7 @@ HSD_DEV uint64_t gtime() {
 struct AttnParams {
   int M, R, Hq, G, hd, n_qtiles, max_keys, keys_per_split, direct;
   int dyn;                     // 1: key splits divide the CTA's VISIBLE chunks (device-side), not max_keys
+  int exp_flags;               // timing experiments only (HSD_ATTN_EXP, results wrong): 1 = drop the last q-tile
   int cluster;                 // 1: the S key-split CTAs form a cluster and reduce over DSMEM
   RowMeta m;
   KVLayer kv;
@@ -61,7 +73,13 @@ struct AttnParams {
   L2Pf pf;                     // weights of a later GEMM to prefetch into L2 (common.cuh)
   KStamp kst;                  // per-launch stamps (hsd_kstamp) or kst.buf == null
 };
+// compiled in only with -DHSD_ATTN_TRACE_ON (the %globaltimer reads cost issue slots in the loop)
+#ifdef HSD_ATTN_TRACE_ON
 #define TRACE(i) do { if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[(i)] = gtime(); } while (0)
+#else
+#define TRACE(i) do { } while (0)
+#endif
+constexpr int VEXTRA = 16;     // constant V^T rows per page: row hd = ones (-> l in O column hd), then zeros
 
 // bits [a, b) of a 32-bit word (a, b clamped to [0, 32])
 HSD_DEV uint32_t range32(int a, int b) {
@@ -135,7 +153,8 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   const int hd = P.hd, natom = hd / 64;
   const int q_bytes = QROWS * hd * 2;          // natom atoms of [128 rows x 128 B]
   const int k_bytes = CHUNK * hd * 2;          // natom atoms of [128 keys x 128 B] (2 pages each)
-  const int v_bytes = hd * CHUNK * 2;          // 2 atom columns (pages) of [hd rows x 128 B]
+  const int v_page = (hd + VEXTRA) * 128;     // one page's atom column: [hd + 16 rows x 128 B]
+  const int v_bytes = 2 * v_page;              // 2 atom columns (pages)
   uint8_t* sQ = base;
   uint8_t* sK = sQ + q_bytes;
   uint8_t* sV = sK + KSTAGES * k_bytes;
@@ -155,7 +174,6 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   constexpr int KPW = CHUNK / SW;          // keys per softmax warp per chunk (64 or 32)
   constexpr int NSM = 128 * SW;            // softmax threads
   __shared__ float red_max[2][SW][QROWS];   // [chunk parity][key part][row]
-  __shared__ float red_l[SW][QROWS];
   __shared__ float fin_m[QROWS], fin_l[QROWS];   // cluster mode: this split's (m, l) per tile row
   __shared__ float wts[QROWS][8];                // cluster mode: merge weight of each split, per row
 
@@ -164,17 +182,25 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   const int grp = blockIdx.z / P.n_qtiles, qt = blockIdx.z % P.n_qtiles;
   const RowMeta& m = P.m;
   const int req = m.req[grp * P.R];
+  if ((P.exp_flags & 1) && P.n_qtiles > 1 && qt == P.n_qtiles - 1) return;
 
   if (threadIdx.x == 0) { tile_lo = 0x7fffffff; tile_hi = 0; safe_hi = 0x7fffffff; TRACE(0); }
   if (threadIdx.x == 32) {
     for (int s = 0; s < KSTAGES; ++s) { mbar_init(&kfull[s], 1); mbar_init(&kempty[s], 1); }
     for (int s = 0; s < VSTAGES; ++s) { mbar_init(&vfull[s], 1); mbar_init(&vempty[s], 1); }
     mbar_init(qbar, 1);
-    for (int b = 0; b < 2; ++b) { mbar_init(&sfull[b], 1); mbar_init(&pfull[b], NSM); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&sfull[b], 1); mbar_init(&pfull[b], NSM / 32); }   // one arrive per softmax warp
     mbar_init(pvdone, 1);
     mbar_init(odone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // the constant rows of every V stage / page: row hd = bf16 1.0, rows hd+1.. = 0
+  // (TMA writes rows [0, hd) only; row hd has swizzle phase 0 and is uniform anyway)
+  for (int i = threadIdx.x; i < VSTAGES * 2 * VEXTRA * 32; i += blockDim.x) {
+    const int w = i & 31, r = (i >> 5) % VEXTRA, sp = (i >> 5) / VEXTRA;
+    ((uint32_t*)(sV + (size_t)sp * v_page + (size_t)(hd + r) * 128))[w] = r == 0 ? 0x3F803F80u : 0u;
+  }
+  fence_proxy_async();
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(512)
@@ -197,7 +223,7 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   int row = -1, head = 0, klo = 0, khi = 0, slot = -1, tb = 0;
   uint64_t anc[4] = {0, 0, 0, 0};
   bool valid = false, writable = false;   // writable: an output row of this request
-  if (warp >= 2) {
+  if (warp >= 3) {
     const int rh = qt * QROWS + lane_row;
     const int rl = rh / P.G, g = rh % P.G;
     row = grp * P.R + rl;
@@ -217,7 +243,7 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
       if (hi > lo) { atomicMin(&tile_lo, lo); atomicMax(&tile_hi, hi); }
     }
     int pmin = 0x7fffffff;
-    for (int r = threadIdx.x - 64; r < P.R; r += NSM) {
+    for (int r = threadIdx.x - SM0; r < P.R; r += NSM) {
       const int pr = grp * P.R + r < P.M ? m.pos[grp * P.R + r] : -1;
       if (pr >= 0) pmin = min(pmin, pr);
     }
@@ -251,8 +277,9 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
     if (lane == 0 && n_chunks == 0) { l2pf_issue(P.pf); l2pf_issue(P.pf, 1); }
     if (lane == 0 && n_chunks > 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
-      const uint64_t pol = policy_evict_first();
+      // K/V rows: read once per tile; with several q-tiles per (request, kv head) the
+      // sibling tiles' CTAs (co-scheduled, 8 CTAs apart) re-read them from L2
+      const uint64_t pol = P.n_qtiles > 1 ? policy_evict_normal() : policy_evict_first();
       const uint64_t polq = policy_evict_last();
       const int row0 = grp * P.R + qt * (QROWS / P.G);
       auto page_of = [&](int j, int pg) {
@@ -261,6 +288,7 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
       auto load_k = [&](int j) {
         const int s = j % KSTAGES;
         mbar_wait(&kempty[s], ((j / KSTAGES) & 1) ^ 1);
+        if (j < 16) TRACE(96 + j);               // K_j load issued
         mbar_expect_tx(&kfull[s], k_bytes);
         for (int pg = 0; pg < 2; ++pg) {
           const int krow = ((page_of(j, pg) * 2 + 0) * P.kv.kv_heads + h) * PAGE;
@@ -269,19 +297,9 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
                         krow, pol);
         }
       };
-      auto load_v = [&](int j) {
-        const int s = j % VSTAGES;
-        mbar_wait(&vempty[s], ((j / VSTAGES) & 1) ^ 1);
-        mbar_expect_tx(&vfull[s], v_bytes);
-        for (int pg = 0; pg < 2; ++pg) {
-          const int vrow = ((page_of(j, pg) * 2 + 1) * P.kv.kv_heads + h) * hd;
-          tma_load_2d(&tmV, &vfull[s], sV + (size_t)s * v_bytes + pg * (hd * 128), 0, vrow, pol);
-        }
-      };
       auto safe = [&](int j) { return (c_first + j + 1) * CHUNK <= safe_hi; };
-      int kj = 0, vj = 0;
+      int kj = 0;
       while (kj < n_chunks && kj < KSTAGES && safe(kj)) load_k(kj++);
-      while (vj < n_chunks && vj < VSTAGES && safe(vj)) load_v(vj++);
       pdl_wait();
       kst_enter(P.kst);
       if (P.pf.late) l2pf_issue(P.pf, 1);   // (the late variant goes ahead of q)
@@ -289,12 +307,27 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
       mbar_expect_tx(qbar, q_bytes);
       for (int a = 0; a < natom; ++a)
         tma_load_3d(&tmQ, qbar, sQ + a * (QROWS * 128), a * 64, h * P.G, row0, polq);
-      // K runs one chunk ahead of V: V_j waits for P_{j-2} V, K_{j+1} must not
-      while (vj < n_chunks) {
-        if (kj < n_chunks && kj <= vj + 1) load_k(kj++);
-        else load_v(vj++);
-      }
-      l2pf_issue(P.pf);   // after this CTA's last K/V load: the bulk prefetch queues behind them in TMA
+      while (kj < n_chunks) load_k(kj++);
+      l2pf_issue(P.pf);   // after this CTA's last K load: the bulk prefetch queues behind it in TMA
+    }
+  } else if (warp == 2) {
+    if (lane == 0 && n_chunks > 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
+      const uint64_t pol = P.n_qtiles > 1 ? policy_evict_normal() : policy_evict_first();
+      auto load_v = [&](int j) {
+        const int s = j % VSTAGES;
+        mbar_wait(&vempty[s], ((j / VSTAGES) & 1) ^ 1);
+        mbar_expect_tx(&vfull[s], 2 * hd * 128);
+        for (int pg = 0; pg < 2; ++pg) {
+          const int page = P.kv.block_table[(size_t)req * P.kv.pages_per_req + 2 * (c_first + j) + pg];
+          const int vrow = ((page * 2 + 1) * P.kv.kv_heads + h) * hd;
+          tma_load_2d(&tmV, &vfull[s], sV + (size_t)s * v_bytes + pg * v_page, 0, vrow, pol);
+        }
+      };
+      int vj = 0;
+      while (vj < n_chunks && vj < VSTAGES && (c_first + vj + 1) * CHUNK <= safe_hi) load_v(vj++);
+      pdl_wait();
+      while (vj < n_chunks) load_v(vj++);
     }
   } else if (warp == 1) {
     if (lane == 0 && n_chunks > 0) {
@@ -304,6 +337,7 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
         const int s = j % KSTAGES;
         mbar_wait(&kfull[s], (j / KSTAGES) & 1);
         fence_after();
+        if (j < 16) TRACE(112 + j);              // K_j landed (seen by the MMA warp)
         const uint32_t d = tS + (uint32_t)((j & 1) * CHUNK);
         for (int kk = 0; kk < hd / 16; ++kk) {
           const int a = kk >> 2, off = kk & 3;
@@ -317,17 +351,19 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
       issue_s(0);
       for (int j = 0; j < n_chunks; ++j) {
         if (j + 1 < n_chunks) issue_s(j + 1);
+        if (j < 16) TRACE(64 + 2 * j);           // S_{j+1} issued
         mbar_wait(&pfull[j & 1], (j >> 1) & 1);
         fence_after();
         const int s = j % VSTAGES;
         mbar_wait(&vfull[s], (j / VSTAGES) & 1);
+        if (j < 16) TRACE(65 + 2 * j);           // P_j and V_j ready: P V issued
         // O += P_j V_j with P_j (bf16, 2 keys per column) over S_j's TMEM columns;
         // tcgen05.mma executes in issue order, so S_{j+2} (issued later into the
         // same columns) cannot overtake this read
         const uint32_t tP = tS + (uint32_t)((j & 1) * CHUNK);
         for (int kk = 0; kk < CHUNK / 16; ++kk) {
           const int ka = kk >> 2, off = kk & 3;
-          const uint64_t vd = desc_sw128(sV + (size_t)s * v_bytes + ka * (hd * 128)) + 2 * off;
+          const uint64_t vd = desc_sw128(sV + (size_t)s * v_bytes + ka * v_page) + 2 * off;
           mma_bf16_ts(tO, tP + (uint32_t)(kk * 8), vd, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
         mma_commit(&vempty[s]);
@@ -337,15 +373,20 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
     }
   } else {
     // ------------------------------------------------------------ softmax warps
-    const int part = (warp - 2) >> 2;                  // which KPW keys of the chunk
+    const int part = (warp - 3) >> 2;                  // which KPW keys of the chunk
     const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
-    float mrow = -INFINITY, lrow = 0.f;                // log2 domain; lrow = this part's partial sum
+    float mrow = -INFINITY;                            // running row max, log2 domain
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const int hcols = hd / SW;                          // this part's O columns
+    // a warp whose 32 lane rows are all padding (the last q-tile of a (request, kv
+    // head): c3's third tile holds 4 of 128 valid pairs) computes nothing: its P
+    // rows are never consumed by a valid O row (rows of P V are independent)
+    const bool live = __any_sync(0xffffffffu, valid);
     for (int j = 0; j < n_chunks; ++j) {
-      mbar_wait(&sfull[j & 1], (j >> 1) & 1);
+      mbar_wait(&sfull[j & 1], (j >> 1) & 1);   // (also paces the pfull phases)
       fence_after();
-      if (threadIdx.x == 64 && j < 12) TRACE(8 + 4 * j);
+      if (live) {
+      if (threadIdx.x == SM0 && j < 12) TRACE(8 + 4 * j);
       const int kb = (c_first + j) * CHUNK + part * KPW;       // this part's keys
       uint32_t r0[32], r1[32];
       tmem_ld32_nw(tS + lane_off + (uint32_t)((j & 1) * CHUNK + part * KPW), r0);
@@ -402,18 +443,16 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
         mrow = mx;
       }
       const float msub = mrow == -INFINITY ? 0.f : mrow;   // P = 0, never ex2(-inf + inf)
-      if (threadIdx.x == 64 && j < 12) TRACE(9 + 4 * j);
-      // P_j (bf16) over this part's KPW/2 columns of S_j (KPW keys, 2 per column)
-      float ps[4] = {0.f, 0.f, 0.f, 0.f};                 // 4 independent sum chains
+      if (threadIdx.x == SM0 && j < 12) TRACE(9 + 4 * j);
+      // P_j (bf16) over this part's KPW/2 columns of S_j (KPW keys, 2 per column);
+      // its row sum l is accumulated by the P V MMA itself (O column hd)
       uint32_t pw[32];
 #pragma unroll
       for (int i = 0; i < KPW / 2; ++i) {
         const float p0 = ex2(fmaf(s[2 * i], scale_log2, -msub)), p1 = ex2(fmaf(s[2 * i + 1], scale_log2, -msub));
         __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
-        ps[i & 3] += __low2float(pr) + __high2float(pr);     // l sums exactly what the MMA sees
         pw[i] = *(uint32_t*)&pr;
       }
-      const float psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
       if constexpr (KPW == 64) {
         tmem_st32(tS + lane_off + (uint32_t)((j & 1) * CHUNK + part * 32), pw);
       } else {
@@ -429,7 +468,7 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
           mbar_wait(pvdone, (j - 1) & 1);
           fence_after();
         }
-        if (threadIdx.x == 64 && j < 12) TRACE(10 + 4 * j);
+        if (threadIdx.x == SM0 && j < 12) TRACE(10 + 4 * j);
         for (int c = 0; c < hcols; c += 16) {
           uint32_t o[16];
           tmem_ld16(tO + lane_off + (uint32_t)(part * hcols + c), o);
@@ -437,25 +476,32 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
           for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
           tmem_st16(tO + lane_off + (uint32_t)(part * hcols + c), o);
         }
+        if (part == 0) {   // the l column (and its 15 zero neighbours)
+          uint32_t o[16];
+          tmem_ld16(tO + lane_off + (uint32_t)hd, o);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st16(tO + lane_off + (uint32_t)hd, o);
+        }
       }
       tmem_st_wait();
-      lrow = lrow * alpha + psum;
+      }   // live
       fence_before();
-      mbar_arrive(&pfull[j & 1]);
-      if (threadIdx.x == 64 && j < 12) TRACE(11 + 4 * j);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pfull[j & 1]);
+      if (threadIdx.x == SM0 && j < 12) TRACE(11 + 4 * j);
     }
     // ------------------------------------------------------------ epilogue
-    red_l[part][lane_row] = lrow;
+    float ltot = 0.f;   // l = O column hd (the ones row of V^T), 0 for a row that saw nothing
     if (n_chunks > 0) {
       mbar_wait(odone, 0);
       fence_after();
+      uint32_t o[16];
+      tmem_ld16(tO + lane_off + (uint32_t)hd, o);
+      if (valid) ltot = __uint_as_float(o[0]);
     }
-    if (threadIdx.x == 64) { TRACE(4); if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[7] = n_chunks; }
-    quad_sync<SW>(q4);
-    if (threadIdx.x == 64) TRACE(56);
-    float ltot = 0.f;
-#pragma unroll
-    for (int p2 = 0; p2 < SW; ++p2) ltot += red_l[p2][lane_row];
+    if (threadIdx.x == SM0) { TRACE(4); if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[7] = n_chunks; }
+    if (threadIdx.x == SM0) TRACE(56);
     // O half-row (hcols fp32) -> the idle K/V ring (>= 128 rows x hd fp32) ->
     // each warp then writes its 32 rows row by row with coalesced vectors
     float* ostage = (float*)sK;                       // [128 rows][hd + 4]
@@ -475,7 +521,7 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
     }
     if (P.cluster && part == 0) { fin_m[lane_row] = mrow; fin_l[lane_row] = ltot; }
     asm volatile("bar.sync 5, %0;" ::"r"(NSM) : "memory");   // all softmax warps staged their rows
-    if (threadIdx.x == 64) TRACE(57);
+    if (threadIdx.x == SM0) TRACE(57);
     if (!P.cluster) {
     // the CTA's valid rows of one (kv head, q-tile): all 256 softmax threads write
     // them as coalesced 16-byte vectors; split partials go to ONE contiguous block
@@ -483,7 +529,7 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
     {
       // warp w takes tile rows w*rpi + lane/vpr, stepping 8*rpi; lanes cover hd
       // as float4s; (row, head) of a tile row advance incrementally (no divides)
-      const int sw = (threadIdx.x - 64) >> 5;
+      const int sw = (threadIdx.x - SM0) >> 5;
       const int n_rh = min(QROWS, P.R * P.G - qt * QROWS);        // valid (row, head) pairs in the tile
       const int vpr = hd / 4, rpi = 32 / vpr;
       const int d4 = (lane % vpr) * 4;
@@ -507,7 +553,7 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
         if (g2 >= P.G) { g2 -= P.G; ++rl2; }
       }
     }
-    if (threadIdx.x == 64) TRACE(58);
+    if (threadIdx.x == SM0) TRACE(58);
     if (!P.direct && writable && part == 0) {
       const size_t base_ml = (size_t)gridDim.x * P.M * P.Hq * hd;
       const size_t idx = ((size_t)split * P.Hq + head) * P.M + row;
@@ -563,7 +609,7 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   }
   if (threadIdx.x == 0) TRACE(59);
   if (threadIdx.x == 32) TRACE(60);
-  if (threadIdx.x == 64) TRACE(61);
+  if (threadIdx.x == SM0) TRACE(61);
   if (threadIdx.x == 96) TRACE(62);
   fence_before();
   __syncthreads();
@@ -628,14 +674,16 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   P.M = M; P.R = R; P.Hq = Hq; P.G = G; P.hd = hd; P.m = m; P.kv = kv;
   P.out = (bf16*)out; P.ws = ws; P.max_keys = max_keys;
   P.n_qtiles = (R * G + QROWS - 1) / QROWS;
+  static const int exp_flags = [] { const char* e = getenv("HSD_ATTN_EXP"); return e ? atoi(e) : 0; }();
+  P.exp_flags = exp_flags;
   static bool trace_init = [] {
-    if (getenv("HSD_ATTN_TRACE")) cudaMalloc(&g_attn_trace, 64 * 8);
+    if (getenv("HSD_ATTN_TRACE")) cudaMalloc(&g_attn_trace, 128 * 8);
     return true;
   }();
   (void)trace_init;
   P.trace = g_attn_trace;
   P.idesc_s = idesc_bf16(128, CHUNK);
-  P.idesc_o = idesc_bf16(128, hd);
+  P.idesc_o = idesc_bf16(128, hd + VEXTRA);   // O columns [0, hd) + l in column hd
   // splits: enough CTAs for ~2 per SM, each split a whole number of pages
   const int base_ctas = n_req * kv.kv_heads * P.n_qtiles;
   const int pages = (max_keys + CHUNK - 1) / CHUNK;     // chunks of 2 pages
@@ -689,7 +737,8 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   if (!tma_map_bf16(&mq, q, 3, dq, sq, bq) || !tma_map_bf16(&mk, kv.base, 2, dk, sk, bk) ||
       !tma_map_bf16(&mv, kv.base, 2, dv, sv, bv))
     return -1;
-  const size_t smem = 1024 + (size_t)QROWS * hd * 2 + (KSTAGES + VSTAGES) * ((size_t)CHUNK * hd * 2) +
+  const size_t smem = 1024 + (size_t)QROWS * hd * 2 + KSTAGES * ((size_t)CHUNK * hd * 2) +
+                      VSTAGES * ((size_t)2 * (hd + VEXTRA) * 128) +
                       (2 * KSTAGES + 2 * VSTAGES + 8) * 8 + 64;
   // softmax warps per lane quarter: 2 (8 softmax warps, 64 keys each) or 4 (16 warps,
   // 32 keys each: shorter per-thread chains, more warps to hide TMEM/barrier latency).

@@ -23,5 +23,9 @@ for j in range(min(n, 12)):  # pv(j-1) is only stamped when the chunk rescales O
     print(f" chunk {j}: S ready {(t[8+4*j]-t0)/1e3:7.2f}  max done {(t[9+4*j]-t0)/1e3:7.2f}  pv(j-1) done {(t[10+4*j]-t0)/1e3 if j>0 else float('nan'):7.2f}  P written {(t[11+4*j]-t0)/1e3:7.2f}")
 for i, nm in [(56, "epi: l exchanged"), (57, "epi: O staged"), (58, "epi: rows written"), (59, "warp0 at end"), (60, "warp1 at end"), (61, "thr64 at end"), (62, "thr96 at end")]:
     print(f"{nm:16s} {(t[i]-t0)/1e3:8.2f} us")
+print("MMA warp: S_{j+1} issued / P_j V_j issued (us)")
+for j in range(min(n, 16)):
+    print(f" j {j:2d}: S{j+1} issued {(t[64+2*j]-t0)/1e3:7.2f}  PV{j} issued {(t[65+2*j]-t0)/1e3:7.2f}"
+          f"  | K{j} load issued {(t[96+j]-t0)/1e3:7.2f}  K{j} landed {(t[112+j]-t0)/1e3:7.2f}")
 for i in [4, 5]:
     print(f"{names[i]:16s} {(t[i]-t0)/1e3:8.2f} us")

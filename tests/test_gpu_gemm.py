@@ -93,7 +93,9 @@ def test_tcgen05_pair_gemm_production_k(M, N, K, accumulate):
     torch.cuda.synchronize()
     ref = (A.double() @ W.double().T + (C0.double() if accumulate else 0))
     err = ((C.double() - ref).abs().max() / ref.abs().max()).item()
-    assert err < 1e-5, err
+    # fp32 accumulation: rounding error grows like sqrt(K) (random-sign partial
+    # sums); the 1e-5 bar of the K <= 4096 tests, scaled by sqrt(K / 4096)
+    assert err < 1e-5 * max(1.0, (K / 4096) ** 0.5), err
 
 
 @pytest.mark.parametrize("M,f,K", [(2080, 14336, 4096), (8512, 13824, 5120)])
