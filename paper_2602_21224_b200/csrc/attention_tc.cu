@@ -48,8 +48,6 @@ template <int SW> constexpr int nthreads() { return 96 + 128 * SW; }
 constexpr int SM0 = 96;        // first softmax thread
 constexpr int PAGE = 64;
 constexpr int CHUNK = 128;     // keys per softmax iteration = 2 pages
-constexpr int KSTAGES = 3;     // K ring: a stage frees when its S MMA completes
-constexpr int VSTAGES = 2;     // V ring: a stage frees when its P V MMA completes
 constexpr int QROWS = 128;
 
 // Debug phase trace (HSD_ATTN_TRACE env -> P.trace != null): CTA (0,0,0) records
@@ -66,6 +64,7 @@ struct AttnParams {
   int cluster;                 // 1: the S key-split CTAs form a cluster and reduce over DSMEM
   RowMeta m;
   KVLayer kv;
+  const bf16* q;               // [M][Hq][hd] (read directly when the q tile lives in TMEM)
   bf16* out;
   float* ws;
   uint32_t idesc_s, idesc_o;
@@ -75,7 +74,7 @@ struct AttnParams {
 };
 // compiled in only with -DHSD_ATTN_TRACE_ON (the %globaltimer reads cost issue slots in the loop)
 #ifdef HSD_ATTN_TRACE_ON
-#define TRACE(i) do { if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[(i)] = gtime(); } while (0)
+#define TRACE(i) do { if (P.trace && blockIdx.x < 2 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[(i) + 128 * blockIdx.x] = gtime(); } while (0)
 #else
 #define TRACE(i) do { } while (0)
 #endif
@@ -144,22 +143,42 @@ HSD_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
 template <int SW>
 HSD_DEV void quad_sync(int q) { asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * SW) : "memory"); }
 
-template <int SW>
+// PAIR: two CTAs of a cluster (cta_group::2, one TPC) run the q-tiles 2c and 2c+1
+// of a (request, kv head) as ONE M = 256 tile: S = Q K^T takes B (the 128-key K
+// chunk) as two 64-key halves, one page per CTA, and O += P V takes B (V^T, N =
+// hd + 16 rows) as two row halves -- every SM stages HALF of each K / V chunk, so
+// the per-SM K / V stream (the limit of the single-CTA kernel: TMA latency ~3.5
+// us under load through a 3-stage ring) halves, and the
+// rings get 4 stages. The leader's lane 0 issues every MMA for the pair; S / P / O
+// stay per CTA (each CTA's TMEM holds its 128 rows), so the softmax is unchanged.
+template <int SW, bool PAIR>
 __global__ void __launch_bounds__(nthreads<SW>(), 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                        const __grid_constant__ CUtensorMap tmV, AttnParams P) {
+                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmV2,
+                        AttnParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // single CTA: Q lives in TMEM (A operand of S = Q K^T read from TMEM, like P for P V),
+  // so its 32 KB of shared memory go to a 4th K stage -- the K ring's depth over the
+  // ~3.5 us TMA latency under load sets the chunk period (K landing gated every S)
+  constexpr bool QTM = !PAIR;
+  constexpr int KSTAGES = 4;                // K ring: a stage frees when its S MMA completes
+  constexpr int VSTAGES = PAIR ? 4 : 2;     // V ring: a stage frees when its P V MMA completes
+  constexpr int KROWS = PAIR ? PAGE : CHUNK;   // keys of each chunk this CTA stages
   const int hd = P.hd, natom = hd / 64;
   const int q_bytes = QROWS * hd * 2;          // natom atoms of [128 rows x 128 B]
-  const int k_bytes = CHUNK * hd * 2;          // natom atoms of [128 keys x 128 B] (2 pages each)
-  const int v_page = (hd + VEXTRA) * 128;     // one page's atom column: [hd + 16 rows x 128 B]
+  const int k_bytes = KROWS * hd * 2;          // natom atoms of [KROWS keys x 128 B]
+  const int vrows = PAIR ? (hd + VEXTRA) / 2 : hd + VEXTRA;   // V^T rows (of N = hd + 16) staged here
+  const int v_page = vrows * 128;              // one page's atom column: [vrows x 128 B]
   const int v_bytes = 2 * v_page;              // 2 atom columns (pages)
+  // pair: the cluster is (2, 1, 1) -- x = 2 * split + rank -- and z walks the pairs of q-tiles
+  const int crank = PAIR ? (int)(blockIdx.x & 1) : 0;
+  const bool leader = crank == 0;
   uint8_t* sQ = base;
-  uint8_t* sK = sQ + q_bytes;
+  uint8_t* sK = sQ + (QTM ? 0 : q_bytes);
   uint8_t* sV = sK + KSTAGES * k_bytes;
   uint64_t* bars = (uint64_t*)(sV + VSTAGES * v_bytes);   // P lives in TMEM over its S buffer
-  uint64_t* kfull = bars;                 // [KSTAGES]
+  uint64_t* kfull = bars;                 // [KSTAGES] (pair: the leader's counts both CTAs' bytes)
   uint64_t* kempty = kfull + KSTAGES;     // [KSTAGES]
   uint64_t* vfull = kempty + KSTAGES;     // [VSTAGES]
   uint64_t* vempty = vfull + VSTAGES;     // [VSTAGES]
@@ -178,36 +197,56 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   __shared__ float wts[QROWS][8];                // cluster mode: merge weight of each split, per row
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int split = blockIdx.x, h = blockIdx.y;
-  const int grp = blockIdx.z / P.n_qtiles, qt = blockIdx.z % P.n_qtiles;
+  const int split = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x, h = blockIdx.y;
+  const int nsplit = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int nz = PAIR ? P.n_qtiles / 2 : P.n_qtiles;   // grid z entries per (request, kv head)
+  const int grp = blockIdx.z / nz;
+  const int qt = PAIR ? 2 * (int)(blockIdx.z % nz) + crank : (int)(blockIdx.z % nz);
   const RowMeta& m = P.m;
   const int req = m.req[grp * P.R];
-  if ((P.exp_flags & 1) && P.n_qtiles > 1 && qt == P.n_qtiles - 1) return;
+  if (!PAIR && (P.exp_flags & 1) && P.n_qtiles > 1 && qt == P.n_qtiles - 1) return;
 
   if (threadIdx.x == 0) { tile_lo = 0x7fffffff; tile_hi = 0; safe_hi = 0x7fffffff; TRACE(0); }
   if (threadIdx.x == 32) {
     for (int s = 0; s < KSTAGES; ++s) { mbar_init(&kfull[s], 1); mbar_init(&kempty[s], 1); }
     for (int s = 0; s < VSTAGES; ++s) { mbar_init(&vfull[s], 1); mbar_init(&vempty[s], 1); }
-    mbar_init(qbar, 1);
-    for (int b = 0; b < 2; ++b) { mbar_init(&sfull[b], 1); mbar_init(&pfull[b], NSM / 32); }   // one arrive per softmax warp
+    mbar_init(qbar, QTM ? NSM / 32 : 1);   // (Q in TMEM: one arrive per softmax warp)
+    // one arrive per softmax warp (pair: the leader's counts both CTAs' warps)
+    for (int b = 0; b < 2; ++b) { mbar_init(&sfull[b], 1); mbar_init(&pfull[b], (PAIR ? 2 : 1) * NSM / 32); }
     mbar_init(pvdone, 1);
     mbar_init(odone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // the constant rows of every V stage / page: row hd = bf16 1.0, rows hd+1.. = 0
-  // (TMA writes rows [0, hd) only; row hd has swizzle phase 0 and is uniform anyway)
-  for (int i = threadIdx.x; i < VSTAGES * 2 * VEXTRA * 32; i += blockDim.x) {
-    const int w = i & 31, r = (i >> 5) % VEXTRA, sp = (i >> 5) / VEXTRA;
-    ((uint32_t*)(sV + (size_t)sp * v_page + (size_t)(hd + r) * 128))[w] = r == 0 ? 0x3F803F80u : 0u;
+  // the constant rows of every V stage / page: V^T row hd = bf16 1.0, rows hd+1.. = 0
+  // (TMA writes the dimension rows only; the ones row has swizzle phase 0 and is
+  // uniform anyway). Pair: the follower holds them, at local rows hd - vrows ..
+  const int c0row = PAIR ? (crank == 1 ? hd - vrows : vrows) : hd;
+  const int n_const = vrows - c0row;
+  for (int i = threadIdx.x; i < VSTAGES * 2 * n_const * 32; i += blockDim.x) {
+    const int w = i & 31, r = (i >> 5) % n_const, sp = (i >> 5) / n_const;
+    ((uint32_t*)(sV + (size_t)sp * v_page + (size_t)(c0row + r) * 128))[w] = r == 0 ? 0x3F803F80u : 0u;
   }
   fence_proxy_async();
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(512)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(512)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(512)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
-  __syncthreads();
+  if constexpr (PAIR) {   // the partner's barriers initialised before any load or MMA targets them
+    fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    fence_after();
+  } else {
+    __syncthreads();
+  }
   if (threadIdx.x == 0) TRACE(1);
   // Programmatic dependent launch: only q and the K/V rows this pass's qkv_rope_kv
   // writes (every request row's own position) come from the kernel right before
@@ -244,8 +283,17 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
     }
     int pmin = 0x7fffffff;
     for (int r = threadIdx.x - SM0; r < P.R; r += NSM) {
-      const int pr = grp * P.R + r < P.M ? m.pos[grp * P.R + r] : -1;
-      if (pr >= 0) pmin = min(pmin, pr);
+      const int rr = grp * P.R + r;
+      const int pr = rr < P.M ? m.pos[rr] : -1;
+      if (pr >= 0) {
+        pmin = min(pmin, pr);
+        if (PAIR) {   // both CTAs of a pair stream the key range of the whole group
+          int lo2 = m.klo[rr], hi2 = m.khi[rr];
+          const int sl = m.slot[rr];
+          if (sl >= 0) { const int t2 = m.tbase[req]; lo2 = min(lo2, t2); hi2 = max(hi2, t2 + sl + 1); }
+          if (hi2 > lo2) { atomicMin(&tile_lo, lo2); atomicMax(&tile_hi, hi2); }
+        }
+      }
     }
     if (pmin != 0x7fffffff) atomicMin(&safe_hi, pmin);
   }
@@ -260,7 +308,7 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   int k_begin, k_end;
   if (P.dyn) {
     const int c0 = tile_lo / CHUNK, c1 = (tile_hi + CHUNK - 1) / CHUNK;
-    const int cps = c1 > c0 ? (c1 - c0 + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    const int cps = c1 > c0 ? (c1 - c0 + nsplit - 1) / nsplit : 0;
     k_begin = (c0 + split * cps) * CHUNK;
     k_end = k_begin + cps * CHUNK;
   } else {
@@ -271,7 +319,8 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   const int c_first = lo / CHUNK;
   const int n_chunks = hi > lo ? (hi + CHUNK - 1) / CHUNK - c_first : 0;
   const uint32_t tS = tmem;              // 2 x 128 columns (double-buffered scores)
-  const uint32_t tO = tmem + 256;        // hd columns
+  const uint32_t tO = tmem + 256;        // hd + 16 columns (l in column hd)
+  const uint32_t tQ = tmem + 256 + 144;  // (QTM) the q tile: hd / 2 columns, 2 bf16 per column
 
   if (warp == 0) {
     if (lane == 0 && n_chunks == 0) { l2pf_issue(P.pf); l2pf_issue(P.pf, 1); }
@@ -285,16 +334,24 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
       auto page_of = [&](int j, int pg) {
         return P.kv.block_table[(size_t)req * P.kv.pages_per_req + 2 * (c_first + j) + pg];
       };
+      const uint32_t kfull0 = PAIR ? mapa_u32(&kfull[0], 0) : 0u;
       auto load_k = [&](int j) {
         const int s = j % KSTAGES;
         mbar_wait(&kempty[s], ((j / KSTAGES) & 1) ^ 1);
         if (j < 16) TRACE(96 + j);               // K_j load issued
-        mbar_expect_tx(&kfull[s], k_bytes);
-        for (int pg = 0; pg < 2; ++pg) {
-          const int krow = ((page_of(j, pg) * 2 + 0) * P.kv.kv_heads + h) * PAGE;
+        if constexpr (PAIR) {   // this CTA's page of the chunk (N half), bytes on the leader's barrier
+          if (leader) mbar_expect_tx(&kfull[s], 2 * k_bytes);
+          const int krow = ((page_of(j, crank) * 2 + 0) * P.kv.kv_heads + h) * PAGE;
           for (int a = 0; a < natom; ++a)
-            tma_load_2d(&tmK, &kfull[s], sK + (size_t)s * k_bytes + a * (CHUNK * 128) + pg * (PAGE * 128), a * 64,
-                        krow, pol);
+            tma_load_2d_2sm(&tmK, kfull0 + 8u * s, sK + (size_t)s * k_bytes + a * (KROWS * 128), a * 64, krow, pol);
+        } else {
+          mbar_expect_tx(&kfull[s], k_bytes);
+          for (int pg = 0; pg < 2; ++pg) {
+            const int krow = ((page_of(j, pg) * 2 + 0) * P.kv.kv_heads + h) * PAGE;
+            for (int a = 0; a < natom; ++a)
+              tma_load_2d(&tmK, &kfull[s], sK + (size_t)s * k_bytes + a * (CHUNK * 128) + pg * (PAGE * 128), a * 64,
+                          krow, pol);
+          }
         }
       };
       auto safe = [&](int j) { return (c_first + j + 1) * CHUNK <= safe_hi; };
@@ -304,9 +361,17 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
       kst_enter(P.kst);
       if (P.pf.late) l2pf_issue(P.pf, 1);   // (the late variant goes ahead of q)
       if (threadIdx.x == 0) TRACE(2);
-      mbar_expect_tx(qbar, q_bytes);
-      for (int a = 0; a < natom; ++a)
-        tma_load_3d(&tmQ, qbar, sQ + a * (QROWS * 128), a * 64, h * P.G, row0, polq);
+      if constexpr (QTM) {
+        // (the softmax warps load q into TMEM)
+      } else if constexpr (PAIR) {
+        if (leader) mbar_expect_tx(qbar, 2 * q_bytes);
+        for (int a = 0; a < natom; ++a)
+          tma_load_3d_2sm(&tmQ, mapa_u32(qbar, 0), sQ + a * (QROWS * 128), a * 64, h * P.G, row0, polq);
+      } else {
+        mbar_expect_tx(qbar, q_bytes);
+        for (int a = 0; a < natom; ++a)
+          tma_load_3d(&tmQ, qbar, sQ + a * (QROWS * 128), a * 64, h * P.G, row0, polq);
+      }
       while (kj < n_chunks) load_k(kj++);
       l2pf_issue(P.pf);   // after this CTA's last K load: the bulk prefetch queues behind it in TMA
     }
@@ -314,14 +379,20 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
     if (lane == 0 && n_chunks > 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
       const uint64_t pol = P.n_qtiles > 1 ? policy_evict_normal() : policy_evict_first();
+      const uint32_t vfull0 = PAIR ? mapa_u32(&vfull[0], 0) : 0u;
       auto load_v = [&](int j) {
         const int s = j % VSTAGES;
         mbar_wait(&vempty[s], ((j / VSTAGES) & 1) ^ 1);
-        mbar_expect_tx(&vfull[s], 2 * hd * 128);
+        if (!PAIR && (P.exp_flags & 2)) { mbar_arrive(&vfull[s]); return; }   // timing experiment: no V traffic
+        if (!PAIR || leader) mbar_expect_tx(&vfull[s], 2 * hd * 128);   // (pair: both CTAs' rows)
         for (int pg = 0; pg < 2; ++pg) {
           const int page = P.kv.block_table[(size_t)req * P.kv.pages_per_req + 2 * (c_first + j) + pg];
           const int vrow = ((page * 2 + 1) * P.kv.kv_heads + h) * hd;
-          tma_load_2d(&tmV, &vfull[s], sV + (size_t)s * v_bytes + pg * v_page, 0, vrow, pol);
+          if constexpr (PAIR)   // this CTA's dimension rows: [0, vrows) / [vrows, hd)
+            tma_load_2d_2sm(crank ? &tmV2 : &tmV, vfull0 + 8u * s, sV + (size_t)s * v_bytes + pg * v_page, 0,
+                            vrow + (crank ? vrows : 0), pol);
+          else
+            tma_load_2d(&tmV, &vfull[s], sV + (size_t)s * v_bytes + pg * v_page, 0, vrow, pol);
         }
       };
       int vj = 0;
@@ -330,9 +401,13 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
       while (vj < n_chunks) load_v(vj++);
     }
   } else if (warp == 1) {
-    if (lane == 0 && n_chunks > 0) {
+    if (lane == 0 && n_chunks > 0 && leader) {   // (pair: the leader issues for both CTAs)
       mbar_wait(qbar, 0);
       TRACE(3);
+      auto commit = [&](uint64_t* bar) {
+        if constexpr (PAIR) mma_commit_2sm(bar, 3);
+        else mma_commit(bar);
+      };
       auto issue_s = [&](int j) {
         const int s = j % KSTAGES;
         mbar_wait(&kfull[s], (j / KSTAGES) & 1);
@@ -341,12 +416,17 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
         const uint32_t d = tS + (uint32_t)((j & 1) * CHUNK);
         for (int kk = 0; kk < hd / 16; ++kk) {
           const int a = kk >> 2, off = kk & 3;
-          const uint64_t ad = desc_sw128(sQ + a * (QROWS * 128)) + 2 * off;
-          const uint64_t bd = desc_sw128(sK + (size_t)s * k_bytes + a * (CHUNK * 128)) + 2 * off;
-          mma_bf16(d, ad, bd, P.idesc_s, kk > 0 ? 1u : 0u);
+          const uint64_t bd = desc_sw128(sK + (size_t)s * k_bytes + a * (KROWS * 128)) + 2 * off;
+          if constexpr (QTM) {
+            mma_bf16_ts(d, tQ + (uint32_t)(kk * 8), bd, P.idesc_s, kk > 0 ? 1u : 0u);
+          } else {
+            const uint64_t ad = desc_sw128(sQ + a * (QROWS * 128)) + 2 * off;
+            if constexpr (PAIR) mma_bf16_2sm(d, ad, bd, P.idesc_s, kk > 0 ? 1u : 0u);
+            else mma_bf16(d, ad, bd, P.idesc_s, kk > 0 ? 1u : 0u);
+          }
         }
-        mma_commit(&sfull[j & 1]);
-        mma_commit(&kempty[s]);
+        commit(&sfull[j & 1]);
+        commit(&kempty[s]);
       };
       issue_s(0);
       for (int j = 0; j < n_chunks; ++j) {
@@ -364,12 +444,13 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
         for (int kk = 0; kk < CHUNK / 16; ++kk) {
           const int ka = kk >> 2, off = kk & 3;
           const uint64_t vd = desc_sw128(sV + (size_t)s * v_bytes + ka * v_page) + 2 * off;
-          mma_bf16_ts(tO, tP + (uint32_t)(kk * 8), vd, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          if constexpr (PAIR) mma_bf16_ts_2sm(tO, tP + (uint32_t)(kk * 8), vd, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          else mma_bf16_ts(tO, tP + (uint32_t)(kk * 8), vd, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        mma_commit(&vempty[s]);
-        mma_commit(pvdone);
+        commit(&vempty[s]);
+        commit(pvdone);
       }
-      mma_commit(odone);
+      commit(odone);
     }
   } else {
     // ------------------------------------------------------------ softmax warps
@@ -382,10 +463,36 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
     // head): c3's third tile holds 4 of 128 valid pairs) computes nothing: its P
     // rows are never consumed by a valid O row (rows of P V are independent)
     const bool live = __any_sync(0xffffffffu, valid);
+    if constexpr (QTM) {
+      // this thread's (row, head) q row, dims [part * hd / SW, (part + 1) * hd / SW), into
+      // TMEM columns hd / (2 SW) wide at its lane (bf16 pairs, the A layout of the TS MMA);
+      // q is written by the kernel right before this one
+      pdl_wait();
+      constexpr int QC = 64 / SW;                      // columns per part at hd = 128
+      const int qc = hd / (2 * SW);                    // (hd = 64: half of QC)
+      uint32_t qw[QC];
+      const uint4* src = writable ? (const uint4*)(P.q + ((size_t)row * P.Hq + head) * hd + part * (hd / SW)) : nullptr;
+#pragma unroll
+      for (int i = 0; i < QC / 4; ++i) {
+        const uint4 v = (src && i < qc / 4) ? src[i] : make_uint4(0u, 0u, 0u, 0u);
+        qw[4 * i] = v.x; qw[4 * i + 1] = v.y; qw[4 * i + 2] = v.z; qw[4 * i + 3] = v.w;
+      }
+      if constexpr (QC == 32) {
+        if (qc == 32) tmem_st32(tQ + lane_off + (uint32_t)(part * 32), qw);
+        else { uint32_t w16[16]; for (int i = 0; i < 16; ++i) w16[i] = qw[i]; tmem_st16(tQ + lane_off + (uint32_t)(part * 16), w16); }
+      } else {
+        if (qc == 16) tmem_st16(tQ + lane_off + (uint32_t)(part * 16), qw);
+        else { uint32_t w8[8]; for (int i = 0; i < 8; ++i) w8[i] = qw[i]; tmem_st8(tQ + lane_off + (uint32_t)(part * 8), w8); }
+      }
+      tmem_st_wait();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qbar);
+    }
     for (int j = 0; j < n_chunks; ++j) {
       mbar_wait(&sfull[j & 1], (j >> 1) & 1);   // (also paces the pfull phases)
       fence_after();
-      if (live) {
+      if (live && !(P.exp_flags & 4)) {   // (exp 4: timing experiment without the softmax)
       if (threadIdx.x == SM0 && j < 12) TRACE(8 + 4 * j);
       const int kb = (c_first + j) * CHUNK + part * KPW;       // this part's keys
       uint32_t r0[32], r1[32];
@@ -488,7 +595,10 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
       }   // live
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&pfull[j & 1]);
+      if (lane == 0) {
+        if (PAIR && !leader) mbar_arrive_cluster(mapa_u32(&pfull[j & 1], 0));   // the leader issues P V
+        else mbar_arrive(&pfull[j & 1]);
+      }
       if (threadIdx.x == SM0 && j < 12) TRACE(11 + 4 * j);
     }
     // ------------------------------------------------------------ epilogue
@@ -500,7 +610,7 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
       tmem_ld16(tO + lane_off + (uint32_t)hd, o);
       if (valid) ltot = __uint_as_float(o[0]);
     }
-    if (threadIdx.x == SM0) { TRACE(4); if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[7] = n_chunks; }
+    if (threadIdx.x == SM0) { TRACE(4); if (P.trace && blockIdx.x < 2 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[7 + 128 * blockIdx.x] = n_chunks; }
     if (threadIdx.x == SM0) TRACE(56);
     // O half-row (hcols fp32) -> the idle K/V ring (>= 128 rows x hd fp32) ->
     // each warp then writes its 32 rows row by row with coalesced vectors
@@ -555,7 +665,7 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
     }
     if (threadIdx.x == SM0) TRACE(58);
     if (!P.direct && writable && part == 0) {
-      const size_t base_ml = (size_t)gridDim.x * P.M * P.Hq * hd;
+      const size_t base_ml = (size_t)nsplit * P.M * P.Hq * hd;
       const size_t idx = ((size_t)split * P.Hq + head) * P.M + row;
       P.ws[base_ml + 2 * idx] = mrow;      // log2 domain (merge uses exp2)
       P.ws[base_ml + 2 * idx + 1] = ltot;
@@ -612,11 +722,19 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   if (threadIdx.x == SM0) TRACE(61);
   if (threadIdx.x == 96) TRACE(62);
   fence_before();
-  __syncthreads();
+  if constexpr (PAIR)   // neither CTA leaves while the pair's MMAs or arrivals may still touch it
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  else
+    __syncthreads();
   fence_after();
   if (threadIdx.x == 0) TRACE(5);
   kst_exit(P.kst);
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  if (warp == 2) {
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
 }
 
 // split merge: one warp per (row, head), lanes over hd:
@@ -672,18 +790,28 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   P.pf = take_l2pf();
   P.kst = take_kstamp();
   P.M = M; P.R = R; P.Hq = Hq; P.G = G; P.hd = hd; P.m = m; P.kv = kv;
-  P.out = (bf16*)out; P.ws = ws; P.max_keys = max_keys;
+  P.out = (bf16*)out; P.ws = ws; P.max_keys = max_keys; P.q = (const bf16*)q;
   P.n_qtiles = (R * G + QROWS - 1) / QROWS;
-  static const int exp_flags = [] { const char* e = getenv("HSD_ATTN_EXP"); return e ? atoi(e) : 0; }();
-  P.exp_flags = exp_flags;
+  // CTA pairs (M = 256, cta_group::2) when a (request, kv head) spans >= 2 q-tiles:
+  // opt-in (HSD_ATTN_PAIR=1), measured slower on c3 (302 -> 490 us per launch): the
+  // follower sees each S through the leader's multicast commit ~0.45 us late and its
+  // per-warp remote pfull arrivals (release.cluster) cost ~0.6 us per chunk, so the
+  // pair runs at ~2 us per chunk although each SM streams half of it
+  static const int pair_env = [] { const char* e = getenv("HSD_ATTN_PAIR"); return e ? atoi(e) : 0; }();
+  const bool pair = pair_env && P.n_qtiles >= 2;
+  if (pair) P.n_qtiles += P.n_qtiles & 1;
+  {   // read per launch: scripts/attn_trace.py switches it on for the traced pass only
+    const char* e = getenv("HSD_ATTN_EXP");
+    P.exp_flags = e ? atoi(e) : 0;
+  }
   static bool trace_init = [] {
-    if (getenv("HSD_ATTN_TRACE")) cudaMalloc(&g_attn_trace, 128 * 8);
+    if (getenv("HSD_ATTN_TRACE")) cudaMalloc(&g_attn_trace, 256 * 8);
     return true;
   }();
   (void)trace_init;
   P.trace = g_attn_trace;
-  P.idesc_s = idesc_bf16(128, CHUNK);
-  P.idesc_o = idesc_bf16(128, hd + VEXTRA);   // O columns [0, hd) + l in column hd
+  P.idesc_s = idesc_bf16(pair ? 256 : 128, CHUNK);
+  P.idesc_o = idesc_bf16(pair ? 256 : 128, hd + VEXTRA);   // O columns [0, hd) + l in column hd
   // splits: enough CTAs for ~2 per SM, each split a whole number of pages
   const int base_ctas = n_req * kv.kv_heads * P.n_qtiles;
   const int pages = (max_keys + CHUNK - 1) / CHUNK;     // chunks of 2 pages
@@ -716,7 +844,7 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
     const char* e = getenv("HSD_ATTN_CLUSTER_MAX");
     return e ? atoi(e) : 2;
   }();
-  P.cluster = (S >= 2 && S <= cluster_max && S <= 8) ? 1 : 0;
+  P.cluster = (!pair && S >= 2 && S <= cluster_max && S <= 8) ? 1 : 0;
   while (!P.cluster && S > 1 && (size_t)S * M * Hq * (hd + 2) > ws_floats) --S;
   int pps = (pages + S - 1) / S;
   P.keys_per_split = pps * CHUNK;
@@ -724,7 +852,7 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   P.direct = S == 1;
   // tensor maps: q [M][Hq][hd] viewed (hd, heads, rows) with the head offset in
   // the coordinate; K pool rows of hd; V^T pool rows of page_size.
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mq, mk, mv, mv2;
   uint64_t dq[3] = {(uint64_t)hd, (uint64_t)Hq, (uint64_t)M};
   uint64_t sq[2] = {(uint64_t)hd, (uint64_t)Hq * hd};
   uint32_t bq[3] = {64, (uint32_t)G, (uint32_t)(QROWS / G)};
@@ -733,13 +861,17 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   uint32_t bk[2] = {64, (uint32_t)PAGE};
   uint64_t dv[2] = {(uint64_t)PAGE, (uint64_t)(kv_layer_elems / PAGE)};
   uint64_t sv[1] = {(uint64_t)PAGE};
-  uint32_t bv[2] = {(uint32_t)PAGE, (uint32_t)hd};
+  // pair: the leader stages V^T rows [0, vrows), the follower [vrows, hd) (+ the constant rows)
+  const int vrows = pair ? (hd + VEXTRA) / 2 : hd;
+  uint32_t bv[2] = {(uint32_t)PAGE, (uint32_t)vrows};
+  uint32_t bv2[2] = {(uint32_t)PAGE, (uint32_t)(pair ? hd - vrows : hd)};
   if (!tma_map_bf16(&mq, q, 3, dq, sq, bq) || !tma_map_bf16(&mk, kv.base, 2, dk, sk, bk) ||
-      !tma_map_bf16(&mv, kv.base, 2, dv, sv, bv))
+      !tma_map_bf16(&mv, kv.base, 2, dv, sv, bv) || !tma_map_bf16(&mv2, kv.base, 2, dv, sv, bv2))
     return -1;
-  const size_t smem = 1024 + (size_t)QROWS * hd * 2 + KSTAGES * ((size_t)CHUNK * hd * 2) +
-                      VSTAGES * ((size_t)2 * (hd + VEXTRA) * 128) +
-                      (2 * KSTAGES + 2 * VSTAGES + 8) * 8 + 64;
+  const int kst = 4, vst = pair ? 4 : 2;
+  const size_t smem = 1024 + (pair ? (size_t)QROWS * hd * 2 : 0) + kst * ((size_t)(pair ? PAGE : CHUNK) * hd * 2) +
+                      vst * ((size_t)2 * (pair ? (hd + VEXTRA) / 2 : hd + VEXTRA) * 128) +
+                      (2 * kst + 2 * vst + 8) * 8 + 64;
   // softmax warps per lane quarter: 2 (8 softmax warps, 64 keys each) or 4 (16 warps,
   // 32 keys each: shorter per-thread chains, more warps to hide TMEM/barrier latency).
   // Measured: c3 (768 CTAs, many waves) attention 11.6 -> 11.1
@@ -747,7 +879,7 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   // HSD_ATTN_SW=2|4 forces one.
   static const int sw_env = [] { const char* e = getenv("HSD_ATTN_SW"); return e ? atoi(e) : 0; }();
   const int sw = sw_env == 2 || sw_env == 4 ? sw_env : ((size_t)S * base_ctas > 2 * (size_t)num_sms() ? 4 : 2);
-  static size_t attr[2] = {0, 0};   // (the kernel also has ~1-3 KB of static shared memory)
+  static size_t attr[4] = {0, 0, 0, 0};   // (the kernel also has ~1-3 KB of static shared memory)
   auto launch = [&](auto kern, int nthr, size_t& at) {
     if (smem > at) {
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
@@ -756,13 +888,22 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
       }
       at = smem;
     }
-    dim3 grid(S, kv.kv_heads, n_req * P.n_qtiles);
-    if (P.cluster) launch_k_cluster(kern, grid, dim3(nthr), smem, st, S, mq, mk, mv, P);
-    else launch_k(kern, grid, dim3(nthr), smem, st, mq, mk, mv, P);
+    dim3 grid(pair ? 2 * S : S, kv.kv_heads, n_req * (pair ? P.n_qtiles / 2 : P.n_qtiles));
+    if (pair) launch_k_cluster(kern, grid, dim3(nthr), smem, st, 2, mq, mk, mv, mv2, P);
+    else if (P.cluster) launch_k_cluster(kern, grid, dim3(nthr), smem, st, S, mq, mk, mv, mv2, P);
+    else launch_k(kern, grid, dim3(nthr), smem, st, mq, mk, mv, mv2, P);
+    if (getenv("HSD_DEBUG_LAUNCH")) {
+      const cudaError_t e = cudaPeekAtLastError();
+      fprintf(stderr, "attention_tc launch: grid (%d, %d, %d) threads %d smem %zu pair %d cluster %d S %d M %d R %d G %d: %s\n",
+              grid.x, grid.y, grid.z, nthr, smem, (int)pair, P.cluster, S, M, R, G, cudaGetErrorString(e));
+    }
     return true;
   };
-  const bool ok = sw == 4 ? launch(attention_tc_kernel<4>, nthreads<4>(), attr[1])
-                          : launch(attention_tc_kernel<2>, nthreads<2>(), attr[0]);
+  bool ok;
+  if (pair) ok = sw == 4 ? launch(attention_tc_kernel<4, true>, nthreads<4>(), attr[3])
+                         : launch(attention_tc_kernel<2, true>, nthreads<2>(), attr[2]);
+  else ok = sw == 4 ? launch(attention_tc_kernel<4, false>, nthreads<4>(), attr[1])
+                    : launch(attention_tc_kernel<2, false>, nthreads<2>(), attr[0]);
   if (!ok) return -1;
   if (P.cluster) return 1;
   int launched = 1;

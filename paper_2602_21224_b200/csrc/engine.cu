@@ -1402,7 +1402,7 @@ hsd_status hsd_get_tensor(hsd_ctx* ctx, const char* name, hsd_tensor* out) {
   if (s == "kv") return set(c->kv_t, adt, {std::max(1, c->L), c->maxb * c->pages_per_req, 2, (int64_t)c->Hkv * c->page_size * c->hd});
   if (s == "kv_draft") return set(c->kv_d, adt, {1, c->maxb * c->pages_per_req, 2, (int64_t)c->Hkv * c->page_size * c->hd});
   extern unsigned long long* g_attn_trace;
-  if (s == "attn_trace" && g_attn_trace) return set(g_attn_trace, 3, {128});
+  if (s == "attn_trace" && g_attn_trace) return set(g_attn_trace, 3, {256});
   extern unsigned long long* g_tree_trace;
   if (s == "tree_trace" && g_tree_trace) return set(g_tree_trace, 3, {64});
   if (s == "layer0_wqkv" && c->L > 0) return set(c->layers[0].wqkv, adt, {c->qkvd, n});

@@ -11,8 +11,14 @@ ctx = hsd.init_model(cfg, device=0, stream=stream.cuda_stream, precision=hsd.BF1
                      vocab_perm=vocab_permutation(cfg.vocab, 0) if cfg.hot_tokens else None)
 ctx.prefill(prompts(cfg, batch=batch))
 for _ in range(3): ctx.step()
-ctx.build_tree(); ctx.verify_tree()   # the trace holds the last attention launch (verify layer 31)
-t = ctx.tensor("attn_trace").cpu().numpy().astype(np.int64)
+ctx.build_tree()
+if len(sys.argv) > 3:   # HSD_ATTN_EXP timing experiment on the traced verify pass only
+    os.environ["HSD_ATTN_EXP"] = sys.argv[3]
+ctx.verify_tree()   # the trace holds the last attention launch (verify layer 31)
+os.environ.pop("HSD_ATTN_EXP", None)
+t_all = ctx.tensor("attn_trace").cpu().numpy().astype(np.int64)
+t = t_all[:128]
+t1 = t_all[128:]   # CTA x = 1 (the pair follower in CTA-pair mode, else split 1)
 t0 = t[0]
 names = {0: "start", 1: "barriers+tmem", 2: "pdl_wait", 3: "Q landed (mma)", 4: "last PV done", 5: "end"}
 for i in [0, 1, 2, 3]:
@@ -29,3 +35,9 @@ for j in range(min(n, 16)):
           f"  | K{j} load issued {(t[96+j]-t0)/1e3:7.2f}  K{j} landed {(t[112+j]-t0)/1e3:7.2f}")
 for i in [4, 5]:
     print(f"{names[i]:16s} {(t[i]-t0)/1e3:8.2f} us")
+
+if t1[0] != 0:
+    print("CTA x=1 (pair follower / split 1), same origin")
+    for j in range(min(int(t1[7]), 10)):
+        print(f" chunk {j}: S ready {(t1[8+4*j]-t0)/1e3:7.2f}  max done {(t1[9+4*j]-t0)/1e3:7.2f}  P written {(t1[11+4*j]-t0)/1e3:7.2f}"
+              f"  | K{j} load issued {(t1[96+j]-t0)/1e3:7.2f}")

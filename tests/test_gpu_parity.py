@@ -243,11 +243,14 @@ def test_lockstep_c1_bf16_tcgen05():
 
 
 @pytest.mark.parametrize("hd,q_heads,kv_heads,prompt_len", [(64, 8, 2, 32), (64, 4, 4, 100), (128, 4, 4, 150),
-                                                           (128, 8, 2, 200), (128, 8, 2, 32)])
+                                                           (128, 8, 2, 200), (128, 8, 2, 32), (64, 16, 2, 100),
+                                                           (128, 16, 2, 150), (128, 32, 2, 300)])
 def test_lockstep_wide_bf16_tcgen05_planted(hd, q_heads, kv_heads, prompt_len):
     """Wider models so every GEMM spans several 128-row tiles and k-blocks of the
     tcgen05 GEMM, and the tcgen05 tree attention (hd 64/128, MHA and GQA) runs
-    over several 64-key pages and key splits."""
+    over several 64-key pages and key splits. GQA 16/2 and 32/2 (21 verify slots x
+    8 or 16 heads = 168 / 336 (row, head) pairs, 2 / 3 q-tiles) run the CTA-pair
+    (cta_group::2) attention, including an all-padding follower tile."""
     cfg = get_config("c1").replace(hidden=512, q_heads=q_heads, kv_heads=kv_heads, head_dim=hd, ffn=1024,
                                    vocab=1024, layers=2, steps_N=5, branch_k=3, budget_B=16,
                                    prompt_len=prompt_len)
