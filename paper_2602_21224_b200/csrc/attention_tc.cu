@@ -737,6 +737,406 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Two q-tiles per CTA (c3 / c4 / c5 verify, every prefill): the per-SM K / V stream
+// is the limit of the one-tile kernel -- each SM pulls ~57 GB/s through TMA at most
+// (scripts/experiments/tma2d_latency.cu) and every q-tile CTA of a (request, kv head)
+// pulls the whole K / V (c3: 3 tiles -> 3x the algorithmic bytes into SMs). Here one
+// CTA runs tiles 2c and 2c+1 (M = 256 rows) on every K / V chunk it loads: the S
+// and P V MMAs run once per tile on the same shared-memory chunk, the 4 x SW softmax
+// warps treat tile A then tile B (the tensor core does tile A's P V and next S while
+// the warps work on tile B), so the bytes streamed per (row, head) halve.
+// TMEM (512 columns): S_A, S_B (one 128-column buffer each: S_t(j+1) is issued after
+// P_t(j) V in the same order, and completes only after it) and O_A, O_B (hd columns).
+// Shared memory: q of both tiles, 2-stage K and V rings. l is summed by the softmax
+// warps (no ones row: no TMEM column left for it).
+template <int SW>
+__global__ void __launch_bounds__(nthreads<SW>(), 1)
+    attention_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                         const __grid_constant__ CUtensorMap tmV, AttnParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  constexpr int KSTAGES = 2, VSTAGES = 2;
+  const int hd = P.hd, natom = hd / 64;
+  const int q_bytes = QROWS * hd * 2;          // one tile: natom atoms of [128 rows x 128 B]
+  const int k_bytes = CHUNK * hd * 2;          // natom atoms of [128 keys x 128 B]
+  const int v_page = hd * 128;                 // one page's V^T atom column [hd rows x 128 B]
+  const int v_bytes = 2 * v_page;
+  uint8_t* sQ = base;                          // [2 tiles]
+  uint8_t* sK = sQ + 2 * q_bytes;
+  uint8_t* sV = sK + KSTAGES * k_bytes;
+  uint64_t* bars = (uint64_t*)(sV + VSTAGES * v_bytes);
+  uint64_t* kfull = bars;                 // [KSTAGES]
+  uint64_t* kempty = kfull + KSTAGES;     // [KSTAGES]
+  uint64_t* vfull = kempty + KSTAGES;     // [VSTAGES]
+  uint64_t* vempty = vfull + VSTAGES;     // [VSTAGES]
+  uint64_t* qbar = vempty + VSTAGES;
+  uint64_t* sfull = qbar + 1;             // [tile]
+  uint64_t* pfull = sfull + 2;            // [tile]
+  uint64_t* odone = pfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(odone + 1);
+  constexpr int KPW = CHUNK / SW;          // keys per softmax warp per chunk
+  constexpr int NSM = 128 * SW;
+  __shared__ int tile_lo, tile_hi, safe_hi, has_b;
+  __shared__ float red_max[2][2][SW][QROWS];   // [chunk parity][tile][key part][row]
+  __shared__ float red_l[2][SW][QROWS];        // [tile][key part][row]
+  __shared__ uint64_t anc_s[2][QROWS][4];      // tree-ancestor bits of every tile row
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int split = blockIdx.x, nsplit = gridDim.x, h = blockIdx.y;
+  const int nz = (P.n_qtiles + 1) / 2;
+  const int grp = blockIdx.z / nz, qt0 = 2 * (int)(blockIdx.z % nz);   // tiles qt0, qt0 + 1
+  const RowMeta& m = P.m;
+  const int req = m.req[grp * P.R];
+
+  if (threadIdx.x == 0) { tile_lo = 0x7fffffff; tile_hi = 0; safe_hi = 0x7fffffff; has_b = 0; TRACE(0); }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < KSTAGES; ++s) { mbar_init(&kfull[s], 1); mbar_init(&kempty[s], 1); }
+    for (int s = 0; s < VSTAGES; ++s) { mbar_init(&vfull[s], 1); mbar_init(&vempty[s], 1); }
+    mbar_init(qbar, 1);
+    for (int t = 0; t < 2; ++t) { mbar_init(&sfull[t], 1); mbar_init(&pfull[t], NSM / 32); }
+    mbar_init(odone, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();
+  // softmax threads: this lane's (row, head) in tile A and in tile B
+  const int q4 = warp & 3, lane_row = q4 * 32 + lane;
+  int row[2] = {-1, -1}, head[2] = {0, 0}, klo[2] = {0, 0}, khi[2] = {0, 0}, slot[2] = {-1, -1};
+  bool valid[2] = {false, false}, writable[2] = {false, false};
+  int tb = 0;
+  if (warp >= 3) {
+    const int part0 = ((warp - 3) >> 2) == 0;
+    for (int t = 0; t < 2; ++t) {
+      const int rh = (qt0 + t) * QROWS + lane_row;
+      const int rl = rh / P.G, g = rh % P.G;
+      row[t] = grp * P.R + rl;
+      head[t] = h * P.G + g;
+      writable[t] = qt0 + t < P.n_qtiles && rl < P.R && row[t] < P.M;
+      valid[t] = writable[t] && m.pos[row[t]] >= 0;
+      if (valid[t]) {
+        klo[t] = m.klo[row[t]]; khi[t] = m.khi[row[t]]; slot[t] = m.slot[row[t]];
+        int lo = klo[t], hi = khi[t];
+        if (slot[t] >= 0) {
+          tb = m.tbase[req];
+          if (part0)
+            for (int w = 0; w < 4; ++w)
+              anc_s[t][lane_row][w] = w < m.anc_words ? m.anc[((size_t)req * m.t_max + slot[t]) * m.anc_words + w] : 0ull;
+          lo = min(lo, tb);
+          hi = max(hi, tb + slot[t] + 1);
+        }
+        if (hi > lo) { atomicMin(&tile_lo, lo); atomicMax(&tile_hi, hi); }
+        if (t == 1) has_b = 1;
+      }
+    }
+    int pmin = 0x7fffffff;
+    for (int r = threadIdx.x - SM0; r < P.R; r += NSM) {
+      const int pr = grp * P.R + r < P.M ? m.pos[grp * P.R + r] : -1;
+      if (pr >= 0) pmin = min(pmin, pr);
+    }
+    if (pmin != 0x7fffffff) atomicMin(&safe_hi, pmin);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int ntile = has_b ? 2 : 1;
+  int k_begin, k_end;
+  if (P.dyn) {
+    const int c0 = tile_lo / CHUNK, c1 = (tile_hi + CHUNK - 1) / CHUNK;
+    const int cps = c1 > c0 ? (c1 - c0 + nsplit - 1) / nsplit : 0;
+    k_begin = (c0 + split * cps) * CHUNK;
+    k_end = k_begin + cps * CHUNK;
+  } else {
+    k_begin = split * P.keys_per_split;
+    k_end = min(P.max_keys, k_begin + P.keys_per_split);
+  }
+  const int lo = max(k_begin, tile_lo), hi = min(k_end, tile_hi);
+  const int c_first = lo / CHUNK;
+  const int n_chunks = hi > lo ? (hi + CHUNK - 1) / CHUNK - c_first : 0;
+  auto tS = [&](int t) { return tmem + (uint32_t)(t * 128); };          // S_t (P_t over its first 64 columns)
+  auto tO = [&](int t) { return tmem + 256u + (uint32_t)(t * 128); };   // O_t: hd columns
+
+  if (warp == 0) {
+    if (lane == 0 && n_chunks == 0) { l2pf_issue(P.pf); l2pf_issue(P.pf, 1); }
+    if (lane == 0 && n_chunks > 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
+      const uint64_t pol = P.n_qtiles > 2 ? policy_evict_normal() : policy_evict_first();
+      const uint64_t polq = policy_evict_last();
+      auto load_k = [&](int j) {
+        const int s = j % KSTAGES;
+        mbar_wait(&kempty[s], ((j / KSTAGES) & 1) ^ 1);
+        mbar_expect_tx(&kfull[s], k_bytes);
+        for (int pg = 0; pg < 2; ++pg) {
+          const int page = P.kv.block_table[(size_t)req * P.kv.pages_per_req + 2 * (c_first + j) + pg];
+          const int krow = ((page * 2 + 0) * P.kv.kv_heads + h) * PAGE;
+          for (int a = 0; a < natom; ++a)
+            tma_load_2d(&tmK, &kfull[s], sK + (size_t)s * k_bytes + a * (CHUNK * 128) + pg * (PAGE * 128), a * 64,
+                        krow, pol);
+        }
+      };
+      int kj = 0;
+      while (kj < n_chunks && kj < KSTAGES && (c_first + kj + 1) * CHUNK <= safe_hi) load_k(kj++);
+      pdl_wait();
+      kst_enter(P.kst);
+      mbar_expect_tx(qbar, ntile * q_bytes);
+      for (int t = 0; t < ntile; ++t) {
+        const int row0 = grp * P.R + (qt0 + t) * (QROWS / P.G);
+        for (int a = 0; a < natom; ++a)
+          tma_load_3d(&tmQ, qbar, sQ + (size_t)t * q_bytes + a * (QROWS * 128), a * 64, h * P.G, row0, polq);
+      }
+      while (kj < n_chunks) load_k(kj++);
+      l2pf_issue(P.pf);
+    }
+  } else if (warp == 2) {
+    if (lane == 0 && n_chunks > 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
+      const uint64_t pol = P.n_qtiles > 2 ? policy_evict_normal() : policy_evict_first();
+      auto load_v = [&](int j) {
+        const int s = j % VSTAGES;
+        mbar_wait(&vempty[s], ((j / VSTAGES) & 1) ^ 1);
+        mbar_expect_tx(&vfull[s], 2 * hd * 128);
+        for (int pg = 0; pg < 2; ++pg) {
+          const int page = P.kv.block_table[(size_t)req * P.kv.pages_per_req + 2 * (c_first + j) + pg];
+          tma_load_2d(&tmV, &vfull[s], sV + (size_t)s * v_bytes + pg * v_page, 0,
+                      ((page * 2 + 1) * P.kv.kv_heads + h) * hd, pol);
+        }
+      };
+      int vj = 0;
+      while (vj < n_chunks && vj < VSTAGES && (c_first + vj + 1) * CHUNK <= safe_hi) load_v(vj++);
+      pdl_wait();
+      while (vj < n_chunks) load_v(vj++);
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n_chunks > 0) {
+      mbar_wait(qbar, 0);
+      auto issue_s = [&](int t, int j) {   // S_t(j) = Q_t K_j^T
+        const int s = j % KSTAGES;
+        for (int kk = 0; kk < hd / 16; ++kk) {
+          const int a = kk >> 2, off = kk & 3;
+          const uint64_t ad = desc_sw128(sQ + (size_t)t * q_bytes + a * (QROWS * 128)) + 2 * off;
+          const uint64_t bd = desc_sw128(sK + (size_t)s * k_bytes + a * (CHUNK * 128)) + 2 * off;
+          mma_bf16(tS(t), ad, bd, P.idesc_s, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&sfull[t]);
+      };
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P_t from TMEM
+        const int s = j % VSTAGES;
+        for (int kk = 0; kk < CHUNK / 16; ++kk) {
+          const int ka = kk >> 2, off = kk & 3;
+          const uint64_t vd = desc_sw128(sV + (size_t)s * v_bytes + ka * v_page) + 2 * off;
+          mma_bf16_ts(tO(t), tS(t) + (uint32_t)(kk * 8), vd, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+      };
+      mbar_wait(&kfull[0], 0);
+      fence_after();
+      for (int t = 0; t < ntile; ++t) issue_s(t, 0);
+      mma_commit(&kempty[0]);
+      for (int j = 0; j < n_chunks; ++j) {
+        const bool more = j + 1 < n_chunks;
+        mbar_wait(&vfull[j % VSTAGES], (j / VSTAGES) & 1);
+        if (j < 16) TRACE(64 + 2 * j);           // V_j landed
+        mbar_wait(&pfull[0], j & 1);
+        fence_after();
+        issue_pv(0, j);
+        if (more) {   // tile A's next scores right behind its P V (S_A overwrites P_A in issue order)
+          mbar_wait(&kfull[(j + 1) % KSTAGES], ((j + 1) / KSTAGES) & 1);
+          fence_after();
+          if (j < 16) TRACE(65 + 2 * j);         // K_{j+1} landed
+          issue_s(0, j + 1);
+        }
+        if (ntile == 2) {
+          mbar_wait(&pfull[1], j & 1);
+          fence_after();
+          issue_pv(1, j);
+        }
+        mma_commit(&vempty[j % VSTAGES]);
+        if (more) {
+          if (ntile == 2) issue_s(1, j + 1);
+          mma_commit(&kempty[(j + 1) % KSTAGES]);
+        }
+      }
+      mma_commit(odone);
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warps
+    const int part = (warp - 3) >> 2;
+    const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const int hcols = hd / SW;
+    float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+    const bool live[2] = {__any_sync(0xffffffffu, valid[0]) != 0, __any_sync(0xffffffffu, valid[1]) != 0};
+    for (int j = 0; j < n_chunks; ++j) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (t >= ntile) break;
+        mbar_wait(&sfull[t], j & 1);   // also: P_t(j-1) V is done (issued before S_t(j))
+        fence_after();
+        if (threadIdx.x == SM0 && j < 12) TRACE(8 + 4 * j + 2 * t);       // S_t(j) ready
+        if (live[t]) {
+          const int kb = (c_first + j) * CHUNK + part * KPW;
+          uint32_t r0[32], r1[32];
+          tmem_ld32_nw(tS(t) + lane_off + (uint32_t)(part * KPW), r0);
+          if constexpr (KPW == 64) tmem_ld32_nw(tS(t) + lane_off + (uint32_t)(part * KPW + 32), r1);
+          uint32_t vm0 = 0u, vm1 = 0xffffffffu;
+          if (valid[t]) {
+            vm0 = range32(klo[t] - kb, khi[t] - kb);
+            if (slot[t] >= 0) {
+              const uint64_t(&an)[4] = anc_s[t][lane_row];
+              uint64_t a4[4] = {an[0], an[1], an[2], an[3]};
+              vm0 |= anc32(a4, kb - tb) & range32(0, m.t_max - (kb - tb));
+              if constexpr (KPW == 64) vm1 = range32(klo[t] - kb - 32, khi[t] - kb - 32) |
+                                             (anc32(a4, kb + 32 - tb) & range32(0, m.t_max - (kb + 32 - tb)));
+            } else if constexpr (KPW == 64) {
+              vm1 = range32(klo[t] - kb - 32, khi[t] - kb - 32);
+            }
+            vm0 &= range32(k_begin - kb, k_end - kb);
+            if constexpr (KPW == 64) vm1 &= range32(k_begin - kb - 32, k_end - kb - 32);
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float s[KPW];
+          if (__all_sync(0xffffffffu, (vm0 & vm1) == 0xffffffffu)) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              s[i] = __uint_as_float(r0[i]);
+              if constexpr (KPW == 64) s[32 + i] = __uint_as_float(r1[i]);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              s[i] = ((vm0 >> i) & 1u) ? __uint_as_float(r0[i]) : -INFINITY;
+              if constexpr (KPW == 64) s[32 + i] = ((vm1 >> i) & 1u) ? __uint_as_float(r1[i]) : -INFINITY;
+            }
+          }
+          float mxp[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mxp[k] = s[k];
+#pragma unroll
+          for (int i = 8; i < KPW; ++i) mxp[i & 7] = fmaxf(mxp[i & 7], s[i]);
+          float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                           fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+          red_max[j & 1][t][part][lane_row] = mx;
+          quad_sync<SW>(q4);
+#pragma unroll
+          for (int p2 = 0; p2 < SW; ++p2) mx = fmaxf(mx, red_max[j & 1][t][p2][lane_row]);
+          mx *= scale_log2;
+          float alpha = 1.f;   // lazy rescale (as in the one-tile kernel)
+          if (mrow[t] == -INFINITY) {
+            mrow[t] = mx;
+          } else if (mx > mrow[t] + 8.f) {
+            alpha = ex2(mrow[t] - mx);
+            mrow[t] = mx;
+          }
+          const float msub = mrow[t] == -INFINITY ? 0.f : mrow[t];
+          float ps[4] = {0.f, 0.f, 0.f, 0.f};
+          uint32_t pw[32];
+#pragma unroll
+          for (int i = 0; i < KPW / 2; ++i) {
+            const float p0 = ex2(fmaf(s[2 * i], scale_log2, -msub)), p1 = ex2(fmaf(s[2 * i + 1], scale_log2, -msub));
+            ps[i & 3] += p0 + p1;
+            __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
+            pw[i] = *(uint32_t*)&pr;
+          }
+          if constexpr (KPW == 64) {
+            tmem_st32(tS(t) + lane_off + (uint32_t)(part * 32), pw);
+          } else {
+            uint32_t pw16[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pw16[i] = pw[i];
+            tmem_st16(tS(t) + lane_off + (uint32_t)(part * 16), pw16);
+          }
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {   // O_t holds P_t(<j) V: S_t(j) completing implies it
+            for (int c = 0; c < hcols; c += 16) {
+              uint32_t o[16];
+              tmem_ld16(tO(t) + lane_off + (uint32_t)(part * hcols + c), o);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st16(tO(t) + lane_off + (uint32_t)(part * hcols + c), o);
+            }
+          }
+          lrow[t] = lrow[t] * alpha + ((ps[0] + ps[1]) + (ps[2] + ps[3]));
+          tmem_st_wait();
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull[t]);
+        if (threadIdx.x == SM0 && j < 12) TRACE(9 + 4 * j + 2 * t);       // P_t(j) written
+      }
+    }
+    // ------------------------------------------------------------ epilogue
+    if (threadIdx.x == SM0 && P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) P.trace[7] = n_chunks;
+    for (int t = 0; t < 2; ++t) red_l[t][part][lane_row] = lrow[t];
+    if (n_chunks > 0) {
+      mbar_wait(odone, 0);
+      fence_after();
+    }
+    float* ostage = (float*)sK;                       // [128 rows][hd + 4] (K / V rings idle now)
+    const int ost = hd + 4;
+    for (int t = 0; t < ntile; ++t) {
+      asm volatile("bar.sync 5, %0;" ::"r"(NSM) : "memory");   // red_l written / the previous tile's rows read
+      float ltot = 0.f;
+#pragma unroll
+      for (int p2 = 0; p2 < SW; ++p2) ltot += red_l[t][p2][lane_row];
+      if (!valid[t]) ltot = 0.f;
+      const float inv = (P.direct && ltot > 0.f) ? 1.0f / ltot : 1.0f;
+      for (int c = 0; c < hcols; c += 16) {
+        uint32_t o[16];
+        if (n_chunks > 0) tmem_ld16(tO(t) + lane_off + (uint32_t)(part * hcols + c), o);
+        else
+          for (int i = 0; i < 16; ++i) o[i] = 0u;
+        float* dst = ostage + lane_row * ost + part * hcols + c;
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          *(float4*)(dst + i) = ltot > 0.f ? make_float4(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv,
+                                                         __uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      asm volatile("bar.sync 5, %0;" ::"r"(NSM) : "memory");   // all rows of tile t staged
+      const int qt = qt0 + t;
+      const int sw = (threadIdx.x - SM0) >> 5;
+      const int n_rh = min(QROWS, P.R * P.G - qt * QROWS);
+      const int vpr = hd / 4, rpi = 32 / vpr;
+      const int d4 = (lane % vpr) * 4;
+      const int step = 4 * SW * rpi, step_rl = step / P.G, step_g = step % P.G;
+      int lr = sw * rpi + lane / vpr;
+      int rl2 = (qt * QROWS + lr) / P.G, g2 = (qt * QROWS + lr) % P.G;
+      for (; lr < n_rh; lr += step) {
+        const int row2 = grp * P.R + rl2, head2 = h * P.G + g2;
+        if (row2 < P.M) {
+          const float4 x = *(const float4*)(ostage + lr * ost + d4);
+          if (P.direct) {
+            const __nv_bfloat162 a = __floats2bfloat162_rn(x.x, x.y), b = __floats2bfloat162_rn(x.z, x.w);
+            *(uint2*)(P.out + ((size_t)row2 * P.Hq + head2) * hd + d4) =
+                make_uint2(*(const uint32_t*)&a, *(const uint32_t*)&b);
+          } else {
+            *(float4*)(P.ws + (((size_t)split * P.Hq + head2) * P.M + row2) * hd + d4) = x;
+          }
+        }
+        rl2 += step_rl;
+        g2 += step_g;
+        if (g2 >= P.G) { g2 -= P.G; ++rl2; }
+      }
+      if (!P.direct && writable[t] && part == 0) {
+        const size_t base_ml = (size_t)nsplit * P.M * P.Hq * hd;
+        const size_t idx = ((size_t)split * P.Hq + head[t]) * P.M + row[t];
+        P.ws[base_ml + 2 * idx] = mrow[t];
+        P.ws[base_ml + 2 * idx + 1] = ltot;
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  kst_exit(P.kst);
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+}
+
 // split merge: one warp per (row, head), lanes over hd:
 // o = sum_s e^{m_s - M} o_s / sum_s e^{m_s - M} l_s
 __global__ void attention_merge_bf16_kernel(const float* __restrict__ ws, int S, int M, int Hq, int hd,
@@ -798,8 +1198,13 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   // per-warp remote pfull arrivals (release.cluster) cost ~0.6 us per chunk, so the
   // pair runs at ~2 us per chunk although each SM streams half of it
   static const int pair_env = [] { const char* e = getenv("HSD_ATTN_PAIR"); return e ? atoi(e) : 0; }();
+  // two q-tiles per CTA (attention_tc2_kernel) whenever a (request, kv head) spans >= 2
+  // q-tiles: c3 / c4 / c5 verify, prefill. HSD_ATTN_TC2=0 keeps one tile per CTA.
+  static const int tc2_env = [] { const char* e = getenv("HSD_ATTN_TC2"); return e ? atoi(e) : 0; }();
+  const bool tc2 = tc2_env && !pair_env && P.n_qtiles >= 2;
   const bool pair = pair_env && P.n_qtiles >= 2;
   if (pair) P.n_qtiles += P.n_qtiles & 1;
+  const int z_per_group = tc2 ? (P.n_qtiles + 1) / 2 : P.n_qtiles;   // CTAs along z per (request, kv head)
   {   // read per launch: scripts/attn_trace.py switches it on for the traced pass only
     const char* e = getenv("HSD_ATTN_EXP");
     P.exp_flags = e ? atoi(e) : 0;
@@ -811,9 +1216,9 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   (void)trace_init;
   P.trace = g_attn_trace;
   P.idesc_s = idesc_bf16(pair ? 256 : 128, CHUNK);
-  P.idesc_o = idesc_bf16(pair ? 256 : 128, hd + VEXTRA);   // O columns [0, hd) + l in column hd
+  P.idesc_o = idesc_bf16(pair ? 256 : 128, tc2 ? hd : hd + VEXTRA);   // O columns [0, hd) (+ l in column hd)
   // splits: enough CTAs for ~2 per SM, each split a whole number of pages
-  const int base_ctas = n_req * kv.kv_heads * P.n_qtiles;
+  const int base_ctas = n_req * kv.kv_heads * z_per_group;
   const int pages = (max_keys + CHUNK - 1) / CHUNK;     // chunks of 2 pages
   // key splits: the kernel holds ~190 KB of shared memory and all 512 TMEM
   // columns (one CTA per SM) and pays ~3 chunk-times of fixed cost per CTA (PDL
@@ -844,7 +1249,7 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
     const char* e = getenv("HSD_ATTN_CLUSTER_MAX");
     return e ? atoi(e) : 2;
   }();
-  P.cluster = (!pair && S >= 2 && S <= cluster_max && S <= 8) ? 1 : 0;
+  P.cluster = (!pair && !tc2 && S >= 2 && S <= cluster_max && S <= 8) ? 1 : 0;
   while (!P.cluster && S > 1 && (size_t)S * M * Hq * (hd + 2) > ws_floats) --S;
   int pps = (pages + S - 1) / S;
   P.keys_per_split = pps * CHUNK;
@@ -868,10 +1273,12 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   if (!tma_map_bf16(&mq, q, 3, dq, sq, bq) || !tma_map_bf16(&mk, kv.base, 2, dk, sk, bk) ||
       !tma_map_bf16(&mv, kv.base, 2, dv, sv, bv) || !tma_map_bf16(&mv2, kv.base, 2, dv, sv, bv2))
     return -1;
-  const int kst = 4, vst = pair ? 4 : 2;
-  const size_t smem = 1024 + (pair ? (size_t)QROWS * hd * 2 : 0) + kst * ((size_t)(pair ? PAGE : CHUNK) * hd * 2) +
-                      vst * ((size_t)2 * (pair ? (hd + VEXTRA) / 2 : hd + VEXTRA) * 128) +
-                      (2 * kst + 2 * vst + 8) * 8 + 64;
+  const int kst = tc2 ? 2 : 4, vst = (pair ? 4 : 2);
+  const size_t smem = tc2 ? 1024 + 2 * (size_t)QROWS * hd * 2 + kst * ((size_t)CHUNK * hd * 2) +
+                                vst * ((size_t)2 * hd * 128) + (2 * kst + 2 * vst + 8) * 8 + 64
+                          : 1024 + (pair ? (size_t)QROWS * hd * 2 : 0) + kst * ((size_t)(pair ? PAGE : CHUNK) * hd * 2) +
+                                vst * ((size_t)2 * (pair ? (hd + VEXTRA) / 2 : hd + VEXTRA) * 128) +
+                                (2 * kst + 2 * vst + 8) * 8 + 64;
   // softmax warps per lane quarter: 2 (8 softmax warps, 64 keys each) or 4 (16 warps,
   // 32 keys each: shorter per-thread chains, more warps to hide TMEM/barrier latency).
   // Measured: c3 (768 CTAs, many waves) attention 11.6 -> 11.1
@@ -879,7 +1286,7 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   // HSD_ATTN_SW=2|4 forces one.
   static const int sw_env = [] { const char* e = getenv("HSD_ATTN_SW"); return e ? atoi(e) : 0; }();
   const int sw = sw_env == 2 || sw_env == 4 ? sw_env : ((size_t)S * base_ctas > 2 * (size_t)num_sms() ? 4 : 2);
-  static size_t attr[4] = {0, 0, 0, 0};   // (the kernel also has ~1-3 KB of static shared memory)
+  static size_t attr[6] = {0, 0, 0, 0, 0, 0};   // (the kernels also have ~2-18 KB of static shared memory)
   auto launch = [&](auto kern, int nthr, size_t& at) {
     if (smem > at) {
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
@@ -888,7 +1295,7 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
       }
       at = smem;
     }
-    dim3 grid(pair ? 2 * S : S, kv.kv_heads, n_req * (pair ? P.n_qtiles / 2 : P.n_qtiles));
+    dim3 grid(pair ? 2 * S : S, kv.kv_heads, n_req * (pair ? P.n_qtiles / 2 : z_per_group));
     if (pair) launch_k_cluster(kern, grid, dim3(nthr), smem, st, 2, mq, mk, mv, mv2, P);
     else if (P.cluster) launch_k_cluster(kern, grid, dim3(nthr), smem, st, S, mq, mk, mv, mv2, P);
     else launch_k(kern, grid, dim3(nthr), smem, st, mq, mk, mv, mv2, P);
@@ -899,8 +1306,21 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
     }
     return true;
   };
+  auto launch3 = [&](auto kern, int nthr, size_t& at) {   // two-tile kernel: (q, K, V) maps
+    if (smem > at) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      at = smem;
+    }
+    launch_k(kern, dim3(S, kv.kv_heads, n_req * z_per_group), dim3(nthr), smem, st, mq, mk, mv, P);
+    return true;
+  };
   bool ok;
-  if (pair) ok = sw == 4 ? launch(attention_tc_kernel<4, true>, nthreads<4>(), attr[3])
+  if (tc2) ok = sw == 4 ? launch3(attention_tc2_kernel<4>, nthreads<4>(), attr[5])
+                        : launch3(attention_tc2_kernel<2>, nthreads<2>(), attr[4]);
+  else if (pair) ok = sw == 4 ? launch(attention_tc_kernel<4, true>, nthreads<4>(), attr[3])
                          : launch(attention_tc_kernel<2, true>, nthreads<2>(), attr[2]);
   else ok = sw == 4 ? launch(attention_tc_kernel<4, false>, nthreads<4>(), attr[1])
                     : launch(attention_tc_kernel<2, false>, nthreads<2>(), attr[0]);

@@ -41,3 +41,10 @@ if t1[0] != 0:
     for j in range(min(int(t1[7]), 10)):
         print(f" chunk {j}: S ready {(t1[8+4*j]-t0)/1e3:7.2f}  max done {(t1[9+4*j]-t0)/1e3:7.2f}  P written {(t1[11+4*j]-t0)/1e3:7.2f}"
               f"  | K{j} load issued {(t1[96+j]-t0)/1e3:7.2f}")
+
+if os.environ.get("TC2_TRACE"):
+    print("two-tile kernel: per chunk  S_A ready / P_A written / S_B ready / P_B written; MMA warp: V_j landed, K_j+1 landed")
+    for j in range(min(int(t[7]), 12)):
+        f = lambda i: (t[i] - t0) / 1e3
+        print(f" chunk {j:2d}: A {f(8+4*j):7.2f} {f(9+4*j):7.2f}   B {f(10+4*j):7.2f} {f(11+4*j):7.2f}   "
+              f"| V{j} {f(64+2*j):7.2f} K{j+1} {f(65+2*j):7.2f}")
