@@ -213,26 +213,6 @@ inline void launch_k_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size
   cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-template <typename... KArgs, typename... Args>
-inline void launch_k_cluster3(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                              dim3 cluster, Args&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cluster.x;
-  attr[0].val.clusterDim.y = cluster.y;
-  attr[0].val.clusterDim.z = cluster.z;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = g_hsd_pdl ? 2 : 1;
-  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
-}
-
 // ---------------------------------------------------------------- error word
 #define DEV_ERR_BAD_TREE 1
 #define DEV_ERR_BAD_TOKEN 2

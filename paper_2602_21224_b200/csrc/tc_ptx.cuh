@@ -104,47 +104,12 @@ HSD_DEV void mma_bf16_2sm(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t ide
       "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
       : "memory");
 }
-// O += P V with A (P) in each CTA's TMEM and B (V^T halves) in each CTA's shared memory
-HSD_DEV void mma_bf16_ts_2sm(uint32_t dtmem, uint32_t atmem, uint64_t bd, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dtmem),
-      "r"(atmem), "l"(bd), "r"(idesc), "r"(acc)
-      : "memory");
-}
-// 3-D tile into this CTA's shared memory, bytes completing on the pair leader's mbarrier
-HSD_DEV void tma_load_3d_2sm(const CUtensorMap* map, uint32_t bar_cluster, void* dst, int c0, int c1, int c2,
-                             uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
-      : "memory");
-}
 // commit the pair's MMAs to the mbarrier at the same offset in the CTAs of `mask`
 HSD_DEV void mma_commit_2sm(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
       "h"(mask)
-      : "memory");
-}
-// commit this CTA's MMAs (cta_group::1) to the mbarrier at the same offset in every CTA of `mask`
-HSD_DEV void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-// TMA 2-D load multicast to the same shared-memory offset (and mbarrier offset) in
-// every CTA of `mask`; each destination's mbarrier receives the box's bytes
-HSD_DEV void tma_load_2d_mc(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, uint16_t mask,
-                            uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
-      " [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
       : "memory");
 }
 HSD_DEV void mbar_arrive_cluster(uint32_t bar_cluster) {

@@ -121,7 +121,8 @@ def run_lockstep(cfg, precision, steps, seed=0, batch=1, planted=False, accept="
                   tcgen05=tcgen05)
     ls = Lockstep(ctx, cfg, m, table, pr, seed=seed, accept=accept, plant=plant, plant_rates=rates, perm=perm,
                   logit_tol=tol or (1e-4 if precision == hsd.FP32_VERIFY else 2e-2),
-                  flag_margin=flag or (1e-4 if precision == hsd.FP32_VERIFY else 1e-2))
+                  flag_margin=flag or (1e-4 if precision == hsd.FP32_VERIFY else 1e-2),
+                  tree_flag_margin=None if precision == hsd.FP32_VERIFY else 2 * (tol or 2e-2))
     first, ofirst = ls.start()
     if planted:
         ctx.set_plant(np.stack(plant))
