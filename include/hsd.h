@@ -48,12 +48,19 @@ enum { HSD_FP32_VERIFY = 0, HSD_BF16 = 1 };          /* hsd_config.precision   *
 enum { HSD_GREEDY = 0, HSD_STOCHASTIC = 1 };         /* hsd_config.accept_mode */
 enum {                                               /* hsd_config.flags       */
   HSD_FLAG_RESAMPLE = 1u << 0,  /* Alg. 2 re-sampling              */
-  HSD_FLAG_FUSION = 1u << 1,    /* verification fusion             */
+  HSD_FLAG_FUSION = 1u << 1,    /* verification fusion. RESAMPLE
+                                   without FUSION = the paper's ablation:
+                                   the re-sampled tree is verified by a dedicated
+                                   extra target pass inside the same step        */
   HSD_FLAG_PLANTED = 1u << 2,   /* planted-continuation perf mode (DESIGN R24) */
   HSD_FLAG_ZERO_TABLE = 1u << 3,/* token info off: Alg. 1 == beam tree */
   HSD_FLAG_TCGEN05 = 1u << 4,   /* bf16 GEMMs on tcgen05 (else SIMT FFMA)       */
-  HSD_FLAG_TABLE_FP8 = 1u << 5  /* token-info table as e4m3 codes + a per-row
+  HSD_FLAG_TABLE_FP8 = 1u << 5, /* token-info table as e4m3 codes + a per-row
                                    fp32 scale (DESIGN R25)        */
+  HSD_FLAG_NO_FIRST_TOKEN = 1u << 6 /* "w/o first token" (Table 4, P:511-533;
+                                   R26): the root pair -- the ground-truth token
+                                   just committed -- enters the draft as
+                                   W_fc [H; 0], without its embedding            */
 };
 
 #define HSD_MAX_PLANT_DEPTH 16
@@ -154,6 +161,16 @@ hsd_status hsd_prefill(hsd_ctx* ctx, int32_t n_req, const int32_t* h_tokens, int
  * reuses the noise of the slot's earlier requests.                             */
 hsd_status hsd_admit(hsd_ctx* ctx, int32_t slot, const int32_t* h_tokens, int32_t len, int32_t req_id,
                      int32_t* d_first);
+
+/* Paged KV (P:95's cache): the block table maps (slot r, logical
+ * page i) to a physical page of the KV pools -- every kernel that reads or writes
+ * K / V (prefill, qkv_rope_kv, tree attention, compaction, the draft layer) goes
+ * through it. h_table: HOST [max_batch, pages_per_req] int32, a permutation of
+ * [0, max_batch * pages_per_req) (pages_per_req = hsd_get_tensor("block_table")
+ * dims[1]); copied. The KV contents are not moved, so set it before hsd_prefill
+ * (the default is the identity). HSD_EINVAL if not a permutation; HSD_ESTATE
+ * inside a staged step. Drops the captured step graphs.                       */
+hsd_status hsd_set_block_table(hsd_ctx* ctx, const int32_t* h_table);
 
 /* Planted mode only: HOST row-major [n_req, stride] greedy continuation tokens
  * indexed by absolute position (R24). Copied. */

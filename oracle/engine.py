@@ -45,12 +45,13 @@ class Request:
 
 class Engine:
     def __init__(self, model, table, cfg, seed=0, accept=None, temperature=None,
-                 resample=True, fusion=True, req_offset=0, plant=None, plant_rates=None):
+                 resample=True, fusion=True, req_offset=0, plant=None, plant_rates=None, first_token=True):
         self.m, self.table, self.cfg = model, table, cfg
         self.seed = seed
         self.accept = accept or cfg.accept
         self.T = cfg.temperature if temperature is None else temperature
         self.resample, self.fusion = resample, fusion
+        self.first_token = first_token   # False: the root pair's draft input omits E(t_p) (R26, Table 4)
         self.req_offset = req_offset
         self.plant, self.plant_rates = plant, plant_rates
         self.reqs = []
@@ -109,8 +110,11 @@ class Engine:
 
     def _draft_prefill(self, q, pairs):
         h = None
+        p_root = len(q.tokens) - 1
         for H_prev, t, j in pairs:
-            x = self.m.draft_input(H_prev, t)
+            # R26 ("w/o first token", Table 4): the root pair -- the ground-truth token
+            # just committed -- enters the draft without its embedding
+            x = self.m.draft_input(H_prev, t, with_token=self.first_token or j != p_root)
             dk = [q.dkv[i][0] for i in range(1, j)]
             dv = [q.dkv[i][1] for i in range(1, j)]
             h, k, v = self.m.draft_one(x, j, dk, dv)
@@ -186,25 +190,50 @@ class Engine:
                 acc, bonus = stochastic_walk(lin, logits, self.T, self.seed, self.req_ids[ri],
                                              self.step_idx, mg)
             mm = len(acc)
-            last = acc[-1] if acc else 0                                   # S4
-            for l in range(self.m.n_layers):
-                q.kv[l][0].extend(path_rows[last][l][0])
-                q.kv[l][1].extend(path_rows[last][l][1])
-            path_slots = [0] + acc
-            new_tokens = [int(lin["tok"][s]) for s in acc] + [int(bonus)]
-            q.pend = [(H[s], new_tokens[j], p + 1 + j) for j, s in enumerate(path_slots)]
-            q.H.extend(H[s] for s in path_slots)
-            q.tokens.extend(new_tokens)
+            new_tokens = self._commit(q, lin, H, path_rows, acc, bonus, append=False)
             pending = None
             if self.resample and N - mm - 1 > r:                          # Alg. 2
                 pending = T.prune(T.resample(L[mm + 1:], int(bonus), k, r, self.table), Br)
             q.pending = pending
             rec = {"L": L, "chain": np.stack(chain), "fresh": fresh, "lin": lin, "H": H,
-                   "logits": logits, "acc": acc, "bonus": int(bonus), "emitted": new_tokens,
+                   "logits": logits, "acc": acc, "bonus": int(bonus), "emitted": list(new_tokens),
                    "pending": pending, "margins": mg, "p": p}
+            if self.resample and not self.fusion and pending is not None and len(pending) > 1:
+                # re-sampling WITHOUT verification fusion (the ablation of
+                # Fig. 12): the re-sampled tree, rooted at the bonus token, is verified in a
+                # dedicated extra pass of the same step (its own random-stream step index)
+                lin2 = T.linearize(pending)
+                H2, logits2, rows2 = self.verify(q, lin2)
+                if self.accept == "greedy":
+                    acc2, bonus2 = greedy_walk(lin2, logits2, mg)
+                else:
+                    acc2, bonus2 = stochastic_walk(lin2, logits2, self.T, self.seed, self.req_ids[ri],
+                                                   self.step_idx + 1, mg)
+                new_tokens = new_tokens + self._commit(q, lin2, H2, rows2, acc2, bonus2, append=True)
+                q.pending = None
+                rec.update({"lin2": lin2, "acc2": acc2, "bonus2": int(bonus2), "emitted": list(new_tokens)})
             self.trace.append((self.step_idx, ri, rec))
             out.append(new_tokens)
+        if self.resample and not self.fusion:
+            self.step_idx += 1      # the extra verify pass counts as a step of the random streams
         return out
+
+    def _commit(self, q, lin, H, path_rows, acc, bonus, append):
+        """S4: the accepted path's KV rows and hidden states, the new draft pairs
+        (H_{j-1}, t_j) (appended to the step's earlier pairs when `append`), the
+        committed tokens. Returns the new tokens."""
+        p = len(q.tokens) - 1
+        last = acc[-1] if acc else 0
+        for l in range(self.m.n_layers):
+            q.kv[l][0].extend(path_rows[last][l][0])
+            q.kv[l][1].extend(path_rows[last][l][1])
+        path_slots = [0] + acc
+        new_tokens = [int(lin["tok"][s]) for s in acc] + [int(bonus)]
+        pairs = [(H[s], new_tokens[j], p + 1 + j) for j, s in enumerate(path_slots)]
+        q.pend = (q.pend + pairs) if append else pairs
+        q.H.extend(H[s] for s in path_slots)
+        q.tokens.extend(new_tokens)
+        return new_tokens
 
     def decode(self, prompts, max_new):
         """Run prefill + steps until every request has max_new new tokens;

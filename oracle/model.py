@@ -157,9 +157,11 @@ class Model:
     # ------------------------------------------------------------------
     # Draft head.
     # ------------------------------------------------------------------
-    def draft_input(self, H_prev: np.ndarray, token: int) -> np.ndarray:
-        """h_0 (+) E(t): W_fc [H_{j-1} ; E(t_j)] (reading R1)."""
-        return self.fc @ np.concatenate([H_prev, self.embed[token]])
+    def draft_input(self, H_prev: np.ndarray, token: int, with_token: bool = True) -> np.ndarray:
+        """h_0 (+) E(t): W_fc [H_{j-1} ; E(t_j)] (reading R1); with_token=False
+        drops the token half, W_fc [H_{j-1} ; 0] (the "w/o first token" ablation, R26)."""
+        e = self.embed[token] if with_token else np.zeros(self.cfg.hidden)
+        return self.fc @ np.concatenate([H_prev, e])
 
     def draft_one(self, x: np.ndarray, pos: int, dk, dv):
         """TransformerLayer(x) at draft position `pos` over draft KV rows dk/dv."""

@@ -91,6 +91,12 @@ __global__ void __launch_bounds__(WT) walk_kernel(AcceptParams P) {
   const int* tok = P.t_tok + req * T;
   const int* par = P.t_par + req * T;
   const int n = P.t_n[req];
+  if (P.append && n == 0) {   // no re-sampled tree to verify for this request
+    if (threadIdx.x == 0) P.acc_n[req] = -1;
+    return;
+  }
+  // append: tokens follow the step's first pass; at most N + 1 emitted per step
+  const int n0 = P.append ? P.n_emitted[req] : 0, cap = P.N - n0;
   if (threadIdx.x == 0) { m_sh = 0; cur_sh = 0; done_sh = 0; }
   __syncthreads();
   if (P.mode == 0) {
@@ -101,7 +107,7 @@ __global__ void __launch_bounds__(WT) walk_kernel(AcceptParams P) {
         int nxt = -1;
         for (int s = cur + 1; s < n; ++s)
           if (par[s] == cur && tok[s] == a) { nxt = s; break; }
-        if (nxt < 0 || m >= P.N) { bonus_sh = a; break; }
+        if (nxt < 0 || m >= cap) { bonus_sh = a; break; }
         acc[m++] = nxt;
         cur = nxt;
       }
@@ -131,7 +137,7 @@ __global__ void __launch_bounds__(WT) walk_kernel(AcceptParams P) {
           else { if (n_excl < 64) excl[n_excl++] = t; S += pc; }
           ++rank;
         }
-        if (took >= 0 && m_sh < P.N) { acc[m_sh++] = took; cur_sh = took; }
+        if (took >= 0 && m_sh < cap) { acc[m_sh++] = took; cur_sh = took; }
         else done_sh = 1;
       }
       __syncthreads();
@@ -145,17 +151,17 @@ __global__ void __launch_bounds__(WT) walk_kernel(AcceptParams P) {
   }
   // outputs
   const int m = m_sh;
-  for (int j = threadIdx.x; j <= P.N; j += blockDim.x) {
+  for (int j = n0 + threadIdx.x; j <= P.N; j += blockDim.x) {
     int v = -1;
-    if (j < m) v = tok[acc[j]];
-    else if (j == m) v = bonus_sh;
+    if (j - n0 < m) v = tok[acc[j - n0]];
+    else if (j - n0 == m) v = bonus_sh;
     P.emitted[req * (P.N + 1) + j] = v;
   }
   for (int j = threadIdx.x; j < P.N; j += blockDim.x) P.acc_slots[req * P.N + j] = j < m ? acc[j] : -1;
   if (threadIdx.x == 0) {
     P.acc_n[req] = m;
     P.bonus[req] = bonus_sh;
-    P.n_emitted[req] = m + 1;
+    P.n_emitted[req] = n0 + m + 1;
   }
 }
 
@@ -167,7 +173,7 @@ __global__ void compact_kernel(CompactParams P) {
   const int req = blockIdx.x, layer = blockIdx.y, kh = blockIdx.z;
   const int kind = kh / P.kv_heads, h = kh % P.kv_heads;
   const int m = P.acc_n[req];
-  if (m == 0) return;
+  if (m <= 0) return;   // (-1: request skipped by the extra verify pass)
   const int p = P.p[req], hd = P.head_dim, ps = P.page_size;
   T* base = (T*)P.kv_base + (size_t)layer * P.layer_stride;
   for (int d = threadIdx.x; d < hd; d += blockDim.x) {
@@ -196,21 +202,72 @@ __global__ void commit_kernel(CommitParams P) {
   const int req = blockIdx.x;
   const int m = P.acc_n[req];
   const int n = P.hidden;
+  if (threadIdx.x == 0 && req == 0) atomicAdd(P.step, 1);   // one random-stream step per verify pass
+  if (m < 0) return;                                        // skipped by the extra verify pass
+  // this pass's tokens start at e0 of the step's emitted row; its pairs at o0 of the pending pairs
+  const int e0 = P.n_emitted[req] - (m + 1), o0 = P.append ? P.n_pend[req] : 0;
   for (int j = 0; j <= m; ++j) {
     int slot = j == 0 ? 0 : P.acc_slots[req * P.N + j - 1];
     const float* src = P.Hverify + ((size_t)req * P.t_max + slot) * n;
-    float* dst = P.pend_H + ((size_t)req * (P.N + 1) + j) * n;
+    float* dst = P.pend_H + ((size_t)req * (P.N + 1) + o0 + j) * n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
   }
+  __syncthreads();   // every thread has read n_pend before thread 0 updates it
   if (threadIdx.x == 0) {
-    for (int j = 0; j <= P.N; ++j)
-      P.pend_tok[req * (P.N + 1) + j] = j <= m ? P.emitted[req * (P.N + 1) + j] : -1;
-    P.n_pend[req] = m + 1;
+    for (int j = o0; j <= P.N; ++j)
+      P.pend_tok[req * (P.N + 1) + j] = j - o0 <= m ? P.emitted[req * (P.N + 1) + e0 + j - o0] : -1;
+    P.n_pend[req] = o0 + m + 1;
     P.root_tok[req] = P.bonus[req];
     P.p[req] += m + 1;
-    if (req == 0) atomicAdd(P.step, 1);
   }
 }
+// the Alg. 2 pending tree as a verify tree (one thread per request; <= 64 nodes)
+__global__ void pending_as_tree_kernel(const int32_t* pt_n, const int32_t* pt_tok, const int32_t* pt_par,
+                                       const int32_t* pt_depth, const float* pt_lj, int br1, int32_t* t_n,
+                                       int32_t* t_tok, int32_t* t_par, int32_t* t_depth, float* t_lj,
+                                       uint64_t* t_anc, int t_max, int anc_words) {
+  pdl_wait();
+  pdl_trigger();
+  const int r = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  const int n = min(pt_n[r], br1);
+  if (n <= 1) { t_n[r] = 0; return; }
+  const int32_t* tk = pt_tok + r * br1;
+  const int32_t* pa = pt_par + r * br1;
+  const float* lj = pt_lj + r * br1;
+  int order[64], slot_of[64];
+  int len = 1, head = 0;
+  order[0] = 0; slot_of[0] = 0;
+  while (head < len) {   // BFS; the children of u by (lj desc, token asc, creation order)
+    const int u = order[head++];
+    int start = len;
+    for (int c = 1; c < n; ++c)
+      if (pa[c] == u) order[len++] = c;
+    for (int i = start + 1; i < len; ++i) {   // insertion sort of the new children
+      const int c = order[i];
+      int j = i - 1;
+      while (j >= start && (lj[order[j]] < lj[c] || (lj[order[j]] == lj[c] && tk[order[j]] > tk[c]))) {
+        order[j + 1] = order[j];
+        --j;
+      }
+      order[j + 1] = c;
+    }
+    for (int i = start; i < len; ++i) slot_of[order[i]] = i;
+  }
+  for (int s = 0; s < len; ++s) {
+    const int i = order[s];
+    const int ps = s == 0 ? -1 : slot_of[pa[i]];
+    t_tok[r * t_max + s] = tk[i];
+    t_par[r * t_max + s] = ps;
+    t_depth[r * t_max + s] = pt_depth[r * br1 + i];
+    t_lj[r * t_max + s] = lj[i];
+    uint64_t* a = t_anc + ((size_t)r * t_max + s) * anc_words;
+    for (int w = 0; w < anc_words; ++w) a[w] = ps >= 0 ? t_anc[((size_t)r * t_max + ps) * anc_words + w] : 0ull;
+    a[s >> 6] |= 1ull << (s & 63);
+  }
+  t_n[r] = len;
+}
+
 // test hook (hsd_debug_gumbel): pair i = one Gumbel-max draw over logits row row[i]
 // with the walk's own device function and Philox stream (seed, req, step, slot[i])
 __global__ void __launch_bounds__(WT) gumbel_debug_kernel(const float* logits, int ld, int V, float invT, uint32_t seed,
@@ -230,6 +287,15 @@ void launch_gumbel_debug(const float* logits, int ld, int V, float temperature, 
   if (n > 0)
     gumbel_debug_kernel<<<n, WT, 0, st>>>(logits, ld, V, 1.0f / temperature, seed, (uint32_t)req, (uint32_t)step, row,
                                           slot, out);
+}
+
+void launch_pending_as_tree(const int32_t* pt_n, const int32_t* pt_tok, const int32_t* pt_par,
+                            const int32_t* pt_depth, const float* pt_lj, int br1, int32_t* t_n, int32_t* t_tok,
+                            int32_t* t_par, int32_t* t_depth, float* t_lj, uint64_t* t_anc, int t_max, int anc_words,
+                            int n_req, cudaStream_t st) {
+  if (n_req > 0)
+    launch_k(pending_as_tree_kernel, n_req, 32, 0, st, pt_n, pt_tok, pt_par, pt_depth, pt_lj, br1, t_n, t_tok, t_par,
+             t_depth, t_lj, t_anc, t_max, anc_words);
 }
 
 void launch_walk(const AcceptParams& P, int n_req, cudaStream_t st) {

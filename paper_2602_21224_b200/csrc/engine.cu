@@ -70,7 +70,7 @@ __global__ void meta_verify_kernel(MetaBuf mb, int T, const int32_t* t_n, const 
 // draft prefill rows r*(N+1) + j: pending pair j at position p - n_pend + 1 + j,
 // causal over the draft KV positions [1, pos] (reading R1/R2).
 __global__ void meta_dprefill_kernel(MetaBuf mb, int R, const int32_t* n_pend, const int32_t* pend_tok,
-                                     const int32_t* p) {
+                                     const int32_t* p, int no_first) {
   pdl_wait();
   pdl_trigger();
   int r = blockIdx.x, j = threadIdx.x;
@@ -85,7 +85,9 @@ __global__ void meta_dprefill_kernel(MetaBuf mb, int R, const int32_t* n_pend, c
   mb.req[row] = r;
   mb.klo[row] = 1;
   mb.khi[row] = act ? pos + 1 : 0;
-  mb.slot[row] = -1;
+  // -2 marks the root pair (the ground-truth token just committed) for the
+  // "w/o first token" ablation (R26): draft_concat drops its embedding
+  mb.slot[row] = (no_first && act && j == np - 1) ? -2 : -1;
 }
 
 // chain step i: row r at position p + i, causal over draft KV [1, p + i]
@@ -570,10 +572,11 @@ static void stage_build(hsd_ctx* c) {
   const int b = c->b, N = c->N, n = c->n, R = N + 1;
   const int kvmax = c->max_pos;
   // S0 (1): draft prefill of the pending pairs x_j = W_fc [H_{j-1}; E(t_j)] (R1)
-  launch_k(meta_dprefill_kernel, b, 32 * ((R + 31) / 32), 0, c->st, c->md, R, c->n_pend, c->pend_tok, c->p);
+  launch_k(meta_dprefill_kernel, b, 32 * ((R + 31) / 32), 0, c->st, c->md, R, c->n_pend, c->pend_tok, c->p,
+           (c->cfg.flags & HSD_FLAG_NO_FIRST_TOKEN) ? 1 : 0);
   RowMeta mdv = c->md.view(nullptr, nullptr, 0, 0);
   c->attn_bytes = attn_bytes_for(c, 1, 0);
-  launch_draft_concat(c->pend_H, c->md.tok, c->md.pos, c->embed, c->dt, b * R, n, c->a, c->st);
+  launch_draft_concat(c->pend_H, c->md.tok, c->md.pos, c->md.slot, c->embed, c->dt, b * R, n, c->a, c->st);
   gemm(c, c->a, 2 * n, c->fc, 2 * n, c->x_d, n, b * R, n, 2 * n, false);
   layer_forward(c, c->draft, c->x_d, b * R, R, b, mdv, kv_layer(c, c->kv_d, 0), kvmax);
   launch_k(gather_last_kernel, b, 256, 0, c->st, c->x_d, R, c->n_pend, n, c->xw, c->chain, N, c->mc, c->p);
@@ -641,6 +644,36 @@ static void stage_verify(hsd_ctx* c) {
   g_hsd_launches += 2;
 }
 
+// S3 + S4 without Alg. 2: walk, KV compaction, commit (append: the dedicated
+// verify pass of the re-sampled tree, fusion off -- tokens / pairs follow the
+// step's first pass)
+static void walk_compact_commit(hsd_ctx* c, int append) {
+  const int b = c->b;
+  AcceptParams A{};
+  A.mode = c->cfg.accept_mode == HSD_STOCHASTIC ? 1 : 0;
+  A.append = append;
+  A.N = c->N; A.t_max = c->T; A.V = c->V; A.temperature = c->cfg.temperature;
+  A.seed = (uint32_t)c->cfg.seed; A.req_id = c->req_id;
+  A.t_tok = c->t_tok; A.t_par = c->t_par; A.t_n = c->t_n; A.argmax = c->argmax; A.logits = c->logits;
+  A.step = c->step;
+  A.acc_n = c->acc_n; A.acc_slots = c->acc_slots; A.bonus = c->bonus; A.emitted = c->emitted;
+  A.n_emitted = c->n_emitted;
+  { Prof pf(c, P_WALK); launch_walk(A, b, c->st); }
+  CompactParams C{};
+  C.kv_base = c->kv_t; C.layer_stride = c->kv_layer_elems; C.block_table = c->block_table;
+  C.pages_per_req = c->pages_per_req; C.page_size = c->page_size; C.kv_heads = c->Hkv; C.head_dim = c->hd;
+  C.N = c->N; C.acc_n = c->acc_n; C.acc_slots = c->acc_slots; C.p = c->p;
+  { Prof pf(c, P_COMPACT, 2.0 * b * c->N * c->L * 2 * c->kd * c->esz); launch_compact(C, b, c->L, c->dt, c->st); }
+  CommitParams M{};
+  M.N = c->N; M.t_max = c->T; M.hidden = c->n; M.Hverify = c->Hver; M.append = append;
+  M.acc_n = c->acc_n; M.acc_slots = c->acc_slots; M.emitted = c->emitted; M.bonus = c->bonus;
+  M.n_emitted = c->n_emitted;
+  M.pend_H = c->pend_H; M.pend_tok = c->pend_tok; M.n_pend = c->n_pend; M.root_tok = c->root_tok; M.p = c->p;
+  M.step = c->step;
+  launch_commit(M, b, c->st);
+  g_hsd_launches += 3;
+}
+
 static void stage_accept(hsd_ctx* c, int32_t* d_emitted, int32_t* d_n) {
   const int b = c->b;
   AcceptParams A{};
@@ -678,8 +711,19 @@ static void stage_accept(hsd_ctx* c, int32_t* d_emitted, int32_t* d_n) {
   M.acc_n = c->acc_n; M.acc_slots = c->acc_slots; M.emitted = c->emitted; M.bonus = c->bonus;
   M.pend_H = c->pend_H; M.pend_tok = c->pend_tok; M.n_pend = c->n_pend; M.root_tok = c->root_tok; M.p = c->p;
   M.step = c->step;
+  M.n_emitted = c->n_emitted;
   launch_commit(M, b, c->st);
   g_hsd_launches += 4;
+  if ((c->cfg.flags & HSD_FLAG_RESAMPLE) && !(c->cfg.flags & HSD_FLAG_FUSION)) {
+    // re-sampling WITHOUT verification fusion (the Fig. 12 ablation): the Alg. 2
+    // tree just built, rooted at the new bonus token, is verified by its own target
+    // pass in this step; the next step's tree is fresh only
+    launch_pending_as_tree(c->pt_n, c->pt_tok, c->pt_par, c->pt_depth, c->pt_lj, c->Br + 1, c->t_n, c->t_tok,
+                           c->t_par, c->t_depth, c->t_lj, c->t_anc, c->T, c->W, b, c->st);
+    g_hsd_launches += 1;
+    stage_verify(c);
+    walk_compact_commit(c, 1);
+  }
   if (d_emitted) cudaMemcpyAsync(d_emitted, c->emitted, sizeof(int32_t) * b * (c->N + 1), cudaMemcpyDeviceToDevice, c->st);
   if (d_n) cudaMemcpyAsync(d_n, c->n_emitted, sizeof(int32_t) * b, cudaMemcpyDeviceToDevice, c->st);
 }
@@ -783,8 +827,8 @@ static hsd_status prefill_one(hsd_ctx* ctx, int r, const int32_t* pt, int P0, in
     CU(cudaMemcpyAsync(c->mp.khi, khi.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
     CU(cudaMemcpyAsync(c->mp.slot, slot.data(), 4 * M, cudaMemcpyHostToDevice, c->st));
     RowMeta m = c->mp.view(nullptr, nullptr, 0, 0);
-    launch_draft_concat(c->H_prompt + (size_t)(j0 - 1) * n, c->mp.tok, c->mp.pos, c->embed, c->dt, M, n, c->a,
-                        c->st);
+    launch_draft_concat(c->H_prompt + (size_t)(j0 - 1) * n, c->mp.tok, c->mp.pos, nullptr, c->embed, c->dt, M, n,
+                        c->a, c->st);
     gemm(c, c->a, 2 * n, c->fc, 2 * n, c->x_p, n, M, n, 2 * n, false);
     layer_forward(c, c->draft, c->x_p, M, M, 1, m, kv_layer(c, c->kv_d, 0), j0 + M);
     g_hsd_launches += 1;
@@ -1153,8 +1197,11 @@ hsd_status hsd_prefill(hsd_ctx* ctx, int32_t n_req, const int32_t* h_tokens, int
 // capacity contract (include/hsd.h): a step writes KV rows up to p + T - 1 and the
 // tree's RoPE positions up to p + N; p itself grows by at most N + 1 per step
 static hsd_status check_capacity(hsd_ctx* c) {
+  // fusion off: the extra verify of the re-sampled tree starts up to N positions later
+  const bool extra = (c->cfg.flags & HSD_FLAG_RESAMPLE) && !(c->cfg.flags & HSD_FLAG_FUSION);
+  const int need = c->T + (extra ? c->N + 1 : 0);
   bool tight = false;
-  for (int r = 0; r < c->b; ++r) tight |= c->p_hi[r] + c->T > c->max_pos;
+  for (int r = 0; r < c->b; ++r) tight |= c->p_hi[r] + need > c->max_pos;
   if (tight) {   // the bound assumes N + 1 tokens per step: refresh it from the device's p
     std::vector<int32_t> p(c->b);
     if (cudaStreamSynchronize(c->st) != cudaSuccess ||
@@ -1163,7 +1210,7 @@ static hsd_status check_capacity(hsd_ctx* c) {
     for (int r = 0; r < c->b; ++r) c->p_hi[r] = p[r];
   }
   for (int r = 0; r < c->b; ++r)
-    if (c->p_hi[r] + c->T > c->max_pos)
+    if (c->p_hi[r] + need > c->max_pos)
       return fail(c, HSD_ESTATE, "context capacity exhausted: slot " + std::to_string(r) + " may hold " +
                                      std::to_string(c->p_hi[r]) + " committed tokens, a step needs " +
                                      std::to_string(c->T) + " more KV rows of " + std::to_string(c->max_pos));
@@ -1189,6 +1236,23 @@ hsd_status hsd_admit(hsd_ctx* ctx, int32_t slot, const int32_t* h_tokens, int32_
   if (st != HSD_OK) return st;
   CU(cudaStreamSynchronize(c->st));
   CU(cudaGetLastError());
+  return HSD_OK;
+}
+
+hsd_status hsd_set_block_table(hsd_ctx* ctx, const int32_t* h_table) {
+  if (!ctx || !h_table) return fail(ctx, HSD_EINVAL, "null block table");
+  hsd_ctx* c = ctx;
+  if (c->stage != 0) return fail(c, HSD_ESTATE, "hsd_set_block_table in the middle of a staged step");
+  const size_t n = (size_t)c->maxb * c->pages_per_req;
+  std::vector<char> seen(n, 0);
+  for (size_t i = 0; i < n; ++i) {
+    const int32_t pg = h_table[i];
+    if (pg < 0 || (size_t)pg >= n || seen[pg]) return fail(c, HSD_EINVAL, "block table is not a permutation of the pages");
+    seen[pg] = 1;
+  }
+  CU(cudaMemcpyAsync(c->block_table, h_table, 4 * n, cudaMemcpyHostToDevice, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  drop_graphs(c);
   return HSD_OK;
 }
 
@@ -1399,6 +1463,7 @@ hsd_status hsd_get_tensor(hsd_ctx* ctx, const char* name, hsd_tensor* out) {
   if (s == "table_scale" && c->table_scale) return set(c->table_scale, 0, {c->Vh});
   if (s == "embed") return set(c->embed, adt, {c->V, n});
   if (s == "head") return set(c->head, adt, {c->V, n});
+  if (s == "block_table") return set(c->block_table, 2, {c->maxb, c->pages_per_req});
   if (s == "kv") return set(c->kv_t, adt, {std::max(1, c->L), c->maxb * c->pages_per_req, 2, (int64_t)c->Hkv * c->page_size * c->hd});
   if (s == "kv_draft") return set(c->kv_d, adt, {1, c->maxb * c->pages_per_req, 2, (int64_t)c->Hkv * c->page_size * c->hd});
   extern unsigned long long* g_attn_trace;

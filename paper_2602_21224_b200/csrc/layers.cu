@@ -349,26 +349,27 @@ void launch_argmax_rows(const float* x, int M, int V, const int32_t* pos, int32_
 // out[r] = [H_{j-1} (fp32 -> T) ; E(t_j)]   (W_fc input, reading R1)
 template <typename T>
 __global__ void draft_concat_kernel(const float* __restrict__ Hprev, const int32_t* __restrict__ tok,
-                                    const int32_t* __restrict__ pos, const T* __restrict__ E, int n,
-                                    T* __restrict__ out) {
+                                    const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
+                                    const T* __restrict__ E, int n, T* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
   int r = blockIdx.x;
   T* o = out + (size_t)r * 2 * n;
   bool active = pos[r] >= 0;
+  const bool with_e = !(slot && slot[r] == -2);   // -2: the root pair without its token (R26)
   const float* h = Hprev + (size_t)r * n;
   const T* e = E + (size_t)(active ? tok[r] : 0) * n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     o[i] = active ? from_f32<T>(h[i]) : from_f32<T>(0.f);
-    o[n + i] = active ? e[i] : from_f32<T>(0.f);
+    o[n + i] = active && with_e ? e[i] : from_f32<T>(0.f);
   }
 }
 
-void launch_draft_concat(const float* Hprev, const int32_t* tok, const int32_t* pos, const void* E,
-                         DType dt, int M, int n, void* out, cudaStream_t st) {
+void launch_draft_concat(const float* Hprev, const int32_t* tok, const int32_t* pos, const int32_t* slot,
+                         const void* E, DType dt, int M, int n, void* out, cudaStream_t st) {
   if (M <= 0) return;
   if (dt == DT_F32)
-    launch_k(draft_concat_kernel<float>, M, 256, 0, st, Hprev, tok, pos, (const float*)E, n, (float*)out);
+    launch_k(draft_concat_kernel<float>, M, 256, 0, st, Hprev, tok, pos, slot, (const float*)E, n, (float*)out);
   else
-    launch_k(draft_concat_kernel<bf16>, M, 256, 0, st, Hprev, tok, pos, (const bf16*)E, n, (bf16*)out);
+    launch_k(draft_concat_kernel<bf16>, M, 256, 0, st, Hprev, tok, pos, slot, (const bf16*)E, n, (bf16*)out);
 }

@@ -21,10 +21,11 @@ STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ES
 FP32_VERIFY, BF16 = 0, 1
 GREEDY, STOCHASTIC = 0, 1
 FLAG_RESAMPLE, FLAG_FUSION, FLAG_PLANTED, FLAG_ZERO_TABLE, FLAG_TCGEN05, FLAG_TABLE_FP8 = 1, 2, 4, 8, 16, 32
+FLAG_NO_FIRST_TOKEN = 1 << 6
 MAX_PLANT_DEPTH = 16
 SHARD_NONE, SHARD_NCCL, SHARD_SIM = 0, 1, 2
 
-EXPORTS = ["hsd_config_defaults", "hsd_init_model", "hsd_prefill", "hsd_set_plant", "hsd_build_tree",
+EXPORTS = ["hsd_config_defaults", "hsd_init_model", "hsd_prefill", "hsd_set_plant", "hsd_set_block_table", "hsd_build_tree",
            "hsd_force_tree", "hsd_verify_tree", "hsd_accept_and_compact", "hsd_step", "hsd_step_host",
            "hsd_sync", "hsd_get_tensor", "hsd_kernel_launches", "hsd_destroy", "hsd_last_error",
            "hsd_profile", "hsd_profile_read", "hsd_debug_gemm", "hsd_nccl_unique_id", "hsd_admit", "hsd_kstamp", "hsd_kstamp_read", "hsd_kstamp_read_attention",
@@ -78,6 +79,7 @@ def load(path: str = LIB_PATH):
         "hsd_init_model": (I32, [P(HsdConfig), C.c_int, VP, P(VP)]),
         "hsd_prefill": (I32, [VP, I32, P(I32), I32, P(I32), VP]),
         "hsd_set_plant": (I32, [VP, P(I32), I32]),
+        "hsd_set_block_table": (I32, [VP, P(I32)]),
         "hsd_build_tree": (I32, [VP, P(TreeView)]),
         "hsd_force_tree": (I32, [VP, P(I32), P(I32), P(I32), P(I32)]),
         "hsd_verify_tree": (I32, [VP, P(VerifyView)]),
@@ -205,6 +207,11 @@ class Context:
         plant = np.atleast_2d(np.asarray(plant, dtype=np.int32))
         a, p = _i32(plant)
         self._check(self.lib.hsd_set_plant(self.h, p, plant.shape[1]))
+
+    def set_block_table(self, table):
+        """hsd_set_block_table: [max_batch, pages_per_req] page permutation (paged KV)."""
+        t, tp = _i32(np.asarray(table, dtype=np.int32).ravel())
+        self._check(self.lib.hsd_set_block_table(self.h, tp))
 
     def build_tree(self):
         v = TreeView()

@@ -47,12 +47,14 @@ def lin_from_gpu(n, tok, par, depth, lj):
 
 
 def kv_rows(ctx, cfg, layer, r, positions, page_size, pages_per_req):
-    """GPU K and V rows [len(positions), Hkv*hd] of request r at `positions`."""
+    """GPU K and V rows [len(positions), Hkv*hd] of request r at `positions`
+    (logical page -> physical page through the context's block table)."""
     kv = ctx.tensor("kv")[layer]                   # [pages, 2, Hkv*ps*hd]
+    bt = ctx.tensor("block_table").cpu().numpy()   # [max_batch, pages_per_req]
     Hkv, hd = cfg.kv_heads, cfg.head_dim
     out_k, out_v = [], []
     for pos in positions:
-        page = r * pages_per_req + pos // page_size
+        page = int(bt[r, pos // page_size])
         slot = pos % page_size
         blk = kv[page].float()
         out_k.append(blk[0].view(Hkv, page_size, hd)[:, slot, :].reshape(-1).cpu().numpy())
@@ -71,10 +73,11 @@ def rel_err(a, b):
 class Lockstep:
     def __init__(self, ctx, cfg, model, table, prompts, seed=0, accept="greedy", temperature=1.0,
                  resample=True, fusion=True, plant=None, plant_rates=None, perm=None,
-                 logit_tol=1e-4, flag_margin=1e-4, page_size=64, tree_flag_margin=None):
+                 logit_tol=1e-4, flag_margin=1e-4, page_size=64, tree_flag_margin=None, first_token=True):
         self.ctx, self.cfg, self.m, self.table = ctx, cfg, model, table
         self.seed, self.accept, self.T = seed, accept, temperature
         self.resample, self.fusion = resample, fusion
+        self.first_token = first_token
         self.plant, self.plant_rates = plant, plant_rates
         self.perm = perm
         self.tol, self.flag = logit_tol, flag_margin
@@ -128,7 +131,8 @@ class Lockstep:
     def _engine(self, r):
         return Engine(self.m, self.table, self.cfg, seed=self.seed, accept=self.accept,
                       temperature=self.T, resample=self.resample, fusion=self.fusion, req_offset=self.req_ids[r],
-                      plant=None if self.plant is None else [self.plant[r]], plant_rates=self.plant_rates)
+                      plant=None if self.plant is None else [self.plant[r]], plant_rates=self.plant_rates,
+                      first_token=self.first_token)
 
     def _margins_ok(self, margins, kinds, scale, flag=None):
         flag = self.flag if flag is None else flag

@@ -12,7 +12,7 @@ import torch
 from synth import get_config, prompts, vocab_permutation
 from oracle.model import Model, layer_tid
 from oracle.table import TokenInfoTable
-from oracle.engine import greedy_decode
+from oracle.engine import Engine, greedy_decode
 from oracle.fp8 import round_e4m3
 from tests.gpu_lockstep import Lockstep
 
@@ -102,12 +102,17 @@ def test_lockstep_c1_fp8_table():
 
 
 def run_lockstep(cfg, precision, steps, seed=0, batch=1, planted=False, accept="greedy", hot=0, tol=None,
-                 flag=None, expect_no_flags=False, tcgen05=False, table_fp8=False, extra_ctx=0):
+                 flag=None, expect_no_flags=False, tcgen05=False, table_fp8=False, extra_ctx=0,
+                 block_table_seed=None, zero_table=False, resample=True, first_token=True):
     perm = vocab_permutation(cfg.vocab, 0) if hot else None
     pr = prompts(cfg, batch=batch)
     m = Model(cfg, seed=seed, precision="fp32" if precision == hsd.FP32_VERIFY else "bf16")
-    table = TokenInfoTable(m, hot_tokens=hot, perm=perm, fp8=table_fp8)
-    plant, rates, flags = None, None, hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION
+    table = TokenInfoTable(m, hot_tokens=hot, perm=perm, fp8=table_fp8, zero=zero_table)
+    plant, rates, flags = None, None, (hsd.FLAG_RESAMPLE if resample else 0) | hsd.FLAG_FUSION
+    if zero_table:
+        flags |= hsd.FLAG_ZERO_TABLE
+    if not first_token:
+        flags |= hsd.FLAG_NO_FIRST_TOKEN
     if table_fp8:
         flags |= hsd.FLAG_TABLE_FP8
     ref = [greedy_decode(m, p, steps * (cfg.steps_N + 1) + cfg.steps_N + 4)[0] for p in pr] \
@@ -119,7 +124,12 @@ def run_lockstep(cfg, precision, steps, seed=0, batch=1, planted=False, accept="
     ctx = ctx_for(cfg, precision, seed=seed, max_batch=batch, flags=flags, accept=accept, vocab_perm=perm,
                   plant_rates=rates, max_ctx=cfg.prompt_len + steps * (cfg.steps_N + 1) + 8 + extra_ctx,
                   tcgen05=tcgen05)
+    if block_table_seed is not None:        # paged KV through a scrambled page map
+        bt = ctx.tensor("block_table")
+        n = bt.shape[0] * bt.shape[1]
+        ctx.set_block_table(np.random.default_rng(block_table_seed).permutation(n).reshape(bt.shape[0], bt.shape[1]))
     ls = Lockstep(ctx, cfg, m, table, pr, seed=seed, accept=accept, plant=plant, plant_rates=rates, perm=perm,
+                  resample=resample, first_token=first_token,
                   logit_tol=tol or (1e-4 if precision == hsd.FP32_VERIFY else 2e-2),
                   flag_margin=flag or (1e-4 if precision == hsd.FP32_VERIFY else 1e-2),
                   tree_flag_margin=None if precision == hsd.FP32_VERIFY else 2 * (tol or 2e-2))
@@ -257,6 +267,113 @@ def test_lockstep_wide_bf16_tcgen05_planted(hd, q_heads, kv_heads, prompt_len):
                                    prompt_len=prompt_len)
     ls, accs = run_lockstep(cfg, hsd.BF16, steps=6, tcgen05=True, planted=True)
     assert ls.max_err["verify"] <= 2e-2 and max(accs) >= 2
+
+
+@pytest.mark.parametrize("variant", ["zero_table", "no_resample"])
+def test_lockstep_ablation_variants(variant):
+    """NEXT-1 ablation toggles (Table 4 / Fig. 12) in full lockstep with the
+    oracle's same variant, fp32-verify, planted acceptance: token info off
+    (HSD_FLAG_ZERO_TABLE: Alg. 1 on the draft logits alone, Fig. 5a) and Alg. 2
+    re-sampling off. Every variant stays the oracle's plain greedy decode (lossless)."""
+    kw = {"zero_table": dict(zero_table=True), "no_resample": dict(resample=False)}[variant]
+    ls, accs = run_lockstep(get_config("c1"), hsd.FP32_VERIFY, steps=10, planted=True, **kw)
+    assert ls.checked["tree"] >= 9 and ls.checked["accept"] >= 9 and max(accs) >= 2
+
+
+def _stream_vs_oracle(flags, steps=12, check_first_draft=False, cfg=None, rates=None, **engine_kw):
+    """GPU hsd_step stream vs an oracle Engine that runs the same variant through the
+    whole decode (no per-step restart: variants whose draft state depends on the step
+    history); planted greedy, fp32-verify. Returns (GPU tokens, oracle engine)."""
+    cfg = cfg or get_config("c1")
+    pr = prompts(cfg)
+    m = Model(cfg, seed=0, precision="fp32")
+    table = TokenInfoTable(m)
+    ref = greedy_decode(m, pr[0], steps * (cfg.steps_N + 1) + 4)[0]
+    plant = [np.concatenate([pr[0], ref])]
+    rates = rates or [1.0, 0.9, 0.8, 0.7, 0.7, 0.7, 0.7, 0.7]
+    ctx = ctx_for(cfg, hsd.FP32_VERIFY, seed=0, flags=flags | hsd.FLAG_PLANTED, plant_rates=rates,
+                  max_ctx=cfg.prompt_len + (steps + 2) * (cfg.steps_N + 1) + 8)
+    ctx.prefill(pr)
+    ctx.set_plant(np.stack(plant))
+    e = Engine(m, table, cfg, seed=0, plant=plant, plant_rates=rates, **engine_kw)
+    first = e.prefill(pr)
+    got = [int(ctx.tensor("root_tok").cpu()[0])]
+    assert got == first
+    for i in range(steps):
+        if check_first_draft and i == 0:     # the variant's draft arithmetic itself (step-1 logits)
+            ctx.build_tree()
+            Lg = ctx.tensor("draft_logits").cpu().numpy()[0].astype(np.float64)
+            ctx.verify_tree()
+            ctx.accept_and_compact()
+            g = [int(t) for t in ctx.tensor("emitted").cpu().numpy()[0, :int(ctx.tensor("n_emitted").cpu()[0])]]
+        else:
+            em, n = ctx.step_host()
+            g = [int(t) for t in em[0, :n[0]]]
+        o = e.step()[0]
+        if check_first_draft and i == 0:
+            Lo = e.trace[-1][2]["L"]
+            assert np.max(np.abs(Lg - Lo)) <= 1e-4 * np.max(np.abs(Lo)), "step-1 draft logits differ"
+        assert g == o, f"step {i + 1} tokens differ: gpu {g} oracle {o}"
+        got += g
+    ctx.sync()
+    assert got == ref[:len(got)], "GPU output != plain greedy decode"
+    ctx.destroy()
+    return got, e
+
+
+def test_no_first_token_variant():
+    """"w/o first token" (Table 4; HSD_FLAG_NO_FIRST_TOKEN, R26): the root
+    pair enters the draft as W_fc [H; 0]. Step-1 draft logits match the oracle's
+    variant (1e-4), every step emits the oracle's tokens, output lossless."""
+    got, e = _stream_vs_oracle(hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | hsd.FLAG_NO_FIRST_TOKEN, check_first_draft=True,
+                               first_token=False)
+    # the variant changes the draft itself (not a no-op)
+    cfg = get_config("c1")
+    m = e.m
+    e_on = Engine(m, TokenInfoTable(m), cfg, seed=0)
+    e_on.prefill(prompts(cfg))
+    e_on.step()
+    assert np.max(np.abs(e_on.trace[-1][2]["L"] - e.trace[0][2]["L"])) > 1e-3
+
+
+def test_fusion_off_dedicated_verify_pass():
+    """Re-sampling WITHOUT verification fusion (HSD_FLAG_RESAMPLE alone): the
+    Alg. 2 tree is verified by its own target pass inside the step. Per step the GPU
+    emits exactly the oracle's tokens (Engine(fusion=False) runs the same extra pass),
+    the stream is the plain greedy decode, and extra passes really emit tokens."""
+    # a deeper draft and lower planted rates so that Alg. 2 (N - m - 1 > r) really fires
+    cfg = get_config("c1").replace(steps_N=6, budget_B=12)
+    got, e = _stream_vs_oracle(hsd.FLAG_RESAMPLE, steps=14, cfg=cfg, rates=[0.9, 0.5, 0.5, 0.5, 0.5, 0.5],
+                               fusion=False)
+    assert sum("acc2" in rec for _, _, rec in e.trace) > 0
+
+
+def test_lockstep_permuted_block_table():
+    """Paged KV with a scrambled block table (hsd_set_block_table): every K / V read
+    and write -- prefill, qkv_rope_kv, the SIMT and tcgen05 tree attention, the draft
+    layer, compaction -- goes through the page map. fp32-verify stays the oracle's
+    plain greedy decode; bf16 tcgen05 (GQA hd 128, multi-page prompts, 2 requests)
+    stays in lockstep, compacted KV rows read back through the same map."""
+    ls, accs = run_lockstep(get_config("c1").replace(batch=2), hsd.FP32_VERIFY, steps=8, batch=2, planted=True,
+                            block_table_seed=5)
+    assert ls.checked["accept"] >= 14 and max(accs) >= 2
+    cfg = get_config("c1").replace(hidden=512, q_heads=8, kv_heads=2, head_dim=128, ffn=1024, vocab=1024,
+                                   layers=2, steps_N=5, branch_k=3, budget_B=16, prompt_len=200, batch=2)
+    ls, accs = run_lockstep(cfg, hsd.BF16, steps=5, batch=2, tcgen05=True, planted=True, block_table_seed=9)
+    assert ls.max_err["verify"] <= 2e-2 and max(accs) >= 2
+
+
+def test_block_table_contract():
+    cfg = get_config("c1")
+    ctx = ctx_for(cfg, hsd.FP32_VERIFY, seed=0)
+    bt = ctx.tensor("block_table").cpu().numpy()
+    assert np.array_equal(bt.ravel(), np.arange(bt.size))          # identity by default
+    bad = bt.copy()
+    bad.flat[0] = bad.flat[1]                                       # not a permutation
+    with pytest.raises(hsd.HsdError) as e:
+        ctx.set_block_table(bad)
+    assert e.value.status == hsd.HSD_EINVAL
+    ctx.destroy()
 
 
 def test_lockstep_attention_capacity_far_above_context():

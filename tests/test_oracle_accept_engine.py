@@ -46,10 +46,16 @@ def test_greedy_lossless_grid(seed, N, k, B, resample, fusion):
         assert o == r[:cfg.max_new]
     acc = [len(rec["acc"]) for _, _, rec in e.trace]
     assert max(acc) >= min(N, 2)  # the planted path really is accepted
+    extra = 0
     for _, _, rec in e.trace:
         lin = rec["lin"]
         assert lin["T"] <= B + (cfg.resample_budget_Br if fusion else 0) + 1
-        assert len(rec["emitted"]) == len(rec["acc"]) + 1
+        n2 = len(rec["acc2"]) + 1 if "acc2" in rec else 0    # fusion off: the dedicated extra verify
+        assert len(rec["emitted"]) == len(rec["acc"]) + 1 + n2
+        assert len(rec["emitted"]) <= N + 1
+        extra += "acc2" in rec
+    if resample and not fusion and N >= 3:
+        assert extra > 0            # the re-sampled tree was really verified on its own
 
 
 def test_unplanted_random_weights_lossless_c1():
@@ -207,3 +213,24 @@ def test_admit_is_lossless_and_uses_the_new_request_id():
     picks = {rid: es.admit(1, pr[2], req_id=rid) for rid in (5, 6, 7, 8)}
     for rid, t in picks.items():
         assert t == gumbel_argmax(logits, 1.0, gumbel_uniforms(1, rid, 0, 0, cfg.vocab))[0]
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_no_first_token_variant_lossless_and_distinct(seed):
+    """R26 ("w/o first token", Table 4): the root pair enters the draft as W_fc [H; 0].
+    The draft changes (different one-pass logits) but the output stays the plain
+    greedy decode -- losslessness does not depend on the draft."""
+    cfg = tiny(steps_N=3, branch_k=2, budget_B=6)
+    m = Model(cfg, seed=seed)
+    pr = prompts(cfg, batch=1, length=8, prompt_seed=40 + seed)
+    ref = greedy_decode(m, pr[0], cfg.max_new + 8)[0]
+    e = Engine(m, TokenInfoTable(m), cfg, first_token=False)
+    out = e.decode(pr, cfg.max_new)
+    assert out[0] == ref[:cfg.max_new]
+    e_on = Engine(m, TokenInfoTable(m), cfg)
+    e_on.prefill(pr)
+    e_on.step()
+    assert np.max(np.abs(e.trace[0][2]["L"] - e_on.trace[0][2]["L"])) > 1e-6
+    # the input of the root pair is W_fc [H; 0]
+    H = np.arange(cfg.hidden, dtype=np.float64) / cfg.hidden
+    assert np.allclose(m.draft_input(H, 3, with_token=False), m.fc[:, :cfg.hidden] @ H)
