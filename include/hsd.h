@@ -57,10 +57,15 @@ enum {                                               /* hsd_config.flags       *
   HSD_FLAG_TCGEN05 = 1u << 4,   /* bf16 GEMMs on tcgen05 (else SIMT FFMA)       */
   HSD_FLAG_TABLE_FP8 = 1u << 5, /* token-info table as e4m3 codes + a per-row
                                    fp32 scale (DESIGN R25)        */
-  HSD_FLAG_NO_FIRST_TOKEN = 1u << 6 /* "w/o first token" (Table 4, P:511-533;
+  HSD_FLAG_NO_FIRST_TOKEN = 1u << 6, /* "w/o first token" (Table 4, P:511-533;
                                    R26): the root pair -- the ground-truth token
                                    just committed -- enters the draft as
                                    W_fc [H; 0], without its embedding            */
+  HSD_FLAG_TOKEN_AR = 1u << 7   /* token-level AR draft (EAGLE-style, NEXT-2;
+                                   R27): each chain step feeds back
+                                   its own top-1 token, x = W_fc [h_i; E(t_i)],
+                                   with one lm_head GEMV per step instead of the
+                                   one-pass head (not with the sharded head)     */
 };
 
 #define HSD_MAX_PLANT_DEPTH 16

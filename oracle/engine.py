@@ -45,13 +45,15 @@ class Request:
 
 class Engine:
     def __init__(self, model, table, cfg, seed=0, accept=None, temperature=None,
-                 resample=True, fusion=True, req_offset=0, plant=None, plant_rates=None, first_token=True):
+                 resample=True, fusion=True, req_offset=0, plant=None, plant_rates=None, first_token=True,
+                 draft_mode="hidden"):
         self.m, self.table, self.cfg = model, table, cfg
         self.seed = seed
         self.accept = accept or cfg.accept
         self.T = cfg.temperature if temperature is None else temperature
         self.resample, self.fusion = resample, fusion
         self.first_token = first_token   # False: the root pair's draft input omits E(t_p) (R26, Table 4)
+        self.draft_mode = draft_mode     # "hidden" (the paper's chain) | "token_ar" (EAGLE-style, R27)
         self.req_offset = req_offset
         self.plant, self.plant_rates = plant, plant_rates
         self.reqs = []
@@ -132,7 +134,10 @@ class Engine:
         for i in range(1, N):
             dk = [tmp[j][0] for j in range(1, p + i)]
             dv = [tmp[j][1] for j in range(1, p + i)]
-            h, k, v = self.m.draft_one(chain[-1], p + i, dk, dv)
+            x = chain[-1]
+            if self.draft_mode == "token_ar":   # R27: feed back the draft's own top-1 token
+                x = self.m.draft_input(chain[-1], argmax_lowest(self.m.logits(chain[-1])))
+            h, k, v = self.m.draft_one(x, p + i, dk, dv)
             tmp[p + i] = (k, v)
             chain.append(h)
         return chain

@@ -583,18 +583,39 @@ static void stage_build(hsd_ctx* c) {
   g_hsd_launches += 3;
   // S0 (2): chain h_{i+1} = TL(h_i) at positions p + i (R2)
   RowMeta mcv = c->mc.view(nullptr, nullptr, 0, 0);
+  const bool token_ar = (c->cfg.flags & HSD_FLAG_TOKEN_AR) != 0;
+  const size_t ldL = (size_t)N * c->V;   // draft_logits [b, N, V]: request rows N * V apart
   for (int i = 1; i < N; ++i) {
     // (chain step i's row metadata was written by gather_last / the previous copy_chain)
+    if (token_ar) {
+      // token-level AR draft (EAGLE-style, NEXT-2, R27): the draft's own top-1 token of
+      // step i is fed back, x_{i+1} = W_fc [h_i ; E(argmax l_i)] -- one lm_head GEMV,
+      // one argmax and one fc GEMM per step instead of the one-pass head below
+      launch_rmsnorm(c->xw, b, n, c->cfg.rms_eps, c->a, c->dt, nullptr, c->st);
+      gemm(c, c->a, n, c->head_rank, n, c->draft_logits + (size_t)(i - 1) * c->V, (int)ldL, b, c->V, n, false,
+           P_HEAD_DRAFT);
+      launch_token_ar_input(c->draft_logits + (size_t)(i - 1) * c->V, ldL, c->V, c->perm_d, c->xw, b, n, c->embed,
+                            c->dt, c->a, c->st);
+      gemm(c, c->a, 2 * n, c->fc, 2 * n, c->xw, n, b, n, 2 * n, false);
+      g_hsd_launches += 2;
+    }
     c->attn_bytes = attn_bytes_for(c, 2, i);
     layer_forward(c, c->draft, c->xw, b, 1, b, mcv, kv_layer(c, c->kv_d, 0), kvmax);
     launch_k(copy_chain_kernel, b, 256, 0, c->st, c->xw, n, c->chain, N, i, c->mc, c->p);
     g_hsd_launches += 1;
   }
-  // S1a: one-pass logits L = RMSNorm_f(H_chain) W_head^T, rank order
-  launch_rmsnorm(c->chain, b * N, n, c->cfg.rms_eps, c->a, c->dt, nullptr, c->st);
-  if (c->shard_mode != HSD_SHARD_NONE) shard_head_draft(c, b * N);
-  else gemm(c, c->a, n, c->head_rank, n, c->draft_logits, c->V, b * N, c->V, n, false, P_HEAD_DRAFT);
-  g_hsd_launches += 1;
+  if (token_ar) {   // the last chain row's logits
+    launch_rmsnorm(c->xw, b, n, c->cfg.rms_eps, c->a, c->dt, nullptr, c->st);
+    gemm(c, c->a, n, c->head_rank, n, c->draft_logits + (size_t)(N - 1) * c->V, (int)ldL, b, c->V, n, false,
+         P_HEAD_DRAFT);
+    g_hsd_launches += 1;
+  } else {
+    // S1a: one-pass logits L = RMSNorm_f(H_chain) W_head^T, rank order
+    launch_rmsnorm(c->chain, b * N, n, c->cfg.rms_eps, c->a, c->dt, nullptr, c->st);
+    if (c->shard_mode != HSD_SHARD_NONE) shard_head_draft(c, b * N);
+    else gemm(c, c->a, n, c->head_rank, n, c->draft_logits, c->V, b * N, c->V, n, false, P_HEAD_DRAFT);
+    g_hsd_launches += 1;
+  }
   // S1b + S1c: Alg. 1, prune, fuse, linearise (+ planting)
   TreeParams P{};
   P.N = N; P.k = c->k; P.B = c->B; P.Br = c->Br; P.r = c->r; P.V = c->V; P.Vh = c->Vh; P.t_max = c->T;
@@ -911,6 +932,10 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     last = why;
     fprintf(stderr, "hsd_init_model: %s\n", why.c_str());
     return HSD_EINVAL;
+  }
+  if (cfg->shard_mode != HSD_SHARD_NONE && (cfg->flags & HSD_FLAG_TOKEN_AR)) {
+    fprintf(stderr, "hsd_init_model: the token-AR draft mode is not combined with the vocab-sharded head\n");
+    return HSD_EUNSUP;
   }
   if (cfg->shard_mode != HSD_SHARD_NONE && cfg->accept_mode != HSD_GREEDY) {
     fprintf(stderr, "hsd_init_model: the vocab-sharded lm_head supports greedy acceptance only\n");

@@ -59,6 +59,8 @@ void launch_qkv_rope_kv(float* qkv, int M, const RowMeta& m, const float* rope_c
 void launch_swiglu(float* gu, int M, int f, void* out, DType dt, const int32_t* pos, cudaStream_t st);
 void launch_interleave_gu(const void* src, int f, int n, void* dst, DType dt, cudaStream_t st);
 void launch_argmax_rows(const float* x, int M, int V, const int32_t* pos, int32_t* out, cudaStream_t st);
+void launch_token_ar_input(const float* L, size_t ldl, int V, const int32_t* perm, const float* h, int M, int n,
+                           const void* E, DType dt, void* out, cudaStream_t st);
 void launch_draft_concat(const float* Hprev, const int32_t* tok, const int32_t* pos, const int32_t* slot,
                          const void* E, DType dt, int M, int n, void* out, cudaStream_t st);
 

@@ -340,6 +340,54 @@ __global__ void argmax_rows_kernel(const float* __restrict__ x, int V, const int
   }
 }
 
+// token-level AR draft input (EAGLE-style, R27): t = argmax of the draft logits row
+// (columns in rank order when perm != null; ties -> lowest TOKEN id), then the fc
+// input row [h_i ; E(t)] (h from the fp32 chain state)
+template <typename T>
+__global__ void token_ar_input_kernel(const float* __restrict__ L, size_t ldl, int V, const int32_t* __restrict__ perm,
+                                      const float* __restrict__ h, int n, const T* __restrict__ E, T* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const int r = blockIdx.x;
+  const float* xr = L + (size_t)r * ldl;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const int t = perm ? perm[i] : i;
+    if (better(xr[i], t, bv, bi)) { bv = xr[i]; bi = t; }
+  }
+  warp_argmax(bv, bi);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { sv[w] = bv; si[w] = bi; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    bv = lane < nw ? sv[lane] : -INFINITY;
+    bi = lane < nw ? si[lane] : 0x7fffffff;
+    warp_argmax(bv, bi);
+    if (lane == 0) si[0] = bi;
+  }
+  __syncthreads();
+  const int tok = si[0];
+  T* o = out + (size_t)r * 2 * n;
+  const T* e = E + (size_t)tok * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    o[i] = from_f32<T>(h[(size_t)r * n + i]);
+    o[n + i] = e[i];
+  }
+}
+
+void launch_token_ar_input(const float* L, size_t ldl, int V, const int32_t* perm, const float* h, int M, int n,
+                           const void* E, DType dt, void* out, cudaStream_t st) {
+  if (M <= 0) return;
+  if (dt == DT_F32)
+    launch_k(token_ar_input_kernel<float>, M, 1024, 0, st, L, ldl, V, perm, h, n, (const float*)E, (float*)out);
+  else
+    launch_k(token_ar_input_kernel<bf16>, M, 1024, 0, st, L, ldl, V, perm, h, n, (const bf16*)E, (bf16*)out);
+}
+
 void launch_argmax_rows(const float* x, int M, int V, const int32_t* pos, int32_t* out, cudaStream_t st) {
   if (M <= 0) return;
   launch_k(argmax_rows_kernel, M, 1024, 0, st, x, V, pos, out);

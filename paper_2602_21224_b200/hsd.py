@@ -22,6 +22,7 @@ FP32_VERIFY, BF16 = 0, 1
 GREEDY, STOCHASTIC = 0, 1
 FLAG_RESAMPLE, FLAG_FUSION, FLAG_PLANTED, FLAG_ZERO_TABLE, FLAG_TCGEN05, FLAG_TABLE_FP8 = 1, 2, 4, 8, 16, 32
 FLAG_NO_FIRST_TOKEN = 1 << 6
+FLAG_TOKEN_AR = 1 << 7
 MAX_PLANT_DEPTH = 16
 SHARD_NONE, SHARD_NCCL, SHARD_SIM = 0, 1, 2
 

@@ -4,9 +4,14 @@ Ablations (c2 shapes, planted continuation R24 so that acceptance is real and
 controlled; the verify / walk / compaction kernels run unmodified):
   full            re-sampling (Alg. 2) + verification fusion        (the method)
   resample-off    no Alg. 2 re-sampled tree                          (P:355-375 off)
-  fusion-off      Alg. 2 tree built every step but never verified    (its cost without its benefit)
+  fusion-off      re-sampling WITHOUT fusion: the Alg. 2 tree is verified by a dedicated
+                  extra target pass in the same step (Fig. 12's "+resampling")
   token-info-off  zero token-info table: Alg. 1 degenerates to a beam tree over the draft
-                  logits alone (Fig. 5a)
+                  logits alone (Fig. 5a; Table 4 "w/o token info")
+  first-token-off the root pair enters the draft without its token embedding (Table 4
+                  "w/o first token", R26)
+  token-ar-draft  NEXT-2: the draft chain feeds back its own top-1 token each step
+                  (EAGLE-style token-level AR, R27) -- lm_head GEMV + argmax + fc per step
 Reported per variant: tau (emitted / step / request), ms / step, tokens / s, and the per-depth
 conditional acceptance P(m >= d | m >= d-1) measured from the emitted counts -- with re-sampling
 off it should reproduce the planted rates a_d (a check of the planted mechanism itself).
@@ -32,17 +37,22 @@ from paper_2602_21224_b200 import hsd
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
-ap.add_argument("--steps", type=int, default=20)
-ap.add_argument("--warmup", type=int, default=5)
+ap.add_argument("--steps", type=int, default=10)
+ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--out", default="")
+ap.add_argument("--batch", type=int, default=0, help="requests per step (more samples of the planted acceptance)")
 a = ap.parse_args()
 cfg = get_config(a.config)
+if a.batch:
+    cfg = cfg.replace(batch=a.batch)
 N, b = cfg.steps_N, cfg.batch
 rates = bench.PLANT_RATES[:N] + [bench.PLANT_RATES[-1]] * max(0, N - len(bench.PLANT_RATES))
 VARIANTS = [("full", hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION),
             ("resample-off", hsd.FLAG_FUSION),
             ("fusion-off", hsd.FLAG_RESAMPLE),
-            ("token-info-off", hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | hsd.FLAG_ZERO_TABLE)]
+            ("token-info-off", hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | hsd.FLAG_ZERO_TABLE),
+            ("first-token-off", hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | hsd.FLAG_NO_FIRST_TOKEN),
+            ("token-ar-draft", hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | hsd.FLAG_TOKEN_AR)]
 stream = torch.cuda.Stream()
 pr = prompts(cfg, batch=b)
 need_ctx = cfg.prompt_len + (a.steps + a.warmup + 12) * (N + 1) * 2 + 16
@@ -53,7 +63,7 @@ for name, flags in VARIANTS:
                          plant_rates=rates, vocab_perm=vocab_permutation(cfg.vocab, 0) if cfg.hot_tokens else None)
     with torch.cuda.stream(stream):
         tau, tps, ms, info, counts = bench.planted_leg(ctx, pr, cfg, b, N, a.steps, a.warmup, stream,
-                                                       return_counts=True, attempts=6)
+                                                       return_counts=True, attempts=8)
     m = counts.reshape(-1) - 1                      # accepted drafts per request-step
     cond = []
     for d in range(1, N + 1):
@@ -86,5 +96,5 @@ for label, M, reps in [("one-pass [b*N rows]", b * N, 1), ("iterative (N x [b ro
     head[label] = round(e0.elapsed_time(e1) * 1e3 / it, 2)
 print(json.dumps({"head_us": head, "rows": b * N, "vocab": cfg.vocab, "hidden": cfg.hidden}), flush=True)
 if a.out:
-    json.dump({"config": a.config, "planted_rates": rates, "steps": a.steps, "ablation": rows, "head_us": head},
+    json.dump({"config": a.config, "batch": b, "planted_rates": rates, "steps": a.steps, "ablation": rows, "head_us": head},
               open(a.out, "w"), indent=1)

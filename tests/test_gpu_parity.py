@@ -336,6 +336,14 @@ def test_no_first_token_variant():
     assert np.max(np.abs(e_on.trace[-1][2]["L"] - e.trace[0][2]["L"])) > 1e-3
 
 
+def test_token_ar_draft_mode():
+    """NEXT-2 token-level AR draft (HSD_FLAG_TOKEN_AR, R27): per-step lm_head GEMV +
+    argmax + fc feeding back the draft's own token. Step-1 draft logits match the
+    oracle's token-AR chain (1e-4), every step emits the oracle's tokens, lossless."""
+    _stream_vs_oracle(hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | hsd.FLAG_TOKEN_AR, check_first_draft=True,
+                      draft_mode="token_ar")
+
+
 def test_fusion_off_dedicated_verify_pass():
     """Re-sampling WITHOUT verification fusion (HSD_FLAG_RESAMPLE alone): the
     Alg. 2 tree is verified by its own target pass inside the step. Per step the GPU

@@ -234,3 +234,21 @@ def test_no_first_token_variant_lossless_and_distinct(seed):
     # the input of the root pair is W_fc [H; 0]
     H = np.arange(cfg.hidden, dtype=np.float64) / cfg.hidden
     assert np.allclose(m.draft_input(H, 3, with_token=False), m.fc[:, :cfg.hidden] @ H)
+
+
+def test_token_ar_draft_mode_lossless_and_distinct():
+    """R27 (NEXT-2): the token-level AR draft feeds back its own top-1
+    token, x_{i+1} = W_fc [h_i ; E(argmax l_i)]. A different draft (different L rows
+    after the first), the same lossless output."""
+    cfg = tiny(steps_N=4, branch_k=2, budget_B=8)
+    m = Model(cfg, seed=3)
+    pr = prompts(cfg, batch=1, length=8, prompt_seed=9)
+    ref = greedy_decode(m, pr[0], cfg.max_new + 8)[0]
+    e = Engine(m, TokenInfoTable(m), cfg, draft_mode="token_ar")
+    assert e.decode(pr, cfg.max_new)[0] == ref[:cfg.max_new]
+    e_h = Engine(m, TokenInfoTable(m), cfg)
+    e_h.prefill(pr)
+    e_h.step()
+    L_tok, L_hid = e.trace[0][2]["L"], e_h.trace[0][2]["L"]
+    assert np.allclose(L_tok[0], L_hid[0])              # h_1 is the same draft prefill output
+    assert np.max(np.abs(L_tok[1:] - L_hid[1:])) > 1e-6
