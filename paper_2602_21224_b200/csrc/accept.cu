@@ -117,10 +117,12 @@ __global__ void __launch_bounds__(WT) walk_kernel(AcceptParams P) {
   } else {
     const float invT = 1.0f / P.temperature;
     const uint32_t rq = (uint32_t)P.req_id[req], st = (uint32_t)(*P.step);
+    const bool sh = P.sh_lse != nullptr;
     while (true) {
       int cur = cur_sh;
-      const float* x = P.logits + ((size_t)req * T + cur) * P.V;
-      float lse = row_lse(x, P.V, invT, red);
+      const size_t row = (size_t)req * T + cur;
+      const float* x = sh ? nullptr : P.logits + row * P.V;
+      const float lse = sh ? P.sh_lse[row] : row_lse(x, P.V, invT, red);
       if (threadIdx.x == 0) {
         n_excl = 0;
         float S = 0.f;
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(WT) walk_kernel(AcceptParams P) {
         for (int s = cur + 1; s < n && took < 0; ++s) {
           if (par[s] != cur) continue;
           int t = tok[s];
-          float pc = expf(x[t] * invT - lse);
+          float pc = expf((sh ? P.sh_tl[row * T + s] : x[t]) * invT - lse);
           u32x4 c = {(uint32_t)cur, (uint32_t)rank, st, rq};
           float u = unit_open(philox4x32_10(c, P.seed, TAG_ACCEPT).x);
           float denom = 1.f - S;
@@ -142,8 +144,22 @@ __global__ void __launch_bounds__(WT) walk_kernel(AcceptParams P) {
       }
       __syncthreads();
       if (done_sh) {
-        int b = gumbel_argmax(x, P.V, invT, P.seed, rq, st, (uint32_t)cur, excl, n_excl, red, redi);
-        if (threadIdx.x == 0) bonus_sh = b;
+        int b = -1;
+        if (sh) {   // the best merged Gumbel candidate that was not rejected (same scores, same order)
+          if (threadIdx.x == 0) {
+            for (int k = 0; k < HSD_SHARD_KG && b < 0; ++k) {
+              const int v = P.sh_gi[row * HSD_SHARD_KG + k];
+              bool ex = false;
+              for (int e = 0; e < n_excl; ++e) ex |= excl[e] == v;
+              if (!ex) b = v;
+            }
+            if (b < 0) b = P.sh_gi[row * HSD_SHARD_KG];   // (unreachable: n_excl < KG is checked at init)
+            bonus_sh = b;
+          }
+        } else {
+          b = gumbel_argmax(x, P.V, invT, P.seed, rq, st, (uint32_t)cur, excl, n_excl, red, redi);
+        }
+        if (threadIdx.x == 0 && !sh) bonus_sh = b;
         break;
       }
     }

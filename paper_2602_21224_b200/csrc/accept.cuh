@@ -14,6 +14,10 @@ struct AcceptParams {
   const int32_t *t_tok, *t_par, *t_n;
   const int32_t* argmax;    // [b, t_max] (greedy)
   const float* logits;      // [b, t_max, V] (stochastic)
+  // stochastic with a vocab-sharded head (no full logits rows): per verify row the
+  // merged lse of l / T, the tree-token logits [t_max], the Gumbel top-KG (value desc)
+  const float *sh_lse, *sh_tl, *sh_gv;
+  const int32_t* sh_gi;
   const int32_t* step;
   int32_t *acc_n, *acc_slots, *bonus, *emitted, *n_emitted;
 };

@@ -277,6 +277,12 @@ struct hsd_ctx {
   float* lslice = nullptr;       // [G * rows, w] this shard's logits columns
   float* lrecv = nullptr;        // [G][rows][wmax] draft-logit column slices (all-to-all target)
   float *pv_loc = nullptr, *pv_all = nullptr;     // partial argmax values [G*rows], [G][G*rows]
+  // stochastic acceptance over the sharded head (shard.cu): per-row records of this
+  // shard's columns [rows_g][rec] and of every shard [G][rows_g][rec]; their merge
+  // for this rank's verify rows (lse, tree-token logits, Gumbel top-KG); the tree
+  // tokens and request ids of every rank's rows (NCCL: all-gathered each step)
+  float *sp_loc = nullptr, *sp_all = nullptr, *sh_lse = nullptr, *sh_tl = nullptr, *sh_gv = nullptr;
+  int32_t *sh_gi = nullptr, *tt_all = nullptr, *rid_all = nullptr;
   int32_t *pi_loc = nullptr, *pi_all = nullptr;   // partial argmax token ids
   std::string nccl_err;          // first collective failure (surfaced as HSD_ENCCL)
   // hsd_kstamp: per-launch %globaltimer stamps of the verify GEMMs inside graph replays
@@ -518,6 +524,42 @@ static void shard_head_verify(hsd_ctx* c, int M) {
   const size_t es = c->esz;
   const int n = c->n, G = c->G, r = c->srank;
   const int* lo = c->shard_lo;
+  if (c->cfg.accept_mode == HSD_STOCHASTIC) {
+    // per-row records over each shard's columns -> merged lse / tree-token logits /
+    // Gumbel top-KG of this rank's rows (shard.cu); the walk never needs full rows
+    const int T = c->T;
+    const size_t rec = stoch_record_floats(T);
+    const uint32_t seed = (uint32_t)c->cfg.seed;
+    const float temp = c->cfg.temperature;
+    if (c->shard_mode == HSD_SHARD_SIM) {
+      for (int s = 0; s < G; ++s) {
+        const int w = lo[s + 1] - lo[s];
+        gemm(c, c->a, n, (const char*)c->head + (size_t)lo[s] * n * es, n, c->lslice, w, M, w, n, false, P_HEAD_VERIFY);
+        { Prof pf(c, P_ROWWISE);
+          launch_stoch_part(c->lslice, M, w, w, lo[s], T, c->t_tok, c->req_id, c->step, seed, temp,
+                            c->sp_all + (size_t)s * M * rec, c->st); }
+      }
+      { Prof pf(c, P_ROWWISE);
+        launch_stoch_merge(c->sp_all, G, (size_t)M, 0, M, T, c->sh_lse, c->sh_tl, c->sh_gv, c->sh_gi, c->st); }
+      g_hsd_launches += G + 1;
+      return;
+    }
+    const int w = lo[r + 1] - lo[r];
+    const int b = c->b;
+    if (!shard_allgather(c->a, c->a_all, (size_t)M * n * es, c->comm, c->st, c->nccl_err)) return;
+    if (!shard_allgather(c->t_tok, c->tt_all, (size_t)b * T * 4, c->comm, c->st, c->nccl_err)) return;
+    if (!shard_allgather(c->req_id, c->rid_all, (size_t)b * 4, c->comm, c->st, c->nccl_err)) return;
+    gemm(c, c->a_all, n, (const char*)c->head + (size_t)lo[r] * n * es, n, c->lslice, w, G * M, w, n, false,
+         P_HEAD_VERIFY);
+    { Prof pf(c, P_ROWWISE);
+      launch_stoch_part(c->lslice, G * M, w, w, lo[r], T, c->tt_all, c->rid_all, c->step, seed, temp, c->sp_loc,
+                        c->st); }
+    if (!shard_allgather(c->sp_loc, c->sp_all, (size_t)G * M * rec * 4, c->comm, c->st, c->nccl_err)) return;
+    { Prof pf(c, P_ROWWISE);
+      launch_stoch_merge(c->sp_all, G, (size_t)G * M, r * M, M, T, c->sh_lse, c->sh_tl, c->sh_gv, c->sh_gi, c->st); }
+    g_hsd_launches += 2;
+    return;
+  }
   if (c->shard_mode == HSD_SHARD_SIM) {
     for (int s = 0; s < G; ++s) {
       const int w = lo[s + 1] - lo[s];
@@ -653,7 +695,7 @@ static void stage_verify(hsd_ctx* c) {
   for (int l = 0; l < c->L; ++l) layer_forward(c, c->layers[l], c->Hver, M, T, b, m, kv_layer(c, c->kv_t, l), c->max_pos);
   c->pass_verify = 0;
   launch_rmsnorm(c->Hver, M, n, c->cfg.rms_eps, c->a, c->dt, c->mv.pos, c->st);
-  if (c->shard_mode != HSD_SHARD_NONE) {   // greedy only (checked at init)
+  if (c->shard_mode != HSD_SHARD_NONE) {
     shard_head_verify(c, M);
   } else {
     gemm(c, c->a, n, c->head, n, c->logits, c->V, M, c->V, n, false, P_HEAD_VERIFY);
@@ -676,6 +718,7 @@ static void walk_compact_commit(hsd_ctx* c, int append) {
   A.N = c->N; A.t_max = c->T; A.V = c->V; A.temperature = c->cfg.temperature;
   A.seed = (uint32_t)c->cfg.seed; A.req_id = c->req_id;
   A.t_tok = c->t_tok; A.t_par = c->t_par; A.t_n = c->t_n; A.argmax = c->argmax; A.logits = c->logits;
+  A.sh_lse = c->sh_lse; A.sh_tl = c->sh_tl; A.sh_gv = c->sh_gv; A.sh_gi = c->sh_gi;   // (null unless sharded + stochastic)
   A.step = c->step;
   A.acc_n = c->acc_n; A.acc_slots = c->acc_slots; A.bonus = c->bonus; A.emitted = c->emitted;
   A.n_emitted = c->n_emitted;
@@ -702,6 +745,7 @@ static void stage_accept(hsd_ctx* c, int32_t* d_emitted, int32_t* d_n) {
   A.N = c->N; A.t_max = c->T; A.V = c->V; A.temperature = c->cfg.temperature;
   A.seed = (uint32_t)c->cfg.seed; A.req_id = c->req_id;
   A.t_tok = c->t_tok; A.t_par = c->t_par; A.t_n = c->t_n; A.argmax = c->argmax; A.logits = c->logits;
+  A.sh_lse = c->sh_lse; A.sh_tl = c->sh_tl; A.sh_gv = c->sh_gv; A.sh_gi = c->sh_gi;   // (null unless sharded + stochastic)
   A.step = c->step;
   A.acc_n = c->acc_n; A.acc_slots = c->acc_slots; A.bonus = c->bonus; A.emitted = c->emitted;
   A.n_emitted = c->n_emitted;
@@ -937,8 +981,11 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     fprintf(stderr, "hsd_init_model: the token-AR draft mode is not combined with the vocab-sharded head\n");
     return HSD_EUNSUP;
   }
-  if (cfg->shard_mode != HSD_SHARD_NONE && cfg->accept_mode != HSD_GREEDY) {
-    fprintf(stderr, "hsd_init_model: the vocab-sharded lm_head supports greedy acceptance only\n");
+  if (cfg->shard_mode != HSD_SHARD_NONE && cfg->accept_mode != HSD_GREEDY &&
+      cfg->branch_k + cfg->resample_budget_Br >= HSD_SHARD_KG) {
+    // a rejected set (the children of one node, <= k + B_r) must leave a candidate in
+    // the merged Gumbel top-KG
+    fprintf(stderr, "hsd_init_model: stochastic + vocab shards needs branch_k + B_r < %d\n", HSD_SHARD_KG);
     return HSD_EUNSUP;
   }
   hsd_ctx* ctx = new hsd_ctx();
@@ -1164,6 +1211,18 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
       c->pv_loc = F((size_t)G * rows); c->pi_loc = I((size_t)G * rows);
       c->pv_all = F((size_t)G * G * rows); c->pi_all = I((size_t)G * G * rows);
       if (c->shard_mode == HSD_SHARD_NCCL) c->a_all = A((size_t)G * rows * n * es);
+      if (cfg->accept_mode == HSD_STOCHASTIC) {
+        const size_t rec = stoch_record_floats(T), vrows = (size_t)b * T;
+        const size_t grow = c->shard_mode == HSD_SHARD_NCCL ? (size_t)G * vrows : vrows;
+        c->sp_loc = F(grow * rec);
+        c->sp_all = F((size_t)G * grow * rec);
+        c->sh_lse = F(vrows);
+        c->sh_tl = F(vrows * T);
+        c->sh_gv = F(vrows * HSD_SHARD_KG);
+        c->sh_gi = I(vrows * HSD_SHARD_KG);
+        c->tt_all = I((size_t)G * vrows);
+        c->rid_all = I((size_t)G * b);
+      }
     }
     if (fail_alloc) { hsd_destroy(c); return HSD_ENOMEM; }
     if (cudaMallocHost(&c->h_pinned, sizeof(int32_t) * (size_t)b * (N + 2)) != cudaSuccess) c->h_pinned = nullptr;
@@ -1477,6 +1536,10 @@ hsd_status hsd_get_tensor(hsd_ctx* ctx, const char* name, hsd_tensor* out) {
   if (s == "pt_depth") return set(c->pt_depth, 2, {b, Br1});
   if (s == "pt_lj") return set(c->pt_lj, 0, {b, Br1});
   if (s == "verify_logits") return set(c->logits, 0, {b, T, c->V});
+  if (s == "shard_lse" && c->sh_lse) return set(c->sh_lse, 0, {b, T});
+  if (s == "shard_tl" && c->sh_tl) return set(c->sh_tl, 0, {b, T, T});
+  if (s == "shard_gv" && c->sh_gv) return set(c->sh_gv, 0, {b, T, HSD_SHARD_KG});
+  if (s == "shard_gi" && c->sh_gi) return set(c->sh_gi, 2, {b, T, HSD_SHARD_KG});
   if (s == "verify_argmax") return set(c->argmax, 2, {b, T});
   if (s == "verify_hidden") return set(c->Hver, 0, {b, T, n});
   if (s == "acc_n") return set(c->acc_n, 2, {b});

@@ -77,6 +77,15 @@ size_t attention_ws_floats(int M, int Hq, int hd, int max_splits);
 // shard.cu: vocab-sharded lm_head -- partial argmax / merge /
 // column scatter kernels and the run-time-loaded NCCL entry points
 #define HSD_MAX_SHARDS 16
+#define HSD_SHARD_KG 16   // Gumbel candidates kept per row and shard (stochastic + vocab shards)
+// stochastic acceptance over a vocab-sharded head (shard.cu): per-row records of a
+// shard's columns, then their merge into lse / tree-token logits / Gumbel top-KG
+void launch_stoch_part(const float* x, int rows, int ld, int w, int col0, int T, const int32_t* tree_tok,
+                       const int32_t* req_id, const int32_t* step, uint32_t seed, float temperature, float* out,
+                       cudaStream_t st);
+void launch_stoch_merge(const float* part, int G, size_t sstride, int row0, int M, int T, float* lse, float* tl,
+                        float* gv, int32_t* gi, cudaStream_t st);
+size_t stoch_record_floats(int T);
 void launch_argmax_part(const float* x, int rows, int ld, int w, int col0, float* outv, int32_t* outi,
                         cudaStream_t st);
 void launch_argmax_merge(const float* pv, const int32_t* pi, int S, int stride, int row0, int M,

@@ -41,6 +41,8 @@ ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--out", default="")
 ap.add_argument("--batch", type=int, default=0, help="requests per step (more samples of the planted acceptance)")
+ap.add_argument("--seeds", default="0,1,2", help="weight seeds; tau / acceptance pooled over the seeds' runs that "
+                                                "stayed on the planted continuation")
 a = ap.parse_args()
 cfg = get_config(a.config)
 if a.batch:
@@ -57,24 +59,39 @@ stream = torch.cuda.Stream()
 pr = prompts(cfg, batch=b)
 need_ctx = cfg.prompt_len + (a.steps + a.warmup + 12) * (N + 1) * 2 + 16
 rows = []
+seeds = [int(x) for x in a.seeds.split(",")]
 for name, flags in VARIANTS:
-    ctx = hsd.init_model(cfg, device=0, stream=stream.cuda_stream, precision=hsd.BF16, seed=0, max_batch=b,
-                         max_ctx=need_ctx + 64 * (N + 1), tcgen05=True, flags=flags | hsd.FLAG_PLANTED,
-                         plant_rates=rates, vocab_perm=vocab_permutation(cfg.vocab, 0) if cfg.hot_tokens else None)
-    with torch.cuda.stream(stream):
-        tau, tps, ms, info, counts = bench.planted_leg(ctx, pr, cfg, b, N, a.steps, a.warmup, stream,
-                                                       return_counts=True, attempts=8)
-    m = counts.reshape(-1) - 1                      # accepted drafts per request-step
+    all_m, ms_l, tps_l, att, on = [], [], [], [], 0
+    for seed in seeds:
+        ctx = hsd.init_model(cfg, device=0, stream=stream.cuda_stream, precision=hsd.BF16, seed=seed, max_batch=b,
+                             max_ctx=need_ctx + 64 * (N + 1), tcgen05=True, flags=flags | hsd.FLAG_PLANTED,
+                             plant_rates=rates,
+                             vocab_perm=vocab_permutation(cfg.vocab, 0) if cfg.hot_tokens else None)
+        with torch.cuda.stream(stream):
+            tau, tps, ms, info, counts = bench.planted_leg(ctx, pr, cfg, b, N, a.steps, a.warmup, stream,
+                                                           return_counts=True, attempts=8)
+        ms_l.append(ms)
+        att.append(info["attempts"])
+        if info["on_continuation"]:   # acceptance statistics only from runs that stayed on the continuation
+            on += 1
+            all_m.append(counts.reshape(-1))
+            tps_l.append(tps)
+        ctx.destroy()
+        del ctx
+        torch.cuda.empty_cache()
+    em = np.concatenate(all_m) if all_m else np.zeros(0)
+    m = em - 1
     cond = []
     for d in range(1, N + 1):
         base = int((m >= d - 1).sum())
         cond.append(round(float((m >= d).sum()) / base, 3) if base else None)
-    rows.append({"variant": name, "tau": round(tau, 3), "ms_per_step": round(ms, 3), "tokens_per_s": round(tps, 1),
-                 "cond_accept_by_depth": cond, **info})
+    ms_mean = float(np.mean(ms_l))
+    tau = float(em.mean()) if em.size else None
+    rows.append({"variant": name, "tau": round(tau, 3) if tau else None, "ms_per_step": round(ms_mean, 3),
+                 "tokens_per_s": round(tau * b / (ms_mean / 1e3), 1) if tau else None,
+                 "cond_accept_by_depth": cond, "samples": int(em.size), "seeds_on_continuation": f"{on}/{len(seeds)}",
+                 "attempts": att})
     print(json.dumps(rows[-1]), flush=True)
-    ctx.destroy()
-    del ctx
-    torch.cuda.empty_cache()
 
 # NEXT-2: one-pass head vs N iterative head GEMMs (weights [V, n] bf16 streamed each time)
 W = (torch.randn(cfg.vocab, cfg.hidden, device="cuda") * 0.01).to(torch.bfloat16)

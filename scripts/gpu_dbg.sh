@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 python -m paper_2602_21224_b200.build > /dev/null
-timeout 1500 python -m pytest tests -m gpu -q -rf -k "fusion_off or first_token" 2>&1 | tail -8 > gpurun_out/dbg.txt
+timeout 900 python -m pytest tests/test_gpu_vocab_shard.py -q -rf 2>&1 | tail -12 > gpurun_out/dbg.txt

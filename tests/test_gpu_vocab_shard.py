@@ -114,3 +114,100 @@ def test_nccl_single_rank_group_in_graph():
     nid = hsd.nccl_unique_id()
     got = _run(cfg, hsd.FP32_VERIFY, steps, shard_mode=hsd.SHARD_NCCL, vocab_shards=1, shard_rank=0, nccl_id=nid)
     assert got == base
+
+
+# ------------------------------------------------------------- stochastic (R13)
+def _stoch(vocab=1024):
+    return _wide(vocab).replace(accept="stochastic")
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_sim_shards_stochastic_fp32_identical(G):
+    """Stochastic acceptance over the vocab-sharded head: per-row records of each
+    shard (max / sum of l/T, Gumbel top-KG, tree-token logits), merged exactly. In
+    fp32-verify the sharded context emits the unsharded context's tokens: Gumbel
+    scores are computed per element by the same expression on bit-identical logits,
+    the lse merge differs only in summation order."""
+    cfg = _stoch()
+    steps = 10
+    base = _run(cfg, hsd.FP32_VERIFY, steps, seed=3)
+    got = _run(cfg, hsd.FP32_VERIFY, steps, seed=3, shard_mode=hsd.SHARD_SIM, vocab_shards=G)
+    assert got == base
+
+
+def _staged_stoch(cfg, precision, G, tcgen05, seed=4):
+    res = []
+    for shard in ({}, dict(shard_mode=hsd.SHARD_SIM, vocab_shards=G)):
+        ctx = hsd.init_model(cfg, device=0, precision=precision, seed=seed, max_ctx=cfg.prompt_len + 64,
+                             tcgen05=tcgen05, stream=torch.cuda.Stream().cuda_stream, **shard)
+        ctx.prefill(prompts(cfg))
+        ctx.build_tree()
+        tree = (ctx.tensor("tree_tok").clone(), ctx.tensor("tree_par").clone(), int(ctx.tensor("tree_n").cpu()[0]))
+        ctx.verify_tree()
+        if shard:
+            out = {k: ctx.tensor("shard_" + k).clone() for k in ("lse", "tl", "gv", "gi")}
+        else:
+            out = {"logits": ctx.tensor("verify_logits").clone()}
+        out["tree"] = tree
+        ctx.accept_and_compact()
+        out["emitted"] = ctx.tensor("emitted").clone()
+        ctx.destroy()
+        res.append(out)
+    return res
+
+
+@pytest.mark.parametrize("G", [2, 5])
+def test_sim_shards_stochastic_partials_match_full_rows(G):
+    """The merged partials against the unsharded context's full verify-logits rows
+    (same tree, fp32-verify): lse = logsumexp(l / T) to fp32 rounding, tree-token
+    logits exactly, the Gumbel top-KG exactly (scores by the walk's own stream)."""
+    cfg = _stoch()
+    T = cfg.budget_B + cfg.resample_budget_Br + 1
+    full, sh = _staged_stoch(cfg, hsd.FP32_VERIFY, G, False)
+    assert all(torch.equal(x, y) for x, y in zip(full["tree"][:2], sh["tree"][:2]))
+    n = full["tree"][2]
+    L = full["logits"][0, :n].double()                    # [n, V]
+    lse = torch.logsumexp(L / cfg.temperature, dim=-1)
+    assert torch.allclose(sh["lse"][0, :n].double(), lse, rtol=0, atol=2e-5 * lse.abs().max().item())
+    tok = full["tree"][0][0, :T].long()
+    tl = sh["tl"][0, :n]
+    for s2 in range(n):
+        assert torch.equal(tl[:, s2], full["logits"][0, :n, tok[s2]])
+    # Gumbel: the walk's kernel draws the same scores -> hsd_debug_gumbel gives the argmax
+    assert torch.equal(sh["emitted"], full["emitted"])
+    gi = sh["gi"][0, :n]
+    assert (gi[:, 1:] != gi[:, :1]).all()                 # distinct candidates, sorted lists
+    assert (sh["gv"][0, :n, 1:] <= sh["gv"][0, :n, :-1]).all()
+
+
+def test_stochastic_shard_contract():
+    """k + B_r must leave a Gumbel candidate after the largest rejected set."""
+    cfg = _stoch().replace(branch_k=8, resample_budget_Br=12)
+    with pytest.raises(hsd.HsdError):
+        hsd.init_model(cfg, device=0, precision=hsd.FP32_VERIFY, seed=0, shard_mode=hsd.SHARD_SIM, vocab_shards=2)
+
+
+@pytest.mark.parametrize("G", [2, 5])
+def test_sim_shards_stochastic_bf16_tcgen05(G):
+    """bf16 tcgen05 with the stochastic sharded head: merged lse within the bf16 bar of
+    the unsharded rows' logsumexp, identical Gumbel-max where the top-2 Gumbel margin is
+    clear (the two contexts' bf16 states differ by rounding, sharded or not)."""
+    cfg = _stoch(1024)
+    full, sh = _staged_stoch(cfg, hsd.BF16, G, True)
+    if not all(torch.equal(x, y) for x, y in zip(full["tree"][:2], sh["tree"][:2])):
+        pytest.skip("trees differ by bf16 rounding")
+    n = full["tree"][2]
+    L = full["logits"][0, :n].double()
+    lse = torch.logsumexp(L / cfg.temperature, dim=-1)
+    assert ((sh["lse"][0, :n].double() - lse).abs() / lse.abs().clamp_min(1)).max().item() <= 2e-2
+
+
+def test_nccl_single_rank_stochastic_in_graph():
+    """The NCCL stochastic path (all-gathers of rows, tree tokens, request ids and
+    records) with a one-rank group inside the step graph == the unsharded context."""
+    cfg = _stoch()
+    steps = 6
+    base = _run(cfg, hsd.FP32_VERIFY, steps, seed=5)
+    got = _run(cfg, hsd.FP32_VERIFY, steps, seed=5, shard_mode=hsd.SHARD_NCCL, vocab_shards=1, shard_rank=0,
+               nccl_id=hsd.nccl_unique_id())
+    assert got == base
