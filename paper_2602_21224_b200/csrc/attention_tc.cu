@@ -112,6 +112,17 @@ HSD_DEV float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA pipe for finite x <= 8 (the lazy running max bounds x): 2^floor(x)
+// times a degree-3 minimax polynomial of the fraction (max rel err ~1e-4, below the
+// bf16 rounding of P); x clamped at -125 (the result is then ~2^-125, not 0 -- used
+// only where every key is visible, so no -inf inputs)
+HSD_DEV float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float fi = floorf(x);
+  const float f = x - fi;
+  const float p = fmaf(fmaf(fmaf(0.0788220f, f, 0.2261575f), f, 0.6951461f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((int)fi << 23));
+}
 HSD_DEV void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) {   // caller issues tcgen05.wait::ld
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -147,7 +158,9 @@ HSD_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
 template <int SW>
 HSD_DEV void quad_sync(int q) { asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * SW) : "memory"); }
 
-template <int SW>
+// NPOLY of each thread's KPW exponentials (fully visible chunks) run on the FMA pipe
+// instead of MUFU (16 ex2 / clock / SM bounds the exponent phase)
+template <int SW, int NPOLY>
 __global__ void __launch_bounds__(nthreads<SW>(), 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -431,7 +444,8 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
       // raw scores, -inf where invisible (scale_log2 > 0 keeps the order, and is
       // folded into the exponent's FFMA below)
       float s[KPW];
-      if (__all_sync(0xffffffffu, (vm0 & vm1) == 0xffffffffu)) {   // whole warp sees all its keys
+      const bool allvis = __all_sync(0xffffffffu, (vm0 & vm1) == 0xffffffffu);
+      if (allvis) {   // whole warp sees all its keys
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           s[i] = __uint_as_float(r0[i]);
@@ -472,11 +486,22 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
       // P_j (bf16) over this part's KPW/2 columns of S_j (KPW keys, 2 per column);
       // its row sum l is accumulated by the P V MMA itself (O column hd)
       uint32_t pw[32];
+      if (NPOLY > 0 && allvis) {
 #pragma unroll
-      for (int i = 0; i < KPW / 2; ++i) {
-        const float p0 = ex2(fmaf(s[2 * i], scale_log2, -msub)), p1 = ex2(fmaf(s[2 * i + 1], scale_log2, -msub));
-        __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
-        pw[i] = *(uint32_t*)&pr;
+        for (int i = 0; i < KPW / 2; ++i) {
+          const float x0 = fmaf(s[2 * i], scale_log2, -msub), x1 = fmaf(s[2 * i + 1], scale_log2, -msub);
+          const bool poly = (i % (KPW / 2 / (NPOLY / 2 > 0 ? NPOLY / 2 : 1))) == 0;   // spread over the row
+          const float p0 = poly ? ex2_poly(x0) : ex2(x0), p1 = poly ? ex2_poly(x1) : ex2(x1);
+          __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
+          pw[i] = *(uint32_t*)&pr;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < KPW / 2; ++i) {
+          const float p0 = ex2(fmaf(s[2 * i], scale_log2, -msub)), p1 = ex2(fmaf(s[2 * i + 1], scale_log2, -msub));
+          __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
+          pw[i] = *(uint32_t*)&pr;
+        }
       }
       if constexpr (KPW == 64) {
         tmem_st32(tS + lane_off + (uint32_t)((j & 1) * CHUNK + part * 32), pw);
@@ -771,7 +796,8 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   // HSD_ATTN_SW=2|4 forces one.
   static const int sw_env = [] { const char* e = getenv("HSD_ATTN_SW"); return e ? atoi(e) : 0; }();
   const int sw = sw_env == 2 || sw_env == 4 ? sw_env : ((size_t)S * base_ctas > 2 * (size_t)num_sms() ? 4 : 2);
-  static size_t attr[2] = {0, 0};   // (the kernel also has ~8-10 KB of static shared memory)
+  static size_t attr[4] = {0, 0, 0, 0};   // (the kernel also has ~8-10 KB of static shared memory)
+  static const int poly_env = [] { const char* e = getenv("HSD_ATTN_POLY"); return e ? atoi(e) : 0; }();
   auto launch = [&](auto kern, int nthr, size_t& at) {
     if (smem > at) {
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
@@ -785,8 +811,11 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
     else launch_k(kern, grid, dim3(nthr), smem, st, mk, mv, P);
     return true;
   };
-  const bool ok = sw == 4 ? launch(attention_tc_kernel<4>, nthreads<4>(), attr[1])
-                          : launch(attention_tc_kernel<2>, nthreads<2>(), attr[0]);
+  const bool ok = poly_env == 8
+                      ? (sw == 4 ? launch(attention_tc_kernel<4, 8>, nthreads<4>(), attr[3])
+                                 : launch(attention_tc_kernel<2, 8>, nthreads<2>(), attr[2]))
+                      : (sw == 4 ? launch(attention_tc_kernel<4, 0>, nthreads<4>(), attr[1])
+                                 : launch(attention_tc_kernel<2, 0>, nthreads<2>(), attr[0]));
   if (!ok) return -1;
   if (P.cluster) return 1;
   int launched = 1;

@@ -31,7 +31,9 @@ constexpr int NT = 1024;
       P.trace[(i)] = t_;                                                                            \
     }                                                                                               \
   } while (0)
-constexpr int CL = 8;       // CTAs per request (one thread-block cluster)
+// CTAs per request (one thread-block cluster): 8, or 4 when the batch has more
+// requests than 8-CTA clusters fit at once (one 1024-thread CTA per SM: c3's 32
+// requests ran as 3 waves of 15 clusters; 4-CTA clusters take them in one wave)
 constexpr int KMAX = 8;
 constexpr int MAXN = 256;
 constexpr int MAXW = MAXN / 64;
@@ -83,6 +85,7 @@ struct Partial {
 //     (exact (max, sum-exp) combination, top-k by rank), appends the children in
 //     frontier order and runs TopkByJointProb -- redundantly and identically, so
 //     no second barrier is needed to publish the frontier.
+template <int CL>
 struct ClusterSm {
   Partial part[2][KMAX][CL];
   int Q[KMAX], Qtok[KMAX], nq;
@@ -107,9 +110,9 @@ HSD_DEV void merge_lists_lanes(int nlists, const float* lv, const int* lj, int k
   }
 }
 
-template <int KT>
+template <int KT, int CL>
 HSD_DEV void build_subtree(const TreeParams& P, int req, int row0, int steps, int root_tok, NodesSm& nd,
-                           ClusterSm& cs) {
+                           ClusterSm<CL>& cs) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -372,7 +375,7 @@ HSD_DEV void prune_nodes(NodesSm& nd, int keep, NodesSm& tmp) {
   __syncthreads();
 }
 
-template <int KT>
+template <int KT, int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(TreeParams P, int mode) {
   TTRACE(0);
   l2pf_issue(P.pf);
@@ -381,7 +384,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(Tre
   l2pf_issue(P.pf, 1);
   pdl_trigger();
   __shared__ NodesSm nd, tmp;
-  __shared__ ClusterSm cs;
+  __shared__ ClusterSm<CL> cs;
   __shared__ int slot_of[MAXN], maxdepth;
   __shared__ uint64_t anc[MAXN][MAXW];
   const int req = blockIdx.x / CL;
@@ -394,7 +397,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(Tre
     int bonus = P.bonus[req];
     int n_remain = P.N - m - 1;
     if (P.resample && n_remain > P.r && n_remain > 0) {
-      build_subtree<KT>(P, req, m + 1, n_remain, bonus, nd, cs);
+      build_subtree<KT, CL>(P, req, m + 1, n_remain, bonus, nd, cs);
       if (!leader) return;
       prune_nodes(nd, P.Br, tmp);
     } else {
@@ -417,7 +420,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT) tree_kernel(Tre
 
   // ---- fresh tree: Alg. 1 over all N rows from the root (last committed token)
   const int root = P.root_tok[req];
-  build_subtree<KT>(P, req, 0, P.N, root, nd, cs);
+  build_subtree<KT, CL>(P, req, 0, P.N, root, nd, cs);
   if (!leader) return;
   TTRACE(40);
   prune_nodes(nd, P.B, tmp);
@@ -557,18 +560,30 @@ void tree_trace_init() {
   if (getenv("HSD_TREE_TRACE") && !g_tree_trace) cudaMalloc(&g_tree_trace, 64 * 8);
 }
 
+int num_sms();   // gemm_tc.cu (cached device SM count)
+
 void launch_tree(const TreeParams& P0, int mode, int n_req, cudaStream_t st) {
   if (n_req <= 0) return;
   TreeParams P = P0;
   P.trace = mode == TREE_MODE_FRESH ? g_tree_trace : nullptr;   // (never mutate the kernel's P: a local copy)
+  static const int cl_env = [] { const char* e = getenv("HSD_TREE_CL"); return e ? atoi(e) : 0; }();
+  const int cl = cl_env == 4 || cl_env == 8 ? cl_env : (n_req * 8 > num_sms() ? 4 : 8);
+  auto go = [&](auto kern, int c) { launch_k(kern, n_req * c, NT, 0, st, P, mode); };
+#define HSD_TREE_CASE(KK)                                              \
+  case KK:                                                             \
+    if (cl == 4) go(tree_kernel<KK, 4>, 4); else go(tree_kernel<KK, 8>, 8); \
+    break;
   switch (P.k) {
-    case 1: launch_k(tree_kernel<1>, n_req * CL, NT, 0, st, P, mode); break;
-    case 2: launch_k(tree_kernel<2>, n_req * CL, NT, 0, st, P, mode); break;
-    case 3: launch_k(tree_kernel<3>, n_req * CL, NT, 0, st, P, mode); break;
-    case 4: launch_k(tree_kernel<4>, n_req * CL, NT, 0, st, P, mode); break;
-    case 5: launch_k(tree_kernel<5>, n_req * CL, NT, 0, st, P, mode); break;
-    case 6: launch_k(tree_kernel<6>, n_req * CL, NT, 0, st, P, mode); break;
-    case 7: launch_k(tree_kernel<7>, n_req * CL, NT, 0, st, P, mode); break;
-    default: launch_k(tree_kernel<8>, n_req * CL, NT, 0, st, P, mode); break;
+    HSD_TREE_CASE(1)
+    HSD_TREE_CASE(2)
+    HSD_TREE_CASE(3)
+    HSD_TREE_CASE(4)
+    HSD_TREE_CASE(5)
+    HSD_TREE_CASE(6)
+    HSD_TREE_CASE(7)
+    default:
+      if (cl == 4) go(tree_kernel<8, 4>, 4); else go(tree_kernel<8, 8>, 8);
+      break;
+#undef HSD_TREE_CASE
   }
 }

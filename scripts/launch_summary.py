@@ -17,7 +17,10 @@ def load(path):
 
 def step_slice(names, which=1):
     tk = [i for i, (n, _) in enumerate(names) if n == 'tree_kernel']
-    # tree_kernel launches come in (fresh, resample) pairs per step
+    # tree_kernel launches come in (fresh, resample) pairs per step; a capture of
+    # exactly one step (scripts/profile_step.py --stage step) is taken whole
+    if len(tk) <= 2:
+        return names
     return names[tk[2 * which]:tk[2 * which + 2]]
 
 if __name__ == '__main__':
