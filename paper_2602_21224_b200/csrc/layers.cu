@@ -114,6 +114,14 @@ constexpr int VROWS = 32;         // rows per V-transpose CTA
 // shared memory and writes it along the rows (lane = row), so consecutive
 // lanes hit consecutive slots -- contiguous for a tree / prompt chunk, whose
 // rows sit at consecutive cache positions.
+// 4 consecutive elements (8-byte aligned for bf16, 16-byte for fp32)
+template <typename T> HSD_DEV void store4(T* d, float4 v);
+template <> HSD_DEV void store4<float>(float* d, float4 v) { *(float4*)d = v; }
+template <> HSD_DEV void store4<bf16>(bf16* d, float4 v) {
+  const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+  *(uint2*)d = make_uint2(*(const uint32_t*)&a, *(const uint32_t*)&b);
+}
+
 template <typename T>
 __device__ void v_transpose_block(float* __restrict__ qkv, const RowMeta& m, int M, int Hq, const KVLayer& kv,
                                   int vb, int zero) {
@@ -197,6 +205,48 @@ __global__ void __launch_bounds__(128) qkv_rope_kv_kernel(float* __restrict__ qk
     // pair (c4: 5 pairs per thread, qkv_rope ~1 ms per layer in the launch list)
     constexpr int RP = 8;
     const int npairs = (Hq + Hkv) * half;
+    if ((half & 3) == 0) {
+      // 4 consecutive rotation pairs per item: float4 loads of both halves and of the
+      // cos / sin rows, 4-element stores (8 bytes of bf16)
+      const int nq4 = npairs / 4, half4 = half / 4;
+      constexpr int RQ = 4;
+      for (int i0 = tid; i0 < nq4; i0 += RQ * nthr) {
+        float4 x1[RQ], x2[RQ], cc[RQ], ss[RQ];
+#pragma unroll
+        for (int u = 0; u < RQ; ++u) {
+          const int i = i0 + u * nthr;
+          if (i < nq4) {
+            const int h = i / half4, j = (i % half4) * 4;
+            x1[u] = *(const float4*)(row + h * hd + j);
+            x2[u] = *(const float4*)(row + h * hd + j + half);
+            cc[u] = *(const float4*)(c + j);
+            ss[u] = *(const float4*)(sn + j);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < RQ; ++u) {
+          const int i = i0 + u * nthr;
+          if (i >= nq4) break;
+          const int h = i / half4, j = (i % half4) * 4;
+          const float4 a = x1[u], b2 = x2[u], co = cc[u], si = ss[u];
+          const float4 y1 = make_float4(a.x * co.x - b2.x * si.x, a.y * co.y - b2.y * si.y, a.z * co.z - b2.z * si.z,
+                                        a.w * co.w - b2.w * si.w);
+          const float4 y2 = make_float4(b2.x * co.x + a.x * si.x, b2.y * co.y + a.y * si.y, b2.z * co.z + a.z * si.z,
+                                        b2.w * co.w + a.w * si.w);
+          T* d1;
+          T* d2;
+          if (h < Hq) {
+            d1 = qo + h * hd + j;
+            d2 = d1 + half;
+          } else {
+            d1 = base + kv_offset(page, 0, Hkv, h - Hq, kv.page_size, hd, slot, j);
+            d2 = d1 + half;
+          }
+          store4<T>(d1, y1);
+          store4<T>(d2, y2);
+        }
+      }
+    } else
     for (int i0 = tid; i0 < npairs; i0 += RP * nthr) {
       float x1[RP], x2[RP], cc[RP], ss[RP];
 #pragma unroll
@@ -229,7 +279,14 @@ __global__ void __launch_bounds__(128) qkv_rope_kv_kernel(float* __restrict__ qk
   // Each element was read by exactly this thread (same tid -> same indices), so
   // re-zeroing the scratch needs no cross-CTA barrier: zero what this thread read.
   if (!zero) return;   // a data-parallel GEMM stored (not accumulated) this scratch
-  if (p >= 0) {
+  if (p >= 0 && (half & 3) == 0) {   // the quads this thread read (vectorised path above)
+    const int half4 = half / 4;
+    for (int i = tid; i < (Hq + Hkv) * half4; i += nthr) {
+      const int h = i / half4, j = (i % half4) * 4;
+      *(float4*)(row + h * hd + j) = make_float4(0.f, 0.f, 0.f, 0.f);
+      *(float4*)(row + h * hd + j + half) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  } else if (p >= 0) {
     for (int i = tid; i < (Hq + Hkv) * half; i += nthr) {
       const int h = i / half, j = i % half;
       row[h * hd + j] = 0.f;
