@@ -536,11 +536,22 @@ def main():
     if not args.no_profile:
         ctx.profile(True)
         kp = min(args.steps, 4)
+        moved_rows = 0   # accepted rows the KV compaction really moved (acc_n of each profiled step)
         with torch.cuda.stream(stream):
             for _ in range(kp):
                 ctx.step()
+                stream.synchronize()
+                moved_rows += int(ctx.tensor("acc_n").clamp(min=0).sum().item())
         stream.synchronize()
         prof = ctx.profile_read()
+        if "compact" in prof:
+            # the library books N rows per request; the kernel moves only the m
+            # accepted rows (it returns at once for m = 0, the usual case on random
+            # weights) -- count the bytes it really moved: read + write of
+            # m x L x 2 x Hkv x hd elements per request
+            cms, cn, _, _ = prof["compact"]
+            esz = 2   # bf16 KV (bench runs hsd.BF16)
+            prof["compact"] = (cms, cn, 2.0 * moved_rows * cfg.layers * 2 * cfg.kv_heads * cfg.head_dim * esz, 0.0)
         ctx.profile(False)
         gbs, tfl, src = peaks()
         # the dominant kernel category with an algorithmic byte count (latency-only
@@ -573,6 +584,8 @@ def main():
                                   "us_per_launch": round(oms * 1e3 / max(on, 1), 2),
                                   "algorithmic_bytes_per_launch": oby / max(on, 1),
                                   "flop_per_byte": round(ofl / oby, 1) if ofl else None}
+                if oc == "compact":
+                    roof_other[oc]["accepted_rows_per_step"] = moved_rows / kp
         roof.update({"kernel": cat, "launches_per_step": pn / kp, "share_of_step": round(pms / total_prof, 4),
                      "peak_source": src + (" HBM copy GB/s" if ai < ridge else " sustained bf16 TFLOP/s (cuBLAS, "
                                                                           "back to back for 4 s)"),

@@ -93,8 +93,11 @@ typedef struct {
   const int32_t* vocab_perm;
   /* planted mode: acceptance rates a_1..a_N (R24)                            */
   float plant_rates[HSD_MAX_PLANT_DEPTH];
-  /* Vocab-sharded lm_head (BASELINE configs[4]). GREEDY only
-   * (stochastic + sharding -> HSD_EUNSUP). shard_mode != HSD_SHARD_NONE splits
+  /* Vocab-sharded lm_head (BASELINE configs[4]). Greedy, and
+   * stochastic through per-row (max, sum exp, Gumbel top-16, tree-token logit)
+   * records merged across shards (R29; needs branch_k + B_r < 16,
+   * else HSD_EUNSUP; the token-AR draft is not combined with sharding ->
+   * HSD_EUNSUP). shard_mode != HSD_SHARD_NONE splits
    * the two per-step heads -- the draft one-pass logits (S1a) and the
    * verify head (S2) -- by vocabulary column: shard s owns columns
    * [lo_s, lo_{s+1}), lo_s = floor(s*V/G / 128) * 128, lo_G = V, G =

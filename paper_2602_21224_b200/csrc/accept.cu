@@ -181,32 +181,70 @@ __global__ void __launch_bounds__(WT) walk_kernel(AcceptParams P) {
   }
 }
 
-// KV compaction: grid (b, layers, 2*Hkv); thread d moves dim d of rows j=1..m.
+// KV compaction (S4, "accepted-path KV is kept"): the accepted slots'
+// rows p + s_j move to the committed rows p + 1 + j. Grid (b, layers, 2*Hkv), one
+// (kind, kv head) block of the paged cache per CTA. Every source row is read into
+// registers before any row is stored (in place: a source p + s_j may be the
+// destination of a later j'). K pages are [slot][hd]: a row is hd contiguous
+// elements, moved as 16-byte vectors (bf16: 16 threads per hd-128 row). V pages
+// are V^T [hd][slot]: one element per (d, j), the m destinations of a d-row
+// being consecutive positions.
 template <typename T>
-__global__ void compact_kernel(CompactParams P) {
+__global__ void __launch_bounds__(256) compact_kernel(CompactParams P) {
   pdl_wait();
   pdl_trigger();
   const int req = blockIdx.x, layer = blockIdx.y, kh = blockIdx.z;
   const int kind = kh / P.kv_heads, h = kh % P.kv_heads;
-  const int m = P.acc_n[req];
+  const int m = min(P.acc_n[req], 16);
   if (m <= 0) return;   // (-1: request skipped by the extra verify pass)
   const int p = P.p[req], hd = P.head_dim, ps = P.page_size;
+  const int32_t* bt = P.block_table + (size_t)req * P.pages_per_req;
+  const int32_t* sl = P.acc_slots + req * P.N;
   T* base = (T*)P.kv_base + (size_t)layer * P.layer_stride;
-  for (int d = threadIdx.x; d < hd; d += blockDim.x) {
-    T vals[16];
+  // one pass, so every load precedes every store: m <= 16 rows, hd <= 128 give at
+  // most 16 x 128 / VW vector items (K) or 16 x 128 scalar items (V, or K with hd
+  // not a multiple of VW) -- within 256 threads x PER
+  constexpr int VW = 16 / sizeof(T);            // elements per 16-byte vector
+  constexpr int PER = 8;
+  if (kind == 0 && hd % VW == 0) {
+    const int vpr = hd / VW, items = m * vpr;     // (row j, vector) items
+    uint4 v[PER / 2];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (j >= m) break;
-      int key = p + P.acc_slots[req * P.N + j];
-      int page = P.block_table[(size_t)req * P.pages_per_req + key / ps];
-      vals[j] = base[kv_offset(page, kind, P.kv_heads, h, ps, hd, key % ps, d)];
+    for (int k = 0; k < PER / 2; ++k) {
+      const int i = k * blockDim.x + threadIdx.x;
+      if (i < items) {
+        const int j = i / vpr, c = (i % vpr) * VW, key = p + sl[j];
+        v[k] = *(const uint4*)(base + kv_offset(bt[key / ps], 0, P.kv_heads, h, ps, hd, key % ps, c));
+      }
     }
+    __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (j >= m) break;
-      int key = p + 1 + j;
-      int page = P.block_table[(size_t)req * P.pages_per_req + key / ps];
-      base[kv_offset(page, kind, P.kv_heads, h, ps, hd, key % ps, d)] = vals[j];
+    for (int k = 0; k < PER / 2; ++k) {
+      const int i = k * blockDim.x + threadIdx.x;
+      if (i < items) {
+        const int j = i / vpr, c = (i % vpr) * VW, key = p + 1 + j;
+        *(uint4*)(base + kv_offset(bt[key / ps], 0, P.kv_heads, h, ps, hd, key % ps, c)) = v[k];
+      }
+    }
+  } else {
+    const int items = m * hd;                     // (d, j) items, j fastest: a d-row's stores are consecutive
+    T v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = k * blockDim.x + threadIdx.x;
+      if (i < items) {
+        const int d = i / m, j = i % m, key = p + sl[j];
+        v[k] = base[kv_offset(bt[key / ps], kind, P.kv_heads, h, ps, hd, key % ps, d)];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = k * blockDim.x + threadIdx.x;
+      if (i < items) {
+        const int d = i / m, j = i % m, key = p + 1 + j;
+        base[kv_offset(bt[key / ps], kind, P.kv_heads, h, ps, hd, key % ps, d)] = v[k];
+      }
     }
   }
 }
@@ -320,8 +358,8 @@ void launch_walk(const AcceptParams& P, int n_req, cudaStream_t st) {
 void launch_compact(const CompactParams& P, int n_req, int layers, DType dt, cudaStream_t st) {
   if (n_req <= 0) return;
   dim3 grid(n_req, layers, 2 * P.kv_heads);
-  if (dt == DT_F32) launch_k(compact_kernel<float>, grid, 128, 0, st, P);
-  else launch_k(compact_kernel<bf16>, grid, 128, 0, st, P);
+  if (dt == DT_F32) launch_k(compact_kernel<float>, grid, 256, 0, st, P);
+  else launch_k(compact_kernel<bf16>, grid, 256, 0, st, P);
 }
 void launch_commit(const CommitParams& P, int n_req, cudaStream_t st) {
   if (n_req > 0) launch_k(commit_kernel, n_req, 256, 0, st, P);

@@ -12,12 +12,20 @@
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/hsd.h"
 #include "kernels.cuh"
 #include "tree.cuh"
 #include "accept.cuh"
 #include "gemm_tc.cuh"
+
+// NVTX stage ranges (host side; visible to nsys / ncu --nvtx around eager and staged
+// calls and around graph capture -- a replayed graph carries no host ranges)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 int64_t g_hsd_launches = 0;
 // Timing ablation (debug only, results become meaningless): HSD_ABLATE is a list
@@ -611,6 +619,7 @@ static void shard_head_draft(hsd_ctx* c, int R) {
 
 // ---------------------------------------------------------------------- stages
 static void stage_build(hsd_ctx* c) {
+  Nvtx nv("hsd S0+S1 draft chain, one-pass logits, Alg. 1 tree");
   const int b = c->b, N = c->N, n = c->n, R = N + 1;
   const int kvmax = c->max_pos;
   // S0 (1): draft prefill of the pending pairs x_j = W_fc [H_{j-1}; E(t_j)] (R1)
@@ -685,6 +694,7 @@ static void stage_build(hsd_ctx* c) {
 }
 
 static void stage_verify(hsd_ctx* c) {
+  Nvtx nv("hsd S2 target tree verify");
   const int b = c->b, T = c->T, n = c->n, M = b * T;
   launch_k(meta_verify_kernel, b, 32 * ((T + 31) / 32), 0, c->st, c->mv, T, c->t_n, c->t_tok, c->t_depth, c->p);
   RowMeta m = c->mv.view(c->p, c->t_anc, T, c->W);
@@ -739,6 +749,7 @@ static void walk_compact_commit(hsd_ctx* c, int append) {
 }
 
 static void stage_accept(hsd_ctx* c, int32_t* d_emitted, int32_t* d_n) {
+  Nvtx nv("hsd S3+S4 walk, compaction, Alg. 2");
   const int b = c->b;
   AcceptParams A{};
   A.mode = c->cfg.accept_mode == HSD_STOCHASTIC ? 1 : 0;
@@ -1244,6 +1255,7 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
 hsd_status hsd_prefill(hsd_ctx* ctx, int32_t n_req, const int32_t* h_tokens, int32_t stride, const int32_t* h_lens,
                        int32_t* d_first) {
   if (!ctx) return HSD_EINVAL;
+  Nvtx nv("hsd prefill");
   hsd_ctx* c = ctx;
   if (n_req < 1 || n_req > c->maxb) return fail(c, HSD_EINVAL, "n_req must be in [1, max_batch]");
   if (!h_tokens || !h_lens || stride < 1) return fail(c, HSD_EINVAL, "null prompt arrays");
@@ -1430,6 +1442,7 @@ hsd_status hsd_accept_and_compact(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n
 
 hsd_status hsd_step(hsd_ctx* ctx, int32_t* d_emitted, int32_t* d_n_emitted) {
   if (!ctx) return HSD_EINVAL;
+  Nvtx nv("hsd step");
   hsd_ctx* c = ctx;
   if (c->b < 1) return fail(c, HSD_ESTATE, "hsd_step before hsd_prefill");
   if (c->stage != 0) return fail(c, HSD_ESTATE, "hsd_step in the middle of a staged step");

@@ -87,12 +87,18 @@ def test_product_never_imports_oracle():
                 assert "import oracle" not in txt and "from oracle" not in txt, f
 
 
-def test_sharded_stochastic_is_unsupported_before_cuda(hsd):
-    """The vocab-sharded lm_head merges partial ARGMAXES only (greedy, SURVEY 8(e));
-    stochastic acceptance with sharding is refused with HSD_EUNSUP, nothing launched."""
-    c, keep = hsd.make_config(get_config("c1"), accept="stochastic", temperature=1.0,
+def test_sharded_stochastic_needs_room_for_a_candidate(hsd):
+    """Stochastic acceptance over the vocab-sharded head merges each shard's Gumbel
+    top-16 (R29): the largest rejected set (<= branch_k + B_r children) must leave
+    a candidate, so branch_k + B_r >= 16 is refused with HSD_EUNSUP before any CUDA
+    call (nothing allocated). The token-AR draft is not combined with sharding."""
+    c, keep = hsd.make_config(get_config("c1").replace(branch_k=8, resample_budget_Br=8), accept="stochastic", temperature=1.0,
                               shard_mode=hsd.SHARD_SIM, vocab_shards=2)
     h = ctypes.c_void_p()
+    s = hsd.load().hsd_init_model(ctypes.byref(c), 0, None, ctypes.byref(h))
+    assert s == hsd.HSD_EUNSUP and not h.value
+    c, keep = hsd.make_config(get_config("c1"), accept="greedy", shard_mode=hsd.SHARD_SIM, vocab_shards=2,
+                              flags=hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION | hsd.FLAG_TOKEN_AR)
     s = hsd.load().hsd_init_model(ctypes.byref(c), 0, None, ctypes.byref(h))
     assert s == hsd.HSD_EUNSUP and not h.value
 

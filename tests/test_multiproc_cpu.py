@@ -20,33 +20,45 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n_req, out):
+def _worker(rank, world, port, case, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import bench
-    lo, hi, kind = bench.plan_shard(n_req, world, rank)
+    cfg_name, batch, bpg, strong = case
+    lo, hi, gb, kind, par = bench.plan_shard(cfg_name, batch, world, rank, batch_per_gpu=bpg, strong=strong)
     ms = 10.0 + rank            # rank 1 is the slow one
     emitted = float(hi - lo) * 3
     ms_max, em_sum = bench.reduce_over_ranks(ms, emitted)
-    out[rank] = (lo, hi, kind, ms_max, em_sum)
+    out[rank] = (lo, hi, gb, kind, ms_max, em_sum)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_req", [1, 5, 64])
-def test_gloo_world2_shard_and_reduce(n_req):
+# (config, config batch, --batch-per-gpu, --strong)
+CASES = [("c3", 32, None, False),   # weak: 32 requests per GPU, global batch 64
+         ("c3", 32, 5, False),      # weak with --batch-per-gpu 5
+         ("c2", 1, None, False),    # batch-1 config: one request per GPU, distinct requests
+         ("c4", 64, None, False),   # strong: the fixed global batch of 64 split 32 / 32
+         ("c5", 5, None, True)]     # strong, uneven: 3 / 2
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_gloo_world2_shard_and_reduce(case):
     world = 2
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), n_req, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), case, out), nprocs=world, join=True)
     res = [out[r] for r in range(world)]
-    assert all(r[3] == 11.0 for r in res)                      # max over ranks
-    if n_req >= world:
-        covered = sorted(i for lo, hi, *_ in res for i in range(lo, hi))
-        assert covered == list(range(n_req))                   # a partition
-        assert all(r[2] == "batch-shard x2" for r in res)
-        assert all(r[4] == 3.0 * n_req for r in res)
+    assert all(r[4] == 11.0 for r in res)                      # max over ranks
+    gb = res[0][2]
+    assert all(r[2] == gb for r in res)
+    covered = sorted(i for lo, hi, *_ in res for i in range(lo, hi))
+    assert covered == list(range(gb))                          # a partition of the global batch
+    assert all(r[5] == 3.0 * gb for r in res)                  # tokens summed over ranks
+    cfg_name, batch, bpg, strong = case
+    if strong or cfg_name in ("c4",):
+        assert all(r[3] == "strong" for r in res) and gb == batch
     else:
-        assert all((r[0], r[1]) == (0, n_req) and r[2] == "replicas x2" for r in res)
+        assert all(r[3] == "weak" for r in res) and gb == world * (bpg or batch)
 
 
 def test_shard_requests_balanced():
