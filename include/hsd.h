@@ -264,7 +264,7 @@ hsd_status hsd_profile_read(hsd_ctx* ctx, const char* category, double* total_ms
  * pointers, row-major with leading dimensions lda/ldw/ldc (elements).
  * dtype 0 = fp32 operands (SIMT FFMA kernel), 1 = bf16 operands; use_tc = 1
  * selects the tcgen05 kernel (bf16 only); use_tc = 2 the data-parallel tcgen05
- * kernel with SwiGLU fused in the epilogue (W rows gate/up interleaved in 64-row
+ * kernel with SwiGLU fused in the epilogue (W rows gate/up interleaved in 16-row
  * groups; C is then a bf16 [M, N/2] output with leading dimension ldc; only for
  * shapes with >= 4 output tiles per SM, else HSD_EUNSUP). Otherwise C is fp32.
  * Asynchronous on `stream`.

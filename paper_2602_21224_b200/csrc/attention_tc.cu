@@ -66,6 +66,7 @@ struct AttnParams {
   int dyn;                     // 1: key splits divide the CTA's VISIBLE chunks (device-side), not max_keys
   int exp_flags;               // timing experiments only (HSD_ATTN_EXP, results wrong): 1 = drop the last q-tile
   int cluster;                 // 1: the S key-split CTAs form a cluster and reduce over DSMEM
+  int light_last;              // 1: the partly filled last q-tiles run after all full ones (HSD_ATTN_ORDER)
   RowMeta m;
   KVLayer kv;
   const bf16* q;               // [M][Hq][hd] (read directly when the q tile lives in TMEM)
@@ -197,7 +198,16 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, nsplit = gridDim.x, h = blockIdx.y;
-  const int grp = blockIdx.z / P.n_qtiles, qt = blockIdx.z % P.n_qtiles;
+  // CTA order: (request, q-tile) request-major, or with P.light_last the partly
+  // filled last q-tile of every request after all full ones (longest first)
+  int grp, qt;
+  if (P.light_last) {
+    const int nf = P.n_qtiles - 1, nfull = nf * (int)(gridDim.z / P.n_qtiles);
+    if ((int)blockIdx.z < nfull) { grp = blockIdx.z / nf; qt = blockIdx.z % nf; }
+    else { grp = blockIdx.z - nfull; qt = nf; }
+  } else {
+    grp = blockIdx.z / P.n_qtiles; qt = blockIdx.z % P.n_qtiles;
+  }
   const RowMeta& m = P.m;
   const int req = m.req[grp * P.R];
   if ((P.exp_flags & 1) && P.n_qtiles > 1 && qt == P.n_qtiles - 1) return;
@@ -726,6 +736,10 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   P.M = M; P.R = R; P.Hq = Hq; P.G = G; P.hd = hd; P.m = m; P.kv = kv;
   P.out = (bf16*)out; P.ws = ws; P.max_keys = max_keys; P.q = (const bf16*)q;
   P.n_qtiles = (R * G + QROWS - 1) / QROWS;
+  {
+    static const int order_env = [] { const char* e = getenv("HSD_ATTN_ORDER"); return e ? atoi(e) : 0; }();
+    P.light_last = order_env == 1 && P.n_qtiles > 1 && (R * G) % QROWS != 0 && (R * G) % QROWS <= QROWS / 2;
+  }
   {   // read per launch: scripts/attn_trace.py switches it on for the traced pass only
     const char* e = getenv("HSD_ATTN_EXP");
     P.exp_flags = e ? atoi(e) : 0;

@@ -1,5 +1,10 @@
 // common.cuh -- shared device helpers of the sm_100a kernels (product side).
 #pragma once
+
+// gate/up weight rows are interleaved in groups of GU_GROUP rows (gate rows of
+// features [16g, 16g+16), then their up rows): the layout the fused SwiGLU
+// epilogues, swiglu_kernel and interleave_gu_kernel share
+constexpr int GU_GROUP = 16;
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -9,6 +14,10 @@
 #define HSD_DEV __device__ __forceinline__
 
 typedef __nv_bfloat16 bf16;
+
+// silu(g) * u with the fast exponential / division (the bf16 SwiGLU epilogues;
+// __fdividef(g, inf) = 0 gives silu(-large) = 0)
+HSD_DEV float silu_mul_fast(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
 
 enum DType { DT_F32 = 0, DT_BF16 = 1, DT_I32 = 2, DT_U64 = 3 };
 

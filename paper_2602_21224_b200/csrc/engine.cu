@@ -471,11 +471,32 @@ static void layer_forward(hsd_ctx* c, const LayerW& w, float* x, int M, int R, i
   // re-zero it; the stream-K one accumulates into the zero-kept scratch big
   const bool qkv_dp = c->use_tc && c->dt == DT_BF16 && gemm_tc_supported(M, c->qkvd, n, n, n) &&
                       gemm_tc_dp(M, c->qkvd, n, false);
-  float* qkv = qkv_dp ? c->big_dp : c->big;
-  gemm(c, c->a, n, w.wqkv, n, qkv, c->qkvd, M, c->qkvd, n, false, -1, true);
-  if (!ablate("rope")) { Prof pf(c, P_ROWWISE);
-    PfScope l2(w.wo, b_o, 0, std::max(cap, b_o), 2);
-    launch_qkv_rope_kv(qkv, M, m, c->rope_cos, c->rope_sin, c->Hq, kv, c->qb, c->dt, c->st, !qkv_dp); }
+  bool qkv_fused = false;
+  if (qkv_dp && !ablate("gemm") && !ablate("rope") && c->kv_layer_elems < (size_t)INT32_MAX && gemm_tc_qkv_ok(M, c->qkvd, n, c->hd, c->Hq, c->Hkv)) {
+    // CTA-pair QKV GEMM whose epilogue applies RoPE and writes bf16 q and the
+    // paged K / V rows itself (no fp32 QKV row, no qkv_rope_kv launch)
+    const int cat = c->pass_verify ? P_GEMM_VERIFY : P_GEMM_DRAFT;
+    const double by = (double)c->qkvd * n * c->esz + (double)M * n * c->esz + (double)M * c->qkvd * 2,
+                 fl = 2.0 * M * c->qkvd * n;
+    Prof pf(c, cat, by, fl);
+    kstamp_next(c, cat, by, fl);
+    QkvEpi e;
+    e.pos = m.pos; e.kvpos = m.kvpos; e.req = m.req; e.rc = c->rope_cos; e.rs = c->rope_sin;
+    e.q_out = (bf16*)c->qb; e.kv_base = kv.base; e.block_table = kv.block_table;
+    e.pages_per_req = kv.pages_per_req; e.page_size = kv.page_size; e.Hq = c->Hq; e.Hkv = c->Hkv; e.hd = c->hd;
+    const int k = gemm_tc_qkv_bf16((const bf16*)c->a, n, (const bf16*)w.wqkv, n, M, c->qkvd, n, e, c->st);
+    g_hsd_launches += k;
+    qkv_fused = k > 0;
+  }
+  if (!qkv_fused) {
+    float* qkv = qkv_dp ? c->big_dp : c->big;
+    gemm(c, c->a, n, w.wqkv, n, qkv, c->qkvd, M, c->qkvd, n, false, -1, true);
+    if (!ablate("rope")) { Prof pf(c, P_ROWWISE);
+      PfScope l2(w.wo, b_o, 0, std::max(cap, b_o), 2);
+      launch_qkv_rope_kv(qkv, M, m, c->rope_cos, c->rope_sin, c->Hq, kv, c->qb, c->dt, c->st, !qkv_dp); }
+  } else {
+    g_hsd_launches -= 1;   // (the rope_kv launch counted below did not happen)
+  }
   if (!ablate("attn")) {
     // algorithmic attention bytes: the request's committed K/V rows once (per
     // kv head) + q/out rows; exact per-row key counts are device-side, so the
@@ -1050,7 +1071,7 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     launch_philox_fill((char*)w.wqkv + (size_t)(c->qd + c->kd) * n * es, c->dt, (size_t)c->kd * n, seed, tid0 + 2,
                        sc(n), c->st);
     launch_philox_fill(w.wo, c->dt, (size_t)n * c->qd, seed, tid0 + 3, sc(c->qd), c->st);
-    // gate (tid+4) then up (tid+5) into a scratch, then interleaved in 64-row
+    // gate (tid+4) then up (tid+5) into a scratch, then interleaved in 16-row
     // groups (see launch_swiglu / gemm_tc_swiglu_bf16)
     launch_philox_fill(c->gu_tmp, c->dt, (size_t)c->f * n, seed, tid0 + 4, sc(n), c->st);
     launch_philox_fill((char*)c->gu_tmp + (size_t)c->f * n * es, c->dt, (size_t)c->f * n, seed, tid0 + 5, sc(n),
@@ -1573,7 +1594,7 @@ hsd_status hsd_get_tensor(hsd_ctx* ctx, const char* name, hsd_tensor* out) {
   if (s == "tree_trace" && g_tree_trace) return set(g_tree_trace, 3, {64});
   if (s == "layer0_wqkv" && c->L > 0) return set(c->layers[0].wqkv, adt, {c->qkvd, n});
   // target layer weights by name, e.g. "layer7_wo" ([out, in] row-major, nn.Linear layout;
-  // gate/up rows interleaved in 64-row groups, see launch_swiglu)
+  // gate/up rows interleaved in GU_GROUP = 16-row groups, see launch_swiglu)
   if (s.rfind("layer", 0) == 0) {
     const size_t us = s.find('_');
     if (us != std::string::npos) {

@@ -30,7 +30,7 @@ constexpr int NTHREADS = 192;    // warp0 TMA, warp1 MMA, warps 2..5 epilogue
 constexpr int NTHREADS2 = 320;   // pair kernel: warps 2..5 and 6..9 = two epilogue groups
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int EPI_LD = BM + 4;   // epilogue stage row stride (floats)
-enum { EPI_ATOMIC = 0, EPI_STORE = 1, EPI_ADD = 2, EPI_SWIGLU = 3 };
+enum { EPI_ATOMIC = 0, EPI_STORE = 1, EPI_ADD = 2, EPI_SWIGLU = 3, EPI_QKV = 4 };
 
 struct TcParams {
   int M, N, K, ldc;
@@ -50,6 +50,7 @@ struct TcParams {
   bf16* H;                        // EPI_SWIGLU output [M, N/2] bf16
   int ldh;
   unsigned long long* trace;      // debug phase trace (HSD_GEMM_TRACE) or null
+  QkvEpi qe;                      // EPI_QKV (pair kernel)
   KStamp kst;                     // per-launch %globaltimer stamps (hsd_kstamp) or kst.buf == null
 };
 HSD_DEV uint64_t gtime_g() {
@@ -251,12 +252,13 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         for (int j = 0; j < 16; ++j) stage_buf[j * EPI_LD + q * 32 + lane] = __uint_as_float(r[j]);
         epi_bar();
         if (P.epi == EPI_SWIGLU) {
-          // rows 0..63 of the tile are gate rows, 64..127 the matching up rows
+          // rows [32g, 32g+16) of the tile are the gate rows of features 16g.., the
+          // next 16 rows their up rows (GU_GROUP interleave)
           const int tk = et >> 3, f8 = (et & 7) * 8;
           const int tok = tt * P.ntile + c0 + tk, f0 = tn * (BM / 2) + f8;
           if (tok < P.M && f0 < P.N / 2) {
-            const float* g = stage_buf + tk * EPI_LD + f8;
-            const float* uu = g + BM / 2;
+            const float* g = stage_buf + tk * EPI_LD + 2 * GU_GROUP * (f8 / GU_GROUP) + f8 % GU_GROUP;
+            const float* uu = g + GU_GROUP;
             uint32_t w[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -350,7 +352,8 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
   uint64_t* tfull = bars + 2 * P.stages;       // [2]
   uint64_t* tempty = bars + 2 * P.stages + 2;  // [2] (leader: one arrival per CTA)
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * P.stages + 4);
-  float* stage_buf = (float*)(bars + 2 * P.stages + 6);
+  float* stage_buf = (float*)(bars + 2 * P.stages + 6);   // 2 groups x [16 tokens][EPI_LD] fp32
+  __shared__ int tmeta[2][16][3];   // EPI_QKV: per group, the chunk's tokens' (pos, K offset, V offset)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = (int)(blockIdx.x & 1);
@@ -455,7 +458,8 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
       const int tm = (int)(t / P.n_tiles_t), tt = (int)(t % P.n_tiles_t);
       mbar_wait(&tfull[buf], aphase);
       fence_after();
-      for (int w = 0; w < wt; ++w) {
+      // (timing experiment HSD_GEMM_EXP bit 4: no epilogue at all -- MMA / operand time only)
+      for (int w = 0; w < ((P.exp & 4) ? 0 : wt); ++w) {
       const int tn = 2 * (tm * wt + w) + rank;        // this CTA's 128-row weight tile
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((buf * wt + w) * P.ntile);
       for (int c0 = 16 * grp; c0 < P.ntile; c0 += 32) {
@@ -463,22 +467,113 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
         tmem_ld16(taddr + c0, r);
 #pragma unroll
         for (int j = 0; j < 16; ++j) stage_g[j * EPI_LD + q * 32 + lane] = __uint_as_float(r[j]);
+        if (P.epi == EPI_QKV && et < 16) {
+          // the chunk's per-token cache offsets (elements, kv head 0, dim 0): pos, K row, V slot
+          const QkvEpi& e = P.qe;
+          const int tok = tt * P.ntile + c0 + et;
+          int pos = -1, ko = 0, vo = -1;
+          if (tok < P.M && (pos = e.pos[tok]) >= 0) {
+            const int kp = e.kvpos[tok];
+            const int page = e.block_table[(size_t)e.req[tok] * e.pages_per_req + kp / e.page_size];
+            const int slot = kp % e.page_size, blk = e.page_size * e.hd;
+            ko = ((page * 2) * e.Hkv) * blk + slot * e.hd;
+            vo = ((page * 2 + 1) * e.Hkv) * blk + slot;
+          }
+          tmeta[grp][et][0] = pos; tmeta[grp][et][1] = ko; tmeta[grp][et][2] = vo;
+        }
         epi_bar_g(grp);
-        if (P.epi == EPI_SWIGLU) {
-          const int tk = et >> 3, f8 = (et & 7) * 8;
+        if (P.epi == EPI_QKV) {
+          // fused RoPE / q / KV writes (qkv_rope_kv's work): the staged chunk holds all
+          // 128 features (whole heads) of 16 tokens, so a dimension's rotation partner
+          // d +- hd/2 is in the same stage row. q / K: a thread takes 16 consecutive
+          // dims of one token (thread -> (token et % 16, dims): conflict-free stage
+          // reads; two 16-byte stores). V (transposed cache, [d][slot]): a thread takes
+          // one dim of the 16 tokens, writing runs of consecutive slots as 8 / 4 / 2
+          // byte vectors; the chunk's per-token cache offsets were computed once
+          // (tmeta) before the stage barrier.
+          const QkvEpi& e = P.qe;
+          const int hd = e.hd, half = hd >> 1;
+          const int h0 = tn * BM / hd;                  // first head of the tile
+          if (!(P.exp & 1) && h0 < e.Hq + e.Hkv) {
+            const int tk = et & 15, f16 = (et >> 4) * 16;
+            const int tok = tt * P.ntile + c0 + tk;
+            const int h = h0 + f16 / hd, d0 = f16 % hd;
+            if (tok < P.M) {
+              const int pos = tmeta[grp][tk][0];
+              const float* src = stage_g + tk * EPI_LD + f16;
+              const float* prt = src + (d0 < half ? half : -half);
+              uint32_t o[8];
+              if (pos >= 0) {
+                const int j0 = d0 & (half - 1);
+                const float4* co = (const float4*)(e.rc + (size_t)pos * half + j0);
+                const float4* si = (const float4*)(e.rs + (size_t)pos * half + j0);
+                const float sg = d0 < half ? -1.f : 1.f;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float4 x = ((const float4*)src)[i], y = ((const float4*)prt)[i], c4 = co[i], s4 = si[i];
+                  const __nv_bfloat162 a0 = __floats2bfloat162_rn(x.x * c4.x + sg * y.x * s4.x, x.y * c4.y + sg * y.y * s4.y);
+                  const __nv_bfloat162 a1 = __floats2bfloat162_rn(x.z * c4.z + sg * y.z * s4.z, x.w * c4.w + sg * y.w * s4.w);
+                  o[2 * i] = *(const uint32_t*)&a0;
+                  o[2 * i + 1] = *(const uint32_t*)&a1;
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o[i] = 0u;
+              }
+              bf16* dst = nullptr;
+              if (h < e.Hq) dst = e.q_out + ((size_t)tok * e.Hq + h) * hd + d0;
+              else if (pos >= 0)
+                dst = (bf16*)e.kv_base + (size_t)tmeta[grp][tk][1] + (size_t)(h - e.Hq) * e.page_size * hd + d0;
+              if (dst) {
+                ((uint4*)dst)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+                ((uint4*)dst)[1] = make_uint4(o[4], o[5], o[6], o[7]);
+              }
+            }
+          } else if (!(P.exp & 1) && h0 < e.Hq + 2 * e.Hkv) {
+            // V heads: thread = one feature (head, dim) of the tile, 16 tokens
+            const int h = h0 + et / hd, d = et % hd;
+            bf16* vb = (bf16*)e.kv_base + (size_t)(h - e.Hq - e.Hkv) * e.page_size * hd + (size_t)d * e.page_size;
+            const int nj = min(16, P.M - (tt * P.ntile + c0));
+            int j = 0;
+            while (j < nj) {
+              const int vo = tmeta[grp][j][2];
+              if (vo < 0) { ++j; continue; }
+              const float x0 = stage_g[j * EPI_LD + et];
+              // run of consecutive cache slots starting at j (same page), up to 4
+              int run = 1;
+              while (run < 4 && j + run < nj && tmeta[grp][j + run][2] == vo + run) ++run;
+              if (run == 4 && (vo & 3) == 0) {
+                const __nv_bfloat162 a0 = __floats2bfloat162_rn(x0, stage_g[(j + 1) * EPI_LD + et]);
+                const __nv_bfloat162 a1 = __floats2bfloat162_rn(stage_g[(j + 2) * EPI_LD + et], stage_g[(j + 3) * EPI_LD + et]);
+                *(uint2*)(vb + vo) = make_uint2(*(const uint32_t*)&a0, *(const uint32_t*)&a1);
+                j += 4;
+              } else if (run >= 2 && (vo & 1) == 0) {
+                *(__nv_bfloat162*)(vb + vo) = __floats2bfloat162_rn(x0, stage_g[(j + 1) * EPI_LD + et]);
+                j += 2;
+              } else {
+                vb[vo] = __float2bfloat16_rn(x0);
+                ++j;
+              }
+            }
+          }
+        } else if (P.epi == EPI_SWIGLU) {
+          // rows [32g, 32g+16) of the tile: gate rows of features 16g.., then their up rows.
+          // Thread -> (token et % 16, 8 features): the 8 threads of a 16-byte load phase
+          // read 8 different token rows (EPI_LD = 132: 4 banks apart), conflict-free
+          // (HSD_GEMM_EXP bit 8, experiment: thread -> (token et / 8, 8 features), each warp
+          // store 4 whole 128-byte lines, 4-way bank conflicts on the stage reads)
+          const int tk = (P.exp & 8) ? et >> 3 : et & 15, f8 = (P.exp & 8) ? (et & 7) * 8 : (et >> 4) * 8;
           const int tok = tt * P.ntile + c0 + tk, f0 = tn * (BM / 2) + f8;
           if (tok < P.M && f0 < P.N / 2 && !(P.exp & 1)) {
-            const float* g = stage_g + tk * EPI_LD + f8;
-            const float* uu = g + BM / 2;
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float a0 = g[2 * e], a1 = g[2 * e + 1];
-              const __nv_bfloat162 hv = __floats2bfloat162_rn(a0 / (1.0f + expf(-a0)) * uu[2 * e],
-                                                              a1 / (1.0f + expf(-a1)) * uu[2 * e + 1]);
-              w[e] = *(const uint32_t*)&hv;
-            }
-            *(uint4*)(P.H + (size_t)tok * P.ldh + f0) = make_uint4(w[0], w[1], w[2], w[3]);
+            const float* g = stage_g + tk * EPI_LD + 2 * GU_GROUP * (f8 / GU_GROUP) + f8 % GU_GROUP;
+            const float4 g0 = *(const float4*)g, g1 = *(const float4*)(g + 4);
+            const float4 u0 = *(const float4*)(g + GU_GROUP), u1 = *(const float4*)(g + GU_GROUP + 4);
+            const __nv_bfloat162 h0 = __floats2bfloat162_rn(silu_mul_fast(g0.x, u0.x), silu_mul_fast(g0.y, u0.y));
+            const __nv_bfloat162 h1 = __floats2bfloat162_rn(silu_mul_fast(g0.z, u0.z), silu_mul_fast(g0.w, u0.w));
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(silu_mul_fast(g1.x, u1.x), silu_mul_fast(g1.y, u1.y));
+            const __nv_bfloat162 h3 = __floats2bfloat162_rn(silu_mul_fast(g1.z, u1.z), silu_mul_fast(g1.w, u1.w));
+            *(uint4*)(P.H + (size_t)tok * P.ldh + f0) =
+                make_uint4(*(const uint32_t*)&h0, *(const uint32_t*)&h1, *(const uint32_t*)&h2, *(const uint32_t*)&h3);
           }
         } else {
           // residual add: all 4 residual vectors of this thread are loaded before the
@@ -656,8 +751,9 @@ static int pair_wt(int M, int N) {
 }
 
 static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float* C, int ldc, int M, int N, int K,
-                           int epi, bf16* H, int ldh, cudaStream_t st, KStamp ks) {
+                           int epi, bf16* H, int ldh, cudaStream_t st, KStamp ks, const QkvEpi* qe = nullptr) {
   TcParams P;
+  if (qe) P.qe = *qe;
   P.M = M; P.N = N; P.K = K; P.ldc = ldc; P.C = C; P.H = H; P.ldh = ldh; P.epi = epi; P.dp = 1;
   P.trace = nullptr;
   P.kst = ks;
@@ -674,7 +770,8 @@ static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float
     P.exp = e ? atoi(e) : 0;
   }
   const int bh = (nt / 2) * BK * 2;
-  int stages = (192 * 1024) / (P.wt * A_BYTES + bh);
+  // ring: the 227 KB less the epilogue stage buffers and barriers
+  int stages = (int)((208 * 1024) / (P.wt * A_BYTES + bh));
   if (stages > 16) stages = 16;
   P.stages = stages;
   P.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nt >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
@@ -688,8 +785,8 @@ static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float
   const size_t smem = 1024 + (size_t)stages * (P.wt * A_BYTES + bh) + (2 * stages + 6) * 8 + 2 * 16 * EPI_LD * 4 + 16;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(gemm_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(gemm_tc2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(gemm_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);   // (+ static tmeta)
+    cudaFuncSetAttribute(gemm_tc2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
     attr_done = true;
   }
   const long pairs = (long)((N + 2 * BM * P.wt - 1) / (2 * BM * P.wt)) * ntt;
@@ -794,4 +891,21 @@ int gemm_tc_swiglu_bf16(const bf16* A, int lda, const bf16* W, int ldw, bf16* H,
   if (swiglu_1cta(M, N))
     return gemm_tc_launch(A, lda, W, ldw, nullptr, 0, M, N, K, EPI_SWIGLU, 1, H, ldh, st, /*allow_pair=*/false);
   return 0;
+}
+
+// QKV GEMM with RoPE / bf16 q / paged K, V writes fused into the CTA-pair epilogue
+// (verify pass at data-parallel shapes: c3 / c4 / c5). Needs whole heads per
+// 128-row weight tile and the pair kernel.
+bool gemm_tc_qkv_ok(int M, int N, int K, int hd, int Hq, int Hkv) {
+  static const bool on = [] { const char* e = getenv("HSD_GEMM_QKV_EPI"); return !(e && atoi(e) == 0); }();
+  static const bool pair_on = [] { const char* e = getenv("HSD_GEMM_2SM"); return !(e && atoi(e) == 0); }();
+  // every 128-row weight tile holds heads of one kind only (q, k or v)
+  return on && pair_on && num_sms() >= 2 && (hd == 64 || hd == 128) && (Hq * hd) % BM == 0 && (Hkv * hd) % BM == 0 &&
+         N == (Hq + 2 * Hkv) * hd && gemm_tc_dp(M, N, K, false);
+}
+
+int gemm_tc_qkv_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K, const QkvEpi& e,
+                     cudaStream_t st) {
+  if (!gemm_tc_qkv_ok(M, N, K, e.hd, e.Hq, e.Hkv)) return 0;
+  return gemm_tc2_launch(A, lda, W, ldw, nullptr, 0, M, N, K, EPI_QKV, nullptr, 0, st, take_kstamp(), &e);
 }

@@ -316,10 +316,12 @@ void launch_qkv_rope_kv(float* qkv, int M, const RowMeta& m, const float* rope_c
 }
 
 // ------------------------------------------------------------------ SwiGLU
-// gu row = 2f values with gate/up INTERLEAVED in 64-feature groups (weight rows
-// of W_gu are stored that way so the data-parallel tcgen05 GEMM can fuse SwiGLU
-// into its epilogue): feature i's gate is column 128*(i/64) + i%64 and its up
-// value 64 columns later. out[i] = silu(gate) * up. grid (M, f/4/256), f % 64 == 0.
+// gu row = 2f values with gate/up INTERLEAVED in GU_GROUP (16) feature groups
+// (weight rows of W_gu are stored that way so the data-parallel tcgen05 GEMM can
+// fuse SwiGLU into its epilogue: a 32-row TMEM lane quarter holds 16 gates and
+// their 16 ups, exchanged by one warp shuffle): feature i's gate is column
+// 2*GU_GROUP*(i/GU_GROUP) + i%GU_GROUP and its up value GU_GROUP columns later.
+// out[i] = silu(gate) * up. grid (M, f/4/256), f % 64 == 0.
 template <typename T>
 __global__ void swiglu_kernel(float* __restrict__ gu, int f, T* __restrict__ out,
                               const int32_t* __restrict__ pos, L2Pf pf) {
@@ -330,9 +332,9 @@ __global__ void swiglu_kernel(float* __restrict__ gu, int f, T* __restrict__ out
   const int r = blockIdx.x;
   const int i = blockIdx.y * blockDim.x + threadIdx.x;   // float4 index
   if (4 * i >= f) return;
-  const int col = 128 * ((4 * i) / 64) + (4 * i) % 64;
+  const int col = 2 * GU_GROUP * ((4 * i) / GU_GROUP) + (4 * i) % GU_GROUP;
   float4* ga = (float4*)(gu + (size_t)r * 2 * f + col);
-  float4* gb = (float4*)(gu + (size_t)r * 2 * f + col + 64);
+  float4* gb = (float4*)(gu + (size_t)r * 2 * f + col + GU_GROUP);
   const float4 a = *ga, u = *gb;
   *ga = make_float4(0.f, 0.f, 0.f, 0.f);   // re-zero the GEMM scratch (see qkv_rope_kv)
   *gb = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -350,12 +352,12 @@ void launch_swiglu(float* gu, int M, int f, void* out, DType dt, const int32_t* 
   else launch_k(swiglu_kernel<bf16>, grid, 256, 0, st, gu, f, (bf16*)out, pos, pf);
 }
 
-// gate rows [0,f) and up rows [f,2f) of src -> interleaved 64-row groups in dst
+// gate rows [0,f) and up rows [f,2f) of src -> interleaved GU_GROUP-row groups in dst
 template <typename T>
 __global__ void interleave_gu_kernel(const T* __restrict__ src, int f, int n, T* __restrict__ dst) {
   const int r = blockIdx.x;                       // destination row
-  const int g = r / 128, o = r % 128;
-  const int srow = o < 64 ? g * 64 + o : f + g * 64 + (o - 64);
+  const int g = r / (2 * GU_GROUP), o = r % (2 * GU_GROUP);
+  const int srow = o < GU_GROUP ? g * GU_GROUP + o : f + g * GU_GROUP + (o - GU_GROUP);
   for (int c = threadIdx.x; c < n; c += blockDim.x) dst[(size_t)r * n + c] = src[(size_t)srow * n + c];
 }
 

@@ -57,13 +57,13 @@ def test_tcgen05_data_parallel_gemm(M, N, K, accumulate):
 
 @pytest.mark.parametrize("M,f,K", [(1024, 14336, 512), (2080, 11008, 256)])
 def test_tcgen05_fused_swiglu(M, f, K):
-    """Gate/up rows interleaved in 64-row groups; h = silu(gate) * up in bf16."""
+    """Gate/up rows interleaved in 16-row groups (GU_GROUP); h = silu(gate) * up in bf16."""
     torch.backends.cuda.matmul.allow_tf32 = False
     g = torch.Generator(device="cuda").manual_seed(M + f)
     A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
     Wg = (torch.randn(f, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
     Wu = (torch.randn(f, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
-    W = torch.stack([Wg.view(f // 64, 64, K), Wu.view(f // 64, 64, K)], dim=1).reshape(2 * f, K).contiguous()
+    W = torch.stack([Wg.view(f // 16, 16, K), Wu.view(f // 16, 16, K)], dim=1).reshape(2 * f, K).contiguous()
     H = torch.zeros(M, f, device="cuda", dtype=torch.bfloat16)
     hsd.debug_gemm(A, W, H, use_tc="swiglu")
     torch.cuda.synchronize()
@@ -106,7 +106,7 @@ def test_tcgen05_fused_swiglu_production_k(M, f, K):
     A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
     Wg = (torch.randn(f, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
     Wu = (torch.randn(f, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
-    W = torch.stack([Wg.view(f // 64, 64, K), Wu.view(f // 64, 64, K)], dim=1).reshape(2 * f, K).contiguous()
+    W = torch.stack([Wg.view(f // 16, 16, K), Wu.view(f // 16, 16, K)], dim=1).reshape(2 * f, K).contiguous()
     H = torch.zeros(M, f, device="cuda", dtype=torch.bfloat16)
     hsd.debug_gemm(A, W, H, use_tc="swiglu")
     torch.cuda.synchronize()
