@@ -15,6 +15,7 @@
 // Tokens / features / K beyond the tensor bounds are zero-filled by TMA.
 #include <cuda.h>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
 #include "gemm_tc.cuh"
@@ -51,6 +52,7 @@ struct TcParams {
   int ldh;
   unsigned long long* trace;      // debug phase trace (HSD_GEMM_TRACE) or null
   QkvEpi qe;                      // EPI_QKV (pair kernel)
+  int tma_out;                    // pair kernel: STORE / ADD / SWIGLU outputs leave by TMA store / reduce-add
   KStamp kst;                     // per-launch %globaltimer stamps (hsd_kstamp) or kst.buf == null
 };
 HSD_DEV uint64_t gtime_g() {
@@ -336,7 +338,8 @@ __global__ void __launch_bounds__(NTHREADS, 2)
 // producer cost ~20 % on every c3 shape (QKV 93 -> 112 us).
 template <int WT>
 __global__ void __launch_bounds__(NTHREADS2, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, TcParams P) {
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                    const __grid_constant__ CUtensorMap tmO, TcParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int half_nt = P.ntile / 2;
@@ -352,7 +355,12 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
   uint64_t* tfull = bars + 2 * P.stages;       // [2]
   uint64_t* tempty = bars + 2 * P.stages + 2;  // [2] (leader: one arrival per CTA)
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * P.stages + 4);
-  float* stage_buf = (float*)(bars + 2 * P.stages + 6);   // 2 groups x [16 tokens][EPI_LD] fp32
+  // epilogue region (1024-aligned): 2 groups x [16 tokens][EPI_LD] fp32 padded stages
+  // (SwiGLU / QKV / thread-store paths); with P.tma_out the same bytes hold dense
+  // stages [2 groups][2 buffers][16][128] fp32 for TMA stores (STORE / ADD), and
+  // SwiGLU's bf16 outputs [2 groups][2 buffers][16][64] (128-byte swizzle) sit at +24 KB
+  uint8_t* const epi_mem = (uint8_t*)(((uintptr_t)(bars + 2 * P.stages + 6) + 1023) & ~(uintptr_t)1023);
+  float* stage_buf = (float*)epi_mem;
   __shared__ int tmeta[2][16][3];   // EPI_QKV: per group, the chunk's tokens' (pos, K offset, V offset)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -451,6 +459,7 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
     kstamp_wait(P.kst);
     const int q = warp & 3, grp = (warp - 2) >> 2, et = threadIdx.x - 64 - 128 * grp;
     float* const stage_g = stage_buf + grp * 16 * EPI_LD;
+    int ck = 0;                                   // this group's chunk counter (TMA-store buffer parity)
     int buf = 0;
     uint32_t aphase = 0;
     for (long ti = 0; ti < my_tiles; ++ti) {
@@ -462,9 +471,30 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
       for (int w = 0; w < ((P.exp & 4) ? 0 : wt); ++w) {
       const int tn = 2 * (tm * wt + w) + rank;        // this CTA's 128-row weight tile
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((buf * wt + w) * P.ntile);
-      for (int c0 = 16 * grp; c0 < P.ntile; c0 += 32) {
+      for (int c0 = 16 * grp; c0 < P.ntile; c0 += 32, ++ck) {
         uint32_t r[16];
         tmem_ld16(taddr + c0, r);
+        if (P.tma_out && (P.epi == EPI_STORE || P.epi == EPI_ADD)) {
+          // [16 tokens][128 features] dense fp32 stage -> one TMA store (or reduce-add
+          // into the residual stream) of the box at (feature tn*128, token row);
+          // rows past M are clipped by the TMA unit. The issuing thread waits until
+          // the store of the chunk before has read its buffer, before barrier B
+          float* sb = (float*)epi_mem + (size_t)(grp * 2 + (ck & 1)) * 16 * BM;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) sb[j * BM + q * 32 + lane] = __uint_as_float(r[j]);
+          fence_proxy_async();
+          epi_bar_g(grp);
+          if (et == 0) {
+            if (!(P.exp & 1)) {
+              if (P.epi == EPI_ADD) tma_reduce_add_2d(&tmO, sb, tn * BM, tt * P.ntile + c0);
+              else tma_store_2d(&tmO, sb, tn * BM, tt * P.ntile + c0);
+              bulk_commit();
+            }
+            bulk_wait_read<1>();
+          }
+          epi_bar_g(grp);
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) stage_g[j * EPI_LD + q * 32 + lane] = __uint_as_float(r[j]);
         if (P.epi == EPI_QKV && et < 16) {
@@ -572,8 +602,23 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
             const __nv_bfloat162 h1 = __floats2bfloat162_rn(silu_mul_fast(g0.z, u0.z), silu_mul_fast(g0.w, u0.w));
             const __nv_bfloat162 h2 = __floats2bfloat162_rn(silu_mul_fast(g1.x, u1.x), silu_mul_fast(g1.y, u1.y));
             const __nv_bfloat162 h3 = __floats2bfloat162_rn(silu_mul_fast(g1.z, u1.z), silu_mul_fast(g1.w, u1.w));
-            *(uint4*)(P.H + (size_t)tok * P.ldh + f0) =
-                make_uint4(*(const uint32_t*)&h0, *(const uint32_t*)&h1, *(const uint32_t*)&h2, *(const uint32_t*)&h3);
+            const uint4 hv = make_uint4(*(const uint32_t*)&h0, *(const uint32_t*)&h1, *(const uint32_t*)&h2,
+                                        *(const uint32_t*)&h3);
+            if (P.tma_out)   // [16][64] bf16 box, 128-byte swizzle: 16-byte unit f8/8 of row tk at unit ^ (tk & 7)
+              *(uint4*)(epi_mem + 24576 + (grp * 2 + (ck & 1)) * 2048 + tk * 128 + (((f8 >> 3) ^ (tk & 7)) << 4)) = hv;
+            else
+              *(uint4*)(P.H + (size_t)tok * P.ldh + f0) = hv;
+          }
+          if (P.tma_out) {
+            fence_proxy_async();
+            epi_bar_g(grp);
+            if (et == 0) {
+              if (!(P.exp & 1)) {
+                tma_store_2d(&tmO, epi_mem + 24576 + (grp * 2 + (ck & 1)) * 2048, tn * (BM / 2), tt * P.ntile + c0);
+                bulk_commit();
+              }
+              bulk_wait_read<1>();
+            }
           }
         } else {
           // residual add: all 4 residual vectors of this thread are loaded before the
@@ -620,6 +665,7 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
       if (et == 0) mbar_arrive_cluster(tempty0 + 8u * buf);
       if (++buf == nbuf) { buf = 0; aphase ^= 1; }
     }
+    if (P.tma_out && et == 0) bulk_wait<0>();   // every TMA store of this group complete
   }
   fence_before();
   __syncthreads();
@@ -675,6 +721,18 @@ int num_sms() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+// output maps for the pair kernel's TMA stores: fp32 C rows (box 128 features x 16
+// tokens, no swizzle) or bf16 SwiGLU rows (box 64 x 16, 128-byte swizzle)
+static bool make_out_map(CUtensorMap* m, const void* ptr, int rows, int cols, int ld, bool f32) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || ((uintptr_t)ptr & 15) || (ld * (f32 ? 4 : 2)) % 16) return false;
+  cuuint64_t d[2] = {(cuuint64_t)cols, (cuuint64_t)rows}, st[1] = {(cuuint64_t)ld * (f32 ? 4 : 2)};
+  cuuint32_t b[2] = {(cuuint32_t)(f32 ? BM : BM / 2), 16u}, es[2] = {1, 1};
+  return fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), d,
+            st, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE, f32 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 static bool make_map(CUtensorMap* m, const void* ptr, int rows, int cols, int ld, int box_rows) {
@@ -770,8 +828,20 @@ static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float
     P.exp = e ? atoi(e) : 0;
   }
   const int bh = (nt / 2) * BK * 2;
-  // ring: the 227 KB less the epilogue stage buffers and barriers
-  int stages = (int)((208 * 1024) / (P.wt * A_BYTES + bh));
+  // outputs by TMA store / reduce-add (HSD_GEMM_TMA_OUT=0: thread stores from the
+  // padded stage): the epilogue then only stages chunks and issues one bulk copy each
+  // (=2: STORE / ADD only, SwiGLU keeps thread stores)
+  static const int tma_out_on = [] { const char* e = getenv("HSD_GEMM_TMA_OUT"); return e ? atoi(e) : 1; }();
+  CUtensorMap mo;
+  memset(&mo, 0, sizeof(mo));
+  P.tma_out = 0;
+  if (tma_out_on && (epi == EPI_STORE || epi == EPI_ADD) && C)
+    P.tma_out = make_out_map(&mo, C, M, N, ldc, true) ? 1 : 0;
+  else if (tma_out_on == 1 && epi == EPI_SWIGLU && H)
+    P.tma_out = make_out_map(&mo, H, M, N / 2, ldh, false) ? 1 : 0;
+  // ring: the 226 KB less the epilogue region (+ its 1024-byte alignment) and barriers
+  const size_t epi_bytes = P.tma_out ? 32768 : 2 * 16 * EPI_LD * 4;
+  int stages = (int)((226 * 1024 - 2048 - epi_bytes - 512) / (P.wt * A_BYTES + bh));
   if (stages > 16) stages = 16;
   P.stages = stages;
   P.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nt >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
@@ -782,7 +852,7 @@ static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float
   CUtensorMap mw, mx;
   if (!make_map(&mw, W, N, K, ldw, BM) || !make_map(&mx, A, M, K, lda, nt / 2)) return 0;
   P.vec4 = (ldc % 4 == 0) && (((uintptr_t)C & 15) == 0);
-  const size_t smem = 1024 + (size_t)stages * (P.wt * A_BYTES + bh) + (2 * stages + 6) * 8 + 2 * 16 * EPI_LD * 4 + 16;
+  const size_t smem = 1024 + (size_t)stages * (P.wt * A_BYTES + bh) + (2 * stages + 6) * 8 + 1024 + epi_bytes;
   static bool attr_done = false;
   if (!attr_done) {
     cudaFuncSetAttribute(gemm_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);   // (+ static tmeta)
@@ -792,8 +862,8 @@ static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float
   const long pairs = (long)((N + 2 * BM * P.wt - 1) / (2 * BM * P.wt)) * ntt;
   const long max_pairs = num_sms() / 2;
   const long grid = 2 * (pairs < max_pairs ? pairs : max_pairs);
-  if (P.wt == 2) launch_k_cluster(gemm_tc2_kernel<2>, dim3((unsigned)grid), dim3(NTHREADS2), smem, st, 2, mw, mx, P);
-  else launch_k_cluster(gemm_tc2_kernel<1>, dim3((unsigned)grid), dim3(NTHREADS2), smem, st, 2, mw, mx, P);
+  if (P.wt == 2) launch_k_cluster(gemm_tc2_kernel<2>, dim3((unsigned)grid), dim3(NTHREADS2), smem, st, 2, mw, mx, mo, P);
+  else launch_k_cluster(gemm_tc2_kernel<1>, dim3((unsigned)grid), dim3(NTHREADS2), smem, st, 2, mw, mx, mo, P);
   return 1;
 }
 

@@ -9,7 +9,7 @@ from synth import get_config
 
 cfg = get_config(sys.argv[1] if len(sys.argv) > 1 else "c3")
 T = 1 + cfg.budget_B + cfg.resample_budget_Br             # tree slots per request
-M = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.batch * T
+M = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else cfg.batch * T
 H, F = cfg.hidden, cfg.ffn
 qkv = (cfg.q_heads + 2 * cfg.kv_heads) * cfg.head_dim
 shapes = [("qkv", M, qkv, H, False), ("o", M, H, cfg.q_heads * cfg.head_dim, True), ("gu", M, 2 * F, H, "swiglu"),
@@ -30,6 +30,8 @@ def timeit(fn, reps=20):
     return e0.elapsed_time(e1) * 1e3 / reps
 
 
+if "--head" in sys.argv:   # the verify lm_head (fp32 logits store) as a fifth shape
+    shapes.append(("head", M, cfg.vocab, H, False))
 tot_h = tot_c = 0.0
 for name, m, n, k, mode in shapes:
     A = torch.randn(m, k, device="cuda").to(torch.bfloat16)
