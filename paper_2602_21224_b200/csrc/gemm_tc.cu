@@ -53,6 +53,8 @@ struct TcParams {
   unsigned long long* trace;      // debug phase trace (HSD_GEMM_TRACE) or null
   QkvEpi qe;                      // EPI_QKV (pair kernel)
   int tma_out;                    // pair kernel: STORE / ADD / SWIGLU outputs leave by TMA store / reduce-add
+  int pre;                        // pair kernel: weight halves of the first stages before griddepcontrol.wait
+  int pf_ahead;                   // pair kernel: L2 prefetch distance (units) of the weight stream, 0 = off
   KStamp kst;                     // per-launch %globaltimer stamps (hsd_kstamp) or kst.buf == null
 };
 HSD_DEV uint64_t gtime_g() {
@@ -398,21 +400,49 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
       const uint64_t pw = policy_evict_first(), px = policy_evict_last();
+      // Weights are never written by a kernel, so the weight halves of the first ring
+      // stages are issued BEFORE griddepcontrol.wait (they overlap the predecessor's
+      // tail); their token halves follow the wait. P.pre = 0 disables it.
+      const long npre = P.pre ? (count < P.stages ? count : P.stages) : 0;
+      auto load_w = [&](long i, int stg) {
+        const long t = tile_of(i);
+        const int kb = (int)(i % P.n_kb), tm = (int)(t / P.n_tiles_t);
+        for (int w = 0; w < wt; ++w)
+          tma_load_2d_2sm(&tmW, full0 + 8u * stg, sA + (size_t)stg * a_bytes + w * A_BYTES, kb * BK,
+                          (2 * (tm * wt + w) + rank) * BM, pw);
+      };
+      auto load_x = [&](long i, int stg) {
+        const long t = tile_of(i);
+        const int kb = (int)(i % P.n_kb), tt = (int)(t % P.n_tiles_t);
+        tma_load_2d_2sm(&tmX, full0 + 8u * stg, sB + (size_t)stg * bh, kb * BK, tt * P.ntile + rank * half_nt, px);
+      };
+      // (experiment HSD_GEMM_PF_AHEAD = d: an L2 prefetch of unit i + d's weight boxes
+      // is issued with unit i's loads -- the weight stream's DRAM latency off the ring)
+      auto prefetch_w = [&](long i) {
+        if (P.pf_ahead <= 0 || i >= count) return;
+        const long t = tile_of(i);
+        const int kb = (int)(i % P.n_kb), tm = (int)(t / P.n_tiles_t);
+        for (int w = 0; w < wt; ++w)
+          asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&tmW), "r"(kb * BK),
+                       "r"((2 * (tm * wt + w) + rank) * BM)
+                       : "memory");
+      };
+      for (long i = 0; i < npre; ++i) {   // ring stages are free at start
+        if (leader) mbar_expect_tx(&full[i], 2u * (a_bytes + bh));
+        load_w(i, (int)i);
+      }
+      for (long i = 0; i < (P.pf_ahead > 0 ? P.pf_ahead : 0); ++i) prefetch_w(npre + i);
       pdl_wait();
     kstamp_wait(P.kst);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (long i = 0; i < count; ++i) {
-        const long t = tile_of(i);
-        const int kb = (int)(i % P.n_kb);
-        const int tm = (int)(t / P.n_tiles_t), tt = (int)(t % P.n_tiles_t);
+      for (long i = 0; i < npre; ++i) load_x(i, (int)i);
+      int stage = (int)(npre % P.stages);
+      uint32_t phase = npre == P.stages ? 1u : 0u;
+      for (long i = npre; i < count; ++i) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (leader) mbar_expect_tx(&full[stage], 2u * (a_bytes + bh));
-        for (int w = 0; w < wt; ++w)
-          tma_load_2d_2sm(&tmW, full0 + 8u * stage, sA + (size_t)stage * a_bytes + w * A_BYTES, kb * BK,
-                          (2 * (tm * wt + w) + rank) * BM, pw);
-        tma_load_2d_2sm(&tmX, full0 + 8u * stage, sB + (size_t)stage * bh, kb * BK, tt * P.ntile + rank * half_nt,
-                        px);
+        load_w(i, stage);
+        load_x(i, stage);
+        prefetch_w(i + P.pf_ahead);
         if (++stage == P.stages) { stage = 0; phase ^= 1; }
       }
     }
@@ -828,6 +858,10 @@ static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float
     P.exp = e ? atoi(e) : 0;
   }
   const int bh = (nt / 2) * BK * 2;
+  static const int pre_env = [] { const char* e = getenv("HSD_GEMM_PRE"); return e ? atoi(e) : 1; }();
+  static const int pf_env = [] { const char* e = getenv("HSD_GEMM_PF_AHEAD"); return e ? atoi(e) : 0; }();
+  P.pre = pre_env;
+  P.pf_ahead = pf_env;
   // outputs by TMA store / reduce-add (HSD_GEMM_TMA_OUT=0: thread stores from the
   // padded stage): the epilogue then only stages chunks and issues one bulk copy each
   // (default 2: STORE / ADD only -- SwiGLU's bf16 output by TMA measured neutral to

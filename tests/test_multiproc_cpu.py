@@ -111,3 +111,83 @@ def test_gloo_world2_vocab_shard_bootstrap():
     assert len(ids[0]) == 128 and ids[0] == ids[1] and any(ids[0])
     assert [out[r][1] for r in range(world)] == [0, 1]
     assert all(out[r][2] == world and out[r][3] == 1 for r in range(world))
+
+
+# ---- R29: stochastic acceptance over a vocab-sharded head, merged across ranks
+KG = 16   # Gumbel candidates per shard record (HSD_SHARD_KG)
+
+
+def _records(L, lo, hi, T, U, tree_tok):
+    """One shard's per-row record over its columns [lo, hi): (max and sum exp of
+    l/T, its top-KG Gumbel scores l/T + G with token ids, the logits of the tree
+    tokens it owns) -- DESIGN.md R29."""
+    z = L[:, lo:hi] / T
+    m = z.max(axis=1)
+    s = np.exp(z - m[:, None]).sum(axis=1)
+    g = z - np.log(-np.log(U[:, lo:hi]))
+    order = np.lexsort((np.arange(lo, hi)[None, :].repeat(len(L), 0), -g), axis=1)[:, :KG]
+    gv = np.take_along_axis(g, order, axis=1)
+    gi = order + lo
+    own = (tree_tok >= lo) & (tree_tok < hi)
+    tl = np.where(own[None, :], L[:, np.clip(tree_tok, 0, L.shape[1] - 1)], np.nan)
+    return m, s, gv, gi, tl
+
+
+def _merge(recs):
+    m = np.stack([r[0] for r in recs])                  # [G, rows]
+    s = np.stack([r[1] for r in recs])
+    M = m.max(axis=0)
+    lse = M + np.log((s * np.exp(m - M)).sum(axis=0))
+    gv = np.concatenate([r[2] for r in recs], axis=1)
+    gi = np.concatenate([r[3] for r in recs], axis=1)
+    order = np.lexsort((gi, -gv), axis=1)[:, :KG]
+    tl = np.nanmax(np.stack([np.where(np.isnan(r[4]), -np.inf, r[4]) for r in recs]), axis=0)
+    return lse, np.take_along_axis(gv, order, 1), np.take_along_axis(gi, order, 1), tl
+
+
+def _stoch_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2602_21224_b200.hsd import vocab_shard_bounds
+    from oracle.philox import gumbel_uniforms
+    V, rows, T = 1000, 6, 0.7
+    rng = np.random.default_rng(11)                     # the same inputs on every rank
+    L = rng.standard_normal((rows, V)) * 3.0
+    tree_tok = rng.choice(V, size=9, replace=False)
+    U = np.stack([gumbel_uniforms(seed=3, req=2, step=1, slot=r, vocab=V) for r in range(rows)])
+    lo = vocab_shard_bounds(V, world)
+    rec = _records(L, lo[rank], lo[rank + 1], T, U, tree_tok)
+    allrec = [None] * world
+    dist.all_gather_object(allrec, rec)                 # the records all-gather (gloo here, NCCL on GPUs)
+    out[rank] = _merge(allrec)
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_stochastic_shard_merge():
+    """World-2 processes each reduce their vocab columns to R29 records, all-gather
+    them and merge: the merged lse is logsumexp(l/T) of the full rows, the tree-token
+    logits are the full rows' values, and the residual Gumbel-max over V minus any
+    rejected set of < 16 tokens (the oracle's gumbel_argmax on the full row) is the
+    best merged candidate outside it."""
+    from oracle.philox import gumbel_uniforms
+    from oracle.accept import gumbel_argmax
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_stoch_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    V, rows, T = 1000, 6, 0.7
+    rng = np.random.default_rng(11)
+    L = rng.standard_normal((rows, V)) * 3.0
+    tree_tok = rng.choice(V, size=9, replace=False)
+    for r in range(world):
+        lse, gv, gi, tl = out[r]
+        ref = np.log(np.exp(L / T - (L / T).max(1, keepdims=True)).sum(1)) + (L / T).max(1)
+        assert np.allclose(lse, ref, rtol=0, atol=1e-12)
+        assert np.array_equal(tl, L[:, tree_tok])
+        for row in range(rows):
+            U = gumbel_uniforms(seed=3, req=2, step=1, slot=row, vocab=V)
+            for k in (0, 4, 15):                       # rejected sets of 0 / 4 / 15 tokens
+                excl = [int(x) for x in gi[row, :k]]
+                want, _ = gumbel_argmax(L[row], T, U, exclude=excl)
+                got = next(int(v) for v in gi[row] if int(v) not in excl)
+                assert got == want
