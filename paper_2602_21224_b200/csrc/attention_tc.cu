@@ -681,6 +681,386 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
 }
 
+
+// ------------------------------------------------------------ dual-tile kernel
+// One CTA = (key split, kv head h, request x PAIR of q-tiles {2p, 2p+1}): one K / V
+// stream feeds 256 (row, head) pairs, so each SM ingests half the K / V bytes per
+// row of the single-tile kernel. Two softmax warp groups (one per q-tile, SW warps
+// per TMEM lane quarter each) ping-pong against the tensor core, FlashAttention-4
+// style: while group A turns S_A(j) into P_A(j), the MMA warp runs P_B(j-1) V and
+// S_B(j); while group B works, P_A(j) V and S_A(j+1).
+//  TMEM (512 columns): S_A | S_B (128 each, single-buffered, P_X written as bf16
+//  over S_X's first 64 columns) | O_A | O_B (hd each). S_X(j+1) is issued after
+//  P_X(j) V (tcgen05.mma executes in issue order), so it cannot overwrite P_X(j)
+//  early; and S_X(j) completing implies P_X(j-1) V completed, so the softmax may
+//  rescale O_X without waiting on another barrier.
+//  Shared memory: q tiles A, B (SW128, written by the softmax threads), a 2-stage K
+//  ring and a 2-stage V^T ring. The row sum l is accumulated by the softmax warps
+//  from the bf16-rounded P the MMA consumes.
+template <int SW> constexpr int dual_threads() { return 96 + 2 * 128 * SW; }
+
+template <int SW>
+__global__ void __launch_bounds__(dual_threads<SW>(), 1)
+    attention_dual_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                          AttnParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  constexpr int KST = 2, VST = 2;
+  const int hd = P.hd, natom = hd / 64;
+  const int q_bytes = QROWS * hd * 2;           // one q tile: natom atoms [128 rows x 128 B]
+  const int k_bytes = CHUNK * hd * 2;           // natom atoms [128 keys x 128 B]
+  const int v_page = hd * 128;                  // [hd rows x 64 keys] bf16
+  const int v_bytes = 2 * v_page;
+  uint8_t* sQ = base;
+  uint8_t* sK = sQ + 2 * q_bytes;
+  uint8_t* sV = sK + KST * k_bytes;
+  uint64_t* bars = (uint64_t*)(sV + VST * v_bytes);
+  uint64_t* kfull = bars;                 // [KST]
+  uint64_t* kempty = kfull + KST;         // [KST]
+  uint64_t* vfull = kempty + KST;         // [VST]
+  uint64_t* vempty = vfull + VST;         // [VST]
+  uint64_t* qbar = vempty + VST;
+  uint64_t* sfull = qbar + 1;             // [2 tiles]
+  uint64_t* pfull = sfull + 2;            // [2 tiles]
+  uint64_t* odone = pfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(odone + 1);
+  __shared__ int tile_lo, tile_hi, safe_hi;
+  constexpr int NSMG = 128 * SW;                // softmax threads per group
+  constexpr int KPW = CHUNK / SW;               // keys per softmax warp per chunk
+  __shared__ float red_max[2][2][SW][QROWS];    // [tile][chunk parity][part][row]
+  __shared__ float red_l[2][SW][QROWS];         // epilogue: l per part
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int split = blockIdx.x, nsplit = gridDim.x, h = blockIdx.y;
+  const int npairs = (P.n_qtiles + 1) / 2;
+  const int grp = blockIdx.z / npairs, tp = blockIdx.z % npairs;
+  const RowMeta& m = P.m;
+  const int req = m.req[grp * P.R];
+  const int RG = P.R * P.G;
+  const bool hasB = (2 * tp + 1) * QROWS < RG;   // (uniform) tile B holds at least one pair
+
+  if (threadIdx.x == 0) { tile_lo = 0x7fffffff; tile_hi = 0; safe_hi = 0x7fffffff; }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < KST; ++s) { mbar_init(&kfull[s], 1); mbar_init(&kempty[s], 1); }
+    for (int s = 0; s < VST; ++s) { mbar_init(&vfull[s], 1); mbar_init(&vempty[s], 1); }
+    mbar_init(qbar, (hasB ? 2 : 1) * NSMG / 32);
+    for (int x = 0; x < 2; ++x) { mbar_init(&sfull[x], 1); mbar_init(&pfull[x], NSMG / 32); }
+    mbar_init(odone, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();
+  // softmax threads: tile X, this lane's (row, head) and its key bounds
+  const int X = warp >= 3 ? (warp - 3) / (4 * SW) : 0;
+  const bool in_tile = warp >= 3 && (X == 0 || hasB);
+  const int q4 = warp & 3;
+  const int lane_row = q4 * 32 + lane;
+  const int part = warp >= 3 ? ((warp - 3) % (4 * SW)) >> 2 : 0;
+  const int qt = 2 * tp + X;
+  int row = -1, head = 0, klo = 0, khi = 0, slot = -1, tb = 0;
+  uint64_t anc[4] = {0, 0, 0, 0};
+  bool valid = false, writable = false;
+  if (in_tile) {
+    const int rh = qt * QROWS + lane_row;
+    const int rl = rh / P.G, g = rh % P.G;
+    row = grp * P.R + rl;
+    head = h * P.G + g;
+    writable = rl < P.R && row < P.M;
+    valid = writable && m.pos[row] >= 0;
+    if (valid) {
+      klo = m.klo[row]; khi = m.khi[row]; slot = m.slot[row];
+      int lo = klo, hi = khi;
+      if (slot >= 0) {
+        tb = m.tbase[req];
+        for (int w = 0; w < m.anc_words && w < 4; ++w)
+          anc[w] = m.anc[((size_t)req * m.t_max + slot) * m.anc_words + w];
+        lo = min(lo, tb);
+        hi = max(hi, tb + slot + 1);
+      }
+      if (hi > lo && part == 0) { atomicMin(&tile_lo, lo); atomicMax(&tile_hi, hi); }
+    }
+  }
+  if (warp >= 3) {
+    int pmin = 0x7fffffff;
+    for (int r = threadIdx.x - SM0; r < P.R; r += 2 * NSMG) {
+      const int rr = grp * P.R + r;
+      const int pr = rr < P.M ? m.pos[rr] : -1;
+      if (pr >= 0) pmin = min(pmin, pr);
+    }
+    if (pmin != 0x7fffffff) atomicMin(&safe_hi, pmin);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  int k_begin, k_end;
+  if (P.dyn) {
+    const int c0 = tile_lo / CHUNK, c1 = (tile_hi + CHUNK - 1) / CHUNK;
+    const int cps = c1 > c0 ? (c1 - c0 + nsplit - 1) / nsplit : 0;
+    k_begin = (c0 + split * cps) * CHUNK;
+    k_end = k_begin + cps * CHUNK;
+  } else {
+    k_begin = split * P.keys_per_split;
+    k_end = min(P.max_keys, k_begin + P.keys_per_split);
+  }
+  const int lo = max(k_begin, tile_lo), hi = min(k_end, tile_hi);
+  const int c_first = lo / CHUNK;
+  const int n_chunks = hi > lo ? (hi + CHUNK - 1) / CHUNK - c_first : 0;
+
+  if (warp == 0) {
+    if (lane == 0 && n_chunks == 0) { l2pf_issue(P.pf); l2pf_issue(P.pf, 1); }
+    if (lane == 0 && n_chunks > 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
+      const uint64_t pol = P.n_qtiles > 2 ? policy_evict_normal() : policy_evict_first();
+      auto load_k = [&](int j) {
+        const int s = j % KST;
+        mbar_wait(&kempty[s], ((j / KST) & 1) ^ 1);
+        mbar_expect_tx(&kfull[s], k_bytes);
+        for (int pg = 0; pg < 2; ++pg) {
+          const int page = P.kv.block_table[(size_t)req * P.kv.pages_per_req + 2 * (c_first + j) + pg];
+          const int krow = ((page * 2 + 0) * P.kv.kv_heads + h) * PAGE;
+          for (int a = 0; a < natom; ++a)
+            tma_load_2d(&tmK, &kfull[s], sK + (size_t)s * k_bytes + a * (CHUNK * 128) + pg * (PAGE * 128), a * 64,
+                        krow, pol);
+        }
+      };
+      int kj = 0;
+      while (kj < n_chunks && kj < KST && (c_first + kj + 1) * CHUNK <= safe_hi) load_k(kj++);
+      pdl_wait();
+      kst_enter(P.kst);
+      while (kj < n_chunks) load_k(kj++);
+      l2pf_issue(P.pf);
+    }
+  } else if (warp == 2) {
+    if (lane == 0 && n_chunks > 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
+      const uint64_t pol = P.n_qtiles > 2 ? policy_evict_normal() : policy_evict_first();
+      auto load_v = [&](int j) {
+        const int s = j % VST;
+        mbar_wait(&vempty[s], ((j / VST) & 1) ^ 1);
+        mbar_expect_tx(&vfull[s], 2 * hd * 128);
+        for (int pg = 0; pg < 2; ++pg) {
+          const int page = P.kv.block_table[(size_t)req * P.kv.pages_per_req + 2 * (c_first + j) + pg];
+          tma_load_2d(&tmV, &vfull[s], sV + (size_t)s * v_bytes + pg * v_page, 0,
+                      ((page * 2 + 1) * P.kv.kv_heads + h) * hd, pol);
+        }
+      };
+      int vj = 0;
+      while (vj < n_chunks && vj < VST && (c_first + vj + 1) * CHUNK <= safe_hi) load_v(vj++);
+      pdl_wait();
+      while (vj < n_chunks) load_v(vj++);
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n_chunks > 0) {
+      mbar_wait(qbar, 0);                       // both q tiles in shared memory
+      fence_after();
+      const int ntile = hasB ? 2 : 1;
+      auto issue_s = [&](int x, int j) {        // S_x(j) = Q_x K_j^T
+        const int s = j % KST;
+        const uint32_t d = tmem + (uint32_t)(x * CHUNK);
+        for (int kk = 0; kk < hd / 16; ++kk) {
+          const int a = kk >> 2, off = kk & 3;
+          const uint64_t ad = desc_sw128(sQ + (size_t)x * q_bytes + a * (QROWS * 128)) + 2 * off;
+          const uint64_t bd = desc_sw128(sK + (size_t)s * k_bytes + a * (CHUNK * 128)) + 2 * off;
+          mma_bf16(d, ad, bd, P.idesc_s, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&sfull[x]);
+      };
+      auto issue_pv = [&](int x, int j) {       // O_x += P_x(j) V_j, P_x from TMEM
+        const int s = j % VST;
+        const uint32_t tO = tmem + 256 + (uint32_t)(x * hd), tP = tmem + (uint32_t)(x * CHUNK);
+        for (int kk = 0; kk < CHUNK / 16; ++kk) {
+          const int ka = kk >> 2, off = kk & 3;
+          const uint64_t vd = desc_sw128(sV + (size_t)s * v_bytes + ka * v_page) + 2 * off;
+          mma_bf16_ts(tO, tP + (uint32_t)(kk * 8), vd, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+      };
+      mbar_wait(&kfull[0], 0);
+      fence_after();
+      for (int x = 0; x < ntile; ++x) issue_s(x, 0);
+      mma_commit(&kempty[0]);
+      for (int j = 0; j < n_chunks; ++j) {
+        const bool more = j + 1 < n_chunks;
+        if (more) { mbar_wait(&kfull[(j + 1) % KST], ((j + 1) / KST) & 1); fence_after(); }
+        mbar_wait(&vfull[j % VST], (j / VST) & 1);
+        fence_after();
+        for (int x = 0; x < ntile; ++x) {
+          mbar_wait(&pfull[x], j & 1);
+          fence_after();
+          issue_pv(x, j);
+          if (more) issue_s(x, j + 1);           // after P_x(j) V: may overwrite P_x(j)
+        }
+        mma_commit(&vempty[j % VST]);
+        if (more) mma_commit(&kempty[(j + 1) % KST]);
+      }
+      mma_commit(odone);
+    }
+  } else if (in_tile) {
+    // ------------------------------------------------------------ softmax group X
+    const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+    float mrow = -INFINITY, lsum = 0.f;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tS = tmem + (uint32_t)(X * CHUNK), tO = tmem + 256 + (uint32_t)(X * hd);
+    const int hcols = hd / SW;
+    const bool live = __any_sync(0xffffffffu, valid);
+    {
+      // this thread's q row, dims [part hd/SW, (part+1) hd/SW), into the SW128 q tile
+      pdl_wait();
+      const int d0 = part * hcols;
+      const uint4* src = writable ? (const uint4*)(P.q + ((size_t)row * P.Hq + head) * hd + d0) : nullptr;
+      uint8_t* qt_base = sQ + (size_t)X * q_bytes;
+      for (int c = 0; c < hcols / 8; ++c) {
+        const int d = d0 + 8 * c, a = d >> 6, ch = (d & 63) >> 3;
+        const uint4 v = src ? src[c] : make_uint4(0u, 0u, 0u, 0u);
+        *(uint4*)(qt_base + a * (QROWS * 128) + lane_row * 128 + ((ch ^ (lane_row & 7)) << 4)) = v;
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qbar);
+    }
+    const int bar_id = 1 + X * 4 + q4;          // the SW warps of this group and lane quarter
+    for (int j = 0; j < n_chunks; ++j) {
+      mbar_wait(&sfull[X], j & 1);
+      fence_after();
+      if (live) {
+        const int kb = (c_first + j) * CHUNK + part * KPW;
+        uint32_t r0[32], r1[32];
+        tmem_ld32_nw(tS + lane_off + (uint32_t)(part * KPW), r0);
+        if constexpr (KPW == 64) tmem_ld32_nw(tS + lane_off + (uint32_t)(part * KPW + 32), r1);
+        uint32_t vm0 = 0u, vm1 = 0xffffffffu;
+        if (valid) {
+          vm0 = range32(klo - kb, khi - kb);
+          if (slot >= 0) vm0 |= anc32(anc, kb - tb) & range32(0, m.t_max - (kb - tb));
+          vm0 &= range32(k_begin - kb, k_end - kb);
+          if constexpr (KPW == 64) {
+            vm1 = range32(klo - kb - 32, khi - kb - 32);
+            if (slot >= 0) vm1 |= anc32(anc, kb + 32 - tb) & range32(0, m.t_max - (kb + 32 - tb));
+            vm1 &= range32(k_begin - kb - 32, k_end - kb - 32);
+          }
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float s[KPW];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          s[i] = ((vm0 >> i) & 1u) ? __uint_as_float(r0[i]) : -INFINITY;
+          if constexpr (KPW == 64) s[32 + i] = ((vm1 >> i) & 1u) ? __uint_as_float(r1[i]) : -INFINITY;
+        }
+        float mxp[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mxp[k] = s[k];
+#pragma unroll
+        for (int i = 8; i < KPW; ++i) mxp[i & 7] = fmaxf(mxp[i & 7], s[i]);
+        float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                         fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+        red_max[X][j & 1][part][lane_row] = mx;
+        asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(32 * SW) : "memory");
+#pragma unroll
+        for (int p2 = 0; p2 < SW; ++p2) mx = fmaxf(mx, red_max[X][j & 1][p2][lane_row]);
+        mx *= scale_log2;
+        float alpha = 1.f;
+        if (mrow == -INFINITY) {
+          mrow = mx;
+        } else if (mx > mrow + 8.f) {
+          alpha = ex2(mrow - mx);
+          mrow = mx;
+        }
+        const float msub = mrow == -INFINITY ? 0.f : mrow;
+        uint32_t pw[32];
+        float ls = 0.f;
+#pragma unroll
+        for (int i = 0; i < KPW / 2; ++i) {
+          const float p0 = ex2(fmaf(s[2 * i], scale_log2, -msub)), p1 = ex2(fmaf(s[2 * i + 1], scale_log2, -msub));
+          __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
+          const float2 pf = __bfloat1622float2(pr);
+          ls += pf.x + pf.y;
+          pw[i] = *(uint32_t*)&pr;
+        }
+        if constexpr (KPW == 64) {
+          tmem_st32(tS + lane_off + (uint32_t)(part * 32), pw);
+        } else {
+          uint32_t pw16[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pw16[i] = pw[i];
+          tmem_st16(tS + lane_off + (uint32_t)(part * 16), pw16);
+        }
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+          // P_X(j-1) V completed before S_X(j) did (issue order): O_X is final up to j-1
+          for (int c = 0; c < hcols; c += 16) {
+            uint32_t o[16];
+            tmem_ld16(tO + lane_off + (uint32_t)(part * hcols + c), o);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st16(tO + lane_off + (uint32_t)(part * hcols + c), o);
+          }
+        }
+        lsum = lsum * alpha + ls;
+        tmem_st_wait();
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pfull[X]);
+    }
+    // ------------------------------------------------------------ epilogue
+    red_l[X][part][lane_row] = lsum;
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(32 * SW) : "memory");
+    float ltot = 0.f;
+#pragma unroll
+    for (int p2 = 0; p2 < SW; ++p2) ltot += red_l[X][p2][lane_row];
+    if (!valid) ltot = 0.f;
+    if (n_chunks > 0) {
+      mbar_wait(odone, 0);
+      fence_after();
+    }
+    const float inv = (P.direct && ltot > 0.f) ? 1.0f / ltot : 1.0f;
+    for (int c = 0; c < hcols; c += 16) {
+      uint32_t o[16];
+      if (n_chunks > 0) tmem_ld16(tO + lane_off + (uint32_t)(part * hcols + c), o);   // (warp-collective)
+      else
+        for (int i = 0; i < 16; ++i) o[i] = 0u;
+      if (writable) {
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = ltot > 0.f ? __uint_as_float(o[i]) * inv : 0.f;
+        const int d = part * hcols + c;
+        if (P.direct) {
+          uint32_t w[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            w[i] = *(const uint32_t*)&b2;
+          }
+          uint4* dst = (uint4*)(P.out + ((size_t)row * P.Hq + head) * hd + d);
+          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        } else {
+          float4* dst = (float4*)(P.ws + (((size_t)split * P.Hq + head) * P.M + row) * hd + d);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      }
+    }
+    if (writable) {
+      if (!P.direct && part == 0) {
+        const size_t base_ml = (size_t)nsplit * P.M * P.Hq * hd;
+        const size_t idx = ((size_t)split * P.Hq + head) * P.M + row;
+        P.ws[base_ml + 2 * idx] = mrow;
+        P.ws[base_ml + 2 * idx + 1] = ltot;
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  kst_exit(P.kst);
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+}
+
 // split merge: one warp per (row, head), lanes over hd:
 // o = sum_s e^{m_s - M} o_s / sum_s e^{m_s - M} l_s
 __global__ void attention_merge_bf16_kernel(const float* __restrict__ ws, int S, int M, int Hq, int hd,
@@ -775,6 +1155,9 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   P.dyn = dyn == 1 && latency_bound;
   static const int s_override = [] { const char* e = getenv("HSD_ATTN_SPLITS"); return e ? atoi(e) : 0; }();
   if (s_override > 0) S = min(s_override, pages);
+  // (experiment: key splits of the one-row draft chain passes only, R = 1)
+  static const int s_draft = [] { const char* e = getenv("HSD_ATTN_SPLITS_DRAFT"); return e ? atoi(e) : 0; }();
+  if (s_draft > 0 && R == 1) S = min(s_draft, pages);
   // two splits reduce inside a 2-CTA cluster over DSMEM (no workspace, no merge
   // kernel): c5 (b = 2) attention 6.8-7.3 -> 6.5 ms. Wider clusters measured
   // slower (c2, S = 4: step 4.95 -> 5.38 ms) -- a 2-CTA cluster fits one TPC's SM
@@ -800,6 +1183,53 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   uint64_t sv[1] = {(uint64_t)PAGE};
   uint32_t bv[2] = {(uint32_t)PAGE, (uint32_t)hd};
   if (!tma_map_bf16(&mk, kv.base, 2, dk, sk, bk) || !tma_map_bf16(&mv, kv.base, 2, dv, sv, bv)) return -1;
+  // Dual-tile kernel (two q-tiles per CTA, one K / V stream; HSD_ATTN_DUAL=0 disables):
+  // when a (request, kv head) has >= 2 q-tiles (c3 / c4 / c5 verify passes)
+  static const int dual_env = [] { const char* e = getenv("HSD_ATTN_DUAL"); return e ? atoi(e) : 0; }();
+  if (dual_env && P.n_qtiles >= 2) {
+    const int npairs = (P.n_qtiles + 1) / 2;
+    const int base2 = n_req * kv.kv_heads * npairs;
+    int S2 = max(1, (2 * num_sms() + base2) / (2 * base2));
+    S2 = min(S2, max(1, pages / 2));
+    if (s_override > 0) S2 = min(s_override, pages);
+    while (S2 > 1 && (size_t)S2 * M * Hq * (hd + 2) > ws_floats) --S2;
+    const bool lb = (pages + S2 - 1) / S2 <= 4;
+    if (dyn && lb) S2 = min(S2, max(1, num_sms() / base2));
+    P.dyn = dyn == 1 && lb;
+    const int pps2 = (pages + S2 - 1) / S2;
+    P.keys_per_split = pps2 * CHUNK;
+    if (!P.dyn) S2 = (pages + pps2 - 1) / pps2;
+    P.direct = S2 == 1;
+    P.cluster = 0;
+    P.idesc_o = idesc_bf16(128, hd);
+    CUtensorMap mk2, mv2;
+    uint64_t dk2[2] = {(uint64_t)hd, (uint64_t)(kv_layer_elems / hd)};
+    uint64_t sk2[1] = {(uint64_t)hd};
+    uint32_t bk2[2] = {64, (uint32_t)PAGE};
+    uint64_t dv2[2] = {(uint64_t)PAGE, (uint64_t)(kv_layer_elems / PAGE)};
+    uint64_t sv2[1] = {(uint64_t)PAGE};
+    uint32_t bv2[2] = {(uint32_t)PAGE, (uint32_t)hd};
+    if (!tma_map_bf16(&mk2, kv.base, 2, dk2, sk2, bk2) || !tma_map_bf16(&mv2, kv.base, 2, dv2, sv2, bv2)) return -1;
+    const size_t smem2 = 1024 + 2 * ((size_t)QROWS * hd * 2) + 2 * ((size_t)CHUNK * hd * 2) + 2 * ((size_t)2 * hd * 128) +
+                         16 * 8 + 64;
+    static size_t attr2 = 0;
+    if (smem2 > attr2) {
+      if (cudaFuncSetAttribute(attention_dual_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+      }
+      attr2 = smem2;
+    }
+    launch_k(attention_dual_kernel<2>, dim3(S2, kv.kv_heads, n_req * npairs), dim3(dual_threads<2>()), smem2, st, mk2,
+             mv2, P);
+    if (S2 > 1) {
+      launch_k(attention_merge_bf16_kernel, (M * Hq + 7) / 8, 256, 0, st, ws, S2, M, Hq, hd, (bf16*)out, take_l2pf(),
+               P.kst);
+      return 2;
+    }
+    return 1;
+  }
   const int kst = 4, vst = 2;
   const size_t smem = 1024 + kst * ((size_t)CHUNK * hd * 2) + vst * ((size_t)2 * (hd + VEXTRA) * 128) +
                       (2 * kst + 2 * vst + 8) * 8 + 64;

@@ -42,7 +42,13 @@ bool g_hsd_pdl = [] {
 }();
 
 namespace {
-constexpr int PREFILL_CHUNK = 1024;
+// prompt rows per prefill forward (HSD_PREFILL_CHUNK, default 4096 = a whole c3
+// prompt): at 1024 rows the pair GEMMs' tile count falls under the data-parallel
+// wave rule at c3 widths (QKV: 96 pair tiles = 1.3 waves) and runs stream-K
+static int prefill_chunk() {
+  static const int v = [] { const char* e = getenv("HSD_PREFILL_CHUNK"); return e ? std::max(256, atoi(e)) : 4096; }();
+  return v;
+}
 constexpr int MAXN_TREE = 256;
 
 // ------------------------------------------------------------------ row metadata kernels
@@ -228,6 +234,7 @@ struct ProfRec { int cat; cudaEvent_t a, b; double bytes, flops; };
 
 struct hsd_ctx {
   hsd_config cfg;
+  int pchunk = 1024;                // prompt rows per prefill forward (prefill_chunk())
   int dev = 0;
   cudaStream_t st = nullptr;
   DType dt = DT_F32;
@@ -875,8 +882,9 @@ static hsd_status prefill_one(hsd_ctx* ctx, int r, const int32_t* pt, int P0, in
   const int n = c->n, N = c->N;
   std::vector<int32_t> tok, pos, kvpos, req, klo, khi, slot;
   // target causal forward over the prompt, chunked
-  for (int s0 = 0; s0 < P0; s0 += PREFILL_CHUNK) {
-    int M = std::min(PREFILL_CHUNK, P0 - s0);
+  const int PC = c->pchunk;
+  for (int s0 = 0; s0 < P0; s0 += PC) {
+    int M = std::min(PC, P0 - s0);
     tok.resize(M); pos.resize(M); kvpos.resize(M); req.resize(M); klo.resize(M); khi.resize(M); slot.resize(M);
     for (int i = 0; i < M; ++i) {
       tok[i] = pt[s0 + i]; pos[i] = s0 + i; kvpos[i] = s0 + i; req[i] = r; klo[i] = 0; khi[i] = s0 + i + 1;
@@ -909,8 +917,8 @@ static hsd_status prefill_one(hsd_ctx* ctx, int r, const int32_t* pt, int P0, in
                                            c->n_pend, c->root_tok, c->p, d_first);
   g_hsd_launches += 2;
   // draft prefill over pairs j = 1..P0-1: x_j = W_fc [H_{j-1}; E(t_j)] (R1)
-  for (int j0 = 1; j0 < P0; j0 += PREFILL_CHUNK) {
-    int M = std::min(PREFILL_CHUNK, P0 - j0);
+  for (int j0 = 1; j0 < P0; j0 += PC) {
+    int M = std::min(PC, P0 - j0);
     tok.resize(M); pos.resize(M); kvpos.resize(M); req.resize(M); klo.resize(M); khi.resize(M); slot.resize(M);
     for (int i = 0; i < M; ++i) {
       int j = j0 + i;
@@ -1199,7 +1207,8 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     c->t_lj = F((size_t)b * T); c->t_anc = (uint64_t*)A((size_t)b * T * c->W * 8);
     c->acc_n = I(b); c->acc_slots = I((size_t)b * N); c->bonus = I(b); c->emitted = I((size_t)b * (N + 1));
     c->n_emitted = I(b);
-    c->Mcap = std::max({b * T, b * (N + 1), PREFILL_CHUNK});
+    c->pchunk = std::min(prefill_chunk(), std::max(256, cfg->max_ctx));
+    c->Mcap = std::max({b * T, b * (N + 1), c->pchunk});
     const int Mc = c->Mcap;
     const size_t wa = std::max({(size_t)2 * n, (size_t)c->qd, (size_t)c->f});
     c->a = A((size_t)Mc * wa * es);
@@ -1215,7 +1224,7 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     c->draft_logits = F((size_t)b * N * V);
     c->logits = F((size_t)std::max(b * T, 1) * V);
     c->argmax = I((size_t)b * T);
-    c->x_p = F((size_t)PREFILL_CHUNK * n);
+    c->x_p = F((size_t)c->pchunk * n);
     c->H_prompt = F((size_t)(cfg->max_ctx + 1) * n);
     c->attn_ws_floats = attention_ws_floats(std::max(b * T, b * (N + 1)), c->Hq, c->hd, 16);
     c->attn_ws = F(c->attn_ws_floats);
@@ -1226,7 +1235,7 @@ hsd_status hsd_init_model(const hsd_config* cfg, int device, void* cuda_stream, 
     meta(c->mv, (size_t)b * T);
     meta(c->md, (size_t)b * (N + 1));
     meta(c->mc, (size_t)b);
-    meta(c->mp, (size_t)PREFILL_CHUNK);
+    meta(c->mp, (size_t)c->pchunk);
     if (cfg->shard_mode != HSD_SHARD_NONE) {
       c->shard_mode = cfg->shard_mode;
       c->G = cfg->vocab_shards;

@@ -776,8 +776,9 @@ bool gemm_tc_supported(int M, int N, int K, int lda, int ldw) {
   return M >= 1 && N >= 1 && K >= 16 && K % 8 == 0 && lda % 8 == 0 && ldw % 8 == 0 && encode_fn() != nullptr;
 }
 
-static void tc_tiles(int M, int& nt, int& n_tok_tiles) {
-  static const int max_nt = [] { const char* e = getenv("HSD_GEMM_MAX_NT"); return e ? atoi(e) : 256; }();
+static void tc_tiles(int M, int& nt, int& n_tok_tiles, int cap = 0) {
+  static const int max_nt_env = [] { const char* e = getenv("HSD_GEMM_MAX_NT"); return e ? atoi(e) : 256; }();
+  const int max_nt = cap > 0 ? cap : max_nt_env;
   n_tok_tiles = (M + max_nt - 1) / max_nt;
   nt = (M + n_tok_tiles - 1) / n_tok_tiles;
   nt = (nt + 15) / 16 * 16;
@@ -817,42 +818,55 @@ bool gemm_tc_dp(int M, int N, int K, bool accumulate) {
   return waves >= 1.5 && eff >= min_eff;
 }
 
-// Super-tile width of the pair kernel: the per-pair L2 -> SM operand bytes of
-// a tile are (256 wt + nt) K 2, and the busiest pair runs ceil(tiles / pairs)
-// tiles, so pick the wt with the smaller ceil(tiles / pairs) (256 wt + nt) --
-// with a 5 % handicap on wt = 2 when it leaves one accumulator buffer (the
-// epilogue then no longer overlaps the next tile's MMAs). c3 (nt 240, 74 pairs):
-// QKV 3 x 496 vs 2 x 752 -> 1; O / down 2 x 496 vs 1 x 752 -> 2; gate/up 14 x 496
-// vs 7 x 752 -> 2. HSD_GEMM_WT=1|2 forces one.
-static int pair_wt(int M, int N) {
+// Tiling of the pair kernel: super-tile width wt (256-row weight tiles per tile)
+// and token tile nt. The per-pair L2 -> SM operand bytes of a tile are
+// (256 wt + nt) K 2 and the busiest pair runs ceil(tiles / pairs) tiles, so pick
+// the (wt, nt) with the smallest ceil(tiles / pairs) (256 wt + nt) -- with a 5 %
+// handicap on wt = 2 when it leaves one accumulator buffer (the epilogue then no
+// longer overlaps the next tile's MMAs). Candidates: the default token tile
+// (tc_tiles) and, opt-in, a narrower one (HSD_GEMM_NT_ALT, e.g. 176). c3 (74
+// pairs): QKV (N 6144) -> wt 1, nt 240 (3 x 496); with nt 176 allowed -> wt 2,
+// nt 176 (2 x 688), 87 vs 100 us with a plain-store epilogue, but no gain in the
+// step, where QKV runs the fused RoPE / KV epilogue and wt 2 leaves it one
+// accumulator buffer; O / down -> wt 2 (1 x 752); gate/up -> wt 2 (7 x 752).
+// HSD_GEMM_WT=1|2 forces the width.
+static void pair_tiling(int M, int N, int& wt_out, int& nt_out, int& ntt_out) {
   static const int env = [] { const char* e = getenv("HSD_GEMM_WT"); return e ? atoi(e) : 0; }();
-  int nt, ntt;
-  tc_tiles(M, nt, ntt);
-  if (env == 1 || env == 2) return env;
+  static const int nt_alt = [] { const char* e = getenv("HSD_GEMM_NT_ALT"); return e ? atoi(e) : 0; }();
   const long pairs = num_sms() / 2;
-  auto cost = [&](int wt) {
-    const long tiles = (long)((N + 2 * BM * wt - 1) / (2 * BM * wt)) * ntt;
-    const double c = (double)((tiles + pairs - 1) / pairs) * (256.0 * wt + nt);
-    return (wt == 2 && 4 * nt > 512) ? c * 1.05 : c;
-  };
-  return cost(2) < cost(1) ? 2 : 1;
+  double best = 1e300;
+  int cands[2] = {0, nt_alt}, nt0 = -1;
+  for (int ci = 0; ci < 2; ++ci) {
+    if (ci == 1 && nt_alt < 16) continue;
+    int nt, ntt;
+    tc_tiles(M, nt, ntt, cands[ci]);
+    if (ci == 0) nt0 = nt;
+    else if (nt >= nt0) continue;                    // the narrower token tile only
+    for (int wt = 1; wt <= 2; ++wt) {
+      if (env == 1 || env == 2) { if (wt != env) continue; }
+      const long tiles = (long)((N + 2 * BM * wt - 1) / (2 * BM * wt)) * ntt;
+      double c = (double)((tiles + pairs - 1) / pairs) * (256.0 * wt + nt);
+      if (wt == 2 && 4 * nt > 512) c *= 1.05;
+      if (c < best) { best = c; wt_out = wt; nt_out = nt; ntt_out = ntt; }
+    }
+  }
 }
 
 static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float* C, int ldc, int M, int N, int K,
                            int epi, bf16* H, int ldh, cudaStream_t st, KStamp ks, const QkvEpi* qe = nullptr) {
-  TcParams P;
+  TcParams P{};   // (value-initialised: every field not set below is 0)
   if (qe) P.qe = *qe;
   P.M = M; P.N = N; P.K = K; P.ldc = ldc; P.C = C; P.H = H; P.ldh = ldh; P.epi = epi; P.dp = 1;
   P.trace = nullptr;
   P.kst = ks;
-  int nt, ntt;
-  tc_tiles(M, nt, ntt);
+  int nt = 0, ntt = 0, wt = 1;
+  pair_tiling(M, N, wt, nt, ntt);
   P.ntile = nt;
   P.n_tiles_t = ntt;
   P.n_tiles_n = (N + BM - 1) / BM;
   P.n_kb = (K + BK - 1) / BK;
   P.units = 0;
-  P.wt = pair_wt(M, N);
+  P.wt = wt;
   {
     const char* e = getenv("HSD_GEMM_EXP");
     P.exp = e ? atoi(e) : 0;
@@ -904,7 +918,7 @@ static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float
 
 static int gemm_tc_launch(const bf16* A, int lda, const bf16* W, int ldw, float* C, int ldc, int M, int N, int K,
                           int epi, int dp, bf16* H, int ldh, cudaStream_t st, bool allow_pair = true) {
-  TcParams P;
+  TcParams P{};   // (value-initialised: every field not set below is 0)
   P.M = M; P.N = N; P.K = K; P.ldc = ldc; P.C = C; P.H = H; P.ldh = ldh; P.epi = epi; P.dp = dp;
   P.wt = 1; P.nbuf = 2; P.exp = 0;
   P.kst = take_kstamp();
