@@ -830,8 +830,13 @@ bool gemm_tc_dp(int M, int N, int K, bool accumulate) {
 // step, where QKV runs the fused RoPE / KV epilogue and wt 2 leaves it one
 // accumulator buffer; O / down -> wt 2 (1 x 752); gate/up -> wt 2 (7 x 752).
 // HSD_GEMM_WT=1|2 forces the width.
-static void pair_tiling(int M, int N, int& wt_out, int& nt_out, int& ntt_out) {
+static void pair_tiling(int M, int N, int& wt_out, int& nt_out, int& ntt_out, bool heavy_epi = false) {
   static const int env = [] { const char* e = getenv("HSD_GEMM_WT"); return e ? atoi(e) : 0; }();
+  // the fused QKV epilogue (RoPE + scattered cache writes) is too long to leave
+  // un-overlapped: with it, only double-buffered (wt = 1) tilings are considered
+  // (c3 prefill QKV, M = 4096: 254 us on wt = 2 / one accumulator buffer).
+  // HSD_GEMM_QKV_WT2=1 lifts the restriction.
+  static const bool qkv_wt2 = [] { const char* e = getenv("HSD_GEMM_QKV_WT2"); return e && atoi(e) == 1; }();
   static const int nt_alt = [] { const char* e = getenv("HSD_GEMM_NT_ALT"); return e ? atoi(e) : 0; }();
   const long pairs = num_sms() / 2;
   double best = 1e300;
@@ -844,6 +849,7 @@ static void pair_tiling(int M, int N, int& wt_out, int& nt_out, int& ntt_out) {
     else if (nt >= nt0) continue;                    // the narrower token tile only
     for (int wt = 1; wt <= 2; ++wt) {
       if (env == 1 || env == 2) { if (wt != env) continue; }
+      else if (heavy_epi && !qkv_wt2 && wt == 2 && 2 * 2 * nt > 512) continue;
       const long tiles = (long)((N + 2 * BM * wt - 1) / (2 * BM * wt)) * ntt;
       double c = (double)((tiles + pairs - 1) / pairs) * (256.0 * wt + nt);
       if (wt == 2 && 4 * nt > 512) c *= 1.05;
@@ -860,7 +866,7 @@ static int gemm_tc2_launch(const bf16* A, int lda, const bf16* W, int ldw, float
   P.trace = nullptr;
   P.kst = ks;
   int nt = 0, ntt = 0, wt = 1;
-  pair_tiling(M, N, wt, nt, ntt);
+  pair_tiling(M, N, wt, nt, ntt, epi == EPI_QKV);
   P.ntile = nt;
   P.n_tiles_t = ntt;
   P.n_tiles_n = (N + BM - 1) / BM;

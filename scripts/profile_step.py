@@ -1,6 +1,6 @@
 """One profiled stage of a speculative step, for ncu --profile-from-start off.
 
-usage: python scripts/profile_step.py CFG [--batch B] [--stage verify|build|step]
+usage: python scripts/profile_step.py CFG [--batch B] [--stage verify|build|step|prefill]
 
 Sets the config up like bench.py (bf16, tcgen05, RESAMPLE|FUSION), prefills,
 runs 3 warm steps, then opens a CUDA profiler range around exactly one staged
@@ -21,7 +21,7 @@ from paper_2602_21224_b200 import hsd
 ap = argparse.ArgumentParser()
 ap.add_argument("config")
 ap.add_argument("--batch", type=int, default=0)
-ap.add_argument("--stage", default="verify", choices=["verify", "build", "step"])
+ap.add_argument("--stage", default="verify", choices=["verify", "build", "step", "prefill"])
 a = ap.parse_args()
 cfg = get_config(a.config)
 if a.batch:
@@ -32,6 +32,15 @@ ctx = hsd.init_model(cfg, device=0, stream=stream.cuda_stream, precision=hsd.BF1
                      max_ctx=cfg.prompt_len + 16 * (N + 1) + 64 * (N + 1),
                      vocab_perm=vocab_permutation(cfg.vocab, 0) if cfg.hot_tokens else None,
                      tcgen05=True, flags=hsd.FLAG_RESAMPLE | hsd.FLAG_FUSION)
+if a.stage == "prefill":   # one request's prefill (target forward + first token + draft prefill)
+    pr1 = prompts(cfg, batch=1)
+    ctx.prefill(pr1)
+    ctx.sync()
+    torch.cuda.profiler.start()
+    ctx.prefill(pr1)
+    ctx.sync()
+    torch.cuda.profiler.stop()
+    sys.exit(0)
 ctx.prefill(prompts(cfg, batch=cfg.batch))
 for _ in range(3):
     ctx.step()
