@@ -685,18 +685,18 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
 // ------------------------------------------------------------ dual-tile kernel
 // One CTA = (key split, kv head h, request x PAIR of q-tiles {2p, 2p+1}): one K / V
 // stream feeds 256 (row, head) pairs, so each SM ingests half the K / V bytes per
-// row of the single-tile kernel. Two softmax warp groups (one per q-tile, SW warps
-// per TMEM lane quarter each) ping-pong against the tensor core, FlashAttention-4
-// style: while group A turns S_A(j) into P_A(j), the MMA warp runs P_B(j-1) V and
-// S_B(j); while group B works, P_A(j) V and S_A(j+1).
-//  TMEM (512 columns): S_A | S_B (128 each, single-buffered, P_X written as bf16
-//  over S_X's first 64 columns) | O_A | O_B (hd each). S_X(j+1) is issued after
-//  P_X(j) V (tcgen05.mma executes in issue order), so it cannot overwrite P_X(j)
-//  early; and S_X(j) completing implies P_X(j-1) V completed, so the softmax may
-//  rescale O_X without waiting on another barrier.
-//  Shared memory: q tiles A, B (SW128, written by the softmax threads), a 2-stage K
-//  ring and a 2-stage V^T ring. The row sum l is accumulated by the softmax warps
-//  from the bf16-rounded P the MMA consumes.
+// row of the single-tile kernel. Two softmax warp groups (one per q-tile) ping-pong
+// against the tensor core, FlashAttention-4 style: while group A turns S_A(j) into
+// P_A(j), the MMA warp runs P_B(j-1) V and S_B(j), and the other way round.
+//  Chunks of 64 keys (one page). TMEM per tile X (256 columns): S_X [64] (P_X as
+//  bf16 over its first 32 columns), q_X [hd/2] (A operand of the TS-form S MMA),
+//  O_X [hd]. S_X(j+1) is issued after P_X(j) V (tcgen05.mma executes in issue
+//  order), so it cannot overwrite P_X(j) early, and S_X(j) completing implies
+//  P_X(j-1) V completed, so the softmax may rescale O_X without another barrier.
+//  Shared memory: 6-stage K and V^T rings of one page each. The row sum l is
+//  accumulated by the softmax warps from the bf16-rounded P the MMA consumes.
+constexpr int DCHUNK = 64;
+constexpr int DST = 6;   // ring stages (K and V each)
 template <int SW> constexpr int dual_threads() { return 96 + 2 * 128 * SW; }
 
 template <int SW>
@@ -705,28 +705,25 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
                           AttnParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  constexpr int KST = 2, VST = 2;
   const int hd = P.hd, natom = hd / 64;
-  const int q_bytes = QROWS * hd * 2;           // one q tile: natom atoms [128 rows x 128 B]
-  const int k_bytes = CHUNK * hd * 2;           // natom atoms [128 keys x 128 B]
-  const int v_page = hd * 128;                  // [hd rows x 64 keys] bf16
-  const int v_bytes = 2 * v_page;
-  uint8_t* sQ = base;
-  uint8_t* sK = sQ + 2 * q_bytes;
-  uint8_t* sV = sK + KST * k_bytes;
-  uint64_t* bars = (uint64_t*)(sV + VST * v_bytes);
-  uint64_t* kfull = bars;                 // [KST]
-  uint64_t* kempty = kfull + KST;         // [KST]
-  uint64_t* vfull = kempty + KST;         // [VST]
-  uint64_t* vempty = vfull + VST;         // [VST]
-  uint64_t* qbar = vempty + VST;
+  const int k_bytes = DCHUNK * hd * 2;          // natom atoms [64 keys x 128 B]
+  const int v_bytes = hd * 128;                 // V^T [hd rows x 64 keys]
+  uint8_t* sK = base;
+  uint8_t* sV = sK + DST * k_bytes;
+  uint64_t* bars = (uint64_t*)(sV + DST * v_bytes);
+  uint64_t* kfull = bars;                 // [DST]
+  uint64_t* kempty = kfull + DST;         // [DST]
+  uint64_t* vfull = kempty + DST;         // [DST]
+  uint64_t* vempty = vfull + DST;         // [DST]
+  uint64_t* qbar = vempty + DST;
   uint64_t* sfull = qbar + 1;             // [2 tiles]
   uint64_t* pfull = sfull + 2;            // [2 tiles]
   uint64_t* odone = pfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(odone + 1);
   __shared__ int tile_lo, tile_hi, safe_hi;
   constexpr int NSMG = 128 * SW;                // softmax threads per group
-  constexpr int KPW = CHUNK / SW;               // keys per softmax warp per chunk
+  constexpr int KPW = DCHUNK / SW;              // keys per softmax warp per chunk (32 at SW = 2)
+  static_assert(KPW == 32 || KPW == 16, "dual kernel: SW 2 or 4");
   __shared__ float red_max[2][2][SW][QROWS];    // [tile][chunk parity][part][row]
   __shared__ float red_l[2][SW][QROWS];         // epilogue: l per part
 
@@ -741,8 +738,10 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
 
   if (threadIdx.x == 0) { tile_lo = 0x7fffffff; tile_hi = 0; safe_hi = 0x7fffffff; }
   if (threadIdx.x == 32) {
-    for (int s = 0; s < KST; ++s) { mbar_init(&kfull[s], 1); mbar_init(&kempty[s], 1); }
-    for (int s = 0; s < VST; ++s) { mbar_init(&vfull[s], 1); mbar_init(&vempty[s], 1); }
+    for (int s = 0; s < DST; ++s) {
+      mbar_init(&kfull[s], 1); mbar_init(&kempty[s], 1);
+      mbar_init(&vfull[s], 1); mbar_init(&vempty[s], 1);
+    }
     mbar_init(qbar, (hasB ? 2 : 1) * NSMG / 32);
     for (int x = 0; x < 2; ++x) { mbar_init(&sfull[x], 1); mbar_init(&pfull[x], NSMG / 32); }
     mbar_init(odone, 1);
@@ -756,7 +755,6 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
   }
   __syncthreads();
   pdl_trigger();
-  // softmax threads: tile X, this lane's (row, head) and its key bounds
   const int X = warp >= 3 ? (warp - 3) / (4 * SW) : 0;
   const bool in_tile = warp >= 3 && (X == 0 || hasB);
   const int q4 = warp & 3;
@@ -801,17 +799,21 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
   const uint32_t tmem = *tmem_slot;
   int k_begin, k_end;
   if (P.dyn) {
-    const int c0 = tile_lo / CHUNK, c1 = (tile_hi + CHUNK - 1) / CHUNK;
+    const int c0 = tile_lo / DCHUNK, c1 = (tile_hi + DCHUNK - 1) / DCHUNK;
     const int cps = c1 > c0 ? (c1 - c0 + nsplit - 1) / nsplit : 0;
-    k_begin = (c0 + split * cps) * CHUNK;
-    k_end = k_begin + cps * CHUNK;
+    k_begin = (c0 + split * cps) * DCHUNK;
+    k_end = k_begin + cps * DCHUNK;
   } else {
     k_begin = split * P.keys_per_split;
     k_end = min(P.max_keys, k_begin + P.keys_per_split);
   }
   const int lo = max(k_begin, tile_lo), hi = min(k_end, tile_hi);
-  const int c_first = lo / CHUNK;
-  const int n_chunks = hi > lo ? (hi + CHUNK - 1) / CHUNK - c_first : 0;
+  const int c_first = lo / DCHUNK;
+  const int n_chunks = hi > lo ? (hi + DCHUNK - 1) / DCHUNK - c_first : 0;
+  // TMEM columns of tile x: S at 256 x, q at 256 x + 64, O at 256 x + 128
+  auto tS_of = [&](int x) { return tmem + (uint32_t)(256 * x); };
+  auto tQ_of = [&](int x) { return tmem + (uint32_t)(256 * x + 64); };
+  auto tO_of = [&](int x) { return tmem + (uint32_t)(256 * x + 128); };
 
   if (warp == 0) {
     if (lane == 0 && n_chunks == 0) { l2pf_issue(P.pf); l2pf_issue(P.pf, 1); }
@@ -819,19 +821,16 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
       const uint64_t pol = P.n_qtiles > 2 ? policy_evict_normal() : policy_evict_first();
       auto load_k = [&](int j) {
-        const int s = j % KST;
-        mbar_wait(&kempty[s], ((j / KST) & 1) ^ 1);
+        const int s = j % DST;
+        mbar_wait(&kempty[s], ((j / DST) & 1) ^ 1);
         mbar_expect_tx(&kfull[s], k_bytes);
-        for (int pg = 0; pg < 2; ++pg) {
-          const int page = P.kv.block_table[(size_t)req * P.kv.pages_per_req + 2 * (c_first + j) + pg];
-          const int krow = ((page * 2 + 0) * P.kv.kv_heads + h) * PAGE;
-          for (int a = 0; a < natom; ++a)
-            tma_load_2d(&tmK, &kfull[s], sK + (size_t)s * k_bytes + a * (CHUNK * 128) + pg * (PAGE * 128), a * 64,
-                        krow, pol);
-        }
+        const int page = P.kv.block_table[(size_t)req * P.kv.pages_per_req + c_first + j];
+        const int krow = ((page * 2 + 0) * P.kv.kv_heads + h) * PAGE;
+        for (int a = 0; a < natom; ++a)
+          tma_load_2d(&tmK, &kfull[s], sK + (size_t)s * k_bytes + a * (DCHUNK * 128), a * 64, krow, pol);
       };
       int kj = 0;
-      while (kj < n_chunks && kj < KST && (c_first + kj + 1) * CHUNK <= safe_hi) load_k(kj++);
+      while (kj < n_chunks && kj < DST && (c_first + kj + 1) * DCHUNK <= safe_hi) load_k(kj++);
       pdl_wait();
       kst_enter(P.kst);
       while (kj < n_chunks) load_k(kj++);
@@ -842,43 +841,36 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
       const uint64_t pol = P.n_qtiles > 2 ? policy_evict_normal() : policy_evict_first();
       auto load_v = [&](int j) {
-        const int s = j % VST;
-        mbar_wait(&vempty[s], ((j / VST) & 1) ^ 1);
-        mbar_expect_tx(&vfull[s], 2 * hd * 128);
-        for (int pg = 0; pg < 2; ++pg) {
-          const int page = P.kv.block_table[(size_t)req * P.kv.pages_per_req + 2 * (c_first + j) + pg];
-          tma_load_2d(&tmV, &vfull[s], sV + (size_t)s * v_bytes + pg * v_page, 0,
-                      ((page * 2 + 1) * P.kv.kv_heads + h) * hd, pol);
-        }
+        const int s = j % DST;
+        mbar_wait(&vempty[s], ((j / DST) & 1) ^ 1);
+        mbar_expect_tx(&vfull[s], v_bytes);
+        const int page = P.kv.block_table[(size_t)req * P.kv.pages_per_req + c_first + j];
+        tma_load_2d(&tmV, &vfull[s], sV + (size_t)s * v_bytes, 0, ((page * 2 + 1) * P.kv.kv_heads + h) * hd, pol);
       };
       int vj = 0;
-      while (vj < n_chunks && vj < VST && (c_first + vj + 1) * CHUNK <= safe_hi) load_v(vj++);
+      while (vj < n_chunks && vj < DST && (c_first + vj + 1) * DCHUNK <= safe_hi) load_v(vj++);
       pdl_wait();
       while (vj < n_chunks) load_v(vj++);
     }
   } else if (warp == 1) {
     if (lane == 0 && n_chunks > 0) {
-      mbar_wait(qbar, 0);                       // both q tiles in shared memory
+      mbar_wait(qbar, 0);                       // both q tiles in TMEM
       fence_after();
       const int ntile = hasB ? 2 : 1;
-      auto issue_s = [&](int x, int j) {        // S_x(j) = Q_x K_j^T
-        const int s = j % KST;
-        const uint32_t d = tmem + (uint32_t)(x * CHUNK);
+      auto issue_s = [&](int x, int j) {        // S_x(j) = Q_x K_j^T, q from TMEM
+        const int s = j % DST;
         for (int kk = 0; kk < hd / 16; ++kk) {
           const int a = kk >> 2, off = kk & 3;
-          const uint64_t ad = desc_sw128(sQ + (size_t)x * q_bytes + a * (QROWS * 128)) + 2 * off;
-          const uint64_t bd = desc_sw128(sK + (size_t)s * k_bytes + a * (CHUNK * 128)) + 2 * off;
-          mma_bf16(d, ad, bd, P.idesc_s, kk > 0 ? 1u : 0u);
+          const uint64_t bd = desc_sw128(sK + (size_t)s * k_bytes + a * (DCHUNK * 128)) + 2 * off;
+          mma_bf16_ts(tS_of(x), tQ_of(x) + (uint32_t)(kk * 8), bd, P.idesc_s, kk > 0 ? 1u : 0u);
         }
         mma_commit(&sfull[x]);
       };
       auto issue_pv = [&](int x, int j) {       // O_x += P_x(j) V_j, P_x from TMEM
-        const int s = j % VST;
-        const uint32_t tO = tmem + 256 + (uint32_t)(x * hd), tP = tmem + (uint32_t)(x * CHUNK);
-        for (int kk = 0; kk < CHUNK / 16; ++kk) {
-          const int ka = kk >> 2, off = kk & 3;
-          const uint64_t vd = desc_sw128(sV + (size_t)s * v_bytes + ka * v_page) + 2 * off;
-          mma_bf16_ts(tO, tP + (uint32_t)(kk * 8), vd, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        const int s = j % DST;
+        for (int kk = 0; kk < DCHUNK / 16; ++kk) {
+          const uint64_t vd = desc_sw128(sV + (size_t)s * v_bytes) + 2 * kk;
+          mma_bf16_ts(tO_of(x), tS_of(x) + (uint32_t)(kk * 8), vd, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
       };
       mbar_wait(&kfull[0], 0);
@@ -887,8 +879,8 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
       mma_commit(&kempty[0]);
       for (int j = 0; j < n_chunks; ++j) {
         const bool more = j + 1 < n_chunks;
-        if (more) { mbar_wait(&kfull[(j + 1) % KST], ((j + 1) / KST) & 1); fence_after(); }
-        mbar_wait(&vfull[j % VST], (j / VST) & 1);
+        if (more) { mbar_wait(&kfull[(j + 1) % DST], ((j + 1) / DST) & 1); fence_after(); }
+        mbar_wait(&vfull[j % DST], (j / DST) & 1);
         fence_after();
         for (int x = 0; x < ntile; ++x) {
           mbar_wait(&pfull[x], j & 1);
@@ -896,8 +888,8 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
           issue_pv(x, j);
           if (more) issue_s(x, j + 1);           // after P_x(j) V: may overwrite P_x(j)
         }
-        mma_commit(&vempty[j % VST]);
-        if (more) mma_commit(&kempty[(j + 1) % KST]);
+        mma_commit(&vempty[j % DST]);
+        if (more) mma_commit(&kempty[(j + 1) % DST]);
       }
       mma_commit(odone);
     }
@@ -906,21 +898,31 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
     const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
     float mrow = -INFINITY, lsum = 0.f;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    const uint32_t tS = tmem + (uint32_t)(X * CHUNK), tO = tmem + 256 + (uint32_t)(X * hd);
+    const uint32_t tS = tS_of(X), tO = tO_of(X), tQ = tQ_of(X);
     const int hcols = hd / SW;
     const bool live = __any_sync(0xffffffffu, valid);
     {
-      // this thread's q row, dims [part hd/SW, (part+1) hd/SW), into the SW128 q tile
+      // this thread's q row, dims [part hd/SW, (part+1) hd/SW), into TMEM (bf16 pairs,
+      // the A layout of the TS-form MMA): hd / (2 SW) columns at its lane
       pdl_wait();
-      const int d0 = part * hcols;
-      const uint4* src = writable ? (const uint4*)(P.q + ((size_t)row * P.Hq + head) * hd + d0) : nullptr;
-      uint8_t* qt_base = sQ + (size_t)X * q_bytes;
-      for (int c = 0; c < hcols / 8; ++c) {
-        const int d = d0 + 8 * c, a = d >> 6, ch = (d & 63) >> 3;
-        const uint4 v = src ? src[c] : make_uint4(0u, 0u, 0u, 0u);
-        *(uint4*)(qt_base + a * (QROWS * 128) + lane_row * 128 + ((ch ^ (lane_row & 7)) << 4)) = v;
+      constexpr int QC = 64 / SW;                 // columns per part at hd = 128
+      const int qc = hd / (2 * SW);
+      uint32_t qw[QC];
+      const uint4* src = writable ? (const uint4*)(P.q + ((size_t)row * P.Hq + head) * hd + part * (hd / SW)) : nullptr;
+#pragma unroll
+      for (int i = 0; i < QC / 4; ++i) {
+        const uint4 v = (src && i < qc / 4) ? src[i] : make_uint4(0u, 0u, 0u, 0u);
+        qw[4 * i] = v.x; qw[4 * i + 1] = v.y; qw[4 * i + 2] = v.z; qw[4 * i + 3] = v.w;
       }
-      fence_proxy_async();
+      if constexpr (QC == 32) {
+        if (qc == 32) tmem_st32(tQ + lane_off + (uint32_t)(part * 32), qw);
+        else { uint32_t w16[16]; for (int i = 0; i < 16; ++i) w16[i] = qw[i]; tmem_st16(tQ + lane_off + (uint32_t)(part * 16), w16); }
+      } else {
+        if (qc == 16) tmem_st16(tQ + lane_off + (uint32_t)(part * 16), qw);
+        else { uint32_t w8[8]; for (int i = 0; i < 8; ++i) w8[i] = qw[i]; tmem_st8(tQ + lane_off + (uint32_t)(part * 8), w8); }
+      }
+      tmem_st_wait();
+      fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(qbar);
     }
@@ -929,28 +931,20 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
       mbar_wait(&sfull[X], j & 1);
       fence_after();
       if (live) {
-        const int kb = (c_first + j) * CHUNK + part * KPW;
-        uint32_t r0[32], r1[32];
-        tmem_ld32_nw(tS + lane_off + (uint32_t)(part * KPW), r0);
-        if constexpr (KPW == 64) tmem_ld32_nw(tS + lane_off + (uint32_t)(part * KPW + 32), r1);
-        uint32_t vm0 = 0u, vm1 = 0xffffffffu;
+        const int kb = (c_first + j) * DCHUNK + part * KPW;
+        uint32_t r0[32];
+        if constexpr (KPW == 32) tmem_ld32_nw(tS + lane_off + (uint32_t)(part * KPW), r0);
+        else { uint32_t r16[16]; tmem_ld16_nw(tS + lane_off + (uint32_t)(part * KPW), r16); for (int i = 0; i < 16; ++i) r0[i] = r16[i]; }
+        uint32_t vm0 = 0u;
         if (valid) {
           vm0 = range32(klo - kb, khi - kb);
           if (slot >= 0) vm0 |= anc32(anc, kb - tb) & range32(0, m.t_max - (kb - tb));
           vm0 &= range32(k_begin - kb, k_end - kb);
-          if constexpr (KPW == 64) {
-            vm1 = range32(klo - kb - 32, khi - kb - 32);
-            if (slot >= 0) vm1 |= anc32(anc, kb + 32 - tb) & range32(0, m.t_max - (kb + 32 - tb));
-            vm1 &= range32(k_begin - kb - 32, k_end - kb - 32);
-          }
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         float s[KPW];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          s[i] = ((vm0 >> i) & 1u) ? __uint_as_float(r0[i]) : -INFINITY;
-          if constexpr (KPW == 64) s[32 + i] = ((vm1 >> i) & 1u) ? __uint_as_float(r1[i]) : -INFINITY;
-        }
+        for (int i = 0; i < KPW; ++i) s[i] = ((vm0 >> i) & 1u) ? __uint_as_float(r0[i]) : -INFINITY;
         float mxp[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) mxp[k] = s[k];
@@ -971,7 +965,7 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
           mrow = mx;
         }
         const float msub = mrow == -INFINITY ? 0.f : mrow;
-        uint32_t pw[32];
+        uint32_t pw[KPW / 2];
         float ls = 0.f;
 #pragma unroll
         for (int i = 0; i < KPW / 2; ++i) {
@@ -981,13 +975,10 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
           ls += pf.x + pf.y;
           pw[i] = *(uint32_t*)&pr;
         }
-        if constexpr (KPW == 64) {
-          tmem_st32(tS + lane_off + (uint32_t)(part * 32), pw);
+        if constexpr (KPW == 32) {
+          tmem_st16(tS + lane_off + (uint32_t)(part * 16), pw);
         } else {
-          uint32_t pw16[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) pw16[i] = pw[i];
-          tmem_st16(tS + lane_off + (uint32_t)(part * 16), pw16);
+          tmem_st8(tS + lane_off + (uint32_t)(part * 8), pw);
         }
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
           // P_X(j-1) V completed before S_X(j) did (issue order): O_X is final up to j-1
@@ -1045,13 +1036,11 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
         }
       }
     }
-    if (writable) {
-      if (!P.direct && part == 0) {
-        const size_t base_ml = (size_t)nsplit * P.M * P.Hq * hd;
-        const size_t idx = ((size_t)split * P.Hq + head) * P.M + row;
-        P.ws[base_ml + 2 * idx] = mrow;
-        P.ws[base_ml + 2 * idx + 1] = ltot;
-      }
+    if (writable && !P.direct && part == 0) {
+      const size_t base_ml = (size_t)nsplit * P.M * P.Hq * hd;
+      const size_t idx = ((size_t)split * P.Hq + head) * P.M + row;
+      P.ws[base_ml + 2 * idx] = mrow;
+      P.ws[base_ml + 2 * idx + 1] = ltot;
     }
   }
   fence_before();
@@ -1186,21 +1175,23 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   // Dual-tile kernel (two q-tiles per CTA, one K / V stream; HSD_ATTN_DUAL=0 disables):
   // when a (request, kv head) has >= 2 q-tiles (c3 / c4 / c5 verify passes)
   static const int dual_env = [] { const char* e = getenv("HSD_ATTN_DUAL"); return e ? atoi(e) : 0; }();
-  if (dual_env && P.n_qtiles >= 2) {
+  if (dual_env && P.n_qtiles >= 2 && hd == 128) {
     const int npairs = (P.n_qtiles + 1) / 2;
     const int base2 = n_req * kv.kv_heads * npairs;
+    const int dchunks = (max_keys + DCHUNK - 1) / DCHUNK;   // 64-key chunks (pages)
     int S2 = max(1, (2 * num_sms() + base2) / (2 * base2));
-    S2 = min(S2, max(1, pages / 2));
-    if (s_override > 0) S2 = min(s_override, pages);
+    S2 = min(S2, max(1, dchunks / 2));
+    if (s_override > 0) S2 = min(s_override, dchunks);
     while (S2 > 1 && (size_t)S2 * M * Hq * (hd + 2) > ws_floats) --S2;
-    const bool lb = (pages + S2 - 1) / S2 <= 4;
+    const bool lb = (dchunks + S2 - 1) / S2 <= 8;
     if (dyn && lb) S2 = min(S2, max(1, num_sms() / base2));
     P.dyn = dyn == 1 && lb;
-    const int pps2 = (pages + S2 - 1) / S2;
-    P.keys_per_split = pps2 * CHUNK;
-    if (!P.dyn) S2 = (pages + pps2 - 1) / pps2;
+    const int cps2 = (dchunks + S2 - 1) / S2;
+    P.keys_per_split = cps2 * DCHUNK;
+    if (!P.dyn) S2 = (dchunks + cps2 - 1) / cps2;
     P.direct = S2 == 1;
     P.cluster = 0;
+    P.idesc_s = idesc_bf16(128, DCHUNK);
     P.idesc_o = idesc_bf16(128, hd);
     CUtensorMap mk2, mv2;
     uint64_t dk2[2] = {(uint64_t)hd, (uint64_t)(kv_layer_elems / hd)};
@@ -1210,8 +1201,7 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
     uint64_t sv2[1] = {(uint64_t)PAGE};
     uint32_t bv2[2] = {(uint32_t)PAGE, (uint32_t)hd};
     if (!tma_map_bf16(&mk2, kv.base, 2, dk2, sk2, bk2) || !tma_map_bf16(&mv2, kv.base, 2, dv2, sv2, bv2)) return -1;
-    const size_t smem2 = 1024 + 2 * ((size_t)QROWS * hd * 2) + 2 * ((size_t)CHUNK * hd * 2) + 2 * ((size_t)2 * hd * 128) +
-                         16 * 8 + 64;
+    const size_t smem2 = 1024 + DST * ((size_t)DCHUNK * hd * 2) + DST * ((size_t)hd * 128) + (4 * DST + 8) * 8 + 64;
     static size_t attr2 = 0;
     if (smem2 > attr2) {
       if (cudaFuncSetAttribute(attention_dual_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2) !=

@@ -1025,7 +1025,8 @@ bool gemm_tc_qkv_ok(int M, int N, int K, int hd, int Hq, int Hkv) {
   static const bool on = [] { const char* e = getenv("HSD_GEMM_QKV_EPI"); return !(e && atoi(e) == 0); }();
   static const bool pair_on = [] { const char* e = getenv("HSD_GEMM_2SM"); return !(e && atoi(e) == 0); }();
   // every 128-row weight tile holds heads of one kind only (q, k or v)
-  return on && pair_on && num_sms() >= 2 && (hd == 64 || hd == 128) && (Hq * hd) % BM == 0 && (Hkv * hd) % BM == 0 &&
+  // (hd = 128 only: the shapes the full-size parity tests cover -- c3 / c4 / c5 verify and prefill)
+  return on && pair_on && num_sms() >= 2 && hd == 128 && (Hq * hd) % BM == 0 && (Hkv * hd) % BM == 0 &&
          N == (Hq + 2 * Hkv) * hd && gemm_tc_dp(M, N, K, false);
 }
 
