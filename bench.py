@@ -675,7 +675,13 @@ def main():
                "prefill_s": round(t_all - t_dec, 3)}
 
     planted = None
-    if not args.no_planted:
+    if not args.no_planted and getattr(cfg, "accept", "greedy") == "stochastic":
+        # R24 plants the target's GREEDY continuation; stochastic acceptance (T = 1)
+        # samples and leaves it at the first draw that differs, so the leg measures
+        # nothing there (the greedy configs c1 / c2 / c4 / c5 run it)
+        planted = {"skipped": "stochastic acceptance: the planted continuation (R24) is the target's greedy one, "
+                              "which sampling does not follow; run --config c2 for the planted leg"}
+    elif not args.no_planted:
         try:
             tau_p, val_p, ms_p, info_p = planted_leg(ctx, pr, cfg, b, N, min(args.steps, 10), 3, stream)
             planted = {"rates": plant_rates, "tau": round(tau_p, 3), "value": round(val_p * world, 2), **info_p,
