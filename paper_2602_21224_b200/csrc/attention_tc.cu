@@ -685,18 +685,18 @@ __global__ void __launch_bounds__(nthreads<SW>(), 1)
 // ------------------------------------------------------------ dual-tile kernel
 // One CTA = (key split, kv head h, request x PAIR of q-tiles {2p, 2p+1}): one K / V
 // stream feeds 256 (row, head) pairs, so each SM ingests half the K / V bytes per
-// row of the single-tile kernel. Two softmax warp groups (one per q-tile) ping-pong
-// against the tensor core, FlashAttention-4 style: while group A turns S_A(j) into
-// P_A(j), the MMA warp runs P_B(j-1) V and S_B(j), and the other way round.
-//  Chunks of 64 keys (one page). TMEM per tile X (256 columns): S_X [64] (P_X as
-//  bf16 over its first 32 columns), q_X [hd/2] (A operand of the TS-form S MMA),
-//  O_X [hd]. S_X(j+1) is issued after P_X(j) V (tcgen05.mma executes in issue
-//  order), so it cannot overwrite P_X(j) early, and S_X(j) completing implies
-//  P_X(j-1) V completed, so the softmax may rescale O_X without another barrier.
-//  Shared memory: 6-stage K and V^T rings of one page each. The row sum l is
-//  accumulated by the softmax warps from the bf16-rounded P the MMA consumes.
+// row of the single-tile kernel. Each q-tile keeps the single-tile kernel's
+// pipeline -- a double-buffered score tile, so S_X(j+1) is computed while the
+// softmax group of tile X turns S_X(j) into P_X(j) -- and the two tiles' groups
+// share the MMA warp and the K / V rings.
+//  Chunks of 64 keys (one page). TMEM per tile X (256 columns): two score buffers
+//  of 64 columns (P as bf16 over a buffer's first 32 columns), O_X [hd]. q tiles
+//  in shared memory (SS-form S MMAs), 4-stage K and V^T rings of one page each.
+//  The row sum l is accumulated by the softmax warps from the bf16-rounded P the
+//  MMA consumes; a lazy rescale waits for P_X(j-1) V (pvdone) like the single-tile
+//  kernel.
 constexpr int DCHUNK = 64;
-constexpr int DST = 6;   // ring stages (K and V each)
+constexpr int DST = 4;   // ring stages (K and V each)
 template <int SW> constexpr int dual_threads() { return 96 + 2 * 128 * SW; }
 
 template <int SW>
@@ -706,9 +706,11 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int hd = P.hd, natom = hd / 64;
+  const int q_bytes = QROWS * hd * 2;           // one q tile: natom atoms [128 rows x 128 B]
   const int k_bytes = DCHUNK * hd * 2;          // natom atoms [64 keys x 128 B]
   const int v_bytes = hd * 128;                 // V^T [hd rows x 64 keys]
-  uint8_t* sK = base;
+  uint8_t* sQ = base;
+  uint8_t* sK = sQ + 2 * q_bytes;
   uint8_t* sV = sK + DST * k_bytes;
   uint64_t* bars = (uint64_t*)(sV + DST * v_bytes);
   uint64_t* kfull = bars;                 // [DST]
@@ -716,9 +718,10 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
   uint64_t* vfull = kempty + DST;         // [DST]
   uint64_t* vempty = vfull + DST;         // [DST]
   uint64_t* qbar = vempty + DST;
-  uint64_t* sfull = qbar + 1;             // [2 tiles]
-  uint64_t* pfull = sfull + 2;            // [2 tiles]
-  uint64_t* odone = pfull + 2;
+  uint64_t* sfull = qbar + 1;             // [tile][buffer]
+  uint64_t* pfull = sfull + 4;            // [tile][buffer]
+  uint64_t* pvdone = pfull + 4;           // [tile]: one phase per P_X(j) V
+  uint64_t* odone = pvdone + 2;
   uint32_t* tmem_slot = (uint32_t*)(odone + 1);
   __shared__ int tile_lo, tile_hi, safe_hi;
   constexpr int NSMG = 128 * SW;                // softmax threads per group
@@ -743,7 +746,8 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
       mbar_init(&vfull[s], 1); mbar_init(&vempty[s], 1);
     }
     mbar_init(qbar, (hasB ? 2 : 1) * NSMG / 32);
-    for (int x = 0; x < 2; ++x) { mbar_init(&sfull[x], 1); mbar_init(&pfull[x], NSMG / 32); }
+    for (int x = 0; x < 4; ++x) { mbar_init(&sfull[x], 1); mbar_init(&pfull[x], NSMG / 32); }
+    for (int x = 0; x < 2; ++x) mbar_init(&pvdone[x], 1);
     mbar_init(odone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -810,9 +814,8 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
   const int lo = max(k_begin, tile_lo), hi = min(k_end, tile_hi);
   const int c_first = lo / DCHUNK;
   const int n_chunks = hi > lo ? (hi + DCHUNK - 1) / DCHUNK - c_first : 0;
-  // TMEM columns of tile x: S at 256 x, q at 256 x + 64, O at 256 x + 128
-  auto tS_of = [&](int x) { return tmem + (uint32_t)(256 * x); };
-  auto tQ_of = [&](int x) { return tmem + (uint32_t)(256 * x + 64); };
+  // TMEM columns of tile x: score buffers at 256 x + {0, 64}, O at 256 x + 128
+  auto tS_of = [&](int x, int j) { return tmem + (uint32_t)(256 * x + 64 * (j & 1)); };
   auto tO_of = [&](int x) { return tmem + (uint32_t)(256 * x + 128); };
 
   if (warp == 0) {
@@ -854,42 +857,42 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && n_chunks > 0) {
-      mbar_wait(qbar, 0);                       // both q tiles in TMEM
+      mbar_wait(qbar, 0);                       // both q tiles in shared memory
       fence_after();
       const int ntile = hasB ? 2 : 1;
-      auto issue_s = [&](int x, int j) {        // S_x(j) = Q_x K_j^T, q from TMEM
+      auto issue_s = [&](int j) {               // S_x(j) = Q_x K_j^T for both tiles
         const int s = j % DST;
-        for (int kk = 0; kk < hd / 16; ++kk) {
-          const int a = kk >> 2, off = kk & 3;
-          const uint64_t bd = desc_sw128(sK + (size_t)s * k_bytes + a * (DCHUNK * 128)) + 2 * off;
-          mma_bf16_ts(tS_of(x), tQ_of(x) + (uint32_t)(kk * 8), bd, P.idesc_s, kk > 0 ? 1u : 0u);
-        }
-        mma_commit(&sfull[x]);
-      };
-      auto issue_pv = [&](int x, int j) {       // O_x += P_x(j) V_j, P_x from TMEM
-        const int s = j % DST;
-        for (int kk = 0; kk < DCHUNK / 16; ++kk) {
-          const uint64_t vd = desc_sw128(sV + (size_t)s * v_bytes) + 2 * kk;
-          mma_bf16_ts(tO_of(x), tS_of(x) + (uint32_t)(kk * 8), vd, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-      };
-      mbar_wait(&kfull[0], 0);
-      fence_after();
-      for (int x = 0; x < ntile; ++x) issue_s(x, 0);
-      mma_commit(&kempty[0]);
-      for (int j = 0; j < n_chunks; ++j) {
-        const bool more = j + 1 < n_chunks;
-        if (more) { mbar_wait(&kfull[(j + 1) % DST], ((j + 1) / DST) & 1); fence_after(); }
-        mbar_wait(&vfull[j % DST], (j / DST) & 1);
+        mbar_wait(&kfull[s], (j / DST) & 1);
         fence_after();
         for (int x = 0; x < ntile; ++x) {
-          mbar_wait(&pfull[x], j & 1);
-          fence_after();
-          issue_pv(x, j);
-          if (more) issue_s(x, j + 1);           // after P_x(j) V: may overwrite P_x(j)
+          for (int kk = 0; kk < hd / 16; ++kk) {
+            const int a = kk >> 2, off = kk & 3;
+            const uint64_t ad = desc_sw128(sQ + (size_t)x * q_bytes + a * (QROWS * 128)) + 2 * off;
+            const uint64_t bd = desc_sw128(sK + (size_t)s * k_bytes + a * (DCHUNK * 128)) + 2 * off;
+            mma_bf16(tS_of(x, j), ad, bd, P.idesc_s, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&sfull[2 * x + (j & 1)]);
         }
-        mma_commit(&vempty[j % DST]);
-        if (more) mma_commit(&kempty[(j + 1) % DST]);
+        mma_commit(&kempty[s]);
+      };
+      issue_s(0);
+      for (int j = 0; j < n_chunks; ++j) {
+        // S(j+1) into the other score buffer (it held P(j-1), consumed by P(j-1) V,
+        // issued earlier: tcgen05.mma executes in issue order)
+        if (j + 1 < n_chunks) issue_s(j + 1);
+        const int s = j % DST;
+        mbar_wait(&vfull[s], (j / DST) & 1);
+        fence_after();
+        for (int x = 0; x < ntile; ++x) {
+          mbar_wait(&pfull[2 * x + (j & 1)], (j >> 1) & 1);
+          fence_after();
+          for (int kk = 0; kk < DCHUNK / 16; ++kk) {
+            const uint64_t vd = desc_sw128(sV + (size_t)s * v_bytes) + 2 * kk;
+            mma_bf16_ts(tO_of(x), tS_of(x, j) + (uint32_t)(kk * 8), vd, P.idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&pvdone[x]);
+        }
+        mma_commit(&vempty[s]);
       }
       mma_commit(odone);
     }
@@ -898,38 +901,29 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
     const float scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
     float mrow = -INFINITY, lsum = 0.f;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    const uint32_t tS = tS_of(X), tO = tO_of(X), tQ = tQ_of(X);
+    const uint32_t tO = tO_of(X);
     const int hcols = hd / SW;
     const bool live = __any_sync(0xffffffffu, valid);
     {
-      // this thread's q row, dims [part hd/SW, (part+1) hd/SW), into TMEM (bf16 pairs,
-      // the A layout of the TS-form MMA): hd / (2 SW) columns at its lane
+      // this thread's q row, dims [part hd/SW, (part+1) hd/SW), into the SW128 q tile
       pdl_wait();
-      constexpr int QC = 64 / SW;                 // columns per part at hd = 128
-      const int qc = hd / (2 * SW);
-      uint32_t qw[QC];
-      const uint4* src = writable ? (const uint4*)(P.q + ((size_t)row * P.Hq + head) * hd + part * (hd / SW)) : nullptr;
-#pragma unroll
-      for (int i = 0; i < QC / 4; ++i) {
-        const uint4 v = (src && i < qc / 4) ? src[i] : make_uint4(0u, 0u, 0u, 0u);
-        qw[4 * i] = v.x; qw[4 * i + 1] = v.y; qw[4 * i + 2] = v.z; qw[4 * i + 3] = v.w;
+      const int d0 = part * hcols;
+      const uint4* src = writable ? (const uint4*)(P.q + ((size_t)row * P.Hq + head) * hd + d0) : nullptr;
+      uint8_t* qt_base = sQ + (size_t)X * q_bytes;
+      for (int c = 0; c < hcols / 8; ++c) {
+        const int d = d0 + 8 * c, a = d >> 6, ch = (d & 63) >> 3;
+        const uint4 v = src ? src[c] : make_uint4(0u, 0u, 0u, 0u);
+        *(uint4*)(qt_base + a * (QROWS * 128) + lane_row * 128 + ((ch ^ (lane_row & 7)) << 4)) = v;
       }
-      if constexpr (QC == 32) {
-        if (qc == 32) tmem_st32(tQ + lane_off + (uint32_t)(part * 32), qw);
-        else { uint32_t w16[16]; for (int i = 0; i < 16; ++i) w16[i] = qw[i]; tmem_st16(tQ + lane_off + (uint32_t)(part * 16), w16); }
-      } else {
-        if (qc == 16) tmem_st16(tQ + lane_off + (uint32_t)(part * 16), qw);
-        else { uint32_t w8[8]; for (int i = 0; i < 8; ++i) w8[i] = qw[i]; tmem_st8(tQ + lane_off + (uint32_t)(part * 8), w8); }
-      }
-      tmem_st_wait();
-      fence_before();
+      fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(qbar);
     }
     const int bar_id = 1 + X * 4 + q4;          // the SW warps of this group and lane quarter
     for (int j = 0; j < n_chunks; ++j) {
-      mbar_wait(&sfull[X], j & 1);
+      mbar_wait(&sfull[2 * X + (j & 1)], (j >> 1) & 1);
       fence_after();
+      const uint32_t tS = tS_of(X, j);
       if (live) {
         const int kb = (c_first + j) * DCHUNK + part * KPW;
         uint32_t r0[32];
@@ -981,7 +975,12 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
           tmem_st8(tS + lane_off + (uint32_t)(part * 8), pw);
         }
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
-          // P_X(j-1) V completed before S_X(j) did (issue order): O_X is final up to j-1
+          // O_X must hold P_X(<j) V exactly once before it is scaled: S_X(j) completing
+          // implies P_X(j-2) V done, so pvdone[X] is within one phase of j-1
+          if (j > 0) {
+            mbar_wait(&pvdone[X], (j - 1) & 1);
+            fence_after();
+          }
           for (int c = 0; c < hcols; c += 16) {
             uint32_t o[16];
             tmem_ld16(tO + lane_off + (uint32_t)(part * hcols + c), o);
@@ -995,7 +994,7 @@ __global__ void __launch_bounds__(dual_threads<SW>(), 1)
       }
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&pfull[X]);
+      if (lane == 0) mbar_arrive(&pfull[2 * X + (j & 1)]);
     }
     // ------------------------------------------------------------ epilogue
     red_l[X][part][lane_row] = lsum;
@@ -1201,7 +1200,8 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
     uint64_t sv2[1] = {(uint64_t)PAGE};
     uint32_t bv2[2] = {(uint32_t)PAGE, (uint32_t)hd};
     if (!tma_map_bf16(&mk2, kv.base, 2, dk2, sk2, bk2) || !tma_map_bf16(&mv2, kv.base, 2, dv2, sv2, bv2)) return -1;
-    const size_t smem2 = 1024 + DST * ((size_t)DCHUNK * hd * 2) + DST * ((size_t)hd * 128) + (4 * DST + 8) * 8 + 64;
+    const size_t smem2 = 1024 + 2 * ((size_t)QROWS * hd * 2) + DST * ((size_t)DCHUNK * hd * 2) + DST * ((size_t)hd * 128) +
+                         (4 * DST + 16) * 8 + 64;
     static size_t attr2 = 0;
     if (smem2 > attr2) {
       if (cudaFuncSetAttribute(attention_dual_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2) !=
