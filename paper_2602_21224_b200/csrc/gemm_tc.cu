@@ -101,7 +101,8 @@ HSD_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 HSD_DEV void epi_bar_g(int g) { asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory"); }
 
 __global__ void __launch_bounds__(NTHREADS, 2)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, TcParams P) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                   const __grid_constant__ CUtensorMap tmO, TcParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned carve-up: [stages x A][stages x B][barriers][epilogue stage]
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -115,6 +116,9 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   uint64_t* tempty = bars + 2 * P.stages + 2;  // [2]
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * P.stages + 4);
   float* stage_buf = (float*)(bars + 2 * P.stages + 6);   // [16 tokens][EPI_LD] fp32
+  // P.tma_out (stream-K partials): dense [2 buffers][16 tokens][128] fp32 stages, 1024-aligned,
+  // each chunk leaves by one TMA bulk reduce-add
+  float* const dstage = (float*)(((uintptr_t)(bars + 2 * P.stages + 6) + 1023) & ~(uintptr_t)1023);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) GTRACE(0);
@@ -236,7 +240,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     pdl_wait();
     kstamp_wait(P.kst);
     const int q = warp & 3, et = threadIdx.x - 64;      // 0..127
-    int buf = 0;
+    int buf = 0, ck = 0;
     uint32_t aphase = 0;
     long i = 0;
     while (i < sc.count) {
@@ -249,9 +253,26 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       fence_after();
       if (threadIdx.x == 64) GTRACE(5);
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * P.ntile);
-      for (int c0 = 0; c0 < P.ntile; c0 += 16) {
+      for (int c0 = 0; c0 < P.ntile; c0 += 16, ++ck) {
         uint32_t r[16];
         tmem_ld16(taddr + c0, r);
+        if (P.tma_out) {
+          // stream-K partial: [16 tokens][128 features] dense stage -> one TMA reduce-add
+          // into the zero-kept fp32 scratch (the issuing thread waits until the previous
+          // chunk's bulk op has read its buffer, before the second barrier)
+          float* sb = dstage + (size_t)(ck & 1) * 16 * BM;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) sb[j * BM + q * 32 + lane] = __uint_as_float(r[j]);
+          fence_proxy_async();
+          epi_bar();
+          if (et == 0) {
+            tma_reduce_add_2d(&tmO, sb, tn * BM, tt * P.ntile + c0);
+            bulk_commit();
+            bulk_wait_read<1>();
+          }
+          epi_bar();
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) stage_buf[j * EPI_LD + q * 32 + lane] = __uint_as_float(r[j]);
         epi_bar();
@@ -312,6 +333,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       if (buf == 0) aphase ^= 1;
       i += seg;
     }
+    if (P.tma_out && et == 0) bulk_wait<0>();   // every bulk reduce of this CTA complete
   }
   fence_before();
   __syncthreads();
@@ -967,7 +989,13 @@ static int gemm_tc_launch(const bf16* A, int lda, const bf16* W, int ldw, float*
   CUtensorMap mw, mx;
   if (!make_map(&mw, W, N, K, ldw, BM) || !make_map(&mx, A, M, K, lda, nt)) return 0;
   P.vec4 = (ldc % 4 == 0) && (((uintptr_t)C & 15) == 0);
+  // stream-K partials by TMA bulk reduce-add (HSD_GEMM_TMA_SK=0: red.add.v4 from the threads)
+  static const int tma_sk = [] { const char* e = getenv("HSD_GEMM_TMA_SK"); return e ? atoi(e) : 1; }();
+  CUtensorMap mo;
+  memset(&mo, 0, sizeof(mo));
+  P.tma_out = (tma_sk && epi == EPI_ATOMIC && C && make_out_map(&mo, C, M, N, ldc, true)) ? 1 : 0;
   size_t smem = 1024 + (size_t)stages * (A_BYTES + b_bytes) + (2 * stages + 6) * 8 + 16 * EPI_LD * 4 + 16;
+  if (P.tma_out) smem = 1024 + (size_t)stages * (A_BYTES + b_bytes) + (2 * stages + 6) * 8 + 1024 + 2 * 16 * BM * 4;
   static bool attr_done = false;
   if (!attr_done) {
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -976,7 +1004,7 @@ static int gemm_tc_launch(const bf16* A, int lda, const bf16* W, int ldw, float*
   const long max_ctas = (long)num_sms() * cps;
   const long work = dp ? (long)P.n_tiles_n * P.n_tiles_t : P.units;
   const long grid = work < max_ctas ? work : max_ctas;
-  launch_k(gemm_tc_kernel, dim3((unsigned)grid), dim3(NTHREADS), smem, st, mw, mx, P);
+  launch_k(gemm_tc_kernel, dim3((unsigned)grid), dim3(NTHREADS), smem, st, mw, mx, mo, P);
   return 1;
 }
 
