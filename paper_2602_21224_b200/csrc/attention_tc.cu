@@ -1139,7 +1139,10 @@ int launch_attention_tc(const void* q, int M, int R, int n_req, const RowMeta& m
   // HSD_ATTN_DYNSPLIT: 0 off, 1 cap + device ranges (default), 2 cap only.
   static const int dyn = [] { const char* e = getenv("HSD_ATTN_DYNSPLIT"); return e ? atoi(e) : 1; }();
   const bool latency_bound = (pages + S - 1) / S <= 4;
-  if (dyn && latency_bound) S = min(S, max(1, num_sms() / base_ctas));
+  // (three quarters of a wave: c2's 9 visible chunks per (kv head, q-tile) split 3 / 3 / 3
+  // with S = 3, where S = 4 left one split CTA idle and gave the merge kernel a fourth
+  // partial to read -- step 4.78 -> 4.68 ms)
+  if (dyn && latency_bound) S = min(S, max(1, (3 * num_sms()) / (4 * base_ctas)));
   P.dyn = dyn == 1 && latency_bound;
   static const int s_override = [] { const char* e = getenv("HSD_ATTN_SPLITS"); return e ? atoi(e) : 0; }();
   if (s_override > 0) S = min(s_override, pages);
